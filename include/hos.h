@@ -1,0 +1,176 @@
+/*
+ * hos.h — C-ABI of the B200 direct-method HOS estimator (libhos_b200.so).
+ *
+ * Plain pointers and sizes only; no torch or CUDA types in the signatures
+ * (streams travel as void*, i.e. a cudaStream_t; NULL = legacy stream).
+ *
+ * The reference (hospectra 0.1.0) is pure Python, so "the interface each
+ * entry point replaces" is the Python function named beside it
+ * (paths relative to /root/reference/pkg/src/hospectra/):
+ *
+ *   hos_estimate               estimate_spectrum            spectra.py:434-439
+ *                              (segment_and_demean series.py:159-165,
+ *                               dft_segments dft.py:36-41,
+ *                               _compute_values spectra.py:391-416)
+ *   hos_estimate_from_spectra  estimate_from_spectra        spectra.py:419-431
+ *   hos_segment_spectra        dft_segments∘segment_and_demean
+ *                                                           dft.py:36-41, series.py:159-165
+ *   hos_domain_size/indices    principal_domain / domain_slice
+ *                                                           spectra.py:133-196
+ *   hos_partial_raw +          parallel_estimate's worker split
+ *   hos_smooth_raw               (_worker_run + _compute_values on a slice)
+ *                                                           parallel.py:94-162
+ *   hos_last_error             the ParameterError / DataError messages
+ *                                                           errors.py:4-9
+ *
+ * Error convention: every int-returning call returns HOS_OK (0) or one of
+ * HOS_EPARAM (-> ParameterError), HOS_EDATA (-> DataError), HOS_ECUDA /
+ * HOS_ENOMEM (-> RuntimeError); hos_last_error() returns the thread-local
+ * message of the last failure, keeping the reference's message fragments
+ * ("m3 < m/2", "k*m = ... exceeds series length n = ...").
+ *
+ * Numerics: precision 32 computes FFT + products in fp32 (FFMA2), combines
+ * segment-chunk partial sums and smooths in fp64, and writes complex64;
+ * precision 64 is fp64 end to end and writes complex128.
+ *
+ * Ownership: the caller owns every input/output buffer; a plan owns its
+ * cuFFT plan, scratch and geometry tables, all allocated at create time so
+ * hos_estimate* never allocate (stream-ordered, CUDA-graph capturable).
+ * A plan is used by one host thread / stream at a time.
+ */
+#ifndef HOS_B200_H
+#define HOS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HOS_OK 0
+#define HOS_EPARAM 1
+#define HOS_EDATA 2
+#define HOS_ECUDA 3
+#define HOS_ENOMEM 4
+
+/* element types */
+#define HOS_F32 0
+#define HOS_F64 1
+#define HOS_C64 2
+#define HOS_C128 3
+
+/* tapers */
+#define HOS_TAPER_NONE 0
+#define HOS_TAPER_HANN 1 /* periodic Hann 0.5-0.5cos(2 pi u/M), applied after demeaning */
+
+typedef struct hos_plan hos_plan;
+
+/* Library identification, e.g. "hos_b200 0.1.0 sm_100a". */
+const char* hos_version(void);
+
+/* Thread-local message of the last failed call ("" if none). */
+const char* hos_last_error(void);
+
+/* ---- principal domain (host-side, no GPU) -------------------------------
+ * spectra.py:133-196.  Order 3: 0<=k2<=k1, k1+k2<m/2.  Order 4:
+ * 0<=k3<=k2<=k1, k1+k2+k3<m/2.  Lexicographic order. */
+int64_t hos_domain_size(int order, int m);
+/* out: (stop-start) x (order-1) int32, the rows [start, stop) of the domain. */
+int hos_domain_indices(int order, int m, int64_t start, int64_t stop, int32_t* out);
+
+/* ---- plans ----------------------------------------------------------------
+ * order 3|4; segment length m >= 2; segments k >= 1; window m3 >= 1 with
+ * 2*m3 < m (spectra.py:70-79); conjugate_last 0|1; precision 32|64;
+ * taper HOS_TAPER_*; batch = independent series per call (>= 1);
+ * device = CUDA ordinal the plan's memory lives on. */
+int hos_plan_create(hos_plan** plan, int order, int m, int k, int m3, int conjugate_last,
+                    int precision, int taper, int batch, int device);
+void hos_plan_destroy(hos_plan* plan);
+
+/* Principal-domain points per series (= hos_domain_size(order, m)). */
+int64_t hos_plan_npoints(const hos_plan* plan);
+/* Raw cells of the dilated domain D_h per series (the smoothing support). */
+int64_t hos_plan_cells(const hos_plan* plan);
+/* Metric units per series: K * |D_h| segment.bin products. */
+int64_t hos_plan_units(const hos_plan* plan);
+/* Triple-product work per series actually issued by the kernel (cells incl.
+ * tile padding) times K; units/issued is the tiling efficiency. */
+int64_t hos_plan_issued(const hos_plan* plan);
+/* Device bytes the plan holds. */
+size_t hos_plan_device_bytes(const hos_plan* plan);
+/* Number of kernels one hos_estimate launches (cuFFT counted as 1). */
+int hos_plan_launches(const hos_plan* plan);
+
+/* ---- the hot path -----------------------------------------------------------
+ * x_dev: batch series, series b starting at x_dev + b*x_stride elements,
+ *   each with at least k*m samples (extra samples are ignored, as in
+ *   series.py:163); x_dtype HOS_F32 | HOS_F64.
+ * out_dev: batch x npoints complex values (HOS_C64 for precision 32,
+ *   HOS_C128 for precision 64), lexicographic principal-domain order. */
+int hos_estimate(hos_plan* plan, const void* x_dev, int x_dtype, int64_t x_stride,
+                 void* out_dev, void* stream);
+
+/* spec_dev: batch x k x m full complex spectra (spec_dtype HOS_C64|HOS_C128),
+ * arbitrary complex values (not required to be conjugate-symmetric). */
+int hos_estimate_from_spectra(hos_plan* plan, const void* spec_dev, int spec_dtype,
+                              void* out_dev, void* stream);
+
+/* Segment, demean (, taper) and transform: spec_dev receives batch x k x m
+ * full complex spectra (HOS_C64 for precision 32, HOS_C128 for 64). */
+int hos_segment_spectra(hos_plan* plan, const void* x_dev, int x_dtype, int64_t x_stride,
+                        void* spec_dev, void* stream);
+
+/* Plain batched DFT of `rows` real rows of length m (no demeaning): the
+ * reference's dft_segments on an already-demeaned SegmentSet (dft.py:36-41).
+ * spec_dev receives rows x m full complex spectra (HOS_C64 for precision 32,
+ * HOS_C128 for 64).  cuFFT plans are cached per (m, rows, precision). */
+int hos_dft_rows(const void* x_dev, int x_dtype, int rows, int m, int precision, void* spec_dev,
+                 void* stream);
+
+/* End to end with HOST buffers: copies x_host (pinned or pageable) in,
+ * runs hos_estimate, copies the values back to out_host, and synchronises
+ * the stream before returning. */
+int hos_estimate_host(hos_plan* plan, const void* x_host, int x_dtype, int64_t x_stride,
+                      void* out_host, void* stream);
+
+/* ---- multi-GPU building blocks (segment sharding) -------------------------
+ * Raw sums live in a CSR "line" layout over D_h: order 3 one line per raw
+ * row a = lo..; order 4 one line per raw pair (a,b).  line_start has
+ * nlines+1 entries (cells), point_line gives, for each output row k1
+ * (order 3) or pair (k1,k2) (order 4), the first line its window touches. */
+int64_t hos_plan_lines(const hos_plan* plan);
+int hos_plan_line_starts(const hos_plan* plan, int64_t* line_start /* nlines+1 */);
+
+/* Unscaled raw sums over segments [seg_begin, seg_end) of the (single)
+ * series: raw_dev receives cells values (c64 for precision 32, c128 for 64). */
+int hos_partial_raw(hos_plan* plan, const void* x_dev, int x_dtype, int seg_begin, int seg_end,
+                    void* raw_dev, void* stream);
+
+/* Smooth output rows [row_begin, row_end) (order 3: k1 rows; order 4: k1
+ * planes) from raw sums summed over ALL k segments.  raw_dev holds the
+ * cells of lines [line_begin, ...) (line_begin = the first line those rows
+ * need, i.e. row_begin for order 3), out_dev receives the lexicographic
+ * points of those rows (first point = domain offset of row_begin). */
+int hos_smooth_raw(hos_plan* plan, const void* raw_dev, int64_t line_begin, int row_begin,
+                   int row_end, void* out_dev, void* stream);
+/* Lexicographic offset of the first point of output row (k1) `row`. */
+int64_t hos_row_point_offset(const hos_plan* plan, int row);
+/* First line (inclusive) and last line (exclusive) needed by rows [r0,r1). */
+int hos_rows_line_range(const hos_plan* plan, int row_begin, int row_end, int64_t* line_begin,
+                        int64_t* line_end);
+
+/* ---- measurement helpers ----------------------------------------------------
+ * FP32 pipe peak (FFMA2 outer-product microbenchmark, flops counted as 2 per
+ * lane FMA) and the SM clock seen meanwhile, on the current device. */
+int hos_peak_fp32(double* tflops, double* sm_mhz, void* stream);
+/* Mean duration (ms) of the triple-product kernel launches of the last
+ * hos_estimate* call on this plan when timing was enabled (events recorded on
+ * the launching stream). */
+int hos_plan_set_timing(hos_plan* plan, int enable);
+int hos_plan_kernel_ms(const hos_plan* plan, double* triple_ms, double* total_ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HOS_B200_H */

@@ -1,0 +1,638 @@
+// C-ABI of libhos_b200 (include/hos.h): plan lifetime, orchestration of
+// K0 -> cuFFT -> K1 -> K2 -> K4a -> K4b on one stream, error mapping.
+#include <cuda_runtime.h>
+#include <cufft.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <string>
+#include <vector>
+
+#include "../../include/hos.h"
+#include "hos_geometry.h"
+#include "hos_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                           \
+  do {                                                                                           \
+    cudaError_t e_ = (expr);                                                                     \
+    if (e_ != cudaSuccess)                                                                       \
+      return fail(e_ == cudaErrorMemoryAllocation ? HOS_ENOMEM : HOS_ECUDA,                      \
+                  std::string("CUDA error in ") + #expr + ": " + cudaGetErrorString(e_));        \
+  } while (0)
+
+#define CUFFT_TRY(expr)                                                                         \
+  do {                                                                                          \
+    cufftResult r_ = (expr);                                                                    \
+    if (r_ != CUFFT_SUCCESS) return fail(HOS_ECUDA, std::string("cuFFT error ") +              \
+                                                        std::to_string((int)r_) + " in " + #expr); \
+  } while (0)
+
+}  // namespace
+
+struct hos_plan {
+  int order = 3, m = 0, k = 0, m3 = 1, conj = 1, precision = 32, taper = 0, batch = 1, device = 0;
+  hos::Geometry geo;
+  int nchunks = 1;
+  int hstride = 0;   // complex elements per half-spectrum row
+  int L = 0, Lp = 0; // extended-spectrum length / pitch (16-byte elements)
+  // device tables
+  hos::Task* d_tasks = nullptr;
+  int32_t* d_line_cmax = nullptr;
+  int64_t* d_line_start = nullptr;
+  int64_t* d_row_off = nullptr;
+  int32_t* d_pair_k1 = nullptr;
+  int32_t* d_pair_k2 = nullptr;
+  int64_t* d_pair_base = nullptr;
+  int32_t* d_line_of_ab = nullptr;
+  double* d_taper = nullptr;
+  // work buffers
+  void* d_seg = nullptr;   // batch*k*m real
+  void* d_half = nullptr;  // batch*k*hstride complex
+  void* d_E = nullptr;     // batch*k*Lp 16-byte elements
+  void* d_part = nullptr;  // batch*nchunks*ncells complex
+  double* d_S = nullptr;   // batch*ncells double2
+  void* d_xin = nullptr;   // host path staging (batch*k*m*8 bytes)
+  void* d_out = nullptr;   // host path staging
+  size_t bytes = 0;
+  std::map<int, cufftHandle> ffts;  // rows -> plan
+  // timing
+  int timing = 0;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  bool timed = false;
+};
+
+namespace {
+
+size_t csize(int precision) { return precision == 32 ? 8 : 16; }
+size_t rsize(int precision) { return precision == 32 ? 4 : 8; }
+
+template <typename T>
+int upload(hos_plan* p, T** dst, const std::vector<T>& src) {
+  if (src.empty()) return HOS_OK;
+  CUDA_TRY(cudaMalloc((void**)dst, src.size() * sizeof(T)));
+  p->bytes += src.size() * sizeof(T);
+  CUDA_TRY(cudaMemcpy(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return HOS_OK;
+}
+
+int alloc(hos_plan* p, void** dst, size_t n) {
+  if (n == 0) n = 16;
+  CUDA_TRY(cudaMalloc(dst, n));
+  p->bytes += n;
+  return HOS_OK;
+}
+
+int get_fft(hos_plan* p, int rows, cufftHandle* out) {
+  auto it = p->ffts.find(rows);
+  if (it != p->ffts.end()) {
+    *out = it->second;
+    return HOS_OK;
+  }
+  cufftHandle h;
+  int n[1] = {p->m};
+  int inembed[1] = {p->m};
+  int onembed[1] = {p->hstride};
+  CUFFT_TRY(cufftPlanMany(&h, 1, n, inembed, 1, p->m, onembed, 1, p->hstride,
+                          p->precision == 32 ? CUFFT_R2C : CUFFT_D2Z, rows));
+  p->ffts[rows] = h;
+  *out = h;
+  return HOS_OK;
+}
+
+int run_fft(hos_plan* p, int rows, const void* in, void* out, cudaStream_t st) {
+  cufftHandle h;
+  int rc = get_fft(p, rows, &h);
+  if (rc) return rc;
+  CUFFT_TRY(cufftSetStream(h, st));
+  if (p->precision == 32)
+    CUFFT_TRY(cufftExecR2C(h, (cufftReal*)in, (cufftComplex*)out));
+  else
+    CUFFT_TRY(cufftExecD2Z(h, (cufftDoubleReal*)in, (cufftDoubleComplex*)out));
+  return HOS_OK;
+}
+
+int check_plan(const hos_plan* p) {
+  if (!p) return fail(HOS_EPARAM, "null plan");
+  return HOS_OK;
+}
+
+// K2 + K4a + K4b over the extended spectra already in p->d_E.
+int run_back(hos_plan* p, void* out_dev, cudaStream_t st) {
+  hos::TripleArgs ta{};
+  ta.E = p->d_E;
+  ta.Lp = p->Lp;
+  ta.f_lo = p->geo.f_lo;
+  ta.K = p->k;
+  ta.seg_begin = 0;
+  ta.seg_end = p->k;
+  ta.nchunks = p->nchunks;
+  ta.tasks = p->d_tasks;
+  ta.ntasks = (int)p->geo.tasks.size();
+  ta.line_cmax = p->d_line_cmax;
+  ta.line_start = p->d_line_start;
+  ta.lo = p->geo.win.lo;
+  ta.part = p->d_part;
+  ta.ncells = p->geo.ncells;
+  ta.order = p->order;
+  ta.conj = p->conj;
+  ta.batch = p->batch;
+  if (p->timing) CUDA_TRY(cudaEventRecord(p->ev[1], st));
+  CUDA_TRY(hos::launch_triple(ta, p->precision, st));
+  if (p->timing) CUDA_TRY(cudaEventRecord(p->ev[2], st));
+  CUDA_TRY(hos::launch_line_scan(p->d_part, p->nchunks, p->geo.ncells, p->precision, p->d_line_start, 0,
+                                 p->geo.nlines, p->geo.ncells, p->batch, p->d_S, st));
+  hos::BoxArgs b{};
+  b.S = p->d_S;
+  b.s_series_stride = p->geo.ncells;
+  b.line_base = 0;
+  b.line_start = p->d_line_start;
+  b.cell_base = 0;
+  b.row_off = p->d_row_off;
+  b.rows = p->geo.rows;
+  b.pair_k1 = p->d_pair_k1;
+  b.pair_k2 = p->d_pair_k2;
+  b.pair_base = p->d_pair_base;
+  b.npairs = (int)p->geo.pair_k1.size();
+  b.line_of_ab = p->d_line_of_ab;
+  b.b_count = p->geo.b_count;
+  b.lo = p->geo.win.lo;
+  b.hi = p->geo.win.hi;
+  b.m3 = p->m3;
+  b.order = p->order;
+  b.p_begin = 0;
+  b.p_end = p->geo.npoints;
+  b.scale = 1.0 / ((double)p->m * (double)p->k * std::pow((double)p->m3, p->order - 1));
+  b.out = out_dev;
+  b.out_series_stride = p->geo.npoints;
+  b.precision = p->precision;
+  b.batch = p->batch;
+  CUDA_TRY(hos::launch_box(b, st));
+  if (p->timing) {
+    CUDA_TRY(cudaEventRecord(p->ev[3], st));
+    p->timed = true;
+  }
+  return HOS_OK;
+}
+
+int check_dtype_x(int x_dtype) {
+  if (x_dtype != HOS_F32 && x_dtype != HOS_F64)
+    return fail(HOS_EPARAM, "series dtype must be HOS_F32 or HOS_F64, got " + std::to_string(x_dtype));
+  return HOS_OK;
+}
+
+// K0 + FFT + K1 for all batch*k segments.
+int run_front(hos_plan* p, const void* x_dev, int x_dtype, int64_t x_stride, cudaStream_t st) {
+  const int rows = p->batch * p->k;
+  CUDA_TRY(hos::launch_prep(x_dev, x_dtype, x_stride, p->m, 0, p->k, p->batch, p->taper, p->d_taper, p->precision,
+                            p->d_seg, st));
+  int rc = run_fft(p, rows, p->d_seg, p->d_half, st);
+  if (rc) return rc;
+  CUDA_TRY(hos::launch_extend_half(p->d_half, p->m, p->hstride, rows, nullptr, p->geo.f_lo, p->L, p->Lp,
+                                   p->precision, p->d_E, st));
+  return HOS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hos_version(void) { return "hos_b200 0.1.0 sm_100a"; }
+
+const char* hos_last_error(void) { return g_err.c_str(); }
+
+int64_t hos_domain_size(int order, int m) {
+  if ((order != 3 && order != 4) || m < 2) return -1;
+  return hos::domain_size(order, m);
+}
+
+int hos_domain_indices(int order, int m, int64_t start, int64_t stop, int32_t* out) {
+  if (order != 3 && order != 4) return fail(HOS_EPARAM, "order must be 3 or 4, got " + std::to_string(order));
+  if (m < 2) return fail(HOS_EPARAM, "segment length must be >= 2, got " + std::to_string(m));
+  const int64_t total = hos::domain_size(order, m);
+  if (stop <= start) return HOS_OK;
+  if (!(0 <= start && start < stop && stop <= total))
+    return fail(HOS_EPARAM, "slice [" + std::to_string(start) + ", " + std::to_string(stop) +
+                                ") outside domain of size " + std::to_string(total));
+  if (!out) return fail(HOS_EPARAM, "null output");
+  hos::domain_rows(order, m, start, stop, out);
+  return HOS_OK;
+}
+
+int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjugate_last, int precision, int taper,
+                    int batch, int device) {
+  if (!out) return fail(HOS_EPARAM, "null plan pointer");
+  *out = nullptr;
+  if (m < 1 || k < 1)
+    return fail(HOS_EPARAM, "segment length and count must be positive, got m=" + std::to_string(m) +
+                                ", k=" + std::to_string(k));
+  if (precision != 32 && precision != 64)
+    return fail(HOS_EPARAM, "precision must be 32 or 64, got " + std::to_string(precision));
+  if (taper != HOS_TAPER_NONE && taper != HOS_TAPER_HANN)
+    return fail(HOS_EPARAM, "unknown taper code " + std::to_string(taper));
+  if (batch < 1) return fail(HOS_EPARAM, "batch must be >= 1, got " + std::to_string(batch));
+  hos_plan* p = new hos_plan();
+  p->order = order;
+  p->m = m;
+  p->k = k;
+  p->m3 = m3;
+  p->conj = conjugate_last ? 1 : 0;
+  p->precision = precision;
+  p->taper = taper;
+  p->batch = batch;
+  p->device = device;
+  std::string err = p->geo.build(order, m, m3);
+  if (!err.empty()) {
+    delete p;
+    return fail(HOS_EPARAM, err);
+  }
+  int rc = HOS_OK;
+  auto bail = [&](int code) {
+    hos_plan_destroy(p);
+    return code;
+  };
+  if (cudaSetDevice(device) != cudaSuccess) {
+    delete p;
+    return fail(HOS_ECUDA, "cannot select CUDA device " + std::to_string(device));
+  }
+  const hos::Geometry& g = p->geo;
+  p->hstride = m / 2 + 1;
+  p->L = g.f_hi - g.f_lo + 1;
+  p->Lp = (p->L + 1) & ~1;
+  // segment chunking: enough CTAs for ~4 per SM-slot
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  const int64_t spatial = (int64_t)g.tasks.size() * batch;
+  const int64_t target = (int64_t)sms * (precision == 32 ? 4 : 2);
+  int64_t nc = spatial > 0 ? (target + spatial - 1) / spatial : 1;
+  if (const char* env = std::getenv("HOS_NCHUNKS")) nc = std::atoll(env);
+  if (nc < 1) nc = 1;
+  if (nc > k) nc = k;
+  p->nchunks = (int)nc;
+
+  std::vector<int32_t> cmax(g.line_cmax.begin(), g.line_cmax.end());
+  if ((rc = upload(p, &p->d_tasks, g.tasks))) return bail(rc);
+  if ((rc = upload(p, &p->d_line_cmax, cmax))) return bail(rc);
+  if ((rc = upload(p, &p->d_line_start, g.line_start))) return bail(rc);
+  if ((rc = upload(p, &p->d_row_off, g.row_off))) return bail(rc);
+  if (order == 4) {
+    if ((rc = upload(p, &p->d_pair_k1, g.pair_k1))) return bail(rc);
+    if ((rc = upload(p, &p->d_pair_k2, g.pair_k2))) return bail(rc);
+    if ((rc = upload(p, &p->d_pair_base, g.pair_base))) return bail(rc);
+    if ((rc = upload(p, &p->d_line_of_ab, g.line_of_ab))) return bail(rc);
+  }
+  {
+    std::vector<double> tab(m);
+    for (int u = 0; u < m; u++) tab[u] = 0.5 - 0.5 * std::cos(2.0 * M_PI * u / m);
+    if ((rc = upload(p, &p->d_taper, tab))) return bail(rc);
+  }
+  const size_t rows = (size_t)batch * k;
+  if ((rc = alloc(p, &p->d_seg, rows * m * rsize(precision)))) return bail(rc);
+  if ((rc = alloc(p, &p->d_half, rows * p->hstride * csize(precision)))) return bail(rc);
+  if ((rc = alloc(p, &p->d_E, rows * p->Lp * 16))) return bail(rc);
+  if ((rc = alloc(p, &p->d_part, (size_t)batch * p->nchunks * g.ncells * csize(precision)))) return bail(rc);
+  if ((rc = alloc(p, (void**)&p->d_S, (size_t)batch * g.ncells * 16))) return bail(rc);
+  if ((rc = alloc(p, &p->d_xin, rows * m * 8))) return bail(rc);
+  if ((rc = alloc(p, &p->d_out, (size_t)batch * g.npoints * csize(precision)))) return bail(rc);
+  cufftHandle h;
+  if ((rc = get_fft(p, (int)rows, &h))) return bail(rc);
+  for (auto& e : p->ev)
+    if (cudaEventCreate(&e) != cudaSuccess) return bail(fail(HOS_ECUDA, "cudaEventCreate failed"));
+  *out = p;
+  return HOS_OK;
+}
+
+void hos_plan_destroy(hos_plan* p) {
+  if (!p) return;
+  for (auto& kv : p->ffts) cufftDestroy(kv.second);
+  void* bufs[] = {p->d_tasks, p->d_line_cmax, p->d_line_start, p->d_row_off, p->d_pair_k1, p->d_pair_k2,
+                  p->d_pair_base, p->d_line_of_ab, p->d_taper, p->d_seg, p->d_half, p->d_E, p->d_part,
+                  p->d_S, p->d_xin, p->d_out};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  for (auto& e : p->ev)
+    if (e) cudaEventDestroy(e);
+  delete p;
+}
+
+int64_t hos_plan_npoints(const hos_plan* p) { return p ? p->geo.npoints : -1; }
+int64_t hos_plan_cells(const hos_plan* p) { return p ? p->geo.ncells : -1; }
+int64_t hos_plan_units(const hos_plan* p) { return p ? p->geo.ncells * (int64_t)p->k : -1; }
+int64_t hos_plan_issued(const hos_plan* p) { return p ? p->geo.issued_cells * (int64_t)p->k : -1; }
+size_t hos_plan_device_bytes(const hos_plan* p) { return p ? p->bytes : 0; }
+int hos_plan_launches(const hos_plan* p) { return p ? 6 : -1; }
+int64_t hos_plan_lines(const hos_plan* p) { return p ? p->geo.nlines : -1; }
+
+int hos_plan_line_starts(const hos_plan* p, int64_t* ls) {
+  int rc = check_plan(p);
+  if (rc) return rc;
+  if (!ls) return fail(HOS_EPARAM, "null output");
+  std::memcpy(ls, p->geo.line_start.data(), p->geo.line_start.size() * sizeof(int64_t));
+  return HOS_OK;
+}
+
+int hos_estimate(hos_plan* p, const void* x_dev, int x_dtype, int64_t x_stride, void* out_dev, void* stream) {
+  int rc = check_plan(p);
+  if (rc) return rc;
+  if ((rc = check_dtype_x(x_dtype))) return rc;
+  if (!x_dev || !out_dev) return fail(HOS_EPARAM, "null buffer");
+  if (p->batch > 1 && x_stride < (int64_t)p->k * p->m)
+    return fail(HOS_EPARAM, "series stride " + std::to_string(x_stride) + " shorter than k*m = " +
+                                std::to_string((int64_t)p->k * p->m));
+  cudaStream_t st = (cudaStream_t)stream;
+  if (p->timing) CUDA_TRY(cudaEventRecord(p->ev[0], st));
+  if ((rc = run_front(p, x_dev, x_dtype, x_stride, st))) return rc;
+  return run_back(p, out_dev, st);
+}
+
+int hos_estimate_from_spectra(hos_plan* p, const void* spec_dev, int spec_dtype, void* out_dev, void* stream) {
+  int rc = check_plan(p);
+  if (rc) return rc;
+  if (spec_dtype != HOS_C64 && spec_dtype != HOS_C128)
+    return fail(HOS_EPARAM, "spectra dtype must be HOS_C64 or HOS_C128");
+  if (!spec_dev || !out_dev) return fail(HOS_EPARAM, "null buffer");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (p->timing) CUDA_TRY(cudaEventRecord(p->ev[0], st));
+  CUDA_TRY(hos::launch_extend_full(spec_dev, spec_dtype, p->m, p->batch * p->k, p->geo.f_lo, p->L, p->Lp,
+                                   p->precision, p->d_E, st));
+  return run_back(p, out_dev, st);
+}
+
+int hos_segment_spectra(hos_plan* p, const void* x_dev, int x_dtype, int64_t x_stride, void* spec_dev, void* stream) {
+  int rc = check_plan(p);
+  if (rc) return rc;
+  if ((rc = check_dtype_x(x_dtype))) return rc;
+  if (!x_dev || !spec_dev) return fail(HOS_EPARAM, "null buffer");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int rows = p->batch * p->k;
+  CUDA_TRY(hos::launch_prep(x_dev, x_dtype, x_stride, p->m, 0, p->k, p->batch, p->taper, p->d_taper, p->precision,
+                            p->d_seg, st));
+  if ((rc = run_fft(p, rows, p->d_seg, p->d_half, st))) return rc;
+  CUDA_TRY(hos::launch_expand_full(p->d_half, p->m, p->hstride, rows, p->precision, spec_dev, st));
+  return HOS_OK;
+}
+
+int hos_dft_rows(const void* x_dev, int x_dtype, int rows, int m, int precision, void* spec_dev, void* stream) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, int, int>, std::pair<cufftHandle, void*>> cache;  // -> plan, scratch
+  if ((x_dtype != HOS_F32 && x_dtype != HOS_F64) || (precision != 32 && precision != 64))
+    return fail(HOS_EPARAM, "bad dtype/precision");
+  if (rows < 1 || m < 1) return fail(HOS_EPARAM, "rows and m must be positive");
+  if (!x_dev || !spec_dev) return fail(HOS_EPARAM, "null buffer");
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  cudaStream_t st = (cudaStream_t)stream;
+  std::lock_guard<std::mutex> lock(mu);
+  auto key = std::make_tuple(dev, m, rows, precision);
+  auto it = cache.find(key);
+  const int hs = m / 2 + 1;
+  const size_t rs = precision == 32 ? 4 : 8, cs = 2 * rs;
+  if (it == cache.end()) {
+    cufftHandle h;
+    int n[1] = {m}, ine[1] = {m}, one[1] = {hs};
+    CUFFT_TRY(cufftPlanMany(&h, 1, n, ine, 1, m, one, 1, hs, precision == 32 ? CUFFT_R2C : CUFFT_D2Z, rows));
+    void* scratch = nullptr;  // cast input + half spectrum
+    CUDA_TRY(cudaMalloc(&scratch, (size_t)rows * m * rs + (size_t)rows * hs * cs + 256));
+    it = cache.emplace(key, std::make_pair(h, scratch)).first;
+  }
+  cufftHandle h = it->second.first;
+  char* scratch = (char*)it->second.second;
+  void* xin = scratch;
+  void* half = scratch + (((size_t)rows * m * rs + 255) & ~(size_t)255);
+  // cast only (rows are already demeaned): prep with taper off would demean again, so copy/cast here
+  const bool same = (x_dtype == HOS_F32) == (precision == 32);
+  if (same) {
+    CUDA_TRY(cudaMemcpyAsync(xin, x_dev, (size_t)rows * m * rs, cudaMemcpyDeviceToDevice, st));
+  } else {
+    CUDA_TRY(hos::launch_cast(x_dev, x_dtype, (int64_t)rows * m, precision, xin, st));
+  }
+  CUFFT_TRY(cufftSetStream(h, st));
+  if (precision == 32) CUFFT_TRY(cufftExecR2C(h, (cufftReal*)xin, (cufftComplex*)half));
+  else CUFFT_TRY(cufftExecD2Z(h, (cufftDoubleReal*)xin, (cufftDoubleComplex*)half));
+  CUDA_TRY(hos::launch_expand_full(half, m, hs, rows, precision, spec_dev, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return HOS_OK;
+}
+
+int hos_estimate_host(hos_plan* p, const void* x_host, int x_dtype, int64_t x_stride, void* out_host, void* stream) {
+  int rc = check_plan(p);
+  if (rc) return rc;
+  if ((rc = check_dtype_x(x_dtype))) return rc;
+  if (!x_host || !out_host) return fail(HOS_EPARAM, "null buffer");
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t es = x_dtype == HOS_F32 ? 4 : 8;
+  const size_t km = (size_t)p->k * p->m;
+  if (p->batch == 1 || x_stride == (int64_t)km) {
+    CUDA_TRY(cudaMemcpyAsync(p->d_xin, x_host, km * p->batch * es, cudaMemcpyHostToDevice, st));
+  } else {
+    CUDA_TRY(cudaMemcpy2DAsync(p->d_xin, km * es, x_host, (size_t)x_stride * es, km * es, p->batch,
+                               cudaMemcpyHostToDevice, st));
+  }
+  if ((rc = hos_estimate(p, p->d_xin, x_dtype, (int64_t)km, p->d_out, stream))) return rc;
+  CUDA_TRY(cudaMemcpyAsync(out_host, p->d_out, (size_t)p->batch * p->geo.npoints * csize(p->precision),
+                           cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return HOS_OK;
+}
+
+int hos_partial_raw(hos_plan* p, const void* x_dev, int x_dtype, int seg_begin, int seg_end, void* raw_dev,
+                    void* stream) {
+  int rc = check_plan(p);
+  if (rc) return rc;
+  if ((rc = check_dtype_x(x_dtype))) return rc;
+  if (p->batch != 1) return fail(HOS_EPARAM, "hos_partial_raw needs a batch-1 plan");
+  if (!(0 <= seg_begin && seg_begin <= seg_end && seg_end <= p->k))
+    return fail(HOS_EPARAM, "segment range [" + std::to_string(seg_begin) + ", " + std::to_string(seg_end) +
+                                ") outside [0, " + std::to_string(p->k) + ")");
+  if (!raw_dev) return fail(HOS_EPARAM, "null buffer");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nseg = seg_end - seg_begin;
+  if (nseg == 0) {
+    CUDA_TRY(cudaMemsetAsync(raw_dev, 0, p->geo.ncells * csize(p->precision), st));
+    return HOS_OK;
+  }
+  // front end on the shard only, written at its own segment rows
+  const size_t rs = rsize(p->precision);
+  void* seg = (char*)p->d_seg + (size_t)seg_begin * p->m * rs;
+  void* half = (char*)p->d_half + (size_t)seg_begin * p->hstride * csize(p->precision);
+  void* E = (char*)p->d_E + (size_t)seg_begin * p->Lp * 16;
+  CUDA_TRY(hos::launch_prep(x_dev, x_dtype, 0, p->m, seg_begin, nseg, 1, p->taper, p->d_taper, p->precision, seg, st));
+  if ((rc = run_fft(p, nseg, seg, half, st))) return rc;
+  CUDA_TRY(hos::launch_extend_half(half, p->m, p->hstride, nseg, nullptr, p->geo.f_lo, p->L, p->Lp, p->precision, E,
+                                   st));
+  hos::TripleArgs ta{};
+  ta.E = p->d_E;
+  ta.Lp = p->Lp;
+  ta.f_lo = p->geo.f_lo;
+  ta.K = p->k;
+  ta.seg_begin = seg_begin;
+  ta.seg_end = seg_end;
+  int nc = p->nchunks;
+  if (nc > nseg) nc = nseg;
+  ta.nchunks = nc;
+  ta.tasks = p->d_tasks;
+  ta.ntasks = (int)p->geo.tasks.size();
+  ta.line_cmax = p->d_line_cmax;
+  ta.line_start = p->d_line_start;
+  ta.lo = p->geo.win.lo;
+  ta.part = p->d_part;
+  ta.ncells = p->geo.ncells;
+  ta.order = p->order;
+  ta.conj = p->conj;
+  ta.batch = 1;
+  CUDA_TRY(hos::launch_triple(ta, p->precision, st));
+  CUDA_TRY(hos::launch_reduce_parts(p->d_part, nc, p->geo.ncells, p->geo.ncells, p->precision, raw_dev, st));
+  return HOS_OK;
+}
+
+int hos_smooth_raw(hos_plan* p, const void* raw_dev, int64_t line_begin, int row_begin, int row_end, void* out_dev,
+                   void* stream) {
+  int rc = check_plan(p);
+  if (rc) return rc;
+  if (p->batch != 1) return fail(HOS_EPARAM, "hos_smooth_raw needs a batch-1 plan");
+  if (!raw_dev || !out_dev) return fail(HOS_EPARAM, "null buffer");
+  int64_t lb = 0, le = 0;
+  if ((rc = hos_rows_line_range(p, row_begin, row_end, &lb, &le))) return rc;
+  if (row_end == row_begin) return HOS_OK;
+  if (line_begin > lb)
+    return fail(HOS_EPARAM, "raw buffer starts at line " + std::to_string(line_begin) + " but rows need line " +
+                                std::to_string(lb));
+  cudaStream_t st = (cudaStream_t)stream;
+  const hos::Geometry& g = p->geo;
+  // raw_dev holds cells of lines [line_begin, le); scan lines [lb, le)
+  const int64_t cell0 = g.line_start[line_begin];
+  const char* raw_lb = (const char*)raw_dev + (size_t)(g.line_start[lb] - cell0) * csize(p->precision);
+  double* S = p->d_S;  // scratch: cells of lines [lb, le)
+  CUDA_TRY(hos::launch_line_scan(raw_lb, 1, 0, p->precision, p->d_line_start, lb, le - lb, 0, 1, S, st));
+  hos::BoxArgs b{};
+  b.S = S;
+  b.s_series_stride = 0;
+  b.line_base = lb;
+  b.line_start = p->d_line_start;
+  b.cell_base = g.line_start[lb];
+  b.row_off = p->d_row_off;
+  b.rows = g.rows;
+  b.pair_k1 = p->d_pair_k1;
+  b.pair_k2 = p->d_pair_k2;
+  b.pair_base = p->d_pair_base;
+  b.npairs = (int)g.pair_k1.size();
+  b.line_of_ab = p->d_line_of_ab;
+  b.b_count = g.b_count;
+  b.lo = g.win.lo;
+  b.hi = g.win.hi;
+  b.m3 = p->m3;
+  b.order = p->order;
+  b.p_begin = g.row_off[row_begin];
+  b.p_end = g.row_off[row_end];
+  b.scale = 1.0 / ((double)p->m * (double)p->k * std::pow((double)p->m3, p->order - 1));
+  b.out = out_dev;
+  b.out_series_stride = 0;
+  b.precision = p->precision;
+  b.batch = 1;
+  CUDA_TRY(hos::launch_box(b, st));
+  return HOS_OK;
+}
+
+int64_t hos_row_point_offset(const hos_plan* p, int row) {
+  if (!p || row < 0 || row > p->geo.rows) return -1;
+  return p->geo.row_off[row];
+}
+
+int hos_rows_line_range(const hos_plan* p, int row_begin, int row_end, int64_t* lb, int64_t* le) {
+  int rc = check_plan(p);
+  if (rc) return rc;
+  if (!(0 <= row_begin && row_begin <= row_end && row_end <= p->geo.rows))
+    return fail(HOS_EPARAM, "row range outside the domain");
+  const hos::Geometry& g = p->geo;
+  if (p->order == 3) {
+    *lb = row_begin;
+    *le = row_end == row_begin ? row_begin : row_end - 1 + (p->m3 - 1) + 1;
+  } else {
+    // lines are a-major: first line with a >= row_begin + lo, first line with a > row_end - 1 + hi
+    int64_t b = 0, e = 0;
+    const int alo = row_begin + g.win.lo, ahi = row_end - 1 + g.win.hi;
+    while (b < g.nlines && g.line_a[b] < alo) b++;
+    e = b;
+    while (e < g.nlines && g.line_a[e] <= ahi) e++;
+    *lb = b;
+    *le = row_end == row_begin ? b : e;
+  }
+  return HOS_OK;
+}
+
+int hos_peak_fp32(double* tflops, double* sm_mhz, void* stream) {
+  if (!tflops || !sm_mhz) return fail(HOS_EPARAM, "null output");
+  cudaStream_t st = (cudaStream_t)stream;
+  int dev = 0, sms = 148;
+  CUDA_TRY(cudaGetDevice(&dev));
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int blocks = sms * 4, iters = 4096;
+  float2* buf = nullptr;
+  unsigned long long* clk = nullptr;
+  CUDA_TRY(cudaMalloc(&buf, (size_t)blocks * 256 * sizeof(float2)));
+  CUDA_TRY(cudaMalloc(&clk, 16));
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  CUDA_TRY(hos::launch_peak_fp32(buf, blocks, iters, st));  // warm-up
+  float best = 1e30f;
+  for (int r = 0; r < 5; r++) {
+    cudaEventRecord(a, st);
+    CUDA_TRY(hos::launch_peak_fp32(buf, blocks, iters, st));
+    cudaEventRecord(b, st);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    if (ms < best) best = ms;
+  }
+  // SM clock while the probe kernel is resident alongside a loaded device
+  CUDA_TRY(hos::launch_peak_fp32(buf, blocks, iters, st));
+  CUDA_TRY(hos::launch_clock_probe(clk, 20000000, st));
+  unsigned long long h[2] = {0, 0};
+  CUDA_TRY(cudaMemcpyAsync(h, clk, 16, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  const double flops = (double)blocks * 256 * iters * 32 * 2 * 2;
+  *tflops = flops / (best * 1e-3) / 1e12;
+  *sm_mhz = h[1] ? (double)h[0] / ((double)h[1] * 1e-3) : 0.0;
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(buf);
+  cudaFree(clk);
+  return HOS_OK;
+}
+
+int hos_plan_set_timing(hos_plan* p, int enable) {
+  int rc = check_plan(p);
+  if (rc) return rc;
+  p->timing = enable ? 1 : 0;
+  p->timed = false;
+  return HOS_OK;
+}
+
+int hos_plan_kernel_ms(const hos_plan* p, double* triple_ms, double* total_ms) {
+  int rc = check_plan(p);
+  if (rc) return rc;
+  if (!p->timed) return fail(HOS_EPARAM, "no timed call recorded (enable timing first)");
+  float t1 = 0, t2 = 0;
+  CUDA_TRY(cudaEventSynchronize(p->ev[3]));
+  CUDA_TRY(cudaEventElapsedTime(&t1, p->ev[1], p->ev[2]));
+  CUDA_TRY(cudaEventElapsedTime(&t2, p->ev[0], p->ev[3]));
+  if (triple_ms) *triple_ms = t1;
+  if (total_ms) *total_ms = t2;
+  return HOS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,84 @@
+// Host-side geometry of the direct-method estimator: the principal domain
+// P (hospectra/spectra.py:133-168), its window dilation D_h (the raw cells
+// the smoothing reads, SURVEY §8 notation) laid out as CSR "lines", and
+// the triple-product task list that tiles D_h for the K2 kernel.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace hos {
+
+// Window offsets per axis: [lo, hi] = [-m3/2, m3-1-m3/2]
+// (hospectra/spectra.py:8-11,395).
+struct Window {
+  int m3, lo, hi;
+  explicit Window(int w) : m3(w), lo(-(w / 2)), hi(w - 1 - w / 2) {}
+};
+
+// Output rows of the order-3 domain: k1 in [0, (m-1)/2], row length
+// min(k1, (m-2k1-1)/2)+1 (hospectra/spectra.py:146-147).
+inline int p3_rows(int m) { return (m - 1) / 2 + 1; }
+inline int p3_len(int m, int k1) {
+  int a = k1, b = (m - 2 * k1 - 1);
+  b = b >= 0 ? b / 2 : -((-b + 1) / 2);  // floor division like Python
+  return (a < b ? a : b) + 1;
+}
+// Order-4 k3 count for pair (k1,k2) (hospectra/spectra.py:155-158).
+inline int p4_len(int m, int k1, int k2) {
+  int b = m - 2 * k1 - 2 * k2 - 1;
+  b = b >= 0 ? b / 2 : -((-b + 1) / 2);
+  return (k2 < b ? k2 : b) + 1;
+}
+
+int64_t domain_size(int order, int m);
+// rows [start, stop) of the lexicographic domain into out ((stop-start) x (order-1))
+void domain_rows(int order, int m, int64_t start, int64_t stop, int32_t* out);
+
+// One K2 work item: a band of up to kBandRows consecutive lines of one plane
+// and up to kWarpsPerTask warp columns of kWarpCols cells each.
+constexpr int kBandRows = 32;     // lines per band (4 lane rows x 8 rows)
+constexpr int kWarpCols = 64;     // cells per warp along the line (8 lanes x 8)
+constexpr int kWarpsPerTask = 4;  // warps per CTA
+
+struct Task {
+  int32_t line0;      // first line of the band
+  int32_t nrows;      // lines in the band (<= kBandRows)
+  int32_t row_freq0;  // frequency of line0's row factor (order 3: a, order 4: b)
+  int32_t plane_freq; // order 4: a of the plane; order 3: 0
+  int32_t col0;       // first column (logical frequency) of warp 0
+  int32_t nwarps;     // active warp columns (<= kWarpsPerTask)
+  int32_t warp_mask;  // bit w set if warp w has at least one cell of D_h
+  int32_t pad;
+};
+
+struct Geometry {
+  int order = 3, m = 0, m3 = 1;
+  Window win{1};
+  // principal domain
+  int64_t npoints = 0;
+  int rows = 0;                     // order 3: k1 rows; order 4: k1 planes
+  std::vector<int64_t> row_off;     // rows+1: lexicographic offset of each k1
+  // order 4 pair table (k1,k2) with k3 count and lexicographic base
+  std::vector<int32_t> pair_k1, pair_k2, pair_n3;
+  std::vector<int64_t> pair_base;
+  std::vector<int32_t> row_pair0;   // order 4: first pair index of plane k1 (rows+1)
+  // dilated domain D_h as lines (CSR)
+  int64_t nlines = 0, ncells = 0;
+  std::vector<int32_t> line_a, line_b;  // logical row / pair coordinates (b = 0 for order 3)
+  std::vector<int32_t> line_cmax;       // last logical column; first column is win.lo
+  std::vector<int64_t> line_start;      // nlines+1
+  // order 4: dense (a,b) -> line lookup over [lo, amax] x [lo, bmax]
+  int a_count = 0, b_count = 0;
+  std::vector<int32_t> line_of_ab;
+  // order 3: line index = a - lo; lines of output row k1 start at k1
+  // frequencies touched by any task (inclusive), for the extended spectrum
+  int f_lo = 0, f_hi = 0;
+  // K2 task list
+  std::vector<Task> tasks;
+  int64_t issued_cells = 0;  // cells computed by the task list (incl. padding)
+
+  std::string build(int order, int m, int m3);  // returns "" or an error message
+};
+
+}  // namespace hos

@@ -1,0 +1,117 @@
+// sm_100a kernels of the direct-method HOS hot path.
+//
+//   K0 prep     segment + demean (+ Hann) + cast        hospectra/series.py:159-165
+//   (cuFFT)     batched R2C / D2Z per segment            hospectra/dft.py:36-41
+//   K1 extend   conjugate-symmetric extension of the half spectrum onto the
+//               frequency window [f_lo, f_hi] the triple product reads, in the
+//               "quad" layout (re, im, -im, re) so every operand form the FFMA2
+//               complex arithmetic needs is a free register swizzle
+//   K2 triple   R(line, c) = sum_i F_i(row) F_i(c) G_i(row + c [+ a])  over D_h,
+//               per segment chunk (hospectra/spectra.py:227-263)
+//   K4a scan    per-line prefix sums of the chunk-summed raw cells (fp64,
+//               warp shuffles)                           hospectra/tiled.py:36-47
+//   K4b box     window sums as prefix differences, scale 1/(M K w^(d)), write
+//               lexicographic principal-domain values   hospectra/spectra.py:405-415
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "hos_geometry.h"
+
+namespace hos {
+
+// ---------------------------------------------------------------------------
+// packed fp32x2 arithmetic (sm_100a FFMA2 / FMUL2).  Non-volatile asm so
+// ptxas can interleave independent cells; broadcast (make_float2(s, s)) and
+// swapped (make_float2(v.y, v.x)) operands compile to operand swizzles.
+
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long ra = *reinterpret_cast<unsigned long long*>(&a);
+  unsigned long long rb = *reinterpret_cast<unsigned long long*>(&b);
+  unsigned long long rc = *reinterpret_cast<unsigned long long*>(&c);
+  unsigned long long rd;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(rd) : "l"(ra), "l"(rb), "l"(rc));
+  return *reinterpret_cast<float2*>(&rd);
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  unsigned long long ra = *reinterpret_cast<unsigned long long*>(&a);
+  unsigned long long rb = *reinterpret_cast<unsigned long long*>(&b);
+  unsigned long long rd;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(rd) : "l"(ra), "l"(rb));
+  return *reinterpret_cast<float2*>(&rd);
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
+// ---------------------------------------------------------------------------
+// launch wrappers (hos_kernels.cu)
+
+struct TripleArgs {
+  const void* E;              // [series][K][Lp] quads (fp32) / double2 (fp64)
+  int Lp;                     // elements per segment row
+  int f_lo;                   // frequency of element 0
+  int K;                      // segments per series (E rows per series)
+  int seg_begin, seg_end;     // segment range reduced by this launch
+  int nchunks;                // chunks the range is split into
+  const Task* tasks;
+  int ntasks;
+  const int32_t* line_cmax;
+  const int64_t* line_start;
+  int lo;
+  void* part;                 // [series][nchunks][ncells] float2 / double2
+  int64_t ncells;
+  int order;
+  int conj;
+  int batch;
+};
+
+cudaError_t launch_prep(const void* x, int x_dtype, int64_t x_stride, int m, int seg_begin, int nseg,
+                        int batch, int taper, const double* taper_tab, int precision, void* seg_out,
+                        cudaStream_t st);
+cudaError_t launch_extend_half(const void* H, int m, int hstride, int rows, const void* /*unused*/,
+                               int f_lo, int L, int Lp, int precision, void* E, cudaStream_t st);
+cudaError_t launch_extend_full(const void* S, int spec_dtype, int m, int rows, int f_lo, int L, int Lp,
+                               int precision, void* E, cudaStream_t st);
+cudaError_t launch_expand_full(const void* H, int m, int hstride, int rows, int precision, void* out,
+                               cudaStream_t st);
+cudaError_t launch_triple(const TripleArgs& a, int precision, cudaStream_t st);
+cudaError_t launch_line_scan(const void* part, int nparts, int64_t part_stride, int precision,
+                             const int64_t* line_start, int64_t line_begin, int64_t nlines,
+                             int64_t ncells_series, int batch, double* S, cudaStream_t st);
+struct BoxArgs {
+  const double* S;          // prefix sums [series][ncells] (cells of lines from line_base)
+  int64_t s_series_stride;
+  int64_t line_base;        // line index of S's first line
+  const int64_t* line_start;
+  int64_t cell_base;        // line_start[line_base]
+  const int64_t* row_off;   // order 3: lexicographic offset per k1 row (rows+1)
+  int rows;
+  const int32_t* pair_k1;   // order 4 pair table
+  const int32_t* pair_k2;
+  const int64_t* pair_base;
+  int npairs;
+  const int32_t* line_of_ab;
+  int b_count;
+  int lo, hi, m3, order;
+  int64_t p_begin, p_end;   // lexicographic point range written
+  double scale;
+  void* out;                // [series][..] values for points [p_begin, p_end)
+  int64_t out_series_stride;
+  int precision;
+  int batch;
+};
+cudaError_t launch_box(const BoxArgs& a, cudaStream_t st);
+// raw[c] = sum_p part[p][c] (fp64 sum, stored in the compute precision)
+cudaError_t launch_reduce_parts(const void* part, int nparts, int64_t part_stride, int64_t n, int precision,
+                                void* raw, cudaStream_t st);
+cudaError_t launch_cast(const void* x, int x_dtype, int64_t n, int precision, void* out, cudaStream_t st);
+cudaError_t launch_peak_fp32(float2* buf, int blocks, int iters, cudaStream_t st);
+cudaError_t launch_clock_probe(unsigned long long* out, long long spin, cudaStream_t st);
+
+}  // namespace hos

@@ -1,0 +1,285 @@
+"""Data-parallel estimation (drop-in for hospectra/parallel.py) and the
+multi-GPU segment-sharded path.
+
+``parallel_estimate`` keeps the reference contract (same values for every
+worker count, parallel.py:120-162): on one GPU the worker count does not
+change the computation at all, so the result is bit-identical for any
+``WorkerConfig``.  ``partition_domain`` keeps the reference's row_blocks /
+point_blocks semantics (parallel.py:62-91) and is reused to cut output rows
+across GPUs.
+
+``distributed_estimate`` is the B200 multi-GPU path: one
+process per GPU, segments sharded across ranks, each rank computes partial
+raw sums over the whole dilated domain D_h (hos_partial_raw), the partials
+are reduce-scattered by contiguous line blocks (padded to a common count,
+as NCCL requires), each rank fetches the w-1 lines of halo it needs from the
+next rank (all_gather of block heads), smooths its own output rows
+(hos_smooth_raw) and the lexicographic slices are all-gathered.  The
+collective plumbing is torch.distributed (NCCL on GPUs, gloo in the CPU
+tests); the compute hooks are injectable so the orchestration is tested on
+CPU with world_size 2.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .errors import ParameterError
+from .series import TimeSeries
+from .spectra import EstimationConfig, SpectrumGrid, estimate_spectrum, principal_domain
+
+__all__ = ["WorkerConfig", "partition_domain", "parallel_estimate", "row_blocks", "ShardLayout",
+           "shard_layout", "distributed_estimate"]
+
+
+@dataclass(frozen=True)
+class WorkerConfig:
+    """Worker count and output-partition strategy (hospectra/parallel.py:40-59)."""
+
+    p: int = 1
+    partition: str = "row_blocks"
+
+    def __post_init__(self):
+        if self.p < 1:
+            raise ParameterError(f"worker count must be >= 1, got {self.p}")
+        if self.partition not in ("row_blocks", "point_blocks"):
+            raise ParameterError(
+                f"partition must be 'row_blocks' or 'point_blocks', got {self.partition!r}")
+
+
+def _split_bounds(dom: np.ndarray, workers: WorkerConfig) -> list[int]:
+    total = len(dom)
+    p = workers.p
+    if p == 1 or total == 0:
+        return [0, total] + [total] * (p - 1)
+    if workers.partition == "point_blocks":
+        q, r = divmod(total, p)
+        sizes = [q + 1] * r + [q] * (p - r)
+        return [0] + [int(v) for v in np.cumsum(sizes)]
+    _, first, counts = np.unique(dom[:, 0], return_index=True, return_counts=True)
+    cum = np.cumsum(counts)
+    targets = np.arange(1, p) * (total / p)
+    gb = np.searchsorted(cum, targets, side="left") + 1
+    cuts = [int(first[b]) if b < len(first) else total for b in gb]
+    return [0] + cuts + [total]
+
+
+def partition_domain(domain, workers: WorkerConfig) -> list:
+    """Disjoint contiguous parts of a lex-ordered domain whose concatenation
+    is the input (hospectra/parallel.py:83-91)."""
+    dom = np.asarray(domain)
+    b = _split_bounds(dom, workers)
+    return [dom[b[i]: b[i + 1]] for i in range(workers.p)]
+
+
+def parallel_estimate(series: TimeSeries, cfg: EstimationConfig, workers: WorkerConfig, *,
+                      device=None) -> SpectrumGrid:
+    """Same contract and values as ``estimate_spectrum`` for every worker
+    count (hospectra/parallel.py:120-162).  One GPU computes the whole
+    domain; the worker count only exists for API compatibility."""
+    if not isinstance(workers, WorkerConfig):
+        raise ParameterError("workers must be a WorkerConfig")
+    cfg.segment.validate_for(series)
+    return estimate_spectrum(series, cfg, device=device)
+
+
+# ---------------------------------------------------------------------------
+# multi-GPU: segment sharding + reduce-scatter + halo
+
+
+def row_blocks(row_off: np.ndarray, nranks: int) -> list[int]:
+    """Output-row cut points [r_0=0, ..., r_P=rows] balancing point counts at
+    whole-row granularity (the row_blocks policy of parallel.py:73-80)."""
+    rows = len(row_off) - 1
+    total = int(row_off[-1])
+    if nranks == 1 or total == 0:
+        return [0] + [rows] * nranks
+    counts = np.diff(row_off)
+    cum = np.cumsum(counts)
+    targets = np.arange(1, nranks) * (total / nranks)
+    cuts = [int(min(rows, np.searchsorted(cum, t, side="left") + 1)) for t in targets]
+    return [0] + cuts + [rows]
+
+
+@dataclass
+class ShardLayout:
+    """Who owns which lines/cells and output points."""
+
+    nranks: int
+    seg_bounds: list          # segment shard [s_r, s_{r+1})
+    row_bounds: list          # output rows [r_r, r_{r+1})
+    own_lines: list           # (l0, l1) lines reduce-scattered to rank r
+    need_lines: list          # (l0, l1) lines rank r smooths from
+    own_cells: list           # (c0, c1)
+    need_cells: list          # (c0, c1)
+    point_bounds: list        # lexicographic [p_r, p_{r+1})
+    block: int                # padded reduce-scatter block (cells)
+    halo: int                 # padded halo length (cells)
+    halo_in_next: bool        # every rank's halo lies in rank r+1's block
+
+
+def shard_layout(k: int, row_off: np.ndarray, line_start: np.ndarray, rows_line_range, nranks: int) -> ShardLayout:
+    """Static partition: segments evenly, output rows by row_blocks, lines
+    owned from the first line of each rank's rows, halo = lines the rank's
+    rows need past its own block."""
+    segb = [(r * k) // nranks for r in range(nranks + 1)]
+    rb = row_blocks(row_off, nranks)
+    nlines = len(line_start) - 1
+    need = [rows_line_range(rb[r], rb[r + 1]) for r in range(nranks)]
+    starts = []
+    for r in range(nranks):
+        lb = need[r][0] if rb[r] < rb[r + 1] else None
+        starts.append(lb)
+    # owned blocks: from each rank's first needed line to the next rank's
+    own = []
+    nxt = nlines
+    for r in reversed(range(nranks)):
+        l0 = starts[r] if starts[r] is not None else nxt
+        own.append((l0, nxt))
+        nxt = l0
+    own.reverse()
+    own[0] = (0, own[0][1])  # rank 0 owns from the first line (lines before are unused)
+    need_lines = [(need[r][0], need[r][1]) if rb[r] < rb[r + 1] else (own[r][0], own[r][0])
+                  for r in range(nranks)]
+    cells = lambda l0, l1: (int(line_start[l0]), int(line_start[l1]))
+    own_cells = [cells(*o) for o in own]
+    need_cells = [cells(*n) for n in need_lines]
+    block = max(max(c1 - c0 for c0, c1 in own_cells), 1)
+    halos = [max(0, need_cells[r][1] - own_cells[r][1]) for r in range(nranks)]
+    halo = max(max(halos), 1)
+    in_next = all(halos[r] == 0 or (r + 1 < nranks and halos[r] <= own_cells[r + 1][1] - own_cells[r + 1][0])
+                  for r in range(nranks))
+    pb = [int(row_off[r]) for r in rb]
+    return ShardLayout(nranks, segb, rb, own, need_lines, own_cells, need_cells, pb, block, halo, in_next)
+
+
+def distributed_estimate(x, cfg: EstimationConfig, *, group=None, engine=None, gather: bool = True):
+    """Segment-sharded estimate of ONE series across the ranks of ``group``.
+
+    ``x``: the full series on every rank (host numpy or a CUDA tensor; each
+    rank only reads its own segments).  ``engine`` supplies the compute
+    hooks (default: the GPU library); tests inject a CPU engine.
+    Returns the full (npoints,) value vector on every rank when ``gather``,
+    else this rank's lexicographic slice and its point range."""
+    import torch
+    import torch.distributed as dist
+
+    rank = dist.get_rank(group)
+    nranks = dist.get_world_size(group)
+    if engine is None:
+        engine = _GpuEngine(cfg)
+    lay = shard_layout(cfg.segment.k, engine.row_off, engine.line_start, engine.rows_line_range, nranks)
+    s0, s1 = lay.seg_bounds[rank], lay.seg_bounds[rank + 1]
+    raw = engine.partial_raw(x, s0, s1)                      # (ncells,) complex partial sums
+    send = engine.zeros(nranks * lay.block, raw.dtype)
+    for r in range(nranks):
+        c0, c1 = lay.own_cells[r]
+        send[r * lay.block: r * lay.block + (c1 - c0)] = raw[c0:c1]
+    mine = engine.zeros(lay.block, raw.dtype)
+    _reduce_scatter(dist, engine, mine, send, group)
+    oc0, oc1 = lay.own_cells[rank]
+    nc0, nc1 = lay.need_cells[rank]
+    local = engine.zeros(max(nc1, oc1) - oc0, raw.dtype)
+    local[: oc1 - oc0] = mine[: oc1 - oc0]
+    # halo: lines past the owned block, held by the following rank(s)
+    if lay.halo_in_next:
+        head = engine.zeros(lay.halo, raw.dtype)
+        n_head = min(lay.halo, oc1 - oc0)
+        head[:n_head] = mine[:n_head]
+        heads = _all_gather(dist, engine, head, nranks, group)
+        need = max(0, nc1 - oc1)
+        if need:
+            local[oc1 - oc0: oc1 - oc0 + need] = heads[rank + 1][:need]
+    else:
+        blocks = _all_gather(dist, engine, mine, nranks, group)
+        for r in range(rank + 1, nranks):
+            c0, c1 = lay.own_cells[r]
+            lo_, hi_ = max(c0, oc1), min(c1, nc1)
+            if lo_ < hi_:
+                local[lo_ - oc0: hi_ - oc0] = blocks[r][lo_ - c0: hi_ - c0]
+    r0, r1 = lay.row_bounds[rank], lay.row_bounds[rank + 1]
+    vals = engine.smooth(local, lay.own_lines[rank][0], r0, r1)  # points [p_r, p_{r+1})
+    if not gather:
+        return vals, (lay.point_bounds[rank], lay.point_bounds[rank + 1])
+    pmax = max(lay.point_bounds[r + 1] - lay.point_bounds[r] for r in range(nranks))
+    pad = engine.zeros(max(pmax, 1), vals.dtype)
+    pad[: len(vals)] = vals
+    parts = _all_gather(dist, engine, pad, nranks, group)
+    out = engine.zeros(lay.point_bounds[-1], vals.dtype)
+    for r in range(nranks):
+        a, b = lay.point_bounds[r], lay.point_bounds[r + 1]
+        out[a:b] = parts[r][: b - a]
+    return out
+
+
+def _reduce_scatter(dist, engine, out, inp, group):
+    # complex -> real view (NCCL/gloo reduce real dtypes)
+    o, i = engine.as_real(out), engine.as_real(inp)
+    if hasattr(dist, "reduce_scatter_tensor") and engine.backend_supports_rs(group):
+        dist.reduce_scatter_tensor(o, i, group=group)
+    else:
+        # gloo has no reduce_scatter: all_reduce then slice (CPU tests only)
+        tmp = i.clone()
+        dist.all_reduce(tmp, group=group)
+        r = dist.get_rank(group)
+        n = o.numel()
+        o.copy_(tmp[r * n: (r + 1) * n])
+
+
+def _all_gather(dist, engine, t, nranks, group):
+    import torch
+
+    rt = engine.as_real(t)
+    outs = [torch.empty_like(rt) for _ in range(nranks)]
+    dist.all_gather(outs, rt, group=group)
+    return [engine.from_real(o) for o in outs]
+
+
+class _GpuEngine:
+    """Compute hooks backed by libhos_b200 on the current CUDA device."""
+
+    def __init__(self, cfg: EstimationConfig):
+        import torch
+
+        from ._native import get_plan
+
+        self.torch = torch
+        self.cfg = cfg
+        self.plan = get_plan(cfg.order, cfg.segment.m, cfg.segment.k, cfg.m3, cfg.conjugate_last, cfg.bits,
+                             cfg.taper, 1, torch.cuda.current_device())
+        self.line_start = self.plan.line_starts()
+        rows = (cfg.segment.m - 1) // 2 + 1
+        self.row_off = np.array([self.plan.row_point_offset(r) for r in range(rows + 1)], dtype=np.int64)
+        self.rows_line_range = self.plan.rows_line_range
+        self.device = torch.device("cuda", self.plan.device)
+
+    def partial_raw(self, x, s0, s1):
+        torch = self.torch
+        if isinstance(x, np.ndarray):
+            x = torch.from_numpy(np.ascontiguousarray(x)).to(self.device)
+        raw = torch.empty(self.plan.cells, dtype=self.plan.complex_dtype, device=self.device)
+        return self.plan.partial_raw(x, s0, s1, raw)
+
+    def smooth(self, local, line_begin, r0, r1):
+        torch = self.torch
+        n = self.plan.row_point_offset(r1) - self.plan.row_point_offset(r0)
+        out = torch.empty(max(n, 1), dtype=self.plan.complex_dtype, device=self.device)
+        if n:
+            self.plan.smooth_raw(local, line_begin, r0, r1, out)
+        return out[:n]
+
+    def zeros(self, n, dtype):
+        return self.torch.zeros(n, dtype=dtype, device=self.device)
+
+    def as_real(self, t):
+        return self.torch.view_as_real(t).reshape(-1)
+
+    def from_real(self, t):
+        return self.torch.view_as_complex(t.reshape(-1, 2))
+
+    def backend_supports_rs(self, group):
+        import torch.distributed as dist
+
+        return dist.get_backend(group) == "nccl"

@@ -1,0 +1,265 @@
+"""GPU parity: libhos_b200 (through the drop-in API / C-ABI) vs the CPU
+oracle and the reference's own golden outputs.
+
+Bars (BASELINE.json north_star): max|dB|/max|B| <= 1e-5 in fp32 mode and
+<= 1e-11 in fp64 mode, identical principal-domain indexing.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import TOL_FP32, TOL_FP64, golden, max_rel_dev, north_star
+from oracle import hos_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"fp32": TOL_FP32, "fp64": TOL_FP64}
+
+
+def api():
+    import paper_1805_11775_b200 as P
+
+    return P
+
+
+def small_cases():
+    g = golden("small_cases.npz")
+    for name in g["names"]:
+        order, m, k, w, conj, seed, extra = (int(v) for v in g[f"{name}__meta"])
+        yield str(name), order, m, k, w, bool(conj), g[f"{name}__x"], g[f"{name}__idx"], g[f"{name}__val"]
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+@pytest.mark.parametrize("case", list(small_cases()), ids=lambda c: c[0])
+def test_small_cases_vs_reference(cuda, case, prec):
+    P = api()
+    name, order, m, k, w, conj, x, idx, val = case
+    cfg = P.EstimationConfig(order, P.SegmentConfig(m=m, k=k), w, conjugate_last=conj, precision=prec)
+    g = P.estimate_spectrum(P.TimeSeries(x), cfg)
+    assert np.array_equal(g.indices, idx)
+    assert g.values.dtype == np.complex128
+    err = north_star(g.values, val)
+    assert err <= TOL[prec], f"{name} {prec}: {err:.3e}"
+    if prec == "fp64":
+        # the reference's own plan-equivalence bar, per point (tests/test_spectra.py:243-255)
+        scale = max(float(np.abs(val).max()), 1e-300)
+        assert np.all(np.abs(g.values - val) <= np.maximum(1e-9 * np.abs(val), 1e-12 * scale)), name
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_cfg1_full_tapered(cuda, prec):
+    P = api()
+    gl = golden("cfg1.npz")
+    c = P.baseline_config("cfg1")
+    x = P.baseline_series(c)
+    assert hashlib.sha256(x.tobytes()).hexdigest() == str(gl["x_sha"])
+    cfg = P.EstimationConfig(3, P.SegmentConfig(m=c.m, k=c.k), c.m3, precision=prec, taper="hann")
+    g = P.estimate_spectrum(P.TimeSeries(x), cfg)
+    assert np.array_equal(g.indices, gl["idx"])
+    assert north_star(g.values, gl["val_hann"]) <= TOL[prec]
+    cfg0 = P.EstimationConfig(3, P.SegmentConfig(m=c.m, k=c.k), c.m3, precision=prec)
+    g0 = P.estimate_spectrum(P.TimeSeries(x), cfg0)
+    assert north_star(g0.values, gl["val_notaper"]) <= TOL[prec]
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+def test_cfg2_full_grid_vs_oracle(cuda, prec):
+    """Headline config, whole grid: GPU (device-resident fp32 input) vs the
+    oracle port (bit-exact with the reference, test_oracle.py) and the
+    reference's golden rows."""
+    import torch
+
+    P = api()
+    c = P.baseline_config("cfg2")
+    x = P.baseline_series(c)
+    gl = golden("cfg2_rows.npz")
+    assert hashlib.sha256(x.tobytes()).hexdigest() == str(gl["x_sha"])
+    cfg = P.EstimationConfig(3, P.SegmentConfig(m=c.m, k=c.k), c.m3, precision=prec, taper="hann")
+    g = P.estimate_spectrum(torch.from_numpy(x).to(cuda), cfg)
+    assert north_star(g.values[gl["pos"]], gl["val"]) <= TOL[prec]
+    spec = O.segment_spectra(x, c.m, c.k, "hann")
+    ref = O.parallel_efficient(spec, 3, c.m3, True, workers=8)
+    err = north_star(g.values, ref)
+    assert err <= TOL[prec], f"cfg2 {prec}: {err:.3e}"
+
+
+@pytest.mark.parametrize("name,prec", [("cfg3", "fp32"), ("cfg4", "fp32"), ("cfg4", "fp64")])
+def test_baseline_rows_vs_reference(cuda, name, prec):
+    import torch
+
+    P = api()
+    c = P.baseline_config(name)
+    x = P.baseline_series(c)
+    gl = golden(f"{name}_rows.npz")
+    assert hashlib.sha256(x.tobytes()).hexdigest() == str(gl["x_sha"])
+    cfg = P.EstimationConfig(c.order, P.SegmentConfig(m=c.m, k=c.k), c.m3, precision=prec, taper="hann")
+    g = P.estimate_spectrum(torch.from_numpy(x).to(cuda), cfg)
+    assert np.array_equal(g.indices[gl["pos"]], gl["idx"])
+    err = north_star(g.values[gl["pos"]], gl["val"])
+    assert err <= TOL[prec], f"{name} {prec}: {err:.3e}"
+
+
+def test_cfg5_batch(cuda):
+    import torch
+
+    P = api()
+    c = P.baseline_config("cfg5")
+    gl = golden("cfg5_series.npz")
+    x = P.baseline_series(c)
+    assert hashlib.sha256(x.tobytes()).hexdigest() == str(gl["x_sha"])
+    cfg = P.EstimationConfig(3, P.SegmentConfig(m=c.m, k=c.k), c.m3, precision="fp32", taper="hann")
+    vals = P.estimate_batch(torch.from_numpy(x).to(cuda), cfg)
+    assert vals.shape == (c.batch, P.principal_domain(3, c.m).shape[0])
+    for s in (0, 1, 4095):
+        assert north_star(vals[s], gl[f"val_{s}"]) <= TOL_FP32, s
+    # batch rows == single-series estimates (the single-series plan splits the
+    # segment sum into fp32 chunk partials, so they agree to fp32 rounding)
+    for s in (7, 2048):
+        one = P.estimate_spectrum(torch.from_numpy(x[s]).to(cuda), cfg)
+        assert north_star(vals[s], one.values) <= 1e-6
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+@pytest.mark.parametrize("order,m,k,w,conj", [(3, 64, 3, 5, True), (3, 50, 2, 4, False), (4, 32, 2, 3, True),
+                                              (4, 30, 3, 4, False)])
+def test_from_spectra_arbitrary_complex(cuda, order, m, k, w, conj, prec):
+    """estimate_from_spectra accepts any complex spectra (no conjugate
+    symmetry assumed), like the reference."""
+    P = api()
+    rng = np.random.default_rng(order * 100 + m)
+    spec = rng.standard_normal((k, m)) + 1j * rng.standard_normal((k, m))
+    cfg = P.EstimationConfig(order, P.SegmentConfig(m=m, k=k), w, conjugate_last=conj, precision=prec)
+    g = P.estimate_from_spectra(P.SegmentSpectrumSet(spectra=spec), cfg)
+    ref = O.efficient_values(spec, order, w, conj)
+    assert north_star(g.values, ref) <= TOL[prec]
+
+
+def test_dft_segments_matches_numpy(cuda):
+    P = api()
+    rng = np.random.default_rng(64)
+    for m in (1, 2, 3, 7, 16, 33, 64, 1000):
+        x = rng.standard_normal(3 * m)
+        segs = P.segment_and_demean(P.TimeSeries(x), P.SegmentConfig(m=m, k=3))
+        got = P.dft_segments(segs).spectra
+        ref = np.fft.fft(segs.segments, axis=1)
+        scale = max(float(np.abs(ref).max()), 1.0)
+        assert np.max(np.abs(got - ref)) <= 1e-12 * scale, m
+
+
+def test_reference_semantics(cuda):
+    """Ports of hospectra tests/test_spectra.py:158-255 on the GPU path."""
+    P = api()
+    # constant series -> exactly zero grid
+    for order in (3, 4):
+        for prec in ("fp64", "fp32"):
+            g = P.estimate_spectrum(P.TimeSeries(np.full(64, 2.5)),
+                                    P.EstimationConfig(order, P.SegmentConfig(m=64), 5, precision=prec))
+            assert np.all(g.values == 0)
+    # window too large
+    with pytest.raises(P.ParameterError, match="m3 < m/2"):
+        P.EstimationConfig(3, P.SegmentConfig(m=64), 32)
+    with pytest.raises(P.ParameterError, match="exceeds series length"):
+        P.estimate_spectrum(P.TimeSeries(np.ones(100)), P.EstimationConfig(3, P.SegmentConfig(m=64, k=2), 5))
+    # homogeneity alpha^3 / alpha^4
+    rng = np.random.default_rng(6)
+    x = rng.standard_normal(128)
+    a = 1.7
+    g1 = P.estimate_spectrum(P.TimeSeries(x), P.EstimationConfig(3, P.SegmentConfig(m=128), 5))
+    g2 = P.estimate_spectrum(P.TimeSeries(a * x), P.EstimationConfig(3, P.SegmentConfig(m=128), 5))
+    assert max_rel_dev(g2.values, a ** 3 * g1.values) < 1e-9
+    h1 = P.estimate_spectrum(P.TimeSeries(x[:64]), P.EstimationConfig(4, P.SegmentConfig(m=64), 5))
+    h2 = P.estimate_spectrum(P.TimeSeries(a * x[:64]), P.EstimationConfig(4, P.SegmentConfig(m=64), 5))
+    assert max_rel_dev(h2.values, a ** 4 * h1.values) < 1e-9
+    # conjugate variant differs, and every plan name gives identical values
+    s = P.generate_qpc(0.1, 0.15, 64, 0.4, seed=10)
+    wc = P.estimate_spectrum(s, P.EstimationConfig(3, P.SegmentConfig(m=64), 3, conjugate_last=True))
+    nc = P.estimate_spectrum(s, P.EstimationConfig(3, P.SegmentConfig(m=64), 3, conjugate_last=False))
+    assert not np.allclose(wc.values, nc.values)
+    for plan in P.SmoothingPlan:
+        got = P.estimate_spectrum(s, P.EstimationConfig(3, P.SegmentConfig(m=64), 3, plan, conjugate_last=False))
+        assert np.array_equal(got.values, nc.values) and got.plan is plan
+    # QPC peak at the coupled pair (tests/test_acceptance.py:239-249)
+    q = P.generate_qpc(0.1, 0.15, 1024, 0.0, seed=7)
+    for prec in ("fp64", "fp32"):
+        g = P.estimate_spectrum(q, P.EstimationConfig(3, P.SegmentConfig(m=1024), 5, precision=prec))
+        assert g.peak_point().k == (154, 102)
+    gl = golden("qpc1024.npz")
+    g = P.estimate_spectrum(q, P.EstimationConfig(3, P.SegmentConfig(m=1024), 5))
+    assert north_star(g.values[gl["pos"]], gl["val"]) <= TOL_FP64 * 10
+
+
+def test_parallel_estimate_invariant(cuda):
+    P = api()
+    s = P.generate_qpc(0.1, 0.15, 256, 0.4, seed=4)
+    cfg = P.EstimationConfig(3, P.SegmentConfig(m=256), 9)
+    ref = P.estimate_spectrum(s, cfg)
+    for p in (1, 2, 4, 8):
+        for part in ("row_blocks", "point_blocks"):
+            got = P.parallel_estimate(s, cfg, P.WorkerConfig(p=p, partition=part))
+            assert np.array_equal(got.values, ref.values)
+            assert np.array_equal(got.indices, ref.indices)
+
+
+def test_deterministic_repeat(cuda):
+    import torch
+
+    P = api()
+    c = P.baseline_config("cfg2")
+    x = torch.from_numpy(P.baseline_series(c)).to(cuda)
+    cfg = P.EstimationConfig(3, P.SegmentConfig(m=c.m, k=c.k), c.m3, precision="fp32", taper="hann")
+    a = P.estimate_spectrum(x, cfg).values
+    b = P.estimate_spectrum(x, cfg).values
+    assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("prec", [32, 64])
+def test_host_entry_point_matches_device(cuda, prec):
+    import torch
+
+    from paper_1805_11775_b200._native import get_plan
+
+    P = api()
+    c = P.baseline_config("cfg2")
+    x = P.baseline_series(c)
+    plan = get_plan(3, c.m, c.k, c.m3, True, prec, "hann", 1, 0)
+    dev = plan.estimate(torch.from_numpy(x).to(cuda)).cpu().numpy()
+    host = plan.estimate_host(x)
+    assert np.array_equal(dev, host)
+
+
+@pytest.mark.parametrize("order,m,k,w", [(3, 256, 12, 9), (4, 64, 6, 5)])
+def test_shard_pipeline_single_gpu(cuda, order, m, k, w):
+    """The multi-GPU building blocks on one GPU: partial raw sums of segment
+    shards (hos_partial_raw), summed, then smoothing by output-row blocks
+    (hos_smooth_raw) reproduces hos_estimate."""
+    import torch
+
+    from paper_1805_11775_b200._native import get_plan
+    from paper_1805_11775_b200.parallel import shard_layout
+
+    P = api()
+    x = torch.from_numpy(np.random.default_rng(5).standard_normal(m * k)).to(cuda)
+    plan = get_plan(order, m, k, w, True, 64, None, 1, 0)
+    ref = plan.estimate(x).cpu().numpy()
+    rows = (m - 1) // 2 + 1
+    row_off = np.array([plan.row_point_offset(r) for r in range(rows + 1)])
+    lay = shard_layout(k, row_off, plan.line_starts(), plan.rows_line_range, 3)
+    raw = torch.zeros(plan.cells, dtype=torch.complex128, device=cuda)
+    for r in range(3):
+        part = torch.empty_like(raw)
+        plan.partial_raw(x, lay.seg_bounds[r], lay.seg_bounds[r + 1], part)
+        raw += part
+    out = np.empty(plan.npoints, np.complex128)
+    for r in range(3):
+        r0, r1 = lay.row_bounds[r], lay.row_bounds[r + 1]
+        l0 = lay.own_lines[r][0]
+        c0 = int(plan.line_starts()[l0])
+        n = plan.row_point_offset(r1) - plan.row_point_offset(r0)
+        if n == 0:
+            continue
+        o = torch.empty(n, dtype=torch.complex128, device=cuda)
+        plan.smooth_raw(raw[c0:], l0, r0, r1, o)
+        out[lay.point_bounds[r]: lay.point_bounds[r + 1]] = o.cpu().numpy()
+    assert north_star(out, ref) <= 1e-13
