@@ -168,6 +168,12 @@ int hos_peak_fp32(double* tflops, double* sm_mhz, void* stream);
  * hos_estimate* call on this plan when timing was enabled (events recorded on
  * the launching stream). */
 int hos_plan_set_timing(hos_plan* plan, int enable);
+/* Diagnostics: K2 CTAs per series, and an optional device buffer of
+ * 8 x nctas x batch uint64 that K2 fills per CTA with {start, first-data,
+ * end (globaltimer ns), smid, warp-0 wait cycles, slots, warp-3 wait
+ * cycles, 0}; NULL disables. */
+int hos_plan_nctas(const hos_plan* plan);
+int hos_plan_set_trace(hos_plan* plan, void* trace_dev);
 int hos_plan_kernel_ms(const hos_plan* plan, double* triple_ms, double* total_ms);
 
 #ifdef __cplusplus

@@ -24,7 +24,7 @@ HOS_OK, HOS_EPARAM, HOS_EDATA, HOS_ECUDA, HOS_ENOMEM = 0, 1, 2, 3, 4
 HOS_F32, HOS_F64, HOS_C64, HOS_C128 = 0, 1, 2, 3
 TAPERS = {None: 0, "none": 0, "hann": 1}
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhos_b200.so")
+LIB_PATH = os.environ.get("HOS_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhos_b200.so")
 
 _i, _i64, _p, _d = ctypes.c_int, ctypes.c_int64, ctypes.c_void_p, ctypes.c_double
 _pp = ctypes.POINTER(ctypes.c_void_p)
@@ -56,6 +56,8 @@ EXPORTED_SYMBOLS = {
     "hos_rows_line_range": (_i, [_p, _i, _i, _p, _p]),
     "hos_peak_fp32": (_i, [_p, _p, _p]),
     "hos_plan_set_timing": (_i, [_p, _i]),
+    "hos_plan_nctas": (_i, [_p]),
+    "hos_plan_set_trace": (_i, [_p, _p]),
     "hos_plan_kernel_ms": (_i, [_p, _p, _p]),
 }
 

@@ -1,5 +1,7 @@
 // C-ABI of libhos_b200 (include/hos.h): plan lifetime, orchestration of
 // K0 -> cuFFT -> K1 -> K2 -> K4a -> K4b on one stream, error mapping.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <cufft.h>
 
@@ -46,11 +48,17 @@ int fail(int code, const std::string& msg) {
 struct hos_plan {
   int order = 3, m = 0, k = 0, m3 = 1, conj = 1, precision = 32, taper = 0, batch = 1, device = 0;
   hos::Geometry geo;
-  int nchunks = 1;
+  int nctas = 1;      // K2 CTAs per series (full-K launch); warps = 4 x nctas
+  int maxslots = 1;   // partial slots allocated per series
+  int occupancy = 1;  // K2 CTAs per SM
+  int sms = 148;
   int hstride = 0;   // complex elements per half-spectrum row
   int L = 0, Lp = 0; // extended-spectrum length / pitch (16-byte elements)
   // device tables
   hos::Task* d_tasks = nullptr;
+  int32_t* d_line_region0 = nullptr;
+  int32_t* d_region_task = nullptr;
+  CUtensorMap map_rows, map_cols[3], map_g[3], map_plane;
   int32_t* d_line_cmax = nullptr;
   int64_t* d_line_start = nullptr;
   int64_t* d_row_off = nullptr;
@@ -63,11 +71,12 @@ struct hos_plan {
   void* d_seg = nullptr;   // batch*k*m real
   void* d_half = nullptr;  // batch*k*hstride complex
   void* d_E = nullptr;     // batch*k*Lp 16-byte elements
-  void* d_part = nullptr;  // batch*nchunks*ncells complex
+  void* d_part = nullptr;  // batch*maxslots*ncells complex
   double* d_S = nullptr;   // batch*ncells double2
   void* d_xin = nullptr;   // host path staging (batch*k*m*8 bytes)
   void* d_out = nullptr;   // host path staging
   size_t bytes = 0;
+  unsigned long long* trace = nullptr;  // optional K2 per-CTA trace (device, 8 x nctas x batch)
   std::map<int, cufftHandle> ffts;  // rows -> plan
   // timing
   int timing = 0;
@@ -130,31 +139,111 @@ int check_plan(const hos_plan* p) {
   return HOS_OK;
 }
 
+// CTAs splitting a launch over nseg segments of `batch` series: one wave of
+// SMs x occupancy CTAs in total, at least 16 work units per CTA (and never
+// more CTAs than units, so every CTA's range is non-empty).
+int nctas_for(const hos_plan* p, int nseg, int batch) {
+  const int64_t work = (int64_t)p->geo.tasks.size() * nseg;
+  int64_t n = 0;
+  if (const char* env = std::getenv("HOS_NCTAS")) n = std::atoll(env);
+  if (n <= 0) {
+    const int64_t slots = (int64_t)p->sms * p->occupancy;
+    n = (slots + batch - 1) / batch;
+    n = std::min<int64_t>(n, std::max<int64_t>(1, work / 16));
+  }
+  n = std::min<int64_t>(n, std::max<int64_t>(1, work));
+  return (int)std::max<int64_t>(1, n);
+}
+
+// partial slots the worst task needs (same arithmetic as the kernels)
+int slots_needed(const hos_plan* p, int nseg, int n) {
+  const int64_t T = (int64_t)p->geo.tasks.size(), W = T * nseg;
+  if (W <= 0) return 1;
+  auto cta = [&](int64_t u) { return ((u + 1) * (int64_t)n - 1) / W; };
+  int best = 1;
+  for (int64_t t = 0; t < T; t++) best = std::max(best, (int)(cta((t + 1) * nseg - 1) - cta(t * nseg) + 1));
+  return best;
+}
+
+hos::SlotInfo slot_info(const hos_plan* p, int nseg, int n) {
+  hos::SlotInfo si{};
+  si.line_region0 = p->d_line_region0;
+  si.region_task = p->d_region_task;
+  si.ntasks = (int)p->geo.tasks.size();
+  si.nseg = nseg;
+  si.nctas = n;
+  return si;
+}
+
+hos::TripleArgs triple_args(const hos_plan* p, int seg_begin, int seg_end, int n, int batch) {
+  hos::TripleArgs x;
+  std::memset(&x, 0, sizeof(x));
+  x.map_rows = p->map_rows;
+  for (int k = 0; k < 3; k++) {
+    x.map_cols[k] = p->map_cols[k];
+    x.map_g[k] = p->map_g[k];
+  }
+  x.map_plane = p->map_plane;
+  x.f_lo = p->geo.f_lo;
+  x.K = p->k;
+  x.seg_begin = seg_begin;
+  x.seg_end = seg_end;
+  x.tasks = p->d_tasks;
+  x.ntasks = (int)p->geo.tasks.size();
+  x.nctas = n;
+  x.line_cmax = p->d_line_cmax;
+  x.line_start = p->d_line_start;
+  x.lo = p->geo.win.lo;
+  x.part = p->d_part;
+  x.ncells = p->geo.ncells;
+  x.maxslots = p->maxslots;
+  x.order = p->order;
+  x.conj = p->conj;
+  x.batch = batch;
+  x.trace = p->trace;
+  return x;
+}
+
+// 2-D tensor maps over E viewed as [rows][2 Lp x 8 bytes]; box = {2 x width,
+// kSegsPerSlot}; the innermost box row is one contiguous run of the segment's
+// spectrum (<= 256 x 8 bytes), boxes past the last row are zero-filled.
+int make_maps(hos_plan* p) {
+  static PFN_cuTensorMapEncodeTiled encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn ||
+        q != cudaDriverEntryPointSuccess)
+      return fail(HOS_ECUDA, "cuTensorMapEncodeTiled is unavailable from the CUDA driver");
+    encode = (PFN_cuTensorMapEncodeTiled)fn;
+  }
+  const cuuint64_t rows = (cuuint64_t)p->batch * p->k;
+  const cuuint64_t dims[2] = {(cuuint64_t)p->Lp * 2, rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)p->Lp * 16};
+  const cuuint32_t estr[2] = {1, 1};
+  struct {
+    CUtensorMap* m;
+    cuuint32_t w;
+  } maps[8] = {{&p->map_rows, 32},  {&p->map_plane, 1}, {&p->map_cols[0], 32}, {&p->map_cols[1], 64},
+               {&p->map_cols[2], 96}, {&p->map_g[0], 63}, {&p->map_g[1], 95},    {&p->map_g[2], 127}};
+  for (auto& mm : maps) {
+    const cuuint32_t box[2] = {2 * mm.w, (cuuint32_t)hos::kSegsPerSlot};
+    CUresult r = encode(mm.m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, p->d_E, dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(HOS_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  }
+  return HOS_OK;
+}
+
 // K2 + K4a + K4b over the extended spectra already in p->d_E.
 int run_back(hos_plan* p, void* out_dev, cudaStream_t st) {
-  hos::TripleArgs ta{};
-  ta.E = p->d_E;
-  ta.Lp = p->Lp;
-  ta.f_lo = p->geo.f_lo;
-  ta.K = p->k;
-  ta.seg_begin = 0;
-  ta.seg_end = p->k;
-  ta.nchunks = p->nchunks;
-  ta.tasks = p->d_tasks;
-  ta.ntasks = (int)p->geo.tasks.size();
-  ta.line_cmax = p->d_line_cmax;
-  ta.line_start = p->d_line_start;
-  ta.lo = p->geo.win.lo;
-  ta.part = p->d_part;
-  ta.ncells = p->geo.ncells;
-  ta.order = p->order;
-  ta.conj = p->conj;
-  ta.batch = p->batch;
+  const hos::TripleArgs ta = triple_args(p, 0, p->k, p->nctas, p->batch);
   if (p->timing) CUDA_TRY(cudaEventRecord(p->ev[1], st));
   CUDA_TRY(hos::launch_triple(ta, p->precision, st));
   if (p->timing) CUDA_TRY(cudaEventRecord(p->ev[2], st));
-  CUDA_TRY(hos::launch_line_scan(p->d_part, p->nchunks, p->geo.ncells, p->precision, p->d_line_start, 0,
-                                 p->geo.nlines, p->geo.ncells, p->batch, p->d_S, st));
+  CUDA_TRY(hos::launch_line_scan(p->d_part, p->maxslots, p->geo.ncells, slot_info(p, p->k, p->nctas), p->precision,
+                                 p->d_line_start, 0, p->geo.nlines, p->geo.ncells, p->batch, p->d_S, st));
   hos::BoxArgs b{};
   b.S = p->d_S;
   b.s_series_stride = p->geo.ncells;
@@ -173,6 +262,11 @@ int run_back(hos_plan* p, void* out_dev, cudaStream_t st) {
   b.hi = p->geo.win.hi;
   b.m3 = p->m3;
   b.order = p->order;
+  b.m = p->m;
+  b.row_begin = 0;
+  b.row_end = p->geo.rows;
+  b.pair_begin = 0;
+  b.pair_end = (int)p->geo.pair_k1.size();
   b.p_begin = 0;
   b.p_end = p->geo.npoints;
   b.scale = 1.0 / ((double)p->m * (double)p->k * std::pow((double)p->m3, p->order - 1));
@@ -272,19 +366,15 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
   p->hstride = m / 2 + 1;
   p->L = g.f_hi - g.f_lo + 1;
   p->Lp = (p->L + 1) & ~1;
-  // segment chunking: enough CTAs for ~4 per SM-slot
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  const int64_t spatial = (int64_t)g.tasks.size() * batch;
-  const int64_t target = (int64_t)sms * (precision == 32 ? 4 : 2);
-  int64_t nc = spatial > 0 ? (target + spatial - 1) / spatial : 1;
-  if (const char* env = std::getenv("HOS_NCHUNKS")) nc = std::atoll(env);
-  if (nc < 1) nc = 1;
-  if (nc > k) nc = k;
-  p->nchunks = (int)nc;
+  cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, device);
+  p->occupancy = hos::triple_occupancy(precision);
+  p->nctas = nctas_for(p, k, batch);
+  p->maxslots = slots_needed(p, k, p->nctas);
 
   std::vector<int32_t> cmax(g.line_cmax.begin(), g.line_cmax.end());
   if ((rc = upload(p, &p->d_tasks, g.tasks))) return bail(rc);
+  if ((rc = upload(p, &p->d_line_region0, g.line_region0))) return bail(rc);
+  if ((rc = upload(p, &p->d_region_task, g.region_task))) return bail(rc);
   if ((rc = upload(p, &p->d_line_cmax, cmax))) return bail(rc);
   if ((rc = upload(p, &p->d_line_start, g.line_start))) return bail(rc);
   if ((rc = upload(p, &p->d_row_off, g.row_off))) return bail(rc);
@@ -303,12 +393,13 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
   if ((rc = alloc(p, &p->d_seg, rows * m * rsize(precision)))) return bail(rc);
   if ((rc = alloc(p, &p->d_half, rows * p->hstride * csize(precision)))) return bail(rc);
   if ((rc = alloc(p, &p->d_E, rows * p->Lp * 16))) return bail(rc);
-  if ((rc = alloc(p, &p->d_part, (size_t)batch * p->nchunks * g.ncells * csize(precision)))) return bail(rc);
+  if ((rc = alloc(p, &p->d_part, (size_t)batch * p->maxslots * g.ncells * csize(precision)))) return bail(rc);
   if ((rc = alloc(p, (void**)&p->d_S, (size_t)batch * g.ncells * 16))) return bail(rc);
   if ((rc = alloc(p, &p->d_xin, rows * m * 8))) return bail(rc);
   if ((rc = alloc(p, &p->d_out, (size_t)batch * g.npoints * csize(precision)))) return bail(rc);
   cufftHandle h;
   if ((rc = get_fft(p, (int)rows, &h))) return bail(rc);
+  if ((rc = make_maps(p))) return bail(rc);
   for (auto& e : p->ev)
     if (cudaEventCreate(&e) != cudaSuccess) return bail(fail(HOS_ECUDA, "cudaEventCreate failed"));
   *out = p;
@@ -318,7 +409,7 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
 void hos_plan_destroy(hos_plan* p) {
   if (!p) return;
   for (auto& kv : p->ffts) cufftDestroy(kv.second);
-  void* bufs[] = {p->d_tasks, p->d_line_cmax, p->d_line_start, p->d_row_off, p->d_pair_k1, p->d_pair_k2,
+  void* bufs[] = {p->d_tasks, p->d_line_region0, p->d_region_task, p->d_line_cmax, p->d_line_start, p->d_row_off, p->d_pair_k1, p->d_pair_k2,
                   p->d_pair_base, p->d_line_of_ab, p->d_taper, p->d_seg, p->d_half, p->d_E, p->d_part,
                   p->d_S, p->d_xin, p->d_out};
   for (void* b : bufs)
@@ -473,28 +564,12 @@ int hos_partial_raw(hos_plan* p, const void* x_dev, int x_dtype, int seg_begin, 
   if ((rc = run_fft(p, nseg, seg, half, st))) return rc;
   CUDA_TRY(hos::launch_extend_half(half, p->m, p->hstride, nseg, nullptr, p->geo.f_lo, p->L, p->Lp, p->precision, E,
                                    st));
-  hos::TripleArgs ta{};
-  ta.E = p->d_E;
-  ta.Lp = p->Lp;
-  ta.f_lo = p->geo.f_lo;
-  ta.K = p->k;
-  ta.seg_begin = seg_begin;
-  ta.seg_end = seg_end;
-  int nc = p->nchunks;
-  if (nc > nseg) nc = nseg;
-  ta.nchunks = nc;
-  ta.tasks = p->d_tasks;
-  ta.ntasks = (int)p->geo.tasks.size();
-  ta.line_cmax = p->d_line_cmax;
-  ta.line_start = p->d_line_start;
-  ta.lo = p->geo.win.lo;
-  ta.part = p->d_part;
-  ta.ncells = p->geo.ncells;
-  ta.order = p->order;
-  ta.conj = p->conj;
-  ta.batch = 1;
+  int n = nctas_for(p, nseg, 1);
+  while (n > 1 && slots_needed(p, nseg, n) > p->maxslots) n--;
+  const hos::TripleArgs ta = triple_args(p, seg_begin, seg_end, n, 1);
   CUDA_TRY(hos::launch_triple(ta, p->precision, st));
-  CUDA_TRY(hos::launch_reduce_parts(p->d_part, nc, p->geo.ncells, p->geo.ncells, p->precision, raw_dev, st));
+  CUDA_TRY(hos::launch_reduce_parts(p->d_part, p->geo.ncells, slot_info(p, nseg, n), p->d_line_start, p->geo.nlines,
+                                    p->geo.win.lo, p->precision, raw_dev, st));
   return HOS_OK;
 }
 
@@ -516,7 +591,8 @@ int hos_smooth_raw(hos_plan* p, const void* raw_dev, int64_t line_begin, int row
   const int64_t cell0 = g.line_start[line_begin];
   const char* raw_lb = (const char*)raw_dev + (size_t)(g.line_start[lb] - cell0) * csize(p->precision);
   double* S = p->d_S;  // scratch: cells of lines [lb, le)
-  CUDA_TRY(hos::launch_line_scan(raw_lb, 1, 0, p->precision, p->d_line_start, lb, le - lb, 0, 1, S, st));
+  hos::SlotInfo plain{};
+  CUDA_TRY(hos::launch_line_scan(raw_lb, 1, 0, plain, p->precision, p->d_line_start, lb, le - lb, 0, 1, S, st));
   hos::BoxArgs b{};
   b.S = S;
   b.s_series_stride = 0;
@@ -535,6 +611,11 @@ int hos_smooth_raw(hos_plan* p, const void* raw_dev, int64_t line_begin, int row
   b.hi = g.win.hi;
   b.m3 = p->m3;
   b.order = p->order;
+  b.m = p->m;
+  b.row_begin = row_begin;
+  b.row_end = row_end;
+  b.pair_begin = p->order == 4 ? g.row_pair0[row_begin] : 0;
+  b.pair_end = p->order == 4 ? g.row_pair0[row_end] : 0;
   b.p_begin = g.row_off[row_begin];
   b.p_end = g.row_off[row_end];
   b.scale = 1.0 / ((double)p->m * (double)p->k * std::pow((double)p->m3, p->order - 1));
@@ -613,6 +694,15 @@ int hos_peak_fp32(double* tflops, double* sm_mhz, void* stream) {
   cudaFree(clk);
   return HOS_OK;
 }
+
+int hos_plan_set_trace(hos_plan* p, void* trace_dev) {
+  int rc = check_plan(p);
+  if (rc) return rc;
+  p->trace = (unsigned long long*)trace_dev;
+  return HOS_OK;
+}
+
+int hos_plan_nctas(const hos_plan* p) { return p ? p->nctas : -1; }
 
 int hos_plan_set_timing(hos_plan* p, int enable) {
   int rc = check_plan(p);

@@ -54,23 +54,49 @@ void domain_rows(int order, int m, int64_t start, int64_t stop, int32_t* out) {
   }
 }
 
-static void add_band_tasks(std::vector<Task>& tasks, int64_t& issued, int line0, int nrows,
-                           int row_freq0, int plane_freq, int lo, int cmax_band) {
+namespace {
+struct RegionRec {
+  int line0, nrows, row_freq0, plane_freq, col0;
+};
+
+void add_band_regions(std::vector<RegionRec>& regs, std::vector<int32_t>& line_region0, int line0, int nrows,
+                      int row_freq0, int plane_freq, int lo, int cmax_band) {
   const int ncols = cmax_band - lo + 1;
-  const int nw = (ncols + kWarpCols - 1) / kWarpCols;
-  for (int w0 = 0; w0 < nw; w0 += kWarpsPerTask) {
+  const int nr = (ncols + kRegionCols - 1) / kRegionCols;
+  for (int l = line0; l < line0 + nrows; l++) line_region0[l] = (int32_t)regs.size();
+  for (int r = 0; r < nr; r++) regs.push_back({line0, nrows, row_freq0, plane_freq, lo + r * kRegionCols});
+}
+
+// group regions 4 at a time, at most 2 bands per task
+void group_tasks(const std::vector<RegionRec>& regs, std::vector<Task>& tasks, std::vector<int32_t>& region_task,
+                 int64_t& issued) {
+  region_task.assign(regs.size(), 0);
+  size_t i = 0;
+  while (i < regs.size()) {
     Task t{};
-    t.line0 = line0;
-    t.nrows = nrows;
-    t.row_freq0 = row_freq0;
-    t.plane_freq = plane_freq;
-    t.col0 = lo + w0 * kWarpCols;
-    t.nwarps = std::min(kWarpsPerTask, nw - w0);
-    t.warp_mask = (1 << t.nwarps) - 1;
+    while (i < regs.size() && t.nreg < kTaskRegions) {
+      const RegionRec& r = regs[i];
+      const bool same = t.nsub > 0 && t.sub[t.nsub - 1].line0 == r.line0 && t.sub[t.nsub - 1].k < kSubRegions;
+      if (!same) {
+        if (t.nsub == 2) break;
+        SubBand& sb = t.sub[t.nsub++];
+        sb.line0 = r.line0;
+        sb.nrows = r.nrows;
+        sb.row_freq0 = r.row_freq0;
+        sb.plane_freq = r.plane_freq;
+        sb.col0 = r.col0;
+        sb.k = 0;
+      }
+      t.sub[t.nsub - 1].k++;
+      region_task[i] = (int32_t)tasks.size();
+      t.nreg++;
+      i++;
+    }
     tasks.push_back(t);
-    issued += int64_t(t.nwarps) * kBandRows * kWarpCols;
+    issued += int64_t(kTaskRegions) * kBandRows * kRegionCols;
   }
 }
+}  // namespace
 
 std::string Geometry::build(int order_, int m_, int m3_) {
   order = order_;
@@ -126,7 +152,10 @@ std::string Geometry::build(int order_, int m_, int m3_) {
 
   line_a.clear(); line_b.clear(); line_cmax.clear(); line_start.clear();
   tasks.clear();
+  line_region0.clear();
+  region_task.clear();
   issued_cells = 0;
+  std::vector<RegionRec> regs;
   if (order == 3) {
     nlines = n3lines;
     line_start.push_back(0);
@@ -137,11 +166,12 @@ std::string Geometry::build(int order_, int m_, int m3_) {
       line_start.push_back(line_start.back() + (cmax3[l] - lo + 1));
     }
     ncells = line_start.back();
+    line_region0.assign(n3lines, 0);
     for (int l0 = 0; l0 < n3lines; l0 += kBandRows) {
       const int nr = std::min(kBandRows, n3lines - l0);
       int cb = lo;
       for (int l = l0; l < l0 + nr; l++) cb = std::max(cb, (int)cmax3[l]);
-      add_band_tasks(tasks, issued_cells, l0, nr, lo + l0, 0, lo, cb);
+      add_band_regions(regs, line_region0, l0, nr, lo + l0, 0, lo, cb);
     }
   } else {
     // lines = raw pairs (a,b) of the order-3 dilation; cols c in [lo, cmax4(a,b)]
@@ -169,28 +199,34 @@ std::string Geometry::build(int order_, int m_, int m3_) {
         line_start.push_back(line_start.back() + (best + hi - lo + 1));
       }
       const int nl = (int)line_a.size() - first_line;
+      line_region0.resize(line_a.size(), 0);
       for (int l0 = 0; l0 < nl; l0 += kBandRows) {
         const int nr = std::min(kBandRows, nl - l0);
         int cb = lo;
         for (int l = first_line + l0; l < first_line + l0 + nr; l++) cb = std::max(cb, (int)line_cmax[l]);
-        add_band_tasks(tasks, issued_cells, first_line + l0, nr, line_b[first_line + l0], a, lo, cb);
+        add_band_regions(regs, line_region0, first_line + l0, nr, line_b[first_line + l0], a, lo, cb);
       }
     }
     nlines = (int64_t)line_a.size();
     ncells = line_start.back();
   }
 
-  // ---- frequencies touched by the task list (extended spectrum range)
+  group_tasks(regs, tasks, region_task, issued_cells);
+
+  // ---- frequencies touched by the TMA boxes of the tasks (extended spectrum range)
   f_lo = order == 3 ? 2 * lo : 3 * lo;
   f_hi = 0;
-  for (const Task& tk : tasks) {
-    const int rmax = tk.row_freq0 + kBandRows - 1;
-    const int cmax = tk.col0 + tk.nwarps * kWarpCols - 1;
-    f_hi = std::max(f_hi, tk.plane_freq + rmax + cmax);
-    f_hi = std::max(f_hi, rmax);
-    f_hi = std::max(f_hi, cmax);
-    f_hi = std::max(f_hi, tk.plane_freq);
-    f_lo = std::min(f_lo, tk.plane_freq + tk.row_freq0 + tk.col0);
+  for (const Task& t : tasks) {
+    for (int s = 0; s < t.nsub; s++) {
+      const SubBand& b = t.sub[s];
+      const int rmax = b.row_freq0 + kBandRows - 1;
+      const int cmax = b.col0 + b.k * kRegionCols - 1;
+      f_hi = std::max(f_hi, b.plane_freq + rmax + cmax);
+      f_hi = std::max(f_hi, rmax);
+      f_hi = std::max(f_hi, cmax);
+      f_hi = std::max(f_hi, b.plane_freq);
+      f_lo = std::min(f_lo, b.plane_freq + b.row_freq0 + b.col0);
+    }
   }
   return "";
 }

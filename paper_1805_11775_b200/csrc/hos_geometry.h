@@ -7,6 +7,12 @@
 #include <string>
 #include <vector>
 
+#ifdef __CUDACC__
+#define HOS_HD __host__ __device__
+#else
+#define HOS_HD
+#endif
+
 namespace hos {
 
 // Window offsets per axis: [lo, hi] = [-m3/2, m3-1-m3/2]
@@ -18,14 +24,14 @@ struct Window {
 
 // Output rows of the order-3 domain: k1 in [0, (m-1)/2], row length
 // min(k1, (m-2k1-1)/2)+1 (hospectra/spectra.py:146-147).
-inline int p3_rows(int m) { return (m - 1) / 2 + 1; }
-inline int p3_len(int m, int k1) {
+HOS_HD inline int p3_rows(int m) { return (m - 1) / 2 + 1; }
+HOS_HD inline int p3_len(int m, int k1) {
   int a = k1, b = (m - 2 * k1 - 1);
   b = b >= 0 ? b / 2 : -((-b + 1) / 2);  // floor division like Python
   return (a < b ? a : b) + 1;
 }
 // Order-4 k3 count for pair (k1,k2) (hospectra/spectra.py:155-158).
-inline int p4_len(int m, int k1, int k2) {
+HOS_HD inline int p4_len(int m, int k1, int k2) {
   int b = m - 2 * k1 - 2 * k2 - 1;
   b = b >= 0 ? b / 2 : -((-b + 1) / 2);
   return (k2 < b ? k2 : b) + 1;
@@ -35,21 +41,33 @@ int64_t domain_size(int order, int m);
 // rows [start, stop) of the lexicographic domain into out ((stop-start) x (order-1))
 void domain_rows(int order, int m, int64_t start, int64_t stop, int32_t* out);
 
-// One K2 work item: a band of up to kBandRows consecutive lines of one plane
-// and up to kWarpsPerTask warp columns of kWarpCols cells each.
-constexpr int kBandRows = 32;     // lines per band (4 lane rows x 8 rows)
-constexpr int kWarpCols = 64;     // cells per warp along the line (8 lanes x 8)
-constexpr int kWarpsPerTask = 4;  // warps per CTA
+// K2 work decomposition.  D_h is cut into regions of up to kBandRows
+// consecutive lines (a "band" of one plane) x kRegionCols columns; the
+// regions, listed band after band, are grouped 4 at a time into tasks (one
+// warp per region).  A task has up to two "sub-bands" A and B of at most 3
+// consecutive regions of one band each (possibly two different bands); a
+// third sub-band closes the task early.  A CTA stages each sub-band's row,
+// column and last factors once per segment and its 4 warps share them.
+constexpr int kBandRows = 32;    // lines per band (4 lane rows x 8 rows)
+constexpr int kRegionCols = 32;  // columns per region (8 lanes x 4)
+constexpr int kTaskRegions = 4;  // regions (warps) per task
+constexpr int kSubRegions = 3;   // regions per sub-band: its G box (31 + 32k quads) must fit one
+                                 // 256 x 8-byte TMA box row
 
-struct Task {
+struct SubBand {
   int32_t line0;      // first line of the band
   int32_t nrows;      // lines in the band (<= kBandRows)
   int32_t row_freq0;  // frequency of line0's row factor (order 3: a, order 4: b)
   int32_t plane_freq; // order 4: a of the plane; order 3: 0
-  int32_t col0;       // first column (logical frequency) of warp 0
-  int32_t nwarps;     // active warp columns (<= kWarpsPerTask)
-  int32_t warp_mask;  // bit w set if warp w has at least one cell of D_h
-  int32_t pad;
+  int32_t col0;       // first column of the task's first region in this band
+  int32_t k;          // regions of the task in this band
+};
+
+struct Task {
+  int32_t nreg;       // regions (warps with work), 1..kTaskRegions
+  int32_t nsub;       // sub-bands, 1..2
+  SubBand sub[2];
+  int32_t pad[2];
 };
 
 struct Geometry {
@@ -74,9 +92,11 @@ struct Geometry {
   // order 3: line index = a - lo; lines of output row k1 start at k1
   // frequencies touched by any task (inclusive), for the extended spectrum
   int f_lo = 0, f_hi = 0;
-  // K2 task list
+  // K2 tasks
   std::vector<Task> tasks;
-  int64_t issued_cells = 0;  // cells computed by the task list (incl. padding)
+  std::vector<int32_t> line_region0;  // per line: index of the region holding its first column
+  std::vector<int32_t> region_task;   // per region: its task
+  int64_t issued_cells = 0;           // cells computed by the tasks (incl. idle warps)
 
   std::string build(int order, int m, int m3);  // returns "" or an error message
 };

@@ -90,6 +90,7 @@ __device__ __forceinline__ C half_lookup(const C* __restrict__ H, int m, int f) 
 
 __global__ void k_extend_half_f32(const float2* __restrict__ H, int m, int hstride, int64_t n, int f_lo, int L,
                                   int Lp, float4* __restrict__ E) {
+  asm volatile("griddepcontrol.launch_dependents;");  // let K2 stage its setup (it waits for our writes)
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = t / L;
     const int j = (int)(t - r * L);
@@ -99,6 +100,7 @@ __global__ void k_extend_half_f32(const float2* __restrict__ H, int m, int hstri
 }
 __global__ void k_extend_half_f64(const double2* __restrict__ H, int m, int hstride, int64_t n, int f_lo, int L,
                                   int Lp, double2* __restrict__ E) {
+  asm volatile("griddepcontrol.launch_dependents;");
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = t / L;
     const int j = (int)(t - r * L);
@@ -119,6 +121,7 @@ cudaError_t launch_extend_half(const void* H, int m, int hstride, int rows, cons
 // From caller-supplied full spectra (estimate_from_spectra): no symmetry assumed.
 template <typename Cin, bool QUAD>
 __global__ void k_extend_full(const Cin* __restrict__ S, int m, int64_t n, int f_lo, int L, int Lp, void* E) {
+  asm volatile("griddepcontrol.launch_dependents;");
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = t / L;
     const int j = (int)(t - r * L);
@@ -168,274 +171,446 @@ cudaError_t launch_expand_full(const void* H, int m, int hstride, int rows, int 
 // ===========================================================================
 // K2: triple / quadruple product over D_h.
 //
-// CTA = one Task: a band of 32 lines x nwarps*64 columns.  Per segment the
-// CTA stages, with cp.async, the row factors (32), the column factors
-// (nwarps*64), the last factors G(row+col[+a]) (32+nwarps*64-1) and, for
-// order 4, the plane factor F(a): 576 16-byte elements per segment slot.
-// fp32: each lane owns an 8x8 cell micro-tile (lanes 4 x 8 -> warp 32x64)
-// and spends 4 FFMA2-class instructions per cell:
+// Work = ntasks x nseg units (a task = 4 regions of 32 x 32 cells, one per
+// warp); the grid's N CTAs (per series) split it into N contiguous, equal
+// ranges, so every CTA does the same work in one wave (N = SMs x occupancy).
+// A CTA walks the tasks its range touches; for each piece (task, segments)
+// every warp accumulates its region in registers and writes ONE partial
+// slot (CTA index - first CTA of the task), fixed by the partition: the fp64
+// combination order in K4a is fixed and results are deterministic.
+//
+// Staging: a 3-slot ring per CTA; a slot holds kSegsPerSlot = 4 segments of
+// each sub-band's row factors (32), column factors (32k), last factors
+// G(row+col[+a]) (31+32k) and, for order 4, F(a) -- one 3-D tensor TMA copy
+// (cp.async.bulk.tensor + mbarrier complete_tx) per operand and sub-band.
+// The last warp to finish a slot refills it: no CTA-wide barrier in the loop.
+//
+// Lane (ta, tb) of a warp owns rows ta+4i (i<8) and columns tb+8j (j<4) of
+// its region: every quarter-warp shared load reads consecutive 16-byte
+// elements (conflict-free) and a lane needs 8 row + 4 column + 14 G values
+// per segment (cell (i,j) reads G at 4(i+2j)).
+// fp32: 4 FFMA2-class instructions per cell,
 //   p    = fa.re * fb + fa.im * (i fb)            (FMUL2 + FFMA2)
 //   acc += p.re * conj(g) + p.im * (i conj(g))    (2 FFMA2; conj toggled)
 // with every operand form a swizzle of the quad (re, im, -im, re).
-// fp64: lanes own 4x8 micro-tiles (8 warps), scalar DFMA.
-// Segment sums run in the compute precision over one chunk; chunks are
-// combined in fp64 by K4a in a fixed order (deterministic, no atomics).
+// fp64: same mapping, scalar DFMA on double2 spectra.
 
-constexpr int kSlotSegs = 2;
-constexpr int kSlots = 3;
-constexpr int kSegElems = 576;  // 32 rows + 256 cols + 287 g + 1 plane
-constexpr int kOffCol = 32, kOffG = 288, kOffPlane = 575;
-constexpr size_t kTripleSmem = sizeof(float4) * kSlots * kSlotSegs * kSegElems;
+#ifndef HOS_K2_SLOTS
+#define HOS_K2_SLOTS 3
+#endif
+#ifndef HOS_K2_MINB
+#define HOS_K2_MINB 3
+#endif
+constexpr int kSlots = HOS_K2_SLOTS;
+// per slot (quads): rows 2 x 128 | cols 4 x 128 | planes 2 x 8 | G 4(31+32k_A) (padded) + 4(31+32k_B)
+constexpr int kSlotQuads = 2 * 128 + 4 * 128 + 2 * 8 + 4 * (62 + 32 * 4) + 8;
+static_assert(kSlotQuads % 8 == 0, "ring slots must stay 128-byte aligned for TMA");
+constexpr size_t kTripleSmem = 16 * (size_t)kSlots * kSlotQuads + 128;
 
-template <typename Q>
-__device__ __forceinline__ void stage_segment(const Q* __restrict__ row, Q* dst, int ncol, int ng, int rbase,
-                                              int cbase, int gbase, int pbase, bool order4, int nthreads) {
-  const int nfirst = 32 + ncol;
-  const int ntot = nfirst + ng + (order4 ? 1 : 0);
-  for (int t = threadIdx.x; t < ntot; t += nthreads) {
-    int src, d;
-    if (t < 32) { src = rbase + t; d = t; }
-    else if (t < nfirst) { src = cbase + (t - 32); d = t; }
-    else if (t < nfirst + ng) { src = gbase + (t - nfirst); d = kOffG + (t - nfirst); }
-    else { src = pbase; d = kOffPlane; }
-    cp_async16(dst + d, row + src);
-  }
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 2-D tensor copy of box {x: 2*width 8-byte elements, y: kSegsPerSlot rows} at (x0 = 2*elem, y0 = row)
+__device__ __forceinline__ void tma_2d(unsigned dst, const CUtensorMap* map, int elem, int row, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(2 * elem), "r"(row), "r"(smem_u32(bar))
+      : "memory");
 }
 
-template <bool CONJ, bool ORDER4>
-__global__ void __launch_bounds__(128, 2) k_triple_f32(TripleArgs a) {
-  extern __shared__ float4 smq[];
-  const int task_id = blockIdx.x / a.nchunks;
-  const int chunk = blockIdx.x - task_id * a.nchunks;
-  const int series = blockIdx.y;
-  const Task tk = a.tasks[task_id];
-  const int nseg = a.seg_end - a.seg_begin;
-  const int s0 = a.seg_begin + (int)((int64_t)nseg * chunk / a.nchunks);
-  const int s1 = a.seg_begin + (int)((int64_t)nseg * (chunk + 1) / a.nchunks);
-  const float4* E = (const float4*)a.E + (int64_t)series * a.K * a.Lp;
-  const int ncol = tk.nwarps * 64;
-  const int ng = 32 + ncol - 1;
-  const int rbase = tk.row_freq0 - a.f_lo;
-  const int cbase = tk.col0 - a.f_lo;
-  const int gbase = tk.plane_freq + tk.row_freq0 + tk.col0 - a.f_lo;
-  const int pbase = tk.plane_freq - a.f_lo;
+// CTA owning work unit u of a W-unit range split into N equal parts.
+__device__ __forceinline__ int64_t cta_of_unit(int64_t u, int64_t W, int N) { return ((u + 1) * (int64_t)N - 1) / W; }
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ta = lane >> 3, tb = lane & 7;
-  const int r0 = ta * 8;
-  const int cw = warp * 64 + tb * 8;  // column offset of the micro-tile within the task
-  const int c0 = tk.col0 + cw;
-  bool active = false;
-  if (warp < tk.nwarps) {
+// partial slots of task t for a launch over nseg segments split across N CTAs
+__device__ __forceinline__ int task_slots(int t, int nseg, int64_t W, int N) {
+  return (int)(cta_of_unit((int64_t)(t + 1) * nseg - 1, W, N) - cta_of_unit((int64_t)t * nseg, W, N) + 1);
+}
+
+// shared-memory layout (quad offsets) of sub-band s of a staged task slot:
+// rows 2 x 128 | cols 128 (k_A + k_B) | planes 2 x 8 | G_A 4(31+32k_A) padded | G_B
+struct SubLayout {
+  int rows, cols, g, plane;
+  int cw;  // column elements per segment (32k)
+  int gw;  // G elements per segment (31 + 32k)
+};
+
+__device__ __forceinline__ SubLayout sub_layout(const Task& t, int s) {
+  const int kA = t.sub[0].k, kB = t.nsub > 1 ? t.sub[1].k : 0;
+  const int plane0 = 128 * t.nsub + 128 * (kA + kB);
+  const int g0 = plane0 + 8 * t.nsub;
+  SubLayout L;
+  L.rows = s ? 128 : 0;
+  L.cols = 128 * t.nsub + (s ? 128 * kA : 0);
+  L.plane = plane0 + (s ? 8 : 0);
+  L.g = s ? g0 + ((4 * (31 + 32 * kA) + 7) & ~7) : g0;
+  const int k = s ? kB : kA;
+  L.cw = 32 * k;
+  L.gw = 31 + 32 * k;
+  return L;
+}
+
+template <typename T>
+struct Cplx;
+template <>
+struct Cplx<float> {
+  using Q = float4;   // staged element (quad)
+  using C = float2;   // accumulator / partial
+};
+template <>
+struct Cplx<double> {
+  using Q = double2;
+  using C = double2;
+};
+
+// one segment of a lane's 8x4 micro-tile: rows/cols/g point at the segment's staged factors
+template <bool CONJ, bool ORDER4>
+__device__ __forceinline__ void cells_f32(const float4* __restrict__ rows, const float4* __restrict__ cols,
+                                          const float4* __restrict__ gs, const float4* __restrict__ plane, int ta,
+                                          int tb, float2 (&acc)[8][4]) {
+  float2 fa[8];
+  float4 fb[4];
+#pragma unroll
+  for (int i = 0; i < 8; i++) fa[i] = *reinterpret_cast<const float2*>(rows + ta + 4 * i);
+  if (ORDER4) {
+    const float4 pa = *plane;
 #pragma unroll
     for (int i = 0; i < 8; i++) {
-      const int r = r0 + i;
-      if (r < tk.nrows && __ldg(a.line_cmax + tk.line0 + r) >= c0) active = true;
+      float2 t = fmul2(make_float2(fa[i].x, fa[i].x), make_float2(pa.x, pa.y));
+      fa[i] = ffma2(make_float2(fa[i].y, fa[i].y), make_float2(pa.z, pa.w), t);
     }
   }
-
-  float2 acc[8][8];
 #pragma unroll
-  for (int i = 0; i < 8; i++)
+  for (int j = 0; j < 4; j++) fb[j] = cols[tb + 8 * j];
+  const float4* gq = gs + ta + tb;
 #pragma unroll
-    for (int j = 0; j < 8; j++) acc[i][j] = make_float2(0.f, 0.f);
-
-  const int nslots = (s1 - s0 + kSlotSegs - 1) / kSlotSegs;
-  auto load_slot = [&](int sl) {
-    float4* buf = smq + (sl % kSlots) * (kSlotSegs * kSegElems);
+  for (int q = 0; q < 14; q++) {
+    const float4 g = gq[4 * q];
 #pragma unroll
-    for (int q = 0; q < kSlotSegs; q++) {
-      const int seg = s0 + sl * kSlotSegs + q;
-      if (seg < s1)
-        stage_segment<float4>(E + (int64_t)seg * a.Lp, buf + q * kSegElems, ncol, ng, rbase, cbase, gbase, pbase,
-                              ORDER4, 128);
-    }
-  };
-#pragma unroll
-  for (int sl = 0; sl < kSlots - 1; sl++) {
-    if (sl < nslots) load_slot(sl);
-    cp_async_commit();
-  }
-  for (int sl = 0; sl < nslots; sl++) {
-    if (sl + kSlots - 1 < nslots) load_slot(sl + kSlots - 1);
-    cp_async_commit();
-    cp_async_wait<kSlots - 1>();
-    __syncthreads();
-    if (active) {
-      const float4* buf = smq + (sl % kSlots) * (kSlotSegs * kSegElems);
-      const int nq = min(kSlotSegs, s1 - (s0 + sl * kSlotSegs));
-      for (int q = 0; q < nq; q++) {
-        const float4* sq = buf + q * kSegElems;
-        float2 fa[8];
-        float4 fb[8];
-#pragma unroll
-        for (int i = 0; i < 8; i++) {
-          const float4 v = sq[r0 + i];
-          fa[i] = make_float2(v.x, v.y);
-        }
-        if (ORDER4) {
-          const float4 pa = sq[kOffPlane];
-#pragma unroll
-          for (int i = 0; i < 8; i++) {
-            float2 t = fmul2(make_float2(fa[i].x, fa[i].x), make_float2(pa.x, pa.y));
-            fa[i] = ffma2(make_float2(fa[i].y, fa[i].y), make_float2(pa.z, pa.w), t);
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < 8; j++) fb[j] = sq[kOffCol + cw + j];
-        const float4* gq = sq + kOffG + r0 + cw;
-#pragma unroll
-        for (int d = 0; d < 15; d++) {
-          const float4 g = gq[d];
-#pragma unroll
-          for (int i = 0; i < 8; i++) {
-            const int j = d - i;
-            if (j < 0 || j > 7) continue;
-            float2 p = fmul2(make_float2(fa[i].x, fa[i].x), make_float2(fb[j].x, fb[j].y));
-            p = ffma2(make_float2(fa[i].y, fa[i].y), make_float2(fb[j].z, fb[j].w), p);
-            if (CONJ) {
-              acc[i][j] = ffma2(make_float2(p.x, p.x), make_float2(g.w, g.z), acc[i][j]);
-              acc[i][j] = ffma2(make_float2(p.y, p.y), make_float2(g.y, g.x), acc[i][j]);
-            } else {
-              acc[i][j] = ffma2(make_float2(p.x, p.x), make_float2(g.x, g.y), acc[i][j]);
-              acc[i][j] = ffma2(make_float2(p.y, p.y), make_float2(g.z, g.w), acc[i][j]);
-            }
-          }
-        }
+    for (int j = 0; j < 4; j++) {
+      const int i = q - 2 * j;
+      if (i < 0 || i > 7) continue;
+      float2 p = fmul2(make_float2(fa[i].x, fa[i].x), make_float2(fb[j].x, fb[j].y));
+      p = ffma2(make_float2(fa[i].y, fa[i].y), make_float2(fb[j].z, fb[j].w), p);
+      if (CONJ) {
+        acc[i][j] = ffma2(make_float2(p.x, p.x), make_float2(g.w, g.z), acc[i][j]);
+        acc[i][j] = ffma2(make_float2(p.y, p.y), make_float2(g.y, g.x), acc[i][j]);
+      } else {
+        acc[i][j] = ffma2(make_float2(p.x, p.x), make_float2(g.x, g.y), acc[i][j]);
+        acc[i][j] = ffma2(make_float2(p.y, p.y), make_float2(g.z, g.w), acc[i][j]);
       }
     }
-    __syncthreads();
-  }
-  cp_async_wait<0>();
-  if (!active) return;
-  float2* P = (float2*)a.part + ((int64_t)series * a.nchunks + chunk) * a.ncells;
-#pragma unroll
-  for (int i = 0; i < 8; i++) {
-    const int r = r0 + i;
-    if (r >= tk.nrows) continue;
-    const int line = tk.line0 + r;
-    const int cm = __ldg(a.line_cmax + line);
-    float2* dst = P + (__ldg(a.line_start + line) - a.lo);
-#pragma unroll
-    for (int j = 0; j < 8; j++)
-      if (c0 + j <= cm) dst[c0 + j] = acc[i][j];
   }
 }
 
 template <bool CONJ, bool ORDER4>
-__global__ void __launch_bounds__(256, 1) k_triple_f64(TripleArgs a) {
-  extern __shared__ double2 smd[];
-  const int task_id = blockIdx.x / a.nchunks;
-  const int chunk = blockIdx.x - task_id * a.nchunks;
+__device__ __forceinline__ void cells_f64(const double2* __restrict__ rows, const double2* __restrict__ cols,
+                                          const double2* __restrict__ gs, const double2* __restrict__ plane, int ta,
+                                          int tb, double2 (&acc)[8][4]) {
+  double2 fa[8], fb[4];
+#pragma unroll
+  for (int i = 0; i < 8; i++) fa[i] = rows[ta + 4 * i];
+  if (ORDER4) {
+    const double2 pa = *plane;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+      const double re = fa[i].x * pa.x - fa[i].y * pa.y;
+      const double im = fa[i].x * pa.y + fa[i].y * pa.x;
+      fa[i] = make_double2(re, im);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; j++) fb[j] = cols[tb + 8 * j];
+  const double2* gq = gs + ta + tb;
+#pragma unroll
+  for (int q = 0; q < 14; q++) {
+    const double2 g = gq[4 * q];
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const int i = q - 2 * j;
+      if (i < 0 || i > 7) continue;
+      const double pr = fma(-fa[i].y, fb[j].y, fa[i].x * fb[j].x);
+      const double pi = fma(fa[i].y, fb[j].x, fa[i].x * fb[j].y);
+      if (CONJ) {
+        acc[i][j].x = fma(pr, g.x, fma(pi, g.y, acc[i][j].x));
+        acc[i][j].y = fma(pi, g.x, fma(-pr, g.y, acc[i][j].y));
+      } else {
+        acc[i][j].x = fma(pr, g.x, fma(-pi, g.y, acc[i][j].x));
+        acc[i][j].y = fma(pr, g.y, fma(pi, g.x, acc[i][j].y));
+      }
+    }
+  }
+}
+
+constexpr int kMaxPieces = 8;
+
+struct PieceRec {
+  int task;      // task index
+  int first;     // first absolute segment
+  int nseg;      // segments
+  int slot0;     // first ring slot of the piece (counted across rounds)
+  int nsl;       // ring slots of the piece
+  int pslot;     // partial slot: CTA - first CTA of the task
+};
+
+template <typename T, bool CONJ, bool ORDER4>
+__global__ void __launch_bounds__(128, sizeof(T) == 4 ? HOS_K2_MINB : 2) k_triple(const __grid_constant__ TripleArgs a) {
+  using Q = typename Cplx<T>::Q;
+  using C = typename Cplx<T>::C;
+  extern __shared__ unsigned char smraw[];
+  __shared__ __align__(8) uint64_t full[kSlots];
+  __shared__ int cnt[kSlots];
+  __shared__ PieceRec pcs[kMaxPieces];
+  __shared__ Task tcache[kMaxPieces];
+  __shared__ int s_np, s_end, s_tnext;
+  const unsigned raw0 = smem_u32(smraw);
+  const unsigned base = (raw0 + 127u) & ~127u;
+  const Q* ring = reinterpret_cast<const Q*>(smraw + (base - raw0));
+  const int c = blockIdx.x;
   const int series = blockIdx.y;
-  const Task tk = a.tasks[task_id];
-  const int nseg = a.seg_end - a.seg_begin;
-  const int s0 = a.seg_begin + (int)((int64_t)nseg * chunk / a.nchunks);
-  const int s1 = a.seg_begin + (int)((int64_t)nseg * (chunk + 1) / a.nchunks);
-  const double2* E = (const double2*)a.E + (int64_t)series * a.K * a.Lp;
-  const int ncol = tk.nwarps * 64;
-  const int ng = 32 + ncol - 1;
-  const int rbase = tk.row_freq0 - a.f_lo;
-  const int cbase = tk.col0 - a.f_lo;
-  const int gbase = tk.plane_freq + tk.row_freq0 + tk.col0 - a.f_lo;
-  const int pbase = tk.plane_freq - a.f_lo;
-
+  const int N = a.nctas;
+  const int nseg_all = a.seg_end - a.seg_begin;
+  const int64_t W = (int64_t)a.ntasks * nseg_all;
+  const int64_t x0 = (int64_t)c * W / N, x1 = (int64_t)(c + 1) * W / N;
+  C* Pbase = (C*)a.part + (int64_t)series * a.maxslots * a.ncells;
+  const int row0 = series * a.K;  // tensor row of segment 0 of this series
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wcol = warp & 3, wrow = warp >> 2;
   const int ta = lane >> 3, tb = lane & 7;
-  const int r0 = wrow * 16 + ta * 4;
-  const int cw = wcol * 64 + tb * 8;
-  const int c0 = tk.col0 + cw;
-  bool active = false;
-  if (wcol < tk.nwarps) {
-#pragma unroll
-    for (int i = 0; i < 4; i++) {
-      const int r = r0 + i;
-      if (r < tk.nrows && __ldg(a.line_cmax + tk.line0 + r) >= c0) active = true;
-    }
+  unsigned long long* tr = a.trace ? a.trace + 8 * ((int64_t)series * N + c) : nullptr;
+  long long wait_cyc = 0, slots_seen = 0;
+  if (tr && threadIdx.x == 0) {
+    unsigned long long t0, sm;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    asm volatile("{ .reg .u32 r; mov.u32 r, %%smid; cvt.u64.u32 %0, r; }" : "=l"(sm));
+    tr[0] = t0;
+    tr[3] = sm;
   }
-  double2 acc[4][8];
-#pragma unroll
-  for (int i = 0; i < 4; i++)
-#pragma unroll
-    for (int j = 0; j < 8; j++) acc[i][j] = make_double2(0.0, 0.0);
 
-  const int nslots = (s1 - s0 + kSlotSegs - 1) / kSlotSegs;
-  auto load_slot = [&](int sl) {
-    double2* buf = smd + (sl % kSlots) * (kSlotSegs * kSegElems);
+  if (threadIdx.x == 0) {
 #pragma unroll
-    for (int q = 0; q < kSlotSegs; q++) {
-      const int seg = s0 + sl * kSlotSegs + q;
-      if (seg < s1)
-        stage_segment<double2>(E + (int64_t)seg * a.Lp, buf + q * kSegElems, ncol, ng, rbase, cbase, gbase, pbase,
-                               ORDER4, 256);
+    for (int b = 0; b < kSlots; b++) {
+      mbar_init(&full[b], 1);
+      cnt[b] = 0;
     }
-  };
-#pragma unroll
-  for (int sl = 0; sl < kSlots - 1; sl++) {
-    if (sl < nslots) load_slot(sl);
-    cp_async_commit();
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    s_tnext = (int)(x0 / nseg_all);
+    s_end = 0;
   }
-  for (int sl = 0; sl < nslots; sl++) {
-    if (sl + kSlots - 1 < nslots) load_slot(sl + kSlots - 1);
-    cp_async_commit();
-    cp_async_wait<kSlots - 1>();
+  if (warp == 1 && lane < 8) {  // pull the tensor-map descriptors in while the piece list is built
+    const CUtensorMap* m = lane == 0 ? &a.map_rows : lane == 1 ? &a.map_plane : lane < 5 ? &a.map_cols[lane - 2]
+                                                                                        : &a.map_g[lane - 5];
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
+  }
+  __syncthreads();
+
+  // rounds of up to kMaxPieces pieces (one round unless the range is tiny and spans many tasks)
+  while (true) {
+    if (threadIdx.x == 0) {
+      int np = 0, slots = s_end, t = s_tnext;
+      for (; t < a.ntasks && np < kMaxPieces && (int64_t)t * nseg_all < x1 && x0 < x1; t++) {
+        const int64_t P0 = (int64_t)t * nseg_all;
+        const int64_t u0 = min(max(x0 - P0, (int64_t)0), (int64_t)nseg_all);
+        const int64_t u1 = min(max(x1 - P0, (int64_t)0), (int64_t)nseg_all);
+        PieceRec r;
+        r.task = t;
+        r.first = a.seg_begin + (int)u0;
+        r.nseg = (int)(u1 - u0);
+        r.nsl = (r.nseg + kSegsPerSlot - 1) / kSegsPerSlot;
+        r.slot0 = slots;
+        r.pslot = (int)(c - cta_of_unit(P0, W, N));
+        slots += r.nsl;
+        pcs[np++] = r;
+      }
+      s_np = np;
+      s_end = slots;
+      s_tnext = t;
+    }
     __syncthreads();
-    if (active) {
-      const double2* buf = smd + (sl % kSlots) * (kSlotSegs * kSegElems);
-      const int nq = min(kSlotSegs, s1 - (s0 + sl * kSlotSegs));
-      for (int q = 0; q < nq; q++) {
-        const double2* sq = buf + q * kSegElems;
-        double2 fa[4], fb[8];
+    const int np = s_np, gend = s_end;
+    if (np == 0) break;
+    if (threadIdx.x < np * (int)(sizeof(Task) / 4)) {  // task records of this round -> smem
+      const int pi = threadIdx.x / (int)(sizeof(Task) / 4), wi = threadIdx.x % (int)(sizeof(Task) / 4);
+      reinterpret_cast<int*>(&tcache[pi])[wi] = __ldg(reinterpret_cast<const int*>(&a.tasks[pcs[pi].task]) + wi);
+    }
+    __syncthreads();
+    const int gbeg = pcs[0].slot0;
+
+    // lane 0 of the calling warp stages slot g into ring slot g % kSlots
+    auto produce = [&](int g) {
+      if (lane == 0) {
+        int p = 0;
+        while (p + 1 < np && pcs[p + 1].slot0 <= g) p++;
+        const PieceRec& r = pcs[p];
+        const Task& tk = tcache[p];
+        const int b = g % kSlots;
+        const unsigned sd = base + 16u * b * kSlotQuads;
+        const int srow = row0 + r.first + (g - r.slot0) * kSegsPerSlot;
+        const int nreg = tk.sub[0].k + (tk.nsub > 1 ? tk.sub[1].k : 0);
+        const unsigned bytes =
+            16u * kSegsPerSlot * (tk.nsub * (32 + 31 + (ORDER4 ? 1 : 0)) + 64 * nreg);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&full[b], bytes);
 #pragma unroll
-        for (int i = 0; i < 4; i++) fa[i] = sq[r0 + i];
-        if (ORDER4) {
-          const double2 pa = sq[kOffPlane];
+        for (int s = 0; s < 2; s++) {
+          if (s >= tk.nsub) break;
+          const SubBand& sb = tk.sub[s];
+          const SubLayout L = sub_layout(tk, s);
+          tma_2d(sd + 16u * L.rows, &a.map_rows, sb.row_freq0 - a.f_lo, srow, &full[b]);
+          tma_2d(sd + 16u * L.cols, &a.map_cols[sb.k - 1], sb.col0 - a.f_lo, srow, &full[b]);
+          tma_2d(sd + 16u * L.g, &a.map_g[sb.k - 1], sb.plane_freq + sb.row_freq0 + sb.col0 - a.f_lo, srow, &full[b]);
+          if (ORDER4) tma_2d(sd + 16u * L.plane, &a.map_plane, sb.plane_freq - a.f_lo, srow, &full[b]);
+        }
+      }
+      __syncwarp();
+    };
+    if (warp == 0) {
+      unsigned long long ta0 = 0, ta1 = 0, ta2 = 0;
+      if (tr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ta0));
+      if (gbeg == 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // E is written by the previous kernel
+      if (tr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ta1));
+      for (int g = gbeg; g < gbeg + kSlots && g < gend; g++) produce(g);
+      if (tr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ta2));
+      if (tr && lane == 0 && gbeg == 0) {
+        tr[7] = ta0;          // piece list ready
+        tr[6] = ta1;          // dependency resolved
+        tr[4] = ta2;          // prologue issued
+      }
+    }
+
+    // pieces with no segments still own partial slots: write zeros
+    for (int p = 0; p < np; p++) {
+      if (pcs[p].nseg != 0) continue;
+      const Task& tk = tcache[p];
+      if (warp >= tk.nreg) continue;
+      const int s = warp < tk.sub[0].k ? 0 : 1;
+      const SubBand& sb = tk.sub[s];
+      const int c0 = sb.col0 + 32 * (warp - (s ? tk.sub[0].k : 0)) + tb;
+      C* P = Pbase + (int64_t)pcs[p].pslot * a.ncells;
+      for (int i = 0; i < 8; i++) {
+        const int r = ta + 4 * i;
+        if (r >= sb.nrows) continue;
+        const int line = sb.line0 + r;
+        const int cm = __ldg(a.line_cmax + line);
+        C* dst = P + (__ldg(a.line_start + line) - a.lo);
+        for (int j = 0; j < 4; j++)
+          if (c0 + 8 * j <= cm) dst[c0 + 8 * j] = C{0, 0};
+      }
+    }
+
+    int p = -1;
+    int c0 = 0, line0 = 0, nrows = 0;
+    int o_rows = 0, o_cols = 0, o_g = 0, o_plane = 0, cw = 0, gw = 0;
+    bool active = false;
+    C acc[8][4];
+    for (int g = gbeg; g < gend; g++) {
+      if (p < 0 || g >= pcs[p].slot0 + pcs[p].nsl) {
+        p++;
+        while (pcs[p].nsl == 0) p++;
+        const Task& tk = tcache[p];
+        active = false;
+        if (warp < tk.nreg) {
+          const int sub = warp < tk.sub[0].k ? 0 : 1;
+          const int j = warp - (sub ? tk.sub[0].k : 0);
+          const SubBand& sb = tk.sub[sub];
+          const SubLayout L = sub_layout(tk, sub);
+          c0 = sb.col0 + 32 * j + tb;
+          line0 = sb.line0;
+          nrows = sb.nrows;
+          o_rows = L.rows;
+          o_cols = L.cols + 32 * j;
+          o_g = L.g + 32 * j;
+          o_plane = L.plane;
+          cw = L.cw;
+          gw = L.gw;
 #pragma unroll
-          for (int i = 0; i < 4; i++) {
-            const double re = fa[i].x * pa.x - fa[i].y * pa.y;
-            const double im = fa[i].x * pa.y + fa[i].y * pa.x;
-            fa[i] = make_double2(re, im);
+          for (int i = 0; i < 8; i++) {
+            const int r = ta + 4 * i;
+            if (r < nrows && __ldg(a.line_cmax + line0 + r) >= c0) active = true;
           }
         }
 #pragma unroll
-        for (int j = 0; j < 8; j++) fb[j] = sq[kOffCol + cw + j];
-        const double2* gq = sq + kOffG + r0 + cw;
+        for (int i = 0; i < 8; i++)
 #pragma unroll
-        for (int d = 0; d < 11; d++) {
-          const double2 g = gq[d];
+          for (int j = 0; j < 4; j++) acc[i][j] = C{0, 0};
+      }
+      const PieceRec& r = pcs[p];
+      const int b = g % kSlots;
+      long long tw0 = 0;
+      if (tr) tw0 = clock64();
+      mbar_wait(&full[b], (unsigned)((g / kSlots) & 1));
+      if (tr) {
+        wait_cyc += clock64() - tw0;
+        slots_seen++;
+      }
+      if (tr && g == 0 && threadIdx.x == 0) {
+        unsigned long long t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        tr[1] = t1;
+      }
+      if (active) {
+        const Q* sq = ring + b * kSlotQuads;
+        const int nq = min(kSegsPerSlot, r.nseg - (g - r.slot0) * kSegsPerSlot);
+        for (int q = 0; q < nq; q++) {
+          if constexpr (sizeof(T) == 4)
+            cells_f32<CONJ, ORDER4>(reinterpret_cast<const float4*>(sq + o_rows + q * 32),
+                                    reinterpret_cast<const float4*>(sq + o_cols + q * cw),
+                                    reinterpret_cast<const float4*>(sq + o_g + q * gw),
+                                    reinterpret_cast<const float4*>(sq + o_plane + q), ta, tb, acc);
+          else
+            cells_f64<CONJ, ORDER4>(reinterpret_cast<const double2*>(sq + o_rows + q * 32),
+                                    reinterpret_cast<const double2*>(sq + o_cols + q * cw),
+                                    reinterpret_cast<const double2*>(sq + o_g + q * gw),
+                                    reinterpret_cast<const double2*>(sq + o_plane + q), ta, tb, acc);
+        }
+      }
+      // the last warp out refills this ring slot with slot g + kSlots
+      __syncwarp();
+      int last = 0;
+      if (lane == 0) {
+        __threadfence_block();
+        last = atomicAdd(&cnt[b], 1) == 3;
+        if (last) cnt[b] = 0;
+      }
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (last && g + kSlots < gend) produce(g + kSlots);
+      if (g == r.slot0 + r.nsl - 1 && active) {
+        C* P = Pbase + (int64_t)r.pslot * a.ncells;
 #pragma unroll
-          for (int i = 0; i < 4; i++) {
-            const int j = d - i;
-            if (j < 0 || j > 7) continue;
-            const double pr = fma(-fa[i].y, fb[j].y, fa[i].x * fb[j].x);
-            const double pi = fma(fa[i].y, fb[j].x, fa[i].x * fb[j].y);
-            if (CONJ) {
-              acc[i][j].x = fma(pr, g.x, fma(pi, g.y, acc[i][j].x));
-              acc[i][j].y = fma(pi, g.x, fma(-pr, g.y, acc[i][j].y));
-            } else {
-              acc[i][j].x = fma(pr, g.x, fma(-pi, g.y, acc[i][j].x));
-              acc[i][j].y = fma(pr, g.y, fma(pi, g.x, acc[i][j].y));
-            }
-          }
+        for (int i = 0; i < 8; i++) {
+          const int rr = ta + 4 * i;
+          if (rr >= nrows) continue;
+          const int line = line0 + rr;
+          const int cm = __ldg(a.line_cmax + line);
+          C* dst = P + (__ldg(a.line_start + line) - a.lo);
+#pragma unroll
+          for (int j = 0; j < 4; j++)
+            if (c0 + 8 * j <= cm) dst[c0 + 8 * j] = acc[i][j];
         }
       }
     }
-    __syncthreads();
+    __syncthreads();  // ring idle before the next round re-primes it
   }
-  cp_async_wait<0>();
-  if (!active) return;
-  double2* P = (double2*)a.part + ((int64_t)series * a.nchunks + chunk) * a.ncells;
-#pragma unroll
-  for (int i = 0; i < 4; i++) {
-    const int r = r0 + i;
-    if (r >= tk.nrows) continue;
-    const int line = tk.line0 + r;
-    const int cm = __ldg(a.line_cmax + line);
-    double2* dst = P + (__ldg(a.line_start + line) - a.lo);
-#pragma unroll
-    for (int j = 0; j < 8; j++)
-      if (c0 + j <= cm) dst[c0 + j] = acc[i][j];
+  if (tr && threadIdx.x == 0) {
+    unsigned long long t2;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2));
+    tr[2] = t2;
+    tr[5] = (unsigned long long)wait_cyc;
   }
 }
 
@@ -444,95 +619,161 @@ static cudaError_t set_smem(K kernel, size_t bytes) {
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
+template <typename T>
+static cudaError_t configure_all() {
+  cudaError_t e;
+  if ((e = set_smem(k_triple<T, true, false>, kTripleSmem)) != cudaSuccess) return e;
+  if ((e = set_smem(k_triple<T, false, false>, kTripleSmem)) != cudaSuccess) return e;
+  if ((e = set_smem(k_triple<T, true, true>, kTripleSmem)) != cudaSuccess) return e;
+  return set_smem(k_triple<T, false, true>, kTripleSmem);
+}
+
+static cudaError_t configure() {
+  static bool done = false;
+  if (done) return cudaSuccess;
+  cudaError_t e;
+  if ((e = configure_all<float>()) != cudaSuccess) return e;
+  if ((e = configure_all<double>()) != cudaSuccess) return e;
+  done = true;
+  return cudaSuccess;
+}
+
+int triple_occupancy(int precision) {
+  if (configure() != cudaSuccess) return 1;
+  int n = 1;
+  if (precision == 32)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_triple<float, true, false>, 128, kTripleSmem);
+  else
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_triple<double, true, false>, 128, kTripleSmem);
+  return n < 1 ? 1 : n;
+}
+
+template <typename T, bool CONJ, bool ORDER4>
+static cudaError_t launch_pdl(const TripleArgs& a, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(a.nctas, a.batch);
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = kTripleSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_triple<T, CONJ, ORDER4>, a);
+}
+
 cudaError_t launch_triple(const TripleArgs& a, int precision, cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e;
-    if ((e = set_smem(k_triple_f32<true, false>, kTripleSmem)) != cudaSuccess) return e;
-    if ((e = set_smem(k_triple_f32<false, false>, kTripleSmem)) != cudaSuccess) return e;
-    if ((e = set_smem(k_triple_f32<true, true>, kTripleSmem)) != cudaSuccess) return e;
-    if ((e = set_smem(k_triple_f32<false, true>, kTripleSmem)) != cudaSuccess) return e;
-    if ((e = set_smem(k_triple_f64<true, false>, kTripleSmem)) != cudaSuccess) return e;
-    if ((e = set_smem(k_triple_f64<false, false>, kTripleSmem)) != cudaSuccess) return e;
-    if ((e = set_smem(k_triple_f64<true, true>, kTripleSmem)) != cudaSuccess) return e;
-    if ((e = set_smem(k_triple_f64<false, true>, kTripleSmem)) != cudaSuccess) return e;
-    configured = true;
-  }
-  if (a.ntasks == 0) return cudaSuccess;
-  dim3 grid(a.ntasks * a.nchunks, a.batch);
+  cudaError_t e = configure();
+  if (e != cudaSuccess) return e;
+  if (a.ntasks == 0 || a.nctas == 0 || a.seg_end <= a.seg_begin) return cudaSuccess;
   const bool o4 = a.order == 4;
   if (precision == 32) {
-    if (a.conj && !o4) k_triple_f32<true, false><<<grid, 128, kTripleSmem, st>>>(a);
-    else if (!a.conj && !o4) k_triple_f32<false, false><<<grid, 128, kTripleSmem, st>>>(a);
-    else if (a.conj) k_triple_f32<true, true><<<grid, 128, kTripleSmem, st>>>(a);
-    else k_triple_f32<false, true><<<grid, 128, kTripleSmem, st>>>(a);
+    if (a.conj && !o4) e = launch_pdl<float, true, false>(a, st);
+    else if (!a.conj && !o4) e = launch_pdl<float, false, false>(a, st);
+    else if (a.conj) e = launch_pdl<float, true, true>(a, st);
+    else e = launch_pdl<float, false, true>(a, st);
   } else {
-    if (a.conj && !o4) k_triple_f64<true, false><<<grid, 256, kTripleSmem, st>>>(a);
-    else if (!a.conj && !o4) k_triple_f64<false, false><<<grid, 256, kTripleSmem, st>>>(a);
-    else if (a.conj) k_triple_f64<true, true><<<grid, 256, kTripleSmem, st>>>(a);
-    else k_triple_f64<false, true><<<grid, 256, kTripleSmem, st>>>(a);
+    if (a.conj && !o4) e = launch_pdl<double, true, false>(a, st);
+    else if (!a.conj && !o4) e = launch_pdl<double, false, false>(a, st);
+    else if (a.conj) e = launch_pdl<double, true, true>(a, st);
+    else e = launch_pdl<double, false, true>(a, st);
   }
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
 // ===========================================================================
 // K4a: per-line inclusive prefix sums (fp64) of the chunk-summed raw cells.
-// One warp per (line, series); 32 cells per step, Kogge-Stone shuffle scan,
-// carry in a register.  The local (per-line) anchoring keeps the fp64 sums
-// exact to ~1e-16 relative (a global fp32 SAT would fail).
+// One CTA per (line, series); each thread sums the segment-chunk partials of
+// one cell (fixed chunk order -> deterministic), then a block scan (warp
+// shuffles + one smem pass over warp totals) with a carry across 256-cell
+// pieces.  The per-line anchoring keeps the fp64 sums exact to ~1e-16
+// relative (a global fp32 summed-area table would fail 1e-5).
+
+constexpr int kScanThreads = 256;
+
+// number of partial slots holding cell `idx` (absolute cell of line l)
+__device__ __forceinline__ int cell_slots(const SlotInfo& si, int nparts, int64_t l, int64_t col) {
+  if (si.line_region0 == nullptr) return nparts;
+  const int t = si.region_task[si.line_region0[l] + (int)(col / kRegionCols)];
+  return task_slots(t, si.nseg, (int64_t)si.ntasks * si.nseg, si.nctas);
+}
 
 template <typename P2>
-__global__ void __launch_bounds__(256) k_line_scan(const P2* __restrict__ part, int nparts, int64_t part_stride,
-                                                   int64_t part_series_stride, const int64_t* __restrict__ line_start,
-                                                   int64_t line_begin, int64_t nlines, int64_t s_series_stride,
-                                                   int batch, double2* __restrict__ S) {
-  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (gw >= nlines * batch) return;
-  const int series = (int)(gw / nlines);
-  const int64_t l = line_begin + (gw - (int64_t)series * nlines);
+__device__ __forceinline__ void sum_slots(const P2* __restrict__ src, int ns, int64_t stride, int64_t idx, double& vr,
+                                          double& vi) {
+  int p = 0;
+  for (; p + 4 <= ns; p += 4) {
+    const P2 v0 = src[(p + 0) * stride + idx];
+    const P2 v1 = src[(p + 1) * stride + idx];
+    const P2 v2 = src[(p + 2) * stride + idx];
+    const P2 v3 = src[(p + 3) * stride + idx];
+    vr += (double)v0.x; vi += (double)v0.y;
+    vr += (double)v1.x; vi += (double)v1.y;
+    vr += (double)v2.x; vi += (double)v2.y;
+    vr += (double)v3.x; vi += (double)v3.y;
+  }
+  for (; p < ns; p++) {
+    const P2 v = src[p * stride + idx];
+    vr += (double)v.x;
+    vi += (double)v.y;
+  }
+}
+
+template <typename P2>
+__global__ void __launch_bounds__(kScanThreads) k_line_scan(const P2* __restrict__ part, int nparts, int64_t part_stride,
+                                                            int64_t part_series_stride, SlotInfo si,
+                                                            const int64_t* __restrict__ line_start, int64_t line_begin,
+                                                            int64_t s_series_stride, double2* __restrict__ S) {
+  __shared__ double2 wsum[kScanThreads / 32];
+  const int64_t l = line_begin + blockIdx.x;
+  const int series = blockIdx.y;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t base = line_start[line_begin];
   const int64_t c0 = line_start[l] - base, c1 = line_start[l + 1] - base;
   const P2* src = part + series * part_series_stride;
   double2* dst = S + series * s_series_stride;
   double cr = 0.0, ci = 0.0;
-  for (int64_t c = c0; c < c1; c += 32) {
-    const int64_t idx = c + lane;
+  for (int64_t c = c0; c < c1; c += kScanThreads) {
+    const int64_t idx = c + threadIdx.x;
     double vr = 0.0, vi = 0.0;
-    if (idx < c1) {
-      for (int p = 0; p < nparts; p++) {
-        const P2 v = src[p * part_stride + idx];
-        vr += (double)v.x;
-        vi += (double)v.y;
-      }
-    }
+    if (idx < c1) sum_slots(src, cell_slots(si, nparts, l, idx - c0), part_stride, idx, vr, vi);
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const double ur = __shfl_up_sync(0xffffffffu, vr, o);
       const double ui = __shfl_up_sync(0xffffffffu, vi, o);
       if (lane >= o) { vr += ur; vi += ui; }
     }
-    vr += cr;
-    vi += ci;
-    if (idx < c1) dst[idx] = make_double2(vr, vi);
-    cr = __shfl_sync(0xffffffffu, vr, 31);
-    ci = __shfl_sync(0xffffffffu, vi, 31);
+    if (lane == 31) wsum[warp] = make_double2(vr, vi);
+    __syncthreads();
+    double pr = cr, pi = ci;
+#pragma unroll
+    for (int w = 0; w < kScanThreads / 32; w++) {
+      if (w < warp) { pr += wsum[w].x; pi += wsum[w].y; }
+    }
+    double tr = cr, ti = ci;
+#pragma unroll
+    for (int w = 0; w < kScanThreads / 32; w++) { tr += wsum[w].x; ti += wsum[w].y; }
+    if (idx < c1) dst[idx] = make_double2(vr + pr, vi + pi);
+    cr = tr;
+    ci = ti;
+    __syncthreads();
   }
 }
 
-cudaError_t launch_line_scan(const void* part, int nparts, int64_t part_stride, int precision,
+cudaError_t launch_line_scan(const void* part, int nparts, int64_t part_stride, const SlotInfo& si, int precision,
                              const int64_t* line_start, int64_t line_begin, int64_t nlines, int64_t ncells_series,
                              int batch, double* S, cudaStream_t st) {
-  const int64_t warps = nlines * batch;
-  const unsigned grid = (unsigned)((warps * 32 + 255) / 256);
-  if (grid == 0) return cudaSuccess;
+  if (nlines <= 0 || batch <= 0) return cudaSuccess;
+  dim3 grid((unsigned)nlines, batch);
   const int64_t pss = part_stride * nparts;
   if (precision == 32)
-    k_line_scan<float2><<<grid, 256, 0, st>>>((const float2*)part, nparts, part_stride, pss, line_start, line_begin,
-                                              nlines, ncells_series, batch, (double2*)S);
+    k_line_scan<float2><<<grid, kScanThreads, 0, st>>>((const float2*)part, nparts, part_stride, pss, si, line_start,
+                                                       line_begin, ncells_series, (double2*)S);
   else
-    k_line_scan<double2><<<grid, 256, 0, st>>>((const double2*)part, nparts, part_stride, pss, line_start, line_begin,
-                                               nlines, ncells_series, batch, (double2*)S);
+    k_line_scan<double2><<<grid, kScanThreads, 0, st>>>((const double2*)part, nparts, part_stride, pss, si, line_start,
+                                                        line_begin, ncells_series, (double2*)S);
   return cudaGetLastError();
 }
 
@@ -540,44 +781,46 @@ cudaError_t launch_line_scan(const void* part, int nparts, int64_t part_stride, 
 // K4b: box sums at the principal-domain points as differences of the line
 // prefix sums, summed over the window's other axis (order 3: w lines;
 // order 4: w x w pair lines), times 1/(M K w^(order-1)).
+// Order 3: grid (k2 blocks, k1 rows, series) — thread (k1, k2) directly.
+// Order 4: grid (pairs, series), one thread per k3.
 
 template <typename OUT>
-__global__ void __launch_bounds__(256) k_box(BoxArgs a) {
-  const int64_t npts = a.p_end - a.p_begin;
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= npts * a.batch) return;
-  const int series = (int)(t / npts);
-  const int64_t p = a.p_begin + (t - (int64_t)series * npts);
+__global__ void __launch_bounds__(128) k_box3(BoxArgs a, int row0) {
+  const int k1 = row0 + blockIdx.y;
+  const int k2 = blockIdx.x * blockDim.x + threadIdx.x;
+  const int series = blockIdx.z;
+  if (k2 >= p3_len(a.m, k1)) return;
   const double2* S = (const double2*)a.S + series * a.s_series_stride;
   double sr = 0.0, si = 0.0;
-  if (a.order == 3) {
-    int lo_r = 0, hi_r = a.rows;  // find k1 with row_off[k1] <= p < row_off[k1+1]
-    while (hi_r - lo_r > 1) {
-      const int mid = (lo_r + hi_r) >> 1;
-      if (__ldg(a.row_off + mid) <= p) lo_r = mid; else hi_r = mid;
+  for (int u = a.lo; u <= a.hi; u++) {
+    const int64_t line = (int64_t)(k1 + u - a.lo);
+    const int64_t cb = __ldg(a.line_start + line) - a.cell_base;
+    const double2 s1 = S[cb + k2 + a.m3 - 1];
+    sr += s1.x;
+    si += s1.y;
+    if (k2 >= 1) {
+      const double2 s0 = S[cb + k2 - 1];
+      sr -= s0.x;
+      si -= s0.y;
     }
-    const int k1 = lo_r;
-    const int k2 = (int)(p - __ldg(a.row_off + k1));
-    for (int u = a.lo; u <= a.hi; u++) {
-      const int64_t line = (int64_t)(k1 + u - a.lo);
-      const int64_t cb = __ldg(a.line_start + line) - a.cell_base;
-      const double2 s1 = S[cb + k2 + a.m3 - 1];
-      sr += s1.x;
-      si += s1.y;
-      if (k2 >= 1) {
-        const double2 s0 = S[cb + k2 - 1];
-        sr -= s0.x;
-        si -= s0.y;
-      }
-    }
-  } else {
-    int lo_p = 0, hi_p = a.npairs;
-    while (hi_p - lo_p > 1) {
-      const int mid = (lo_p + hi_p) >> 1;
-      if (__ldg(a.pair_base + mid) <= p) lo_p = mid; else hi_p = mid;
-    }
-    const int k1 = __ldg(a.pair_k1 + lo_p), k2 = __ldg(a.pair_k2 + lo_p);
-    const int k3 = (int)(p - __ldg(a.pair_base + lo_p));
+  }
+  const int64_t p = __ldg(a.row_off + k1) + k2;
+  OUT* out = (OUT*)a.out + series * a.out_series_stride;
+  out[p - a.p_begin].x = sr * a.scale;
+  out[p - a.p_begin].y = si * a.scale;
+}
+
+template <typename OUT>
+__global__ void __launch_bounds__(64) k_box4(BoxArgs a, int pair0) {
+  const int pair = pair0 + blockIdx.x;
+  const int series = blockIdx.y;
+  const int k1 = __ldg(a.pair_k1 + pair), k2 = __ldg(a.pair_k2 + pair);
+  const int64_t base = __ldg(a.pair_base + pair);
+  const int n3 = p4_len(a.m, k1, k2);
+  const double2* S = (const double2*)a.S + series * a.s_series_stride;
+  OUT* out = (OUT*)a.out + series * a.out_series_stride;
+  for (int k3 = threadIdx.x; k3 < n3; k3 += blockDim.x) {
+    double sr = 0.0, si = 0.0;
     for (int u = a.lo; u <= a.hi; u++) {
       const int32_t* lrow = a.line_of_ab + (int64_t)(k1 + u - a.lo) * a.b_count;
       for (int v = a.lo; v <= a.hi; v++) {
@@ -593,18 +836,26 @@ __global__ void __launch_bounds__(256) k_box(BoxArgs a) {
         }
       }
     }
+    out[base + k3 - a.p_begin].x = sr * a.scale;
+    out[base + k3 - a.p_begin].y = si * a.scale;
   }
-  OUT* out = (OUT*)a.out + series * a.out_series_stride;
-  out[p - a.p_begin].x = sr * a.scale;
-  out[p - a.p_begin].y = si * a.scale;
 }
 
 cudaError_t launch_box(const BoxArgs& a, cudaStream_t st) {
-  const int64_t n = (a.p_end - a.p_begin) * a.batch;
-  if (n <= 0) return cudaSuccess;
-  const unsigned grid = (unsigned)((n + 255) / 256);
-  if (a.precision == 32) k_box<float2><<<grid, 256, 0, st>>>(a);
-  else k_box<double2><<<grid, 256, 0, st>>>(a);
+  if (a.p_end <= a.p_begin || a.batch <= 0) return cudaSuccess;
+  if (a.order == 3) {
+    if (a.row_end <= a.row_begin) return cudaSuccess;
+    int mx = 1;
+    for (int r = a.row_begin; r < a.row_end; r++) mx = max(mx, p3_len(a.m, r));
+    dim3 grid((mx + 127) / 128, a.row_end - a.row_begin, a.batch);
+    if (a.precision == 32) k_box3<float2><<<grid, 128, 0, st>>>(a, a.row_begin);
+    else k_box3<double2><<<grid, 128, 0, st>>>(a, a.row_begin);
+  } else {
+    if (a.pair_end <= a.pair_begin) return cudaSuccess;
+    dim3 grid(a.pair_end - a.pair_begin, a.batch);
+    if (a.precision == 32) k_box4<float2><<<grid, 64, 0, st>>>(a, a.pair_begin);
+    else k_box4<double2><<<grid, 64, 0, st>>>(a, a.pair_begin);
+  }
   return cudaGetLastError();
 }
 
@@ -612,27 +863,28 @@ cudaError_t launch_box(const BoxArgs& a, cudaStream_t st) {
 // Segment-chunk reduction for the multi-GPU path (fixed order, fp64 sum).
 
 template <typename P2>
-__global__ void k_reduce_parts(const P2* __restrict__ part, int nparts, int64_t stride, int64_t n, P2* __restrict__ raw) {
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-    double sr = 0.0, si = 0.0;
-    for (int p = 0; p < nparts; p++) {
-      const P2 v = part[p * stride + t];
-      sr += (double)v.x;
-      si += (double)v.y;
-    }
-    raw[t].x = sr;
-    raw[t].y = si;
+__global__ void __launch_bounds__(256) k_reduce_parts(const P2* __restrict__ part, int64_t stride, SlotInfo si,
+                                                      const int64_t* __restrict__ line_start, P2* __restrict__ raw) {
+  const int64_t l = blockIdx.x;
+  const int64_t c0 = line_start[l], c1 = line_start[l + 1];
+  for (int64_t idx = c0 + threadIdx.x; idx < c1; idx += blockDim.x) {
+    double sr = 0.0, si_ = 0.0;
+    sum_slots(part, cell_slots(si, 1, l, idx - c0), stride, idx, sr, si_);
+    raw[idx].x = sr;
+    raw[idx].y = si_;
   }
 }
 
-cudaError_t launch_reduce_parts(const void* part, int nparts, int64_t part_stride, int64_t n, int precision, void* raw,
-                                cudaStream_t st) {
-  if (n <= 0) return cudaSuccess;
+cudaError_t launch_reduce_parts(const void* part, int64_t part_stride, const SlotInfo& si, const int64_t* line_start,
+                                int64_t nlines, int lo, int precision, void* raw, cudaStream_t st) {
+  (void)lo;
+  if (nlines <= 0) return cudaSuccess;
   if (precision == 32)
-    k_reduce_parts<float2><<<grid_for(n, 256), 256, 0, st>>>((const float2*)part, nparts, part_stride, n, (float2*)raw);
+    k_reduce_parts<float2><<<(unsigned)nlines, 256, 0, st>>>((const float2*)part, part_stride, si, line_start,
+                                                             (float2*)raw);
   else
-    k_reduce_parts<double2><<<grid_for(n, 256), 256, 0, st>>>((const double2*)part, nparts, part_stride, n,
-                                                               (double2*)raw);
+    k_reduce_parts<double2><<<(unsigned)nlines, 256, 0, st>>>((const double2*)part, part_stride, si, line_start,
+                                                              (double2*)raw);
   return cudaGetLastError();
 }
 

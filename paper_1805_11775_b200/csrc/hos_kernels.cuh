@@ -13,6 +13,7 @@
 //   K4b box     window sums as prefix differences, scale 1/(M K w^(d)), write
 //               lexicographic principal-domain values   hospectra/spectra.py:405-415
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdint>
 
@@ -53,23 +54,42 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // launch wrappers (hos_kernels.cu)
 
 struct TripleArgs {
-  const void* E;              // [series][K][Lp] quads (fp32) / double2 (fp64)
-  int Lp;                     // elements per segment row
+  // 2-D tensor maps over the extended spectra viewed as [rows=batch*K][2 Lp x 8 bytes]
+  // (one 16-byte spectrum element = 2 x 8 bytes; fp32 quads or fp64 complex),
+  // boxes of kSegsPerSlot segments x (2 x width) 8-byte elements:
+  CUtensorMap map_rows;      // 32 elements        (row factors of a band)
+  CUtensorMap map_cols[3];   // 32k elements       (column factors of k regions)
+  CUtensorMap map_g[3];      // 31 + 32k elements  (last factors G(row+col[+a]))
+  CUtensorMap map_plane;     // 1 element          (order 4: F(a))
   int f_lo;                   // frequency of element 0
   int K;                      // segments per series (E rows per series)
   int seg_begin, seg_end;     // segment range reduced by this launch
-  int nchunks;                // chunks the range is split into
   const Task* tasks;
   int ntasks;
+  int nctas;                  // CTAs per series splitting the work (<= work units)
   const int32_t* line_cmax;
   const int64_t* line_start;
   int lo;
-  void* part;                 // [series][nchunks][ncells] float2 / double2
+  void* part;                 // [series][maxslots][ncells] float2 / double2
   int64_t ncells;
+  int maxslots;
   int order;
   int conj;
   int batch;
+  unsigned long long* trace;  // optional: per CTA {start, first data, end, smid} (globaltimer ns)
 };
+
+constexpr int kSegsPerSlot = 4;   // segments per TMA box / ring slot
+
+// Where the partial slots of a K2 launch are (for the K4a / reduce readers).
+struct SlotInfo {
+  const int32_t* line_region0;  // nullptr: plain buffer with `nparts` parts
+  const int32_t* region_task;
+  int ntasks, nseg, nctas;
+};
+
+// occupancy (CTAs / SM) of the triple-product kernel
+int triple_occupancy(int precision);
 
 cudaError_t launch_prep(const void* x, int x_dtype, int64_t x_stride, int m, int seg_begin, int nseg,
                         int batch, int taper, const double* taper_tab, int precision, void* seg_out,
@@ -81,7 +101,7 @@ cudaError_t launch_extend_full(const void* S, int spec_dtype, int m, int rows, i
 cudaError_t launch_expand_full(const void* H, int m, int hstride, int rows, int precision, void* out,
                                cudaStream_t st);
 cudaError_t launch_triple(const TripleArgs& a, int precision, cudaStream_t st);
-cudaError_t launch_line_scan(const void* part, int nparts, int64_t part_stride, int precision,
+cudaError_t launch_line_scan(const void* part, int nparts, int64_t part_stride, const SlotInfo& si, int precision,
                              const int64_t* line_start, int64_t line_begin, int64_t nlines,
                              int64_t ncells_series, int batch, double* S, cudaStream_t st);
 struct BoxArgs {
@@ -98,8 +118,10 @@ struct BoxArgs {
   int npairs;
   const int32_t* line_of_ab;
   int b_count;
-  int lo, hi, m3, order;
-  int64_t p_begin, p_end;   // lexicographic point range written
+  int lo, hi, m3, order, m;
+  int row_begin, row_end;   // order 3: output rows k1 written
+  int pair_begin, pair_end; // order 4: pairs written
+  int64_t p_begin, p_end;   // lexicographic point range written (out[0] = point p_begin)
   double scale;
   void* out;                // [series][..] values for points [p_begin, p_end)
   int64_t out_series_stride;
@@ -108,8 +130,8 @@ struct BoxArgs {
 };
 cudaError_t launch_box(const BoxArgs& a, cudaStream_t st);
 // raw[c] = sum_p part[p][c] (fp64 sum, stored in the compute precision)
-cudaError_t launch_reduce_parts(const void* part, int nparts, int64_t part_stride, int64_t n, int precision,
-                                void* raw, cudaStream_t st);
+cudaError_t launch_reduce_parts(const void* part, int64_t part_stride, const SlotInfo& si, const int64_t* line_start,
+                                int64_t nlines, int lo, int precision, void* raw, cudaStream_t st);
 cudaError_t launch_cast(const void* x, int x_dtype, int64_t n, int precision, void* out, cudaStream_t st);
 cudaError_t launch_peak_fp32(float2* buf, int blocks, int iters, cudaStream_t st);
 cudaError_t launch_clock_probe(unsigned long long* out, long long spin, cudaStream_t st);
