@@ -253,10 +253,7 @@ def run_ours(args):
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
-    if world == 1:
-        plan.set_timing(True)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    tri = []
     sampler = ClockSampler(local)
     if dist is not None:
         dist.barrier()
@@ -265,24 +262,31 @@ def run_ours(args):
     for i in range(args.steps):
         flush.fill_(i & 0xFF)
         ev[i][0].record(stream)
-        step()
+        step()  # the whole pipeline replays as one CUDA graph
         ev[i][1].record(stream)
-        if world == 1:
-            # triple-product kernel time of this step (events on the launching stream)
-            ev[i][1].synchronize()
-            tri.append(plan.kernel_ms()[0])
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
     sampler.stop()
+    # per-stage device times (events between the kernels on the launching
+    # stream; direct launches, L2 flushed before each call) for the roofline
+    tri, stages = [], {}
+    if world == 1:
+        plan.set_timing(True)
+        for i in range(max(5, min(args.steps, 50))):
+            flush.fill_(i & 0xFF)
+            step()
+            st = plan.stage_ms()
+            tri.append(st["triple"])
+            for k_, v_ in st.items():
+                stages.setdefault(k_, []).append(v_)
+        plan.set_timing(False)
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = sum(step_ms)
     if dist is not None:
         t = torch.tensor([total_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
-    if world == 1:
-        plan.set_timing(False)
     ms_per_step = total_ms / args.steps
     value = units / (ms_per_step * 1e-3)
 
@@ -330,12 +334,13 @@ def run_ours(args):
         peak_tf, probe_mhz = peak_fp32(lib, cstream)
         roof = None
         if tri:
-            t_tri = statistics.mean(tri)
+            t_tri = statistics.median(tri)
             achieved = FLOPS_PER_UNIT * units / (t_tri * 1e-3) / 1e12
             roof = {"bound": "fp32", "achieved": round(achieved, 3), "peak": round(peak_tf, 3), "unit": "TFLOP/s",
                     "frac": round(achieved / peak_tf, 4), "traffic": load_traffic(args.config),
                     "kernel": "k_triple_f32 (FFMA2 triple product)", "kernel_ms": round(t_tri, 5),
                     "kernel_share_of_step": round(t_tri / ms_per_step, 3),
+                    "stage_us": {k_: round(statistics.median(v_) * 1e3, 2) for k_, v_ in stages.items()},
                     "peak_source": f"live FFMA2 outer-product microbenchmark (hos_peak_fp32) at {probe_mhz:.0f} MHz; "
                                    "MEASURED_PEAKS.json has no FP32 figure",
                     "tiling_efficiency": round(plan.units / plan.issued, 4)}

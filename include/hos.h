@@ -175,6 +175,10 @@ int hos_plan_set_timing(hos_plan* plan, int enable);
 int hos_plan_nctas(const hos_plan* plan);
 int hos_plan_set_trace(hos_plan* plan, void* trace_dev);
 int hos_plan_kernel_ms(const hos_plan* plan, double* triple_ms, double* total_ms);
+/* Per-stage durations (ms) of the last timed call: prep, FFT, extend,
+ * triple product, line scan, box (6 values; the triple product includes
+ * the PDL-overlapped prologue). */
+int hos_plan_stage_ms(const hos_plan* plan, double* ms6);
 
 #ifdef __cplusplus
 }

@@ -59,6 +59,7 @@ EXPORTED_SYMBOLS = {
     "hos_plan_nctas": (_i, [_p]),
     "hos_plan_set_trace": (_i, [_p, _p]),
     "hos_plan_kernel_ms": (_i, [_p, _p, _p]),
+    "hos_plan_stage_ms": (_i, [_p, _p]),
 }
 
 _lib = None
@@ -254,6 +255,11 @@ class Plan:
 
     def set_timing(self, on: bool):
         raise_for(lib().hos_plan_set_timing(self.handle, int(on)))
+
+    def stage_ms(self):
+        out = (ctypes.c_double * 6)()
+        raise_for(lib().hos_plan_stage_ms(self.handle, out))
+        return dict(zip(("prep", "fft", "extend", "triple", "scan", "box"), list(out)))
 
     def kernel_ms(self):
         t, tot = ctypes.c_double(), ctypes.c_double()

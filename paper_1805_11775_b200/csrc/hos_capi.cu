@@ -78,9 +78,24 @@ struct hos_plan {
   size_t bytes = 0;
   unsigned long long* trace = nullptr;  // optional K2 per-CTA trace (device, 8 x nctas x batch)
   std::map<int, cufftHandle> ffts;  // rows -> plan
+  // CUDA graphs of the whole stream-ordered pipeline, one per buffer binding
+  struct GraphKey {
+    int kind;  // 0 estimate, 1 from_spectra, 2 host (pinned)
+    const void* in;
+    int dtype;
+    int64_t stride;
+    void* out;
+    bool operator<(const GraphKey& o) const {
+      return std::tie(kind, in, dtype, stride, out) < std::tie(o.kind, o.in, o.dtype, o.stride, o.out);
+    }
+  };
+  std::map<GraphKey, cudaGraphExec_t> graphs;
+  cudaStream_t cap = nullptr;  // capture stream
+  bool use_graphs = true;
   // timing
   int timing = 0;
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  // stage events: 0 start | 1 prep | 2 fft | 3 extend | 4 triple | 5 scan | 6 box
+  cudaEvent_t ev[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   bool timed = false;
 };
 
@@ -239,11 +254,11 @@ int make_maps(hos_plan* p) {
 // K2 + K4a + K4b over the extended spectra already in p->d_E.
 int run_back(hos_plan* p, void* out_dev, cudaStream_t st) {
   const hos::TripleArgs ta = triple_args(p, 0, p->k, p->nctas, p->batch);
-  if (p->timing) CUDA_TRY(cudaEventRecord(p->ev[1], st));
   CUDA_TRY(hos::launch_triple(ta, p->precision, st));
-  if (p->timing) CUDA_TRY(cudaEventRecord(p->ev[2], st));
+  if (p->timing) CUDA_TRY(cudaEventRecord(p->ev[4], st));
   CUDA_TRY(hos::launch_line_scan(p->d_part, p->maxslots, p->geo.ncells, slot_info(p, p->k, p->nctas), p->precision,
                                  p->d_line_start, 0, p->geo.nlines, p->geo.ncells, p->batch, p->d_S, st));
+  if (p->timing) CUDA_TRY(cudaEventRecord(p->ev[5], st));
   hos::BoxArgs b{};
   b.S = p->d_S;
   b.s_series_stride = p->geo.ncells;
@@ -276,7 +291,7 @@ int run_back(hos_plan* p, void* out_dev, cudaStream_t st) {
   b.batch = p->batch;
   CUDA_TRY(hos::launch_box(b, st));
   if (p->timing) {
-    CUDA_TRY(cudaEventRecord(p->ev[3], st));
+    CUDA_TRY(cudaEventRecord(p->ev[6], st));
     p->timed = true;
   }
   return HOS_OK;
@@ -293,10 +308,42 @@ int run_front(hos_plan* p, const void* x_dev, int x_dtype, int64_t x_stride, cud
   const int rows = p->batch * p->k;
   CUDA_TRY(hos::launch_prep(x_dev, x_dtype, x_stride, p->m, 0, p->k, p->batch, p->taper, p->d_taper, p->precision,
                             p->d_seg, st));
+  if (p->timing) CUDA_TRY(cudaEventRecord(p->ev[1], st));
   int rc = run_fft(p, rows, p->d_seg, p->d_half, st);
   if (rc) return rc;
+  if (p->timing) CUDA_TRY(cudaEventRecord(p->ev[2], st));
   CUDA_TRY(hos::launch_extend_half(p->d_half, p->m, p->hstride, rows, nullptr, p->geo.f_lo, p->L, p->Lp,
                                    p->precision, p->d_E, st));
+  if (p->timing) CUDA_TRY(cudaEventRecord(p->ev[3], st));
+  return HOS_OK;
+}
+
+// Run `body(stream)` through a cached CUDA graph keyed by the buffer binding
+// (captured on the plan's private stream on first use, replayed on `st`).
+template <typename F>
+int run_graph(hos_plan* p, const hos_plan::GraphKey& key, cudaStream_t st, F body) {
+  auto it = p->graphs.find(key);
+  if (it == p->graphs.end()) {
+    cudaGraph_t graph = nullptr;
+    CUDA_TRY(cudaStreamBeginCapture(p->cap, cudaStreamCaptureModeThreadLocal));
+    int rc = body(p->cap);
+    cudaError_t e = cudaStreamEndCapture(p->cap, &graph);
+    if (rc) {
+      if (graph) cudaGraphDestroy(graph);
+      return rc;
+    }
+    CUDA_TRY(e);
+    cudaGraphExec_t exec = nullptr;
+    e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    CUDA_TRY(e);
+    if (p->graphs.size() >= 16) {  // bound the cache
+      cudaGraphExecDestroy(p->graphs.begin()->second);
+      p->graphs.erase(p->graphs.begin());
+    }
+    it = p->graphs.emplace(key, exec).first;
+  }
+  CUDA_TRY(cudaGraphLaunch(it->second, st));
   return HOS_OK;
 }
 
@@ -402,12 +449,17 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
   if ((rc = make_maps(p))) return bail(rc);
   for (auto& e : p->ev)
     if (cudaEventCreate(&e) != cudaSuccess) return bail(fail(HOS_ECUDA, "cudaEventCreate failed"));
+  if (cudaStreamCreateWithFlags(&p->cap, cudaStreamNonBlocking) != cudaSuccess)
+    return bail(fail(HOS_ECUDA, "cudaStreamCreate failed"));
+  if (const char* env = std::getenv("HOS_NO_GRAPH")) p->use_graphs = std::atoi(env) == 0;
   *out = p;
   return HOS_OK;
 }
 
 void hos_plan_destroy(hos_plan* p) {
   if (!p) return;
+  for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);
+  if (p->cap) cudaStreamDestroy(p->cap);
   for (auto& kv : p->ffts) cufftDestroy(kv.second);
   void* bufs[] = {p->d_tasks, p->d_line_region0, p->d_region_task, p->d_line_cmax, p->d_line_start, p->d_row_off, p->d_pair_k1, p->d_pair_k2,
                   p->d_pair_base, p->d_line_of_ab, p->d_taper, p->d_seg, p->d_half, p->d_E, p->d_part,
@@ -444,9 +496,16 @@ int hos_estimate(hos_plan* p, const void* x_dev, int x_dtype, int64_t x_stride, 
     return fail(HOS_EPARAM, "series stride " + std::to_string(x_stride) + " shorter than k*m = " +
                                 std::to_string((int64_t)p->k * p->m));
   cudaStream_t st = (cudaStream_t)stream;
-  if (p->timing) CUDA_TRY(cudaEventRecord(p->ev[0], st));
-  if ((rc = run_front(p, x_dev, x_dtype, x_stride, st))) return rc;
-  return run_back(p, out_dev, st);
+  if (p->timing || p->trace || !p->use_graphs) {
+    if (p->timing) CUDA_TRY(cudaEventRecord(p->ev[0], st));
+    if ((rc = run_front(p, x_dev, x_dtype, x_stride, st))) return rc;
+    return run_back(p, out_dev, st);
+  }
+  const hos_plan::GraphKey key{0, x_dev, x_dtype, x_stride, out_dev};
+  return run_graph(p, key, st, [&](cudaStream_t s) {
+    int r = run_front(p, x_dev, x_dtype, x_stride, s);
+    return r ? r : run_back(p, out_dev, s);
+  });
 }
 
 int hos_estimate_from_spectra(hos_plan* p, const void* spec_dev, int spec_dtype, void* out_dev, void* stream) {
@@ -456,10 +515,17 @@ int hos_estimate_from_spectra(hos_plan* p, const void* spec_dev, int spec_dtype,
     return fail(HOS_EPARAM, "spectra dtype must be HOS_C64 or HOS_C128");
   if (!spec_dev || !out_dev) return fail(HOS_EPARAM, "null buffer");
   cudaStream_t st = (cudaStream_t)stream;
-  if (p->timing) CUDA_TRY(cudaEventRecord(p->ev[0], st));
-  CUDA_TRY(hos::launch_extend_full(spec_dev, spec_dtype, p->m, p->batch * p->k, p->geo.f_lo, p->L, p->Lp,
-                                   p->precision, p->d_E, st));
-  return run_back(p, out_dev, st);
+  auto body = [&](cudaStream_t s) -> int {
+    if (p->timing) CUDA_TRY(cudaEventRecord(p->ev[0], s));
+    CUDA_TRY(hos::launch_extend_full(spec_dev, spec_dtype, p->m, p->batch * p->k, p->geo.f_lo, p->L, p->Lp,
+                                     p->precision, p->d_E, s));
+    if (p->timing)
+      for (int i = 1; i <= 3; i++) CUDA_TRY(cudaEventRecord(p->ev[i], s));
+    return run_back(p, out_dev, s);
+  };
+  if (p->timing || p->trace || !p->use_graphs) return body(st);
+  const hos_plan::GraphKey key{1, spec_dev, spec_dtype, 0, out_dev};
+  return run_graph(p, key, st, body);
 }
 
 int hos_segment_spectra(hos_plan* p, const void* x_dev, int x_dtype, int64_t x_stride, void* spec_dev, void* stream) {
@@ -526,15 +592,32 @@ int hos_estimate_host(hos_plan* p, const void* x_host, int x_dtype, int64_t x_st
   cudaStream_t st = (cudaStream_t)stream;
   const size_t es = x_dtype == HOS_F32 ? 4 : 8;
   const size_t km = (size_t)p->k * p->m;
-  if (p->batch == 1 || x_stride == (int64_t)km) {
-    CUDA_TRY(cudaMemcpyAsync(p->d_xin, x_host, km * p->batch * es, cudaMemcpyHostToDevice, st));
+  auto body = [&](cudaStream_t s) -> int {
+    if (p->batch == 1 || x_stride == (int64_t)km) {
+      CUDA_TRY(cudaMemcpyAsync(p->d_xin, x_host, km * p->batch * es, cudaMemcpyHostToDevice, s));
+    } else {
+      CUDA_TRY(cudaMemcpy2DAsync(p->d_xin, km * es, x_host, (size_t)x_stride * es, km * es, p->batch,
+                                 cudaMemcpyHostToDevice, s));
+    }
+    int r = run_front(p, p->d_xin, x_dtype, (int64_t)km, s);
+    if (!r) r = run_back(p, p->d_out, s);
+    if (r) return r;
+    CUDA_TRY(cudaMemcpyAsync(out_host, p->d_out, (size_t)p->batch * p->geo.npoints * csize(p->precision),
+                             cudaMemcpyDeviceToHost, s));
+    return HOS_OK;
+  };
+  // graphs only with page-locked host buffers (pageable copies are not capturable)
+  cudaPointerAttributes ai{}, ao{};
+  const bool pinned = cudaPointerGetAttributes(&ai, x_host) == cudaSuccess && ai.type == cudaMemoryTypeHost &&
+                      cudaPointerGetAttributes(&ao, out_host) == cudaSuccess && ao.type == cudaMemoryTypeHost;
+  cudaGetLastError();
+  if (pinned && p->use_graphs && !p->timing && !p->trace) {
+    const hos_plan::GraphKey key{2, x_host, x_dtype, x_stride, out_host};
+    if ((rc = run_graph(p, key, st, body))) return rc;
   } else {
-    CUDA_TRY(cudaMemcpy2DAsync(p->d_xin, km * es, x_host, (size_t)x_stride * es, km * es, p->batch,
-                               cudaMemcpyHostToDevice, st));
+    if (p->timing) CUDA_TRY(cudaEventRecord(p->ev[0], st));
+    if ((rc = body(st))) return rc;
   }
-  if ((rc = hos_estimate(p, p->d_xin, x_dtype, (int64_t)km, p->d_out, stream))) return rc;
-  CUDA_TRY(cudaMemcpyAsync(out_host, p->d_out, (size_t)p->batch * p->geo.npoints * csize(p->precision),
-                           cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   return HOS_OK;
 }
@@ -717,11 +800,25 @@ int hos_plan_kernel_ms(const hos_plan* p, double* triple_ms, double* total_ms) {
   if (rc) return rc;
   if (!p->timed) return fail(HOS_EPARAM, "no timed call recorded (enable timing first)");
   float t1 = 0, t2 = 0;
-  CUDA_TRY(cudaEventSynchronize(p->ev[3]));
-  CUDA_TRY(cudaEventElapsedTime(&t1, p->ev[1], p->ev[2]));
-  CUDA_TRY(cudaEventElapsedTime(&t2, p->ev[0], p->ev[3]));
+  CUDA_TRY(cudaEventSynchronize(p->ev[6]));
+  CUDA_TRY(cudaEventElapsedTime(&t1, p->ev[3], p->ev[4]));
+  CUDA_TRY(cudaEventElapsedTime(&t2, p->ev[0], p->ev[6]));
   if (triple_ms) *triple_ms = t1;
   if (total_ms) *total_ms = t2;
+  return HOS_OK;
+}
+
+int hos_plan_stage_ms(const hos_plan* p, double* ms6) {
+  int rc = check_plan(p);
+  if (rc) return rc;
+  if (!p->timed) return fail(HOS_EPARAM, "no timed call recorded (enable timing first)");
+  if (!ms6) return fail(HOS_EPARAM, "null output");
+  CUDA_TRY(cudaEventSynchronize(p->ev[6]));
+  for (int i = 0; i < 6; i++) {
+    float t = 0;
+    CUDA_TRY(cudaEventElapsedTime(&t, p->ev[i], p->ev[i + 1]));
+    ms6[i] = t;
+  }
   return HOS_OK;
 }
 
