@@ -495,7 +495,7 @@ __global__ void __launch_bounds__(128, sizeof(T) == 4 ? HOS_K2_MINB : 2) k_tripl
 
     // pieces with no segments still own partial slots: write zeros
     for (int p = 0; p < np; p++) {
-      if (pcs[p].nseg != 0) continue;
+      if (pcs[p].nseg != 0 || a.accumulate) continue;
       const Task& tk = tcache[p];
       if (warp >= tk.nreg) continue;
       const int s = warp < tk.sub[0].k ? 0 : 1;
@@ -600,7 +600,14 @@ __global__ void __launch_bounds__(128, sizeof(T) == 4 ? HOS_K2_MINB : 2) k_tripl
           C* dst = P + (__ldg(a.line_start + line) - a.lo);
 #pragma unroll
           for (int j = 0; j < 4; j++)
-            if (c0 + 8 * j <= cm) dst[c0 + 8 * j] = acc[i][j];
+            if (c0 + 8 * j <= cm) {
+              if (a.accumulate) {
+                const C v = dst[c0 + 8 * j];
+                dst[c0 + 8 * j] = C{v.x + acc[i][j].x, v.y + acc[i][j].y};
+              } else {
+                dst[c0 + 8 * j] = acc[i][j];
+              }
+            }
         }
       }
     }

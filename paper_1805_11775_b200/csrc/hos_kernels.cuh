@@ -77,6 +77,7 @@ struct TripleArgs {
   int conj;
   int batch;
   unsigned long long* trace;  // optional: per CTA {start, first data, end, smid} (globaltimer ns)
+  int accumulate;             // add into the partial slots (chunked launches after the first)
 };
 
 constexpr int kSegsPerSlot = 4;   // segments per TMA box / ring slot

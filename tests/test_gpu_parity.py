@@ -225,8 +225,17 @@ def test_host_entry_point_matches_device(cuda, prec):
     x = P.baseline_series(c)
     plan = get_plan(3, c.m, c.k, c.m3, True, prec, "hann", 1, 0)
     dev = plan.estimate(torch.from_numpy(x).to(cuda)).cpu().numpy()
-    host = plan.estimate_host(x)
+    host = plan.estimate_host(x)  # pageable: same launch sequence as the device path
     assert np.array_equal(dev, host)
+    # pinned buffers: the chunked, copy-overlapped pipeline (segment-chunk partial
+    # sums accumulate in a different fp32 order, so compare with a tolerance)
+    xp = torch.from_numpy(x).pin_memory()
+    op = torch.empty(plan.npoints, dtype=torch.complex64 if prec == 32 else torch.complex128).pin_memory()
+    for _ in range(2):  # capture + replay
+        pinned = plan.estimate_host(xp.numpy(), op.numpy()).copy()
+        assert north_star(pinned, dev) <= (1e-6 if prec == 32 else 1e-13)
+    gl = golden("cfg2_rows.npz")
+    assert north_star(pinned.astype(np.complex128)[gl["pos"]], gl["val"]) <= TOL[f"fp{prec}"]
 
 
 @pytest.mark.parametrize("order,m,k,w", [(3, 256, 12, 9), (4, 64, 6, 5)])
