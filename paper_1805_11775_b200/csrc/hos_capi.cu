@@ -56,6 +56,7 @@ struct hos_plan {
   int L = 0, Lp = 0; // extended-spectrum length / pitch (16-byte elements)
   // device tables
   hos::Task* d_tasks = nullptr;
+  hos::Region* d_regions = nullptr;
   int32_t* d_line_region0 = nullptr;
   int32_t* d_region_task = nullptr;
   CUtensorMap map_rows, map_cols[3], map_g[3], map_plane;
@@ -161,8 +162,12 @@ int check_plan(const hos_plan* p) {
 // CTAs splitting a launch over nseg segments of `batch` series: one wave of
 // SMs x occupancy CTAs in total, at least 16 work units per CTA (and never
 // more CTAs than units, so every CTA's range is non-empty).
+int64_t work_items(const hos_plan* p) {
+  return hos::triple_warp_kernel() ? (int64_t)p->geo.regions.size() : (int64_t)p->geo.tasks.size();
+}
+
 int nctas_for(const hos_plan* p, int nseg, int batch) {
-  const int64_t work = (int64_t)p->geo.tasks.size() * nseg;
+  const int64_t work = work_items(p) * nseg;
   int64_t n = 0;
   if (const char* env = std::getenv("HOS_NCTAS")) n = std::atoll(env);
   if (n <= 0) {
@@ -175,10 +180,16 @@ int nctas_for(const hos_plan* p, int nseg, int batch) {
 }
 
 // partial slots the worst task needs (same arithmetic as the kernels)
+// warps splitting the warp kernel's work for an n-CTA launch (never more than units)
+int64_t nwarps_for(const hos_plan* p, int nseg, int n) {
+  return std::max<int64_t>(1, std::min<int64_t>((int64_t)n * hos::kTripleWarps, work_items(p) * nseg));
+}
+
 int slots_needed(const hos_plan* p, int nseg, int n) {
-  const int64_t T = (int64_t)p->geo.tasks.size(), W = T * nseg;
+  const int64_t T = work_items(p), W = T * nseg;
   if (W <= 0) return 1;
-  auto cta = [&](int64_t u) { return ((u + 1) * (int64_t)n - 1) / W; };
+  const int64_t parts = hos::triple_warp_kernel() ? nwarps_for(p, nseg, n) : n;
+  auto cta = [&](int64_t u) { return ((u + 1) * parts - 1) / W; };
   int best = 1;
   for (int64_t t = 0; t < T; t++) best = std::max(best, (int)(cta((t + 1) * nseg - 1) - cta(t * nseg) + 1));
   return best;
@@ -191,6 +202,9 @@ hos::SlotInfo slot_info(const hos_plan* p, int nseg, int n) {
   si.ntasks = (int)p->geo.tasks.size();
   si.nseg = nseg;
   si.nctas = n;
+  si.nregions = (int)p->geo.regions.size();
+  si.nwarps = nwarps_for(p, nseg, n);
+  if (hos::triple_warp_kernel()) si.region_task = nullptr;
   return si;
 }
 
@@ -209,6 +223,11 @@ hos::TripleArgs triple_args(const hos_plan* p, int seg_begin, int seg_end, int n
   x.seg_end = seg_end;
   x.tasks = p->d_tasks;
   x.ntasks = (int)p->geo.tasks.size();
+  x.E = p->d_E;
+  x.Lp = p->Lp;
+  x.regions = p->d_regions;
+  x.nregions = (int)p->geo.regions.size();
+  x.nwarps = nwarps_for(p, seg_end - seg_begin, n);
   x.nctas = n;
   x.line_cmax = p->d_line_cmax;
   x.line_start = p->d_line_start;
@@ -472,6 +491,7 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
 
   std::vector<int32_t> cmax(g.line_cmax.begin(), g.line_cmax.end());
   if ((rc = upload(p, &p->d_tasks, g.tasks))) return bail(rc);
+  if ((rc = upload(p, &p->d_regions, g.regions))) return bail(rc);
   if ((rc = upload(p, &p->d_line_region0, g.line_region0))) return bail(rc);
   if ((rc = upload(p, &p->d_region_task, g.region_task))) return bail(rc);
   if ((rc = upload(p, &p->d_line_cmax, cmax))) return bail(rc);
@@ -521,7 +541,7 @@ void hos_plan_destroy(hos_plan* p) {
   if (p->cap2) cudaStreamDestroy(p->cap2);
   for (auto e : p->chunk_ev) cudaEventDestroy(e);
   for (auto& kv : p->ffts) cufftDestroy(kv.second);
-  void* bufs[] = {p->d_tasks, p->d_line_region0, p->d_region_task, p->d_line_cmax, p->d_line_start, p->d_row_off, p->d_pair_k1, p->d_pair_k2,
+  void* bufs[] = {p->d_tasks, p->d_regions, p->d_line_region0, p->d_region_task, p->d_line_cmax, p->d_line_start, p->d_row_off, p->d_pair_k1, p->d_pair_k2,
                   p->d_pair_base, p->d_line_of_ab, p->d_taper, p->d_seg, p->d_half, p->d_E, p->d_part,
                   p->d_S, p->d_xin, p->d_out};
   for (void* b : bufs)

@@ -212,6 +212,17 @@ std::string Geometry::build(int order_, int m_, int m3_) {
   }
 
   group_tasks(regs, tasks, region_task, issued_cells);
+  regions.clear();
+  for (const RegionRec& r : regs) {
+    Region g{};
+    g.line0 = r.line0;
+    g.nrows = r.nrows;
+    g.row_freq0 = r.row_freq0;
+    g.plane_freq = r.plane_freq;
+    g.col0 = r.col0;
+    regions.push_back(g);
+  }
+  issued_cells = (int64_t)regions.size() * kBandRows * kRegionCols;
 
   // ---- frequencies touched by the TMA boxes of the tasks (extended spectrum range)
   f_lo = order == 3 ? 2 * lo : 3 * lo;

@@ -63,6 +63,15 @@ struct SubBand {
   int32_t k;          // regions of the task in this band
 };
 
+struct Region {
+  int32_t line0;      // first line of the band
+  int32_t nrows;      // lines in the band (<= kBandRows)
+  int32_t row_freq0;  // frequency of line0's row factor (order 3: a, order 4: b)
+  int32_t plane_freq; // order 4: a of the plane; order 3: 0
+  int32_t col0;       // first column of the region
+  int32_t pad[3];
+};
+
 struct Task {
   int32_t nreg;       // regions (warps with work), 1..kTaskRegions
   int32_t nsub;       // sub-bands, 1..2
@@ -96,6 +105,7 @@ struct Geometry {
   std::vector<Task> tasks;
   std::vector<int32_t> line_region0;  // per line: index of the region holding its first column
   std::vector<int32_t> region_task;   // per region: its task
+  std::vector<Region> regions;        // flat region list (band after band)
   int64_t issued_cells = 0;           // cells computed by the tasks (incl. idle warps)
 
   std::string build(int order, int m, int m3);  // returns "" or an error message

@@ -2,6 +2,8 @@
 #include "hos_kernels.cuh"
 
 #include <cuda_runtime.h>
+#include <cstdlib>
+#include <string>
 
 namespace hos {
 
@@ -202,8 +204,9 @@ cudaError_t launch_expand_full(const void* H, int m, int hstride, int rows, int 
 #define HOS_K2_MINB 3
 #endif
 constexpr int kSlots = HOS_K2_SLOTS;
-// per slot (quads): rows 2 x 128 | cols 4 x 128 | planes 2 x 8 | G 4(31+32k_A) (padded) + 4(31+32k_B)
-constexpr int kSlotQuads = 2 * 128 + 4 * 128 + 2 * 8 + 4 * (62 + 32 * 4) + 8;
+// per slot (quads, S = kSegsPerSlot): rows 2 x 32S | cols 4 x 32S | planes 2 x 8 | G S(31+32k_A) (padded) + S(31+32k_B)
+constexpr int kSlotQuads =
+    ((2 * 32 * kSegsPerSlot + 4 * 32 * kSegsPerSlot + 2 * 8 + kSegsPerSlot * (62 + 32 * 4) + 8) + 7) / 8 * 8;
 static_assert(kSlotQuads % 8 == 0, "ring slots must stay 128-byte aligned for TMA");
 constexpr size_t kTripleSmem = 16 * (size_t)kSlots * kSlotQuads + 128;
 
@@ -253,13 +256,14 @@ struct SubLayout {
 
 __device__ __forceinline__ SubLayout sub_layout(const Task& t, int s) {
   const int kA = t.sub[0].k, kB = t.nsub > 1 ? t.sub[1].k : 0;
-  const int plane0 = 128 * t.nsub + 128 * (kA + kB);
-  const int g0 = plane0 + 8 * t.nsub;
+  constexpr int S = kSegsPerSlot, PB = (S + 7) / 8 * 8;  // plane block, 128 B multiple
+  const int plane0 = 32 * S * t.nsub + 32 * S * (kA + kB);
+  const int g0 = plane0 + PB * t.nsub;
   SubLayout L;
-  L.rows = s ? 128 : 0;
-  L.cols = 128 * t.nsub + (s ? 128 * kA : 0);
-  L.plane = plane0 + (s ? 8 : 0);
-  L.g = s ? g0 + ((4 * (31 + 32 * kA) + 7) & ~7) : g0;
+  L.rows = s ? 32 * S : 0;
+  L.cols = 32 * S * t.nsub + (s ? 32 * S * kA : 0);
+  L.plane = plane0 + (s ? PB : 0);
+  L.g = s ? g0 + ((S * (31 + 32 * kA) + 7) & ~7) : g0;
   const int k = s ? kB : kA;
   L.cw = 32 * k;
   L.gw = 31 + 32 * k;
@@ -421,25 +425,40 @@ __global__ void __launch_bounds__(128, sizeof(T) == 4 ? HOS_K2_MINB : 2) k_tripl
 
   // rounds of up to kMaxPieces pieces (one round unless the range is tiny and spans many tasks)
   while (true) {
-    if (threadIdx.x == 0) {
-      int np = 0, slots = s_end, t = s_tnext;
-      for (; t < a.ntasks && np < kMaxPieces && (int64_t)t * nseg_all < x1 && x0 < x1; t++) {
+    if (warp == 0) {  // lane l builds piece l of this round (the 64-bit divisions run in parallel)
+      const int t = s_tnext + lane;
+      const bool valid = lane < kMaxPieces && t < a.ntasks && (int64_t)t * nseg_all < x1 && x0 < x1;
+      PieceRec r{};
+      if (valid) {
         const int64_t P0 = (int64_t)t * nseg_all;
         const int64_t u0 = min(max(x0 - P0, (int64_t)0), (int64_t)nseg_all);
         const int64_t u1 = min(max(x1 - P0, (int64_t)0), (int64_t)nseg_all);
-        PieceRec r;
         r.task = t;
         r.first = a.seg_begin + (int)u0;
         r.nseg = (int)(u1 - u0);
         r.nsl = (r.nseg + kSegsPerSlot - 1) / kSegsPerSlot;
-        r.slot0 = slots;
         r.pslot = (int)(c - cta_of_unit(P0, W, N));
-        slots += r.nsl;
-        pcs[np++] = r;
       }
-      s_np = np;
-      s_end = slots;
-      s_tnext = t;
+      int incl = r.nsl;  // inclusive prefix of slots over the lanes
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+      const int np = __popc(vmask);  // valid lanes are a prefix
+      const int base = s_end;
+      __syncwarp();
+      if (valid) {
+        r.slot0 = base + incl - r.nsl;
+        pcs[lane] = r;
+      }
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      if (lane == 0) {
+        s_np = np;
+        s_end = base + total;
+        s_tnext += np;
+      }
     }
     __syncthreads();
     const int np = s_np, gend = s_end;
@@ -479,14 +498,14 @@ __global__ void __launch_bounds__(128, sizeof(T) == 4 ? HOS_K2_MINB : 2) k_tripl
       }
       __syncwarp();
     };
-    if (warp == 0) {
+    if (gbeg + warp < gend && warp < kSlots) {  // the warps issue the prologue slots in parallel
       unsigned long long ta0 = 0, ta1 = 0, ta2 = 0;
       if (tr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ta0));
       if (gbeg == 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // E is written by the previous kernel
       if (tr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ta1));
-      for (int g = gbeg; g < gbeg + kSlots && g < gend; g++) produce(g);
+      for (int g = gbeg + warp; g < gbeg + kSlots && g < gend; g += 4) produce(g);
       if (tr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ta2));
-      if (tr && lane == 0 && gbeg == 0) {
+      if (tr && lane == 0 && gbeg == 0 && warp == 0) {
         tr[7] = ta0;          // piece list ready
         tr[6] = ta1;          // dependency resolved
         tr[4] = ta2;          // prologue issued
@@ -621,14 +640,218 @@ __global__ void __launch_bounds__(128, sizeof(T) == 4 ? HOS_K2_MINB : 2) k_tripl
   }
 }
 
+// ===========================================================================
+// K2 (default): warp-independent triple / quadruple product.
+//
+// Work = nregions x nseg units (a region is 32 x 32 cells of D_h); the
+// nwarps warps of the launch take equal contiguous unit ranges, so every
+// warp does the same work and warps never wait for each other.  A warp walks
+// its (region, segment) units in order; per unit its 32 lanes stage the
+// segment's 32 row factors, 32 column factors, 63 last factors G(row+col
+// [+a]) (and F(a) for order 4) with cp.async into a private ring of unit
+// PAIRS: the loads of the next pairs overlap the arithmetic of the current
+// one, and the two units of a pair are computed in one straight-line block
+// so the scheduler can overlap one segment's shared loads with the other's
+// FFMA2 chains.  Each (warp, region) piece writes ONE partial slot (warp index -
+// first warp of the region), fixed by the partition: the fp64 combination
+// order in K4a is fixed and results are deterministic.
+#ifndef HOS_K2_PAIRS
+#define HOS_K2_PAIRS 3
+#endif
+constexpr int kWarpPairs = HOS_K2_PAIRS;  // ring of unit pairs per warp (kWarpPairs-1 pairs in flight)
+constexpr int kUnitQuads = 128;           // rows 32 | cols 32 | G 63 | plane 1
+constexpr size_t kWarpTripleSmem = 16 * (size_t)kTripleWarps * 2 * kWarpPairs * kUnitQuads;
+
+__device__ __forceinline__ void cp_async16_cg(unsigned dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+
+// warp owning work unit u of a W-unit range split into N equal parts
+__device__ __forceinline__ int64_t warp_of_unit(int64_t u, int64_t W, int64_t N) { return ((u + 1) * N - 1) / W; }
+
+__device__ __forceinline__ int region_slots(int r, int nseg, int64_t W, int64_t N) {
+  return (int)(warp_of_unit((int64_t)(r + 1) * nseg - 1, W, N) - warp_of_unit((int64_t)r * nseg, W, N) + 1);
+}
+
+template <typename T, bool CONJ, bool ORDER4>
+__device__ __forceinline__ void warp_cells(const typename Cplx<T>::Q* q, int ta, int tb,
+                                           typename Cplx<T>::C (&acc)[8][4]) {
+  if constexpr (sizeof(T) == 4)
+    cells_f32<CONJ, ORDER4>(reinterpret_cast<const float4*>(q), reinterpret_cast<const float4*>(q + 32),
+                            reinterpret_cast<const float4*>(q + 64), reinterpret_cast<const float4*>(q + 127), ta, tb,
+                            acc);
+  else
+    cells_f64<CONJ, ORDER4>(reinterpret_cast<const double2*>(q), reinterpret_cast<const double2*>(q + 32),
+                            reinterpret_cast<const double2*>(q + 64), reinterpret_cast<const double2*>(q + 127), ta,
+                            tb, acc);
+}
+
+template <typename T, bool CONJ, bool ORDER4>
+__global__ void __launch_bounds__(128, sizeof(T) == 4 ? 3 : 2) k_triple_w(const __grid_constant__ TripleArgs a) {
+  using Q = typename Cplx<T>::Q;
+  using C = typename Cplx<T>::C;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ta = lane >> 3, tb = lane & 7;
+  const int series = blockIdx.y;
+  const int64_t Nw = a.nwarps;
+  const int64_t gw = (int64_t)blockIdx.x * kTripleWarps + warp;
+  if (gw >= Nw) return;
+  const int nseg = a.seg_end - a.seg_begin;
+  const int64_t W = (int64_t)a.nregions * nseg;
+  const int64_t u0 = gw * W / Nw, u1 = (gw + 1) * W / Nw;
+  if (u0 >= u1) return;
+  const Q* E = (const Q*)a.E + ((int64_t)series * a.K + a.seg_begin) * a.Lp;
+  C* Pbase = (C*)a.part + (int64_t)series * a.maxslots * a.ncells;
+  const Q* ring = reinterpret_cast<const Q*>(smraw) + warp * (2 * kWarpPairs * kUnitQuads);
+  const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring) + 16u * lane;
+  const int Lp = a.Lp, f_lo = a.f_lo;
+  const int total = (int)(u1 - u0);
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // E is written by the previous kernel
+
+  // producer: stages the warp's (region, segment) units two at a time, kWarpPairs-1 pairs ahead
+  int p_todo = total;
+  int p_r = (int)(u0 / nseg);
+  int p_left = 0;  // units left in the producer's current region
+  const Q *p_row = nullptr, *p_col = nullptr, *p_g = nullptr, *p_pl = nullptr;
+  int p_slot = 0;  // pair slot
+  auto p_enter = [&](int r, int seg) {
+    const Region g = a.regions[r];
+    const Q* base = E + (int64_t)seg * Lp;
+    p_row = base + (g.row_freq0 - f_lo) + lane;
+    p_col = base + (g.col0 - f_lo) + lane;
+    p_g = base + (g.plane_freq + g.row_freq0 + g.col0 - f_lo) + lane;
+    p_pl = base + (g.plane_freq - f_lo);
+    p_left = nseg - seg;
+  };
+  p_enter(p_r, (int)(u0 - (int64_t)p_r * nseg));
+  auto stage_unit = [&](unsigned d) {
+    cp_async16_cg(d, p_row);
+    cp_async16_cg(d + 16u * 32, p_col);
+    cp_async16_cg(d + 16u * 64, p_g);
+    if (lane < 31) cp_async16_cg(d + 16u * 96, p_g + 32);
+    if (ORDER4 && lane == 31) cp_async16_cg(d + 16u * (127 - 31), p_pl);
+    p_row += Lp;
+    p_col += Lp;
+    p_g += Lp;
+    p_pl += Lp;
+    if (--p_todo > 0 && --p_left == 0) p_enter(++p_r, 0);
+  };
+  auto stage_pair = [&]() {
+    const unsigned d = ring_s + 16u * (2 * kUnitQuads) * p_slot;
+    if (p_todo > 0) stage_unit(d);
+    if (p_todo > 0) stage_unit(d + 16u * kUnitQuads);
+    p_slot = p_slot + 1 == kWarpPairs ? 0 : p_slot + 1;
+    asm volatile("cp.async.commit_group;" ::: "memory");  // always commit: uniform group counting
+  };
+#pragma unroll
+  for (int d = 0; d < kWarpPairs - 1; d++) stage_pair();
+
+  int r = (int)(u0 / nseg);
+  int left = min(total, nseg - (int)(u0 - (int64_t)r * nseg));  // this warp's units in region r
+  int c0 = 0, line0 = 0, nrows = 0;
+  bool active = false, warp_active = false;
+  C acc[8][4];
+  auto enter = [&]() {
+    const Region rg = a.regions[r];
+    c0 = rg.col0 + tb;
+    line0 = rg.line0;
+    nrows = rg.nrows;
+    active = false;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+      const int rr = ta + 4 * i;
+      if (rr < nrows && __ldg(a.line_cmax + line0 + rr) >= c0) active = true;
+    }
+    warp_active = __any_sync(0xffffffffu, active);
+#pragma unroll
+    for (int i = 0; i < 8; i++)
+#pragma unroll
+      for (int j = 0; j < 4; j++) acc[i][j] = C{0, 0};
+  };
+  auto finalize = [&]() {  // this warp's partial slot of region r
+    if (!active) return;
+    const int pslot = (int)(gw - warp_of_unit((int64_t)r * nseg, W, Nw));
+    C* P = Pbase + (int64_t)pslot * a.ncells;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+      const int rr = ta + 4 * i;
+      if (rr >= nrows) continue;
+      const int line = line0 + rr;
+      const int cm = __ldg(a.line_cmax + line);
+      C* dst = P + (__ldg(a.line_start + line) - a.lo);
+#pragma unroll
+      for (int j = 0; j < 4; j++)
+        if (c0 + 8 * j <= cm) {
+          if (a.accumulate) {
+            const C v = dst[c0 + 8 * j];
+            dst[c0 + 8 * j] = C{v.x + acc[i][j].x, v.y + acc[i][j].y};
+          } else {
+            dst[c0 + 8 * j] = acc[i][j];
+          }
+        }
+    }
+  };
+  enter();
+  int c_slot = 0;
+  for (int pos = 0; pos < total; pos += 2) {
+    __syncwarp();  // every lane is done with the pair slot the next stage overwrites
+    stage_pair();
+    asm volatile("cp.async.wait_group %0;" ::"n"(kWarpPairs - 1) : "memory");
+    __syncwarp();  // the pair's data, copied by all lanes, is visible
+    const Q* q = ring + c_slot * (2 * kUnitQuads);
+    const int cnt = min(2, total - pos);
+    if (cnt == 2 && left >= 2) {  // fast path: both units in region r, one straight-line block
+      if (warp_active) {
+        warp_cells<T, CONJ, ORDER4>(q, ta, tb, acc);
+        warp_cells<T, CONJ, ORDER4>(q + kUnitQuads, ta, tb, acc);
+      }
+      left -= 2;
+    } else {
+      for (int t = 0; t < cnt; t++) {
+        if (left == 0) {
+          finalize();
+          r++;
+          left = min(total - pos - t, nseg);
+          enter();
+        }
+        if (warp_active) warp_cells<T, CONJ, ORDER4>(q + t * kUnitQuads, ta, tb, acc);
+        left--;
+      }
+    }
+    if (left == 0 && pos + 2 < total) {
+      finalize();
+      r++;
+      left = min(total - pos - 2, nseg);
+      enter();
+    }
+    c_slot = c_slot + 1 == kWarpPairs ? 0 : c_slot + 1;
+  }
+  finalize();
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
 template <typename K>
 static cudaError_t set_smem(K kernel, size_t bytes) {
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
+int triple_warp_kernel() {
+  static int v = -1;
+  if (v < 0) {
+    const char* env = std::getenv("HOS_K2");
+    v = (env && std::string(env) == "tma") ? 0 : 1;
+  }
+  return v;
+}
+
 template <typename T>
 static cudaError_t configure_all() {
   cudaError_t e;
+  if ((e = set_smem(k_triple_w<T, true, false>, kWarpTripleSmem)) != cudaSuccess) return e;
+  if ((e = set_smem(k_triple_w<T, false, false>, kWarpTripleSmem)) != cudaSuccess) return e;
+  if ((e = set_smem(k_triple_w<T, true, true>, kWarpTripleSmem)) != cudaSuccess) return e;
+  if ((e = set_smem(k_triple_w<T, false, true>, kWarpTripleSmem)) != cudaSuccess) return e;
   if ((e = set_smem(k_triple<T, true, false>, kTripleSmem)) != cudaSuccess) return e;
   if ((e = set_smem(k_triple<T, false, false>, kTripleSmem)) != cudaSuccess) return e;
   if ((e = set_smem(k_triple<T, true, true>, kTripleSmem)) != cudaSuccess) return e;
@@ -648,7 +871,12 @@ static cudaError_t configure() {
 int triple_occupancy(int precision) {
   if (configure() != cudaSuccess) return 1;
   int n = 1;
-  if (precision == 32)
+  if (triple_warp_kernel()) {
+    if (precision == 32)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_triple_w<float, true, false>, 128, kWarpTripleSmem);
+    else
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_triple_w<double, true, false>, 128, kWarpTripleSmem);
+  } else if (precision == 32)
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_triple<float, true, false>, 128, kTripleSmem);
   else
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_triple<double, true, false>, 128, kTripleSmem);
@@ -658,15 +886,17 @@ int triple_occupancy(int precision) {
 template <typename T, bool CONJ, bool ORDER4>
 static cudaError_t launch_pdl(const TripleArgs& a, cudaStream_t st) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(a.nctas, a.batch);
+  const bool warpk = triple_warp_kernel();
+  cfg.gridDim = dim3(warpk ? (unsigned)((a.nwarps + kTripleWarps - 1) / kTripleWarps) : a.nctas, a.batch);
   cfg.blockDim = dim3(128);
-  cfg.dynamicSmemBytes = kTripleSmem;
+  cfg.dynamicSmemBytes = warpk ? kWarpTripleSmem : kTripleSmem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if (warpk) return cudaLaunchKernelEx(&cfg, k_triple_w<T, CONJ, ORDER4>, a);
   return cudaLaunchKernelEx(&cfg, k_triple<T, CONJ, ORDER4>, a);
 }
 
@@ -703,8 +933,9 @@ constexpr int kScanThreads = 256;
 // number of partial slots holding cell `idx` (absolute cell of line l)
 __device__ __forceinline__ int cell_slots(const SlotInfo& si, int nparts, int64_t l, int64_t col) {
   if (si.line_region0 == nullptr) return nparts;
-  const int t = si.region_task[si.line_region0[l] + (int)(col / kRegionCols)];
-  return task_slots(t, si.nseg, (int64_t)si.ntasks * si.nseg, si.nctas);
+  const int r = si.line_region0[l] + (int)(col / kRegionCols);
+  if (si.region_task == nullptr) return region_slots(r, si.nseg, (int64_t)si.nregions * si.nseg, si.nwarps);
+  return task_slots(si.region_task[r], si.nseg, (int64_t)si.ntasks * si.nseg, si.nctas);
 }
 
 template <typename P2>

@@ -61,12 +61,17 @@ struct TripleArgs {
   CUtensorMap map_cols[3];   // 32k elements       (column factors of k regions)
   CUtensorMap map_g[3];      // 31 + 32k elements  (last factors G(row+col[+a]))
   CUtensorMap map_plane;     // 1 element          (order 4: F(a))
+  const void* E;              // [series][K][Lp] 16-byte elements (warp-independent kernel)
+  int Lp;
   int f_lo;                   // frequency of element 0
   int K;                      // segments per series (E rows per series)
   int seg_begin, seg_end;     // segment range reduced by this launch
   const Task* tasks;
   int ntasks;
   int nctas;                  // CTAs per series splitting the work (<= work units)
+  const Region* regions;      // warp-independent kernel: flat region list
+  int nregions;
+  int64_t nwarps;             // warps splitting the region x segment work (<= units)
   const int32_t* line_cmax;
   const int64_t* line_start;
   int lo;
@@ -80,17 +85,26 @@ struct TripleArgs {
   int accumulate;             // add into the partial slots (chunked launches after the first)
 };
 
-constexpr int kSegsPerSlot = 4;   // segments per TMA box / ring slot
+#ifndef HOS_K2_SEGS
+#define HOS_K2_SEGS 4
+#endif
+constexpr int kSegsPerSlot = HOS_K2_SEGS;  // segments per TMA box / ring slot
+
+constexpr int kTripleWarps = 4;   // warps per CTA of the triple-product kernels
 
 // Where the partial slots of a K2 launch are (for the K4a / reduce readers).
 struct SlotInfo {
   const int32_t* line_region0;  // nullptr: plain buffer with `nparts` parts
-  const int32_t* region_task;
+  const int32_t* region_task;   // TMA kernel: slots are per task; nullptr: per region (warp kernel)
   int ntasks, nseg, nctas;
+  int nregions;
+  int64_t nwarps;
 };
 
 // occupancy (CTAs / SM) of the triple-product kernel
 int triple_occupancy(int precision);
+// 1: the warp-independent cp.async kernel (default), 0: the CTA-shared TMA kernel
+int triple_warp_kernel();
 
 cudaError_t launch_prep(const void* x, int x_dtype, int64_t x_stride, int m, int seg_begin, int nseg,
                         int batch, int taper, const double* taper_tab, int precision, void* seg_out,
