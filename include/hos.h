@@ -168,12 +168,15 @@ int hos_peak_fp32(double* tflops, double* sm_mhz, void* stream);
  * hos_estimate* call on this plan when timing was enabled (events recorded on
  * the launching stream). */
 int hos_plan_set_timing(hos_plan* plan, int enable);
-/* Diagnostics: K2 CTAs per series, and an optional device buffer of
- * 8 x nctas x batch uint64 that K2 fills per CTA with {start, first-data,
- * end (globaltimer ns), smid, warp-0 wait cycles, slots, warp-3 wait
- * cycles, 0}; NULL disables. */
+/* Diagnostics: K2 CTAs per series (4 warps each). */
 int hos_plan_nctas(const hos_plan* plan);
-int hos_plan_set_trace(hos_plan* plan, void* trace_dev);
+/* Diagnostics: mean per-launch device time (ms) of each stage {prep, fft,
+ * extend, triple, scan, box}, each launched `reps` times back to back between
+ * two events on `stream` after one full estimate of x_dev (same arguments as
+ * hos_estimate).  Resolves sub-microsecond changes that single event pairs
+ * (~1 us granularity) cannot. */
+int hos_plan_time_stages(hos_plan* plan, const void* x_dev, int x_dtype, int64_t x_stride, void* out_dev, int reps,
+                         double* ms6, void* stream);
 int hos_plan_kernel_ms(const hos_plan* plan, double* triple_ms, double* total_ms);
 /* Per-stage durations (ms) of the last timed call: prep, FFT, extend,
  * triple product, line scan, box (6 values; the triple product includes

@@ -57,9 +57,9 @@ EXPORTED_SYMBOLS = {
     "hos_peak_fp32": (_i, [_p, _p, _p]),
     "hos_plan_set_timing": (_i, [_p, _i]),
     "hos_plan_nctas": (_i, [_p]),
-    "hos_plan_set_trace": (_i, [_p, _p]),
     "hos_plan_kernel_ms": (_i, [_p, _p, _p]),
     "hos_plan_stage_ms": (_i, [_p, _p]),
+    "hos_plan_time_stages": (_i, [_p, _p, _i, _i64, _p, _i, _p, _p]),
 }
 
 _lib = None
@@ -260,6 +260,20 @@ class Plan:
         out = (ctypes.c_double * 6)()
         raise_for(lib().hos_plan_stage_ms(self.handle, out))
         return dict(zip(("prep", "fft", "extend", "triple", "scan", "box"), list(out)))
+
+    def time_stages(self, x, reps=20, out=None):
+        """Mean per-launch device ms of each stage over `reps` back-to-back
+        launches (after one full estimate of x; x as in estimate())."""
+        torch = _torch()
+        if out is None:
+            out = self.empty_out()
+        n = x.shape[-1]
+        stride = x.stride(0) if x.dim() == 2 else n
+        dt = HOS_F32 if x.dtype == torch.float32 else HOS_F64
+        res = (ctypes.c_double * 6)()
+        raise_for(lib().hos_plan_time_stages(self.handle, ctypes.c_void_p(x.data_ptr()), dt, stride,
+                                             ctypes.c_void_p(out.data_ptr()), reps, res, self._stream()))
+        return dict(zip(("prep", "fft", "extend", "triple", "scan", "box"), list(res)))
 
     def kernel_ms(self):
         t, tot = ctypes.c_double(), ctypes.c_double()

@@ -1,7 +1,5 @@
 // C-ABI of libhos_b200 (include/hos.h): plan lifetime, orchestration of
 // K0 -> cuFFT -> K1 -> K2 -> K4a -> K4b on one stream, error mapping.
-#include <cuda.h>
-#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <cufft.h>
 
@@ -53,13 +51,10 @@ struct hos_plan {
   int occupancy = 1;  // K2 CTAs per SM
   int sms = 148;
   int hstride = 0;   // complex elements per half-spectrum row
-  int L = 0, Lp = 0; // extended-spectrum length / pitch (16-byte elements)
+  int L = 0, Lp = 0; // extended-spectrum length / pitch (complex elements)
   // device tables
-  hos::Task* d_tasks = nullptr;
   hos::Region* d_regions = nullptr;
   int32_t* d_line_region0 = nullptr;
-  int32_t* d_region_task = nullptr;
-  CUtensorMap map_rows, map_cols[3], map_g[3], map_plane;
   int32_t* d_line_cmax = nullptr;
   int64_t* d_line_start = nullptr;
   int64_t* d_row_off = nullptr;
@@ -71,13 +66,12 @@ struct hos_plan {
   // work buffers
   void* d_seg = nullptr;   // batch*k*m real
   void* d_half = nullptr;  // batch*k*hstride complex
-  void* d_E = nullptr;     // batch*k*Lp 16-byte elements
+  void* d_E = nullptr;     // batch*k*Lp complex elements
   void* d_part = nullptr;  // batch*maxslots*ncells complex
   double* d_S = nullptr;   // batch*ncells double2
   void* d_xin = nullptr;   // host path staging (batch*k*m*8 bytes)
   void* d_out = nullptr;   // host path staging
   size_t bytes = 0;
-  unsigned long long* trace = nullptr;  // optional K2 per-CTA trace (device, 8 x nctas x batch)
   std::map<int, cufftHandle> ffts;  // rows -> plan
   // CUDA graphs of the whole stream-ordered pipeline, one per buffer binding
   struct GraphKey {
@@ -162,9 +156,7 @@ int check_plan(const hos_plan* p) {
 // CTAs splitting a launch over nseg segments of `batch` series: one wave of
 // SMs x occupancy CTAs in total, at least 16 work units per CTA (and never
 // more CTAs than units, so every CTA's range is non-empty).
-int64_t work_items(const hos_plan* p) {
-  return hos::triple_warp_kernel() ? (int64_t)p->geo.regions.size() : (int64_t)p->geo.tasks.size();
-}
+int64_t work_items(const hos_plan* p) { return (int64_t)p->geo.regions.size(); }
 
 int nctas_for(const hos_plan* p, int nseg, int batch) {
   const int64_t work = work_items(p) * nseg;
@@ -179,8 +171,7 @@ int nctas_for(const hos_plan* p, int nseg, int batch) {
   return (int)std::max<int64_t>(1, n);
 }
 
-// partial slots the worst task needs (same arithmetic as the kernels)
-// warps splitting the warp kernel's work for an n-CTA launch (never more than units)
+// warps splitting K2's work for an n-CTA launch (never more than units)
 int64_t nwarps_for(const hos_plan* p, int nseg, int n) {
   return std::max<int64_t>(1, std::min<int64_t>((int64_t)n * hos::kTripleWarps, work_items(p) * nseg));
 }
@@ -188,47 +179,35 @@ int64_t nwarps_for(const hos_plan* p, int nseg, int n) {
 int slots_needed(const hos_plan* p, int nseg, int n) {
   const int64_t T = work_items(p), W = T * nseg;
   if (W <= 0) return 1;
-  const int64_t parts = hos::triple_warp_kernel() ? nwarps_for(p, nseg, n) : n;
-  auto cta = [&](int64_t u) { return ((u + 1) * parts - 1) / W; };
+  // partial slots the worst region needs (same arithmetic as the kernel)
+  const int64_t parts = nwarps_for(p, nseg, n);
+  auto warp = [&](int64_t u) { return ((u + 1) * parts - 1) / W; };
   int best = 1;
-  for (int64_t t = 0; t < T; t++) best = std::max(best, (int)(cta((t + 1) * nseg - 1) - cta(t * nseg) + 1));
+  for (int64_t t = 0; t < T; t++) best = std::max(best, (int)(warp((t + 1) * nseg - 1) - warp(t * nseg) + 1));
   return best;
 }
 
 hos::SlotInfo slot_info(const hos_plan* p, int nseg, int n) {
   hos::SlotInfo si{};
   si.line_region0 = p->d_line_region0;
-  si.region_task = p->d_region_task;
-  si.ntasks = (int)p->geo.tasks.size();
   si.nseg = nseg;
-  si.nctas = n;
   si.nregions = (int)p->geo.regions.size();
   si.nwarps = nwarps_for(p, nseg, n);
-  if (hos::triple_warp_kernel()) si.region_task = nullptr;
   return si;
 }
 
 hos::TripleArgs triple_args(const hos_plan* p, int seg_begin, int seg_end, int n, int batch) {
   hos::TripleArgs x;
   std::memset(&x, 0, sizeof(x));
-  x.map_rows = p->map_rows;
-  for (int k = 0; k < 3; k++) {
-    x.map_cols[k] = p->map_cols[k];
-    x.map_g[k] = p->map_g[k];
-  }
-  x.map_plane = p->map_plane;
   x.f_lo = p->geo.f_lo;
   x.K = p->k;
   x.seg_begin = seg_begin;
   x.seg_end = seg_end;
-  x.tasks = p->d_tasks;
-  x.ntasks = (int)p->geo.tasks.size();
   x.E = p->d_E;
   x.Lp = p->Lp;
   x.regions = p->d_regions;
   x.nregions = (int)p->geo.regions.size();
   x.nwarps = nwarps_for(p, seg_end - seg_begin, n);
-  x.nctas = n;
   x.line_cmax = p->d_line_cmax;
   x.line_start = p->d_line_start;
   x.lo = p->geo.win.lo;
@@ -238,41 +217,8 @@ hos::TripleArgs triple_args(const hos_plan* p, int seg_begin, int seg_end, int n
   x.order = p->order;
   x.conj = p->conj;
   x.batch = batch;
-  x.trace = p->trace;
   x.accumulate = 0;
   return x;
-}
-
-// 2-D tensor maps over E viewed as [rows][2 Lp x 8 bytes]; box = {2 x width,
-// kSegsPerSlot}; the innermost box row is one contiguous run of the segment's
-// spectrum (<= 256 x 8 bytes), boxes past the last row are zero-filled.
-int make_maps(hos_plan* p) {
-  static PFN_cuTensorMapEncodeTiled encode = nullptr;
-  if (!encode) {
-    void* fn = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn ||
-        q != cudaDriverEntryPointSuccess)
-      return fail(HOS_ECUDA, "cuTensorMapEncodeTiled is unavailable from the CUDA driver");
-    encode = (PFN_cuTensorMapEncodeTiled)fn;
-  }
-  const cuuint64_t rows = (cuuint64_t)p->batch * p->k;
-  const cuuint64_t dims[2] = {(cuuint64_t)p->Lp * 2, rows};
-  const cuuint64_t strides[1] = {(cuuint64_t)p->Lp * 16};
-  const cuuint32_t estr[2] = {1, 1};
-  struct {
-    CUtensorMap* m;
-    cuuint32_t w;
-  } maps[8] = {{&p->map_rows, 32},  {&p->map_plane, 1}, {&p->map_cols[0], 32}, {&p->map_cols[1], 64},
-               {&p->map_cols[2], 96}, {&p->map_g[0], 63}, {&p->map_g[1], 95},    {&p->map_g[2], 127}};
-  for (auto& mm : maps) {
-    const cuuint32_t box[2] = {2 * mm.w, (cuuint32_t)hos::kSegsPerSlot};
-    CUresult r = encode(mm.m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, p->d_E, dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return fail(HOS_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
-  }
-  return HOS_OK;
 }
 
 // K2 + K4a + K4b over the extended spectra already in p->d_E.
@@ -471,7 +417,10 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
   const hos::Geometry& g = p->geo;
   p->hstride = m / 2 + 1;
   p->L = g.f_hi - g.f_lo + 1;
-  p->Lp = (p->L + 1) & ~1;
+  // +4 elements: fp32 operands are staged from the 16-byte-aligned element at
+  // or below their start, in whole 16-byte chunks (K2), so a copy may read up
+  // to 3 elements past the last frequency; even pitch keeps rows 16-byte aligned
+  p->Lp = (p->L + 4 + 1) & ~1;
   cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, device);
   p->occupancy = hos::triple_occupancy(precision);
   p->nctas = nctas_for(p, k, batch);
@@ -490,10 +439,8 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
   }
 
   std::vector<int32_t> cmax(g.line_cmax.begin(), g.line_cmax.end());
-  if ((rc = upload(p, &p->d_tasks, g.tasks))) return bail(rc);
   if ((rc = upload(p, &p->d_regions, g.regions))) return bail(rc);
   if ((rc = upload(p, &p->d_line_region0, g.line_region0))) return bail(rc);
-  if ((rc = upload(p, &p->d_region_task, g.region_task))) return bail(rc);
   if ((rc = upload(p, &p->d_line_cmax, cmax))) return bail(rc);
   if ((rc = upload(p, &p->d_line_start, g.line_start))) return bail(rc);
   if ((rc = upload(p, &p->d_row_off, g.row_off))) return bail(rc);
@@ -511,7 +458,9 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
   const size_t rows = (size_t)batch * k;
   if ((rc = alloc(p, &p->d_seg, rows * m * rsize(precision)))) return bail(rc);
   if ((rc = alloc(p, &p->d_half, rows * p->hstride * csize(precision)))) return bail(rc);
-  if ((rc = alloc(p, &p->d_E, rows * p->Lp * 16))) return bail(rc);
+  if ((rc = alloc(p, &p->d_E, rows * p->Lp * csize(precision)))) return bail(rc);
+  if (cudaMemset(p->d_E, 0, rows * p->Lp * csize(precision)) != cudaSuccess)  // pad elements stay defined
+    return bail(fail(HOS_ECUDA, "cudaMemset failed"));
   if ((rc = alloc(p, &p->d_part, (size_t)batch * p->maxslots * g.ncells * csize(precision)))) return bail(rc);
   if ((rc = alloc(p, (void**)&p->d_S, (size_t)batch * g.ncells * 16))) return bail(rc);
   if ((rc = alloc(p, &p->d_xin, rows * m * 8))) return bail(rc);
@@ -519,7 +468,6 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
   cufftHandle h;
   if ((rc = get_fft(p, (int)rows, &h))) return bail(rc);
   if (p->e2e_chunks > 1 && (rc = get_fft(p, k / p->e2e_chunks, &h))) return bail(rc);  // no allocation in captures
-  if ((rc = make_maps(p))) return bail(rc);
   for (auto& e : p->ev)
     if (cudaEventCreate(&e) != cudaSuccess) return bail(fail(HOS_ECUDA, "cudaEventCreate failed"));
   if (cudaStreamCreateWithFlags(&p->cap, cudaStreamNonBlocking) != cudaSuccess ||
@@ -541,7 +489,7 @@ void hos_plan_destroy(hos_plan* p) {
   if (p->cap2) cudaStreamDestroy(p->cap2);
   for (auto e : p->chunk_ev) cudaEventDestroy(e);
   for (auto& kv : p->ffts) cufftDestroy(kv.second);
-  void* bufs[] = {p->d_tasks, p->d_regions, p->d_line_region0, p->d_region_task, p->d_line_cmax, p->d_line_start, p->d_row_off, p->d_pair_k1, p->d_pair_k2,
+  void* bufs[] = {p->d_regions, p->d_line_region0, p->d_line_cmax, p->d_line_start, p->d_row_off, p->d_pair_k1, p->d_pair_k2,
                   p->d_pair_base, p->d_line_of_ab, p->d_taper, p->d_seg, p->d_half, p->d_E, p->d_part,
                   p->d_S, p->d_xin, p->d_out};
   for (void* b : bufs)
@@ -576,7 +524,7 @@ int hos_estimate(hos_plan* p, const void* x_dev, int x_dtype, int64_t x_stride, 
     return fail(HOS_EPARAM, "series stride " + std::to_string(x_stride) + " shorter than k*m = " +
                                 std::to_string((int64_t)p->k * p->m));
   cudaStream_t st = (cudaStream_t)stream;
-  if (p->timing || p->trace || !p->use_graphs) {
+  if (p->timing || !p->use_graphs) {
     if (p->timing) CUDA_TRY(cudaEventRecord(p->ev[0], st));
     if ((rc = run_front(p, x_dev, x_dtype, x_stride, st))) return rc;
     return run_back(p, out_dev, st);
@@ -603,7 +551,7 @@ int hos_estimate_from_spectra(hos_plan* p, const void* spec_dev, int spec_dtype,
       for (int i = 1; i <= 3; i++) CUDA_TRY(cudaEventRecord(p->ev[i], s));
     return run_back(p, out_dev, s);
   };
-  if (p->timing || p->trace || !p->use_graphs) return body(st);
+  if (p->timing || !p->use_graphs) return body(st);
   const hos_plan::GraphKey key{1, spec_dev, spec_dtype, 0, out_dev};
   return run_graph(p, key, st, body);
 }
@@ -713,7 +661,7 @@ int hos_estimate_host(hos_plan* p, const void* x_host, int x_dtype, int64_t x_st
       mark(5 + 4 * j, s);
       void* seg = (char*)p->d_seg + (size_t)sb * p->m * rs;
       void* half = (char*)p->d_half + (size_t)sb * p->hstride * cs;
-      void* E = (char*)p->d_E + (size_t)sb * p->Lp * 16;
+      void* E = (char*)p->d_E + (size_t)sb * p->Lp * csize(p->precision);
       CUDA_TRY(hos::launch_prep(p->d_xin, x_dtype, 0, p->m, sb, kc, 1, p->taper, p->d_taper, p->precision, seg, s));
       int r = run_fft(p, kc, seg, half, s);
       if (r) return r;
@@ -755,7 +703,7 @@ int hos_estimate_host(hos_plan* p, const void* x_host, int x_dtype, int64_t x_st
     return HOS_OK;
   }
   for (auto e : dev) cudaEventDestroy(e);
-  if (pinned && p->use_graphs && !p->timing && !p->trace) {
+  if (pinned && p->use_graphs && !p->timing) {
     const hos_plan::GraphKey key{2, x_host, x_dtype, x_stride, out_host};
     if (p->e2e_chunks > 1 && p->batch == 1) {
       if ((rc = run_graph(p, key, st, chunked))) return rc;
@@ -790,7 +738,7 @@ int hos_partial_raw(hos_plan* p, const void* x_dev, int x_dtype, int seg_begin, 
   const size_t rs = rsize(p->precision);
   void* seg = (char*)p->d_seg + (size_t)seg_begin * p->m * rs;
   void* half = (char*)p->d_half + (size_t)seg_begin * p->hstride * csize(p->precision);
-  void* E = (char*)p->d_E + (size_t)seg_begin * p->Lp * 16;
+  void* E = (char*)p->d_E + (size_t)seg_begin * p->Lp * csize(p->precision);
   CUDA_TRY(hos::launch_prep(x_dev, x_dtype, 0, p->m, seg_begin, nseg, 1, p->taper, p->d_taper, p->precision, seg, st));
   if ((rc = run_fft(p, nseg, seg, half, st))) return rc;
   CUDA_TRY(hos::launch_extend_half(half, p->m, p->hstride, nseg, nullptr, p->geo.f_lo, p->L, p->Lp, p->precision, E,
@@ -926,13 +874,6 @@ int hos_peak_fp32(double* tflops, double* sm_mhz, void* stream) {
   return HOS_OK;
 }
 
-int hos_plan_set_trace(hos_plan* p, void* trace_dev) {
-  int rc = check_plan(p);
-  if (rc) return rc;
-  p->trace = (unsigned long long*)trace_dev;
-  return HOS_OK;
-}
-
 int hos_plan_nctas(const hos_plan* p) { return p ? p->nctas : -1; }
 
 int hos_plan_set_timing(hos_plan* p, int enable) {
@@ -954,6 +895,63 @@ int hos_plan_kernel_ms(const hos_plan* p, double* triple_ms, double* total_ms) {
   if (triple_ms) *triple_ms = t1;
   if (total_ms) *total_ms = t2;
   return HOS_OK;
+}
+
+int hos_plan_time_stages(hos_plan* p, const void* x_dev, int x_dtype, int64_t x_stride, void* out_dev, int reps,
+                         double* ms6, void* stream) {
+  int rc = check_plan(p);
+  if (rc) return rc;
+  if ((rc = check_dtype_x(x_dtype))) return rc;
+  if (!ms6 || reps < 1) return fail(HOS_EPARAM, "null output or reps < 1");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int saved = p->timing;
+  p->timing = 0;
+  rc = hos_estimate(p, x_dev, x_dtype, x_stride, out_dev, stream);  // fills every intermediate buffer
+  p->timing = saved;
+  if (rc) return rc;
+  const int rows = p->batch * p->k;
+  const hos::TripleArgs ta = triple_args(p, 0, p->k, p->nctas, p->batch);
+  cudaEvent_t e0, e1;
+  CUDA_TRY(cudaEventCreate(&e0));
+  CUDA_TRY(cudaEventCreate(&e1));
+  for (int s = 0; s < 6 && !rc; s++) {
+    CUDA_TRY(cudaEventRecord(e0, st));
+    for (int r = 0; r < reps && !rc; r++) {
+      cudaError_t e = cudaSuccess;
+      switch (s) {
+        case 0:
+          e = hos::launch_prep(x_dev, x_dtype, x_stride, p->m, 0, p->k, p->batch, p->taper, p->d_taper, p->precision,
+                               p->d_seg, st);
+          break;
+        case 1:
+          rc = run_fft(p, rows, p->d_seg, p->d_half, st);
+          break;
+        case 2:
+          e = hos::launch_extend_half(p->d_half, p->m, p->hstride, rows, nullptr, p->geo.f_lo, p->L, p->Lp,
+                                      p->precision, p->d_E, st);
+          break;
+        case 3:
+          e = hos::launch_triple(ta, p->precision, st);
+          break;
+        case 4:
+          e = hos::launch_line_scan(p->d_part, p->maxslots, p->geo.ncells, slot_info(p, p->k, p->nctas),
+                                    p->precision, p->d_line_start, 0, p->geo.nlines, p->geo.ncells, p->batch, p->d_S,
+                                    st);
+          break;
+        default:
+          rc = run_box(p, out_dev, st);
+      }
+      if (e != cudaSuccess) rc = fail(HOS_ECUDA, std::string("CUDA error: ") + cudaGetErrorString(e));
+    }
+    CUDA_TRY(cudaEventRecord(e1, st));
+    CUDA_TRY(cudaEventSynchronize(e1));
+    float ms = 0;
+    CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+    ms6[s] = ms / reps;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return rc;
 }
 
 int hos_plan_stage_ms(const hos_plan* p, double* ms6) {

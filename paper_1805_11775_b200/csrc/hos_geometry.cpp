@@ -1,4 +1,4 @@
-// Geometry of P, D_h and the K2 task list (see hos_geometry.h).
+// Geometry of P, D_h and the K2 regions (see hos_geometry.h).
 #include "hos_geometry.h"
 
 #include <algorithm>
@@ -67,35 +67,6 @@ void add_band_regions(std::vector<RegionRec>& regs, std::vector<int32_t>& line_r
   for (int r = 0; r < nr; r++) regs.push_back({line0, nrows, row_freq0, plane_freq, lo + r * kRegionCols});
 }
 
-// group regions 4 at a time, at most 2 bands per task
-void group_tasks(const std::vector<RegionRec>& regs, std::vector<Task>& tasks, std::vector<int32_t>& region_task,
-                 int64_t& issued) {
-  region_task.assign(regs.size(), 0);
-  size_t i = 0;
-  while (i < regs.size()) {
-    Task t{};
-    while (i < regs.size() && t.nreg < kTaskRegions) {
-      const RegionRec& r = regs[i];
-      const bool same = t.nsub > 0 && t.sub[t.nsub - 1].line0 == r.line0 && t.sub[t.nsub - 1].k < kSubRegions;
-      if (!same) {
-        if (t.nsub == 2) break;
-        SubBand& sb = t.sub[t.nsub++];
-        sb.line0 = r.line0;
-        sb.nrows = r.nrows;
-        sb.row_freq0 = r.row_freq0;
-        sb.plane_freq = r.plane_freq;
-        sb.col0 = r.col0;
-        sb.k = 0;
-      }
-      t.sub[t.nsub - 1].k++;
-      region_task[i] = (int32_t)tasks.size();
-      t.nreg++;
-      i++;
-    }
-    tasks.push_back(t);
-    issued += int64_t(kTaskRegions) * kBandRows * kRegionCols;
-  }
-}
 }  // namespace
 
 std::string Geometry::build(int order_, int m_, int m3_) {
@@ -151,9 +122,7 @@ std::string Geometry::build(int order_, int m_, int m3_) {
   }
 
   line_a.clear(); line_b.clear(); line_cmax.clear(); line_start.clear();
-  tasks.clear();
   line_region0.clear();
-  region_task.clear();
   issued_cells = 0;
   std::vector<RegionRec> regs;
   if (order == 3) {
@@ -211,8 +180,9 @@ std::string Geometry::build(int order_, int m_, int m3_) {
     ncells = line_start.back();
   }
 
-  group_tasks(regs, tasks, region_task, issued_cells);
   regions.clear();
+  f_lo = order == 3 ? 2 * lo : 3 * lo;
+  f_hi = 0;
   for (const RegionRec& r : regs) {
     Region g{};
     g.line0 = r.line0;
@@ -221,24 +191,12 @@ std::string Geometry::build(int order_, int m_, int m3_) {
     g.plane_freq = r.plane_freq;
     g.col0 = r.col0;
     regions.push_back(g);
+    // frequencies the region's staged operands cover
+    const int rmax = r.row_freq0 + kBandRows - 1, cmax = r.col0 + kRegionCols - 1;
+    f_hi = std::max({f_hi, r.plane_freq + rmax + cmax, rmax, cmax, r.plane_freq});
+    f_lo = std::min({f_lo, r.plane_freq + r.row_freq0 + r.col0, r.row_freq0, r.col0, r.plane_freq});
   }
   issued_cells = (int64_t)regions.size() * kBandRows * kRegionCols;
-
-  // ---- frequencies touched by the TMA boxes of the tasks (extended spectrum range)
-  f_lo = order == 3 ? 2 * lo : 3 * lo;
-  f_hi = 0;
-  for (const Task& t : tasks) {
-    for (int s = 0; s < t.nsub; s++) {
-      const SubBand& b = t.sub[s];
-      const int rmax = b.row_freq0 + kBandRows - 1;
-      const int cmax = b.col0 + b.k * kRegionCols - 1;
-      f_hi = std::max(f_hi, b.plane_freq + rmax + cmax);
-      f_hi = std::max(f_hi, rmax);
-      f_hi = std::max(f_hi, cmax);
-      f_hi = std::max(f_hi, b.plane_freq);
-      f_lo = std::min(f_lo, b.plane_freq + b.row_freq0 + b.col0);
-    }
-  }
   return "";
 }
 

@@ -1,7 +1,7 @@
 // Host-side geometry of the direct-method estimator: the principal domain
 // P (hospectra/spectra.py:133-168), its window dilation D_h (the raw cells
 // the smoothing reads, SURVEY §8 notation) laid out as CSR "lines", and
-// the triple-product task list that tiles D_h for the K2 kernel.
+// the 32 x 32 regions that tile D_h for the K2 kernel.
 #pragma once
 #include <cstdint>
 #include <string>
@@ -42,26 +42,10 @@ int64_t domain_size(int order, int m);
 void domain_rows(int order, int m, int64_t start, int64_t stop, int32_t* out);
 
 // K2 work decomposition.  D_h is cut into regions of up to kBandRows
-// consecutive lines (a "band" of one plane) x kRegionCols columns; the
-// regions, listed band after band, are grouped 4 at a time into tasks (one
-// warp per region).  A task has up to two "sub-bands" A and B of at most 3
-// consecutive regions of one band each (possibly two different bands); a
-// third sub-band closes the task early.  A CTA stages each sub-band's row,
-// column and last factors once per segment and its 4 warps share them.
+// consecutive lines (a "band" of one plane) x kRegionCols columns; a warp
+// owns one region at a time (K2 splits regions x segments across warps).
 constexpr int kBandRows = 32;    // lines per band (4 lane rows x 8 rows)
 constexpr int kRegionCols = 32;  // columns per region (8 lanes x 4)
-constexpr int kTaskRegions = 4;  // regions (warps) per task
-constexpr int kSubRegions = 3;   // regions per sub-band: its G box (31 + 32k quads) must fit one
-                                 // 256 x 8-byte TMA box row
-
-struct SubBand {
-  int32_t line0;      // first line of the band
-  int32_t nrows;      // lines in the band (<= kBandRows)
-  int32_t row_freq0;  // frequency of line0's row factor (order 3: a, order 4: b)
-  int32_t plane_freq; // order 4: a of the plane; order 3: 0
-  int32_t col0;       // first column of the task's first region in this band
-  int32_t k;          // regions of the task in this band
-};
 
 struct Region {
   int32_t line0;      // first line of the band
@@ -70,13 +54,6 @@ struct Region {
   int32_t plane_freq; // order 4: a of the plane; order 3: 0
   int32_t col0;       // first column of the region
   int32_t pad[3];
-};
-
-struct Task {
-  int32_t nreg;       // regions (warps with work), 1..kTaskRegions
-  int32_t nsub;       // sub-bands, 1..2
-  SubBand sub[2];
-  int32_t pad[2];
 };
 
 struct Geometry {
@@ -99,14 +76,12 @@ struct Geometry {
   int a_count = 0, b_count = 0;
   std::vector<int32_t> line_of_ab;
   // order 3: line index = a - lo; lines of output row k1 start at k1
-  // frequencies touched by any task (inclusive), for the extended spectrum
+  // frequencies any region reads (inclusive), for the extended spectrum
   int f_lo = 0, f_hi = 0;
-  // K2 tasks
-  std::vector<Task> tasks;
-  std::vector<int32_t> line_region0;  // per line: index of the region holding its first column
-  std::vector<int32_t> region_task;   // per region: its task
+  // K2 regions
   std::vector<Region> regions;        // flat region list (band after band)
-  int64_t issued_cells = 0;           // cells computed by the tasks (incl. idle warps)
+  std::vector<int32_t> line_region0;  // per line: index of the region holding its first column
+  int64_t issued_cells = 0;           // cells computed by K2 (regions x 32 x 32)
 
   std::string build(int order, int m, int m3);  // returns "" or an error message
 };

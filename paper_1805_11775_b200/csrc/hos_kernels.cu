@@ -74,7 +74,7 @@ cudaError_t launch_prep(const void* x, int x_dtype, int64_t x_stride, int m, int
 // ===========================================================================
 // K1: extended spectrum over frequencies [f_lo, f_lo+L).  Real input makes
 // F(M-f) = conj F(f), so the R2C half spectrum suffices (SURVEY §7 hard
-// part 3).  fp32 rows hold quads (re, im, -im, re); fp64 rows double2.
+// part 3).  Rows hold float2 (fp32) or double2 (fp64) elements.
 
 __device__ __forceinline__ int fmod_pos(int f, int m) {
   int r = f % m;
@@ -91,13 +91,12 @@ __device__ __forceinline__ C half_lookup(const C* __restrict__ H, int m, int f) 
 }
 
 __global__ void k_extend_half_f32(const float2* __restrict__ H, int m, int hstride, int64_t n, int f_lo, int L,
-                                  int Lp, float4* __restrict__ E) {
+                                  int Lp, float2* __restrict__ E) {
   asm volatile("griddepcontrol.launch_dependents;");  // let K2 stage its setup (it waits for our writes)
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = t / L;
     const int j = (int)(t - r * L);
-    const float2 v = half_lookup(H + r * hstride, m, f_lo + j);
-    E[r * Lp + j] = make_float4(v.x, v.y, -v.y, v.x);
+    E[r * Lp + j] = half_lookup(H + r * hstride, m, f_lo + j);
   }
 }
 __global__ void k_extend_half_f64(const double2* __restrict__ H, int m, int hstride, int64_t n, int f_lo, int L,
@@ -114,23 +113,22 @@ cudaError_t launch_extend_half(const void* H, int m, int hstride, int rows, cons
                                int precision, void* E, cudaStream_t st) {
   const int64_t n = (int64_t)rows * L;
   if (precision == 32)
-    k_extend_half_f32<<<grid_for(n, 256), 256, 0, st>>>((const float2*)H, m, hstride, n, f_lo, L, Lp, (float4*)E);
+    k_extend_half_f32<<<grid_for(n, 256), 256, 0, st>>>((const float2*)H, m, hstride, n, f_lo, L, Lp, (float2*)E);
   else
     k_extend_half_f64<<<grid_for(n, 256), 256, 0, st>>>((const double2*)H, m, hstride, n, f_lo, L, Lp, (double2*)E);
   return cudaGetLastError();
 }
 
 // From caller-supplied full spectra (estimate_from_spectra): no symmetry assumed.
-template <typename Cin, bool QUAD>
+template <typename Cin, bool F32>
 __global__ void k_extend_full(const Cin* __restrict__ S, int m, int64_t n, int f_lo, int L, int Lp, void* E) {
   asm volatile("griddepcontrol.launch_dependents;");
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = t / L;
     const int j = (int)(t - r * L);
     const Cin v = S[r * m + fmod_pos(f_lo + j, m)];
-    if (QUAD) {
-      const float re = (float)v.x, im = (float)v.y;
-      ((float4*)E)[r * Lp + j] = make_float4(re, im, -im, re);
+    if (F32) {
+      ((float2*)E)[r * Lp + j] = make_float2((float)v.x, (float)v.y);
     } else {
       ((double2*)E)[r * Lp + j] = make_double2((double)v.x, (double)v.y);
     }
@@ -171,154 +169,114 @@ cudaError_t launch_expand_full(const void* H, int m, int hstride, int rows, int 
 }
 
 // ===========================================================================
-// K2: triple / quadruple product over D_h.
+// K2: triple / quadruple product over D_h (hospectra/spectra.py:227-263).
 //
-// Work = ntasks x nseg units (a task = 4 regions of 32 x 32 cells, one per
-// warp); the grid's N CTAs (per series) split it into N contiguous, equal
-// ranges, so every CTA does the same work in one wave (N = SMs x occupancy).
-// A CTA walks the tasks its range touches; for each piece (task, segments)
-// every warp accumulates its region in registers and writes ONE partial
-// slot (CTA index - first CTA of the task), fixed by the partition: the fp64
-// combination order in K4a is fixed and results are deterministic.
+// Work = nregions x nseg units (a region is 32 x 32 cells of D_h: 32 lines x
+// 32 columns); the nwarps warps of the launch take equal contiguous unit
+// ranges, so every warp does the same work and warps never wait for each
+// other.  A warp walks its (region, segment) units in order; per unit its 32
+// lanes stage the segment's 32 row factors, 32 column factors, 63 last
+// factors G(row+col[+a]) (and F(a) for order 4) with 16-byte cp.async chunks
+// into a private ring of unit PAIRS: the loads of the next pairs overlap the
+// arithmetic of the current one, and the two units of a pair are computed in
+// one straight-line block so the scheduler overlaps one segment's shared
+// loads with the other's FFMA2 chains.  Each (warp, region) piece writes ONE
+// partial slot (warp index - first warp of the region), fixed by the
+// partition: the fp64 combination order in K4a is fixed and results are
+// deterministic.
 //
-// Staging: a 3-slot ring per CTA; a slot holds kSegsPerSlot = 4 segments of
-// each sub-band's row factors (32), column factors (32k), last factors
-// G(row+col[+a]) (31+32k) and, for order 4, F(a) -- one 3-D tensor TMA copy
-// (cp.async.bulk.tensor + mbarrier complete_tx) per operand and sub-band.
-// The last warp to finish a slot refills it: no CTA-wide barrier in the loop.
-//
-// Lane (ta, tb) of a warp owns rows ta+4i (i<8) and columns tb+8j (j<4) of
-// its region: every quarter-warp shared load reads consecutive 16-byte
-// elements (conflict-free) and a lane needs 8 row + 4 column + 14 G values
-// per segment (cell (i,j) reads G at 4(i+2j)).
-// fp32: 4 FFMA2-class instructions per cell,
-//   p    = fa.re * fb + fa.im * (i fb)            (FMUL2 + FFMA2)
-//   acc += p.re * conj(g) + p.im * (i conj(g))    (2 FFMA2; conj toggled)
-// with every operand form a swizzle of the quad (re, im, -im, re).
+// Lane (ta, tb) owns rows ta+4i (i<8) and columns tb+8j (j<4) of its region:
+// 8 row + 4 column + 14 G values per segment (cell (i,j) reads G at 4(i+2j));
+// every shared load is a broadcast over <= 11 consecutive 8-byte values.
+// fp32 spectra are plain float2 (8 bytes): a 16-byte "quad" layout would
+// double the shared-memory wavefronts, which bound this kernel (ncu r01:
+// LSU data pipe 71% busy at 46% FMA).  The operand forms the complex FFMA2
+// products need are built in registers, once per column / G value:
+//   p    = fa.re * fb + fa.im * (-fb.im, fb.re)           (FMUL2 + FFMA2)
+//   acc += p.re * conj(g) + p.im * (g.im, g.re)           (2 FFMA2, CONJ)
+//   acc += p.re * g       + p.im * (-g.im, g.re)          (2 FFMA2, !CONJ)
 // fp64: same mapping, scalar DFMA on double2 spectra.
-
-#ifndef HOS_K2_SLOTS
-#define HOS_K2_SLOTS 3
-#endif
-#ifndef HOS_K2_MINB
-#define HOS_K2_MINB 3
-#endif
-constexpr int kSlots = HOS_K2_SLOTS;
-// per slot (quads, S = kSegsPerSlot): rows 2 x 32S | cols 4 x 32S | planes 2 x 8 | G S(31+32k_A) (padded) + S(31+32k_B)
-constexpr int kSlotQuads =
-    ((2 * 32 * kSegsPerSlot + 4 * 32 * kSegsPerSlot + 2 * 8 + kSegsPerSlot * (62 + 32 * 4) + 8) + 7) / 8 * 8;
-static_assert(kSlotQuads % 8 == 0, "ring slots must stay 128-byte aligned for TMA");
-constexpr size_t kTripleSmem = 16 * (size_t)kSlots * kSlotQuads + 128;
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-// 2-D tensor copy of box {x: 2*width 8-byte elements, y: kSegsPerSlot rows} at (x0 = 2*elem, y0 = row)
-__device__ __forceinline__ void tma_2d(unsigned dst, const CUtensorMap* map, int elem, int row, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(2 * elem), "r"(row), "r"(smem_u32(bar))
-      : "memory");
-}
-
-// CTA owning work unit u of a W-unit range split into N equal parts.
-__device__ __forceinline__ int64_t cta_of_unit(int64_t u, int64_t W, int N) { return ((u + 1) * (int64_t)N - 1) / W; }
-
-// partial slots of task t for a launch over nseg segments split across N CTAs
-__device__ __forceinline__ int task_slots(int t, int nseg, int64_t W, int N) {
-  return (int)(cta_of_unit((int64_t)(t + 1) * nseg - 1, W, N) - cta_of_unit((int64_t)t * nseg, W, N) + 1);
-}
-
-// shared-memory layout (quad offsets) of sub-band s of a staged task slot:
-// rows 2 x 128 | cols 128 (k_A + k_B) | planes 2 x 8 | G_A 4(31+32k_A) padded | G_B
-struct SubLayout {
-  int rows, cols, g, plane;
-  int cw;  // column elements per segment (32k)
-  int gw;  // G elements per segment (31 + 32k)
-};
-
-__device__ __forceinline__ SubLayout sub_layout(const Task& t, int s) {
-  const int kA = t.sub[0].k, kB = t.nsub > 1 ? t.sub[1].k : 0;
-  constexpr int S = kSegsPerSlot, PB = (S + 7) / 8 * 8;  // plane block, 128 B multiple
-  const int plane0 = 32 * S * t.nsub + 32 * S * (kA + kB);
-  const int g0 = plane0 + PB * t.nsub;
-  SubLayout L;
-  L.rows = s ? 32 * S : 0;
-  L.cols = 32 * S * t.nsub + (s ? 32 * S * kA : 0);
-  L.plane = plane0 + (s ? PB : 0);
-  L.g = s ? g0 + ((S * (31 + 32 * kA) + 7) & ~7) : g0;
-  const int k = s ? kB : kA;
-  L.cw = 32 * k;
-  L.gw = 31 + 32 * k;
-  return L;
-}
 
 template <typename T>
 struct Cplx;
 template <>
 struct Cplx<float> {
-  using Q = float4;   // staged element (quad)
-  using C = float2;   // accumulator / partial
+  using C = float2;  // spectrum element / accumulator / partial
+  static constexpr int kUnitChunks = 68;  // rows 17 | cols 17 | G 32 | plane 1 (+1 pad) 16-byte chunks
 };
 template <>
 struct Cplx<double> {
-  using Q = double2;
   using C = double2;
+  static constexpr int kUnitChunks = 128;  // rows 32 | cols 32 | G 63 | plane 1
 };
 
-// one segment of a lane's 8x4 micro-tile: rows/cols/g point at the segment's staged factors
-template <bool CONJ, bool ORDER4>
-__device__ __forceinline__ void cells_f32(const float4* __restrict__ rows, const float4* __restrict__ cols,
-                                          const float4* __restrict__ gs, const float4* __restrict__ plane, int ta,
-                                          int tb, float2 (&acc)[8][4]) {
-  float2 fa[8];
-  float4 fb[4];
+// chunk offsets of the operands inside a staged unit
+template <typename T>
+struct UnitLayout;
+template <>
+struct UnitLayout<float> {
+  static constexpr int rows = 0, cols = 17, g = 34, plane = 66;
+  static constexpr int row_chunks = 17, col_chunks = 17, g_chunks = 32;
+};
+template <>
+struct UnitLayout<double> {
+  static constexpr int rows = 0, cols = 32, g = 64, plane = 127;
+  static constexpr int row_chunks = 32, col_chunks = 32, g_chunks = 63;
+};
+
+__device__ __forceinline__ float2 neg_swap(float2 v) {  // (-v.im, v.re) = i v
+  return make_float2(__int_as_float(__float_as_int(v.y) ^ 0x80000000), v.x);
+}
+// conj(*p) from its own shared load: the negation happens in place in the
+// loaded register pair, and FFMA2's free operand swap turns (re, -im) into
+// (-im, re) = i * value -- no register copies (ptxas duplicates pairs built
+// with neg_swap on values that stay live).
+__device__ __forceinline__ float2 lds_conj(const float2* p) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];"
+               : "=f"(v.x), "=f"(v.y)
+               : "r"((unsigned)__cvta_generic_to_shared(p)));
+  v.y = -v.y;
+  return v;
+}
+
+// one segment of a lane's 8x4 micro-tile: rows/cols/g point at the segment's
+// staged factors.  Two accumulators per cell, aR += g.re p and aI += g.im p
+// (p = F(row) F(col) [F(a)]): the last factor enters only as broadcast
+// scalars, so no operand form of it has to be built, and the two updates of
+// a cell are independent FFMA2s.  The cell value is aR -+ i aI (CONJ: -).
+template <bool ORDER4>
+__device__ __forceinline__ void cells_f32(const float2* __restrict__ rows, const float2* __restrict__ cols,
+                                          const float2* __restrict__ gs, const float2* __restrict__ plane, int ta,
+                                          int tb, float2 (&aR)[8][4], float2 (&aI)[8][4]) {
+  float2 fa[8], fb[4], fbc[4];
 #pragma unroll
-  for (int i = 0; i < 8; i++) fa[i] = *reinterpret_cast<const float2*>(rows + ta + 4 * i);
+  for (int i = 0; i < 8; i++) fa[i] = rows[ta + 4 * i];
   if (ORDER4) {
-    const float4 pa = *plane;
+    const float2 pa = *plane, pac = lds_conj(plane);
 #pragma unroll
     for (int i = 0; i < 8; i++) {
-      float2 t = fmul2(make_float2(fa[i].x, fa[i].x), make_float2(pa.x, pa.y));
-      fa[i] = ffma2(make_float2(fa[i].y, fa[i].y), make_float2(pa.z, pa.w), t);
+      const float2 t = fmul2(make_float2(fa[i].x, fa[i].x), pa);
+      fa[i] = ffma2(make_float2(fa[i].y, fa[i].y), make_float2(pac.y, pac.x), t);
     }
   }
 #pragma unroll
-  for (int j = 0; j < 4; j++) fb[j] = cols[tb + 8 * j];
-  const float4* gq = gs + ta + tb;
+  for (int j = 0; j < 4; j++) {
+    fb[j] = cols[tb + 8 * j];
+    fbc[j] = lds_conj(cols + tb + 8 * j);
+  }
+  const float2* gq = gs + ta + tb;
 #pragma unroll
   for (int q = 0; q < 14; q++) {
-    const float4 g = gq[4 * q];
+    const float2 g = gq[4 * q];
 #pragma unroll
     for (int j = 0; j < 4; j++) {
       const int i = q - 2 * j;
       if (i < 0 || i > 7) continue;
-      float2 p = fmul2(make_float2(fa[i].x, fa[i].x), make_float2(fb[j].x, fb[j].y));
-      p = ffma2(make_float2(fa[i].y, fa[i].y), make_float2(fb[j].z, fb[j].w), p);
-      if (CONJ) {
-        acc[i][j] = ffma2(make_float2(p.x, p.x), make_float2(g.w, g.z), acc[i][j]);
-        acc[i][j] = ffma2(make_float2(p.y, p.y), make_float2(g.y, g.x), acc[i][j]);
-      } else {
-        acc[i][j] = ffma2(make_float2(p.x, p.x), make_float2(g.x, g.y), acc[i][j]);
-        acc[i][j] = ffma2(make_float2(p.y, p.y), make_float2(g.z, g.w), acc[i][j]);
-      }
+      float2 p = fmul2(make_float2(fa[i].x, fa[i].x), fb[j]);
+      p = ffma2(make_float2(fa[i].y, fa[i].y), make_float2(fbc[j].y, fbc[j].x), p);
+      aR[i][j] = ffma2(make_float2(g.x, g.x), p, aR[i][j]);
+      aI[i][j] = ffma2(make_float2(g.y, g.y), p, aI[i][j]);
     }
   }
 }
@@ -362,305 +320,14 @@ __device__ __forceinline__ void cells_f64(const double2* __restrict__ rows, cons
   }
 }
 
-constexpr int kMaxPieces = 8;
-
-struct PieceRec {
-  int task;      // task index
-  int first;     // first absolute segment
-  int nseg;      // segments
-  int slot0;     // first ring slot of the piece (counted across rounds)
-  int nsl;       // ring slots of the piece
-  int pslot;     // partial slot: CTA - first CTA of the task
-};
-
-template <typename T, bool CONJ, bool ORDER4>
-__global__ void __launch_bounds__(128, sizeof(T) == 4 ? HOS_K2_MINB : 2) k_triple(const __grid_constant__ TripleArgs a) {
-  using Q = typename Cplx<T>::Q;
-  using C = typename Cplx<T>::C;
-  extern __shared__ unsigned char smraw[];
-  __shared__ __align__(8) uint64_t full[kSlots];
-  __shared__ int cnt[kSlots];
-  __shared__ PieceRec pcs[kMaxPieces];
-  __shared__ Task tcache[kMaxPieces];
-  __shared__ int s_np, s_end, s_tnext;
-  const unsigned raw0 = smem_u32(smraw);
-  const unsigned base = (raw0 + 127u) & ~127u;
-  const Q* ring = reinterpret_cast<const Q*>(smraw + (base - raw0));
-  const int c = blockIdx.x;
-  const int series = blockIdx.y;
-  const int N = a.nctas;
-  const int nseg_all = a.seg_end - a.seg_begin;
-  const int64_t W = (int64_t)a.ntasks * nseg_all;
-  const int64_t x0 = (int64_t)c * W / N, x1 = (int64_t)(c + 1) * W / N;
-  C* Pbase = (C*)a.part + (int64_t)series * a.maxslots * a.ncells;
-  const int row0 = series * a.K;  // tensor row of segment 0 of this series
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ta = lane >> 3, tb = lane & 7;
-  unsigned long long* tr = a.trace ? a.trace + 8 * ((int64_t)series * N + c) : nullptr;
-  long long wait_cyc = 0, slots_seen = 0;
-  if (tr && threadIdx.x == 0) {
-    unsigned long long t0, sm;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    asm volatile("{ .reg .u32 r; mov.u32 r, %%smid; cvt.u64.u32 %0, r; }" : "=l"(sm));
-    tr[0] = t0;
-    tr[3] = sm;
-  }
-
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int b = 0; b < kSlots; b++) {
-      mbar_init(&full[b], 1);
-      cnt[b] = 0;
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    s_tnext = (int)(x0 / nseg_all);
-    s_end = 0;
-  }
-  if (warp == 1 && lane < 8) {  // pull the tensor-map descriptors in while the piece list is built
-    const CUtensorMap* m = lane == 0 ? &a.map_rows : lane == 1 ? &a.map_plane : lane < 5 ? &a.map_cols[lane - 2]
-                                                                                        : &a.map_g[lane - 5];
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
-  }
-  __syncthreads();
-
-  // rounds of up to kMaxPieces pieces (one round unless the range is tiny and spans many tasks)
-  while (true) {
-    if (warp == 0) {  // lane l builds piece l of this round (the 64-bit divisions run in parallel)
-      const int t = s_tnext + lane;
-      const bool valid = lane < kMaxPieces && t < a.ntasks && (int64_t)t * nseg_all < x1 && x0 < x1;
-      PieceRec r{};
-      if (valid) {
-        const int64_t P0 = (int64_t)t * nseg_all;
-        const int64_t u0 = min(max(x0 - P0, (int64_t)0), (int64_t)nseg_all);
-        const int64_t u1 = min(max(x1 - P0, (int64_t)0), (int64_t)nseg_all);
-        r.task = t;
-        r.first = a.seg_begin + (int)u0;
-        r.nseg = (int)(u1 - u0);
-        r.nsl = (r.nseg + kSegsPerSlot - 1) / kSegsPerSlot;
-        r.pslot = (int)(c - cta_of_unit(P0, W, N));
-      }
-      int incl = r.nsl;  // inclusive prefix of slots over the lanes
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-      }
-      const unsigned vmask = __ballot_sync(0xffffffffu, valid);
-      const int np = __popc(vmask);  // valid lanes are a prefix
-      const int base = s_end;
-      __syncwarp();
-      if (valid) {
-        r.slot0 = base + incl - r.nsl;
-        pcs[lane] = r;
-      }
-      const int total = __shfl_sync(0xffffffffu, incl, 31);
-      if (lane == 0) {
-        s_np = np;
-        s_end = base + total;
-        s_tnext += np;
-      }
-    }
-    __syncthreads();
-    const int np = s_np, gend = s_end;
-    if (np == 0) break;
-    if (threadIdx.x < np * (int)(sizeof(Task) / 4)) {  // task records of this round -> smem
-      const int pi = threadIdx.x / (int)(sizeof(Task) / 4), wi = threadIdx.x % (int)(sizeof(Task) / 4);
-      reinterpret_cast<int*>(&tcache[pi])[wi] = __ldg(reinterpret_cast<const int*>(&a.tasks[pcs[pi].task]) + wi);
-    }
-    __syncthreads();
-    const int gbeg = pcs[0].slot0;
-
-    // lane 0 of the calling warp stages slot g into ring slot g % kSlots
-    auto produce = [&](int g) {
-      if (lane == 0) {
-        int p = 0;
-        while (p + 1 < np && pcs[p + 1].slot0 <= g) p++;
-        const PieceRec& r = pcs[p];
-        const Task& tk = tcache[p];
-        const int b = g % kSlots;
-        const unsigned sd = base + 16u * b * kSlotQuads;
-        const int srow = row0 + r.first + (g - r.slot0) * kSegsPerSlot;
-        const int nreg = tk.sub[0].k + (tk.nsub > 1 ? tk.sub[1].k : 0);
-        const unsigned bytes =
-            16u * kSegsPerSlot * (tk.nsub * (32 + 31 + (ORDER4 ? 1 : 0)) + 64 * nreg);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&full[b], bytes);
-#pragma unroll
-        for (int s = 0; s < 2; s++) {
-          if (s >= tk.nsub) break;
-          const SubBand& sb = tk.sub[s];
-          const SubLayout L = sub_layout(tk, s);
-          tma_2d(sd + 16u * L.rows, &a.map_rows, sb.row_freq0 - a.f_lo, srow, &full[b]);
-          tma_2d(sd + 16u * L.cols, &a.map_cols[sb.k - 1], sb.col0 - a.f_lo, srow, &full[b]);
-          tma_2d(sd + 16u * L.g, &a.map_g[sb.k - 1], sb.plane_freq + sb.row_freq0 + sb.col0 - a.f_lo, srow, &full[b]);
-          if (ORDER4) tma_2d(sd + 16u * L.plane, &a.map_plane, sb.plane_freq - a.f_lo, srow, &full[b]);
-        }
-      }
-      __syncwarp();
-    };
-    if (gbeg + warp < gend && warp < kSlots) {  // the warps issue the prologue slots in parallel
-      unsigned long long ta0 = 0, ta1 = 0, ta2 = 0;
-      if (tr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ta0));
-      if (gbeg == 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // E is written by the previous kernel
-      if (tr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ta1));
-      for (int g = gbeg + warp; g < gbeg + kSlots && g < gend; g += 4) produce(g);
-      if (tr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ta2));
-      if (tr && lane == 0 && gbeg == 0 && warp == 0) {
-        tr[7] = ta0;          // piece list ready
-        tr[6] = ta1;          // dependency resolved
-        tr[4] = ta2;          // prologue issued
-      }
-    }
-
-    // pieces with no segments still own partial slots: write zeros
-    for (int p = 0; p < np; p++) {
-      if (pcs[p].nseg != 0 || a.accumulate) continue;
-      const Task& tk = tcache[p];
-      if (warp >= tk.nreg) continue;
-      const int s = warp < tk.sub[0].k ? 0 : 1;
-      const SubBand& sb = tk.sub[s];
-      const int c0 = sb.col0 + 32 * (warp - (s ? tk.sub[0].k : 0)) + tb;
-      C* P = Pbase + (int64_t)pcs[p].pslot * a.ncells;
-      for (int i = 0; i < 8; i++) {
-        const int r = ta + 4 * i;
-        if (r >= sb.nrows) continue;
-        const int line = sb.line0 + r;
-        const int cm = __ldg(a.line_cmax + line);
-        C* dst = P + (__ldg(a.line_start + line) - a.lo);
-        for (int j = 0; j < 4; j++)
-          if (c0 + 8 * j <= cm) dst[c0 + 8 * j] = C{0, 0};
-      }
-    }
-
-    int p = -1;
-    int c0 = 0, line0 = 0, nrows = 0;
-    int o_rows = 0, o_cols = 0, o_g = 0, o_plane = 0, cw = 0, gw = 0;
-    bool active = false;
-    C acc[8][4];
-    for (int g = gbeg; g < gend; g++) {
-      if (p < 0 || g >= pcs[p].slot0 + pcs[p].nsl) {
-        p++;
-        while (pcs[p].nsl == 0) p++;
-        const Task& tk = tcache[p];
-        active = false;
-        if (warp < tk.nreg) {
-          const int sub = warp < tk.sub[0].k ? 0 : 1;
-          const int j = warp - (sub ? tk.sub[0].k : 0);
-          const SubBand& sb = tk.sub[sub];
-          const SubLayout L = sub_layout(tk, sub);
-          c0 = sb.col0 + 32 * j + tb;
-          line0 = sb.line0;
-          nrows = sb.nrows;
-          o_rows = L.rows;
-          o_cols = L.cols + 32 * j;
-          o_g = L.g + 32 * j;
-          o_plane = L.plane;
-          cw = L.cw;
-          gw = L.gw;
-#pragma unroll
-          for (int i = 0; i < 8; i++) {
-            const int r = ta + 4 * i;
-            if (r < nrows && __ldg(a.line_cmax + line0 + r) >= c0) active = true;
-          }
-        }
-#pragma unroll
-        for (int i = 0; i < 8; i++)
-#pragma unroll
-          for (int j = 0; j < 4; j++) acc[i][j] = C{0, 0};
-      }
-      const PieceRec& r = pcs[p];
-      const int b = g % kSlots;
-      long long tw0 = 0;
-      if (tr) tw0 = clock64();
-      mbar_wait(&full[b], (unsigned)((g / kSlots) & 1));
-      if (tr) {
-        wait_cyc += clock64() - tw0;
-        slots_seen++;
-      }
-      if (tr && g == 0 && threadIdx.x == 0) {
-        unsigned long long t1;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-        tr[1] = t1;
-      }
-      if (active) {
-        const Q* sq = ring + b * kSlotQuads;
-        const int nq = min(kSegsPerSlot, r.nseg - (g - r.slot0) * kSegsPerSlot);
-        for (int q = 0; q < nq; q++) {
-          if constexpr (sizeof(T) == 4)
-            cells_f32<CONJ, ORDER4>(reinterpret_cast<const float4*>(sq + o_rows + q * 32),
-                                    reinterpret_cast<const float4*>(sq + o_cols + q * cw),
-                                    reinterpret_cast<const float4*>(sq + o_g + q * gw),
-                                    reinterpret_cast<const float4*>(sq + o_plane + q), ta, tb, acc);
-          else
-            cells_f64<CONJ, ORDER4>(reinterpret_cast<const double2*>(sq + o_rows + q * 32),
-                                    reinterpret_cast<const double2*>(sq + o_cols + q * cw),
-                                    reinterpret_cast<const double2*>(sq + o_g + q * gw),
-                                    reinterpret_cast<const double2*>(sq + o_plane + q), ta, tb, acc);
-        }
-      }
-      // the last warp out refills this ring slot with slot g + kSlots
-      __syncwarp();
-      int last = 0;
-      if (lane == 0) {
-        __threadfence_block();
-        last = atomicAdd(&cnt[b], 1) == 3;
-        if (last) cnt[b] = 0;
-      }
-      last = __shfl_sync(0xffffffffu, last, 0);
-      if (last && g + kSlots < gend) produce(g + kSlots);
-      if (g == r.slot0 + r.nsl - 1 && active) {
-        C* P = Pbase + (int64_t)r.pslot * a.ncells;
-#pragma unroll
-        for (int i = 0; i < 8; i++) {
-          const int rr = ta + 4 * i;
-          if (rr >= nrows) continue;
-          const int line = line0 + rr;
-          const int cm = __ldg(a.line_cmax + line);
-          C* dst = P + (__ldg(a.line_start + line) - a.lo);
-#pragma unroll
-          for (int j = 0; j < 4; j++)
-            if (c0 + 8 * j <= cm) {
-              if (a.accumulate) {
-                const C v = dst[c0 + 8 * j];
-                dst[c0 + 8 * j] = C{v.x + acc[i][j].x, v.y + acc[i][j].y};
-              } else {
-                dst[c0 + 8 * j] = acc[i][j];
-              }
-            }
-        }
-      }
-    }
-    __syncthreads();  // ring idle before the next round re-primes it
-  }
-  if (tr && threadIdx.x == 0) {
-    unsigned long long t2;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2));
-    tr[2] = t2;
-    tr[5] = (unsigned long long)wait_cyc;
-  }
-}
-
-// ===========================================================================
-// K2 (default): warp-independent triple / quadruple product.
-//
-// Work = nregions x nseg units (a region is 32 x 32 cells of D_h); the
-// nwarps warps of the launch take equal contiguous unit ranges, so every
-// warp does the same work and warps never wait for each other.  A warp walks
-// its (region, segment) units in order; per unit its 32 lanes stage the
-// segment's 32 row factors, 32 column factors, 63 last factors G(row+col
-// [+a]) (and F(a) for order 4) with cp.async into a private ring of unit
-// PAIRS: the loads of the next pairs overlap the arithmetic of the current
-// one, and the two units of a pair are computed in one straight-line block
-// so the scheduler can overlap one segment's shared loads with the other's
-// FFMA2 chains.  Each (warp, region) piece writes ONE partial slot (warp index -
-// first warp of the region), fixed by the partition: the fp64 combination
-// order in K4a is fixed and results are deterministic.
 #ifndef HOS_K2_PAIRS
 #define HOS_K2_PAIRS 3
 #endif
 constexpr int kWarpPairs = HOS_K2_PAIRS;  // ring of unit pairs per warp (kWarpPairs-1 pairs in flight)
-constexpr int kUnitQuads = 128;           // rows 32 | cols 32 | G 63 | plane 1
-constexpr size_t kWarpTripleSmem = 16 * (size_t)kTripleWarps * 2 * kWarpPairs * kUnitQuads;
+template <typename T>
+constexpr size_t warp_triple_smem() {
+  return 16 * (size_t)kTripleWarps * 2 * kWarpPairs * Cplx<T>::kUnitChunks;
+}
 
 __device__ __forceinline__ void cp_async16_cg(unsigned dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
@@ -673,23 +340,76 @@ __device__ __forceinline__ int region_slots(int r, int nseg, int64_t W, int64_t 
   return (int)(warp_of_unit((int64_t)(r + 1) * nseg - 1, W, N) - warp_of_unit((int64_t)r * nseg, W, N) + 1);
 }
 
+// chunks of a staged unit that are copied (the rest is padding)
+template <typename T, bool ORDER4>
+__device__ __forceinline__ bool chunk_valid(int c) {
+  return c < UnitLayout<T>::plane + (ORDER4 ? 1 : 0);
+}
+// Source of (valid) chunk c of a staged unit, as an element offset from the
+// segment's E row.  fp32 operands are copied from the 16-byte-aligned element
+// at or below their start; the consumer adds the operand's shift (0 or 1).
+template <typename T>
+__device__ __forceinline__ int chunk_src(int c, int o_row, int o_col, int o_g, int o_pl) {
+  using L = UnitLayout<T>;
+  constexpr int per = sizeof(T) == 4 ? 2 : 1;  // elements per chunk
+  auto floor_al = [](int o) { return sizeof(T) == 4 ? (o & ~1) : o; };
+  if (c < L::cols) return floor_al(o_row) + per * (c - L::rows);
+  if (c < L::g) return floor_al(o_col) + per * (c - L::cols);
+  if (c < L::plane) return floor_al(o_g) + per * (c - L::g);
+  return floor_al(o_pl);
+}
+
+// per-lane accumulators of a region: fp32 keeps aR / aI (see cells_f32), fp64 the cell value
+template <typename T>
+struct Acc;
+template <>
+struct Acc<float> {
+  float2 r[8][4], i[8][4];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int a = 0; a < 8; a++)
+#pragma unroll
+      for (int b = 0; b < 4; b++) r[a][b] = i[a][b] = make_float2(0.f, 0.f);
+  }
+  template <bool CONJ>
+  __device__ __forceinline__ float2 cell(int a, int b) const {
+    return CONJ ? make_float2(r[a][b].x + i[a][b].y, r[a][b].y - i[a][b].x)
+                : make_float2(r[a][b].x - i[a][b].y, r[a][b].y + i[a][b].x);
+  }
+};
+template <>
+struct Acc<double> {
+  double2 v[8][4];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int a = 0; a < 8; a++)
+#pragma unroll
+      for (int b = 0; b < 4; b++) v[a][b] = make_double2(0.0, 0.0);
+  }
+  template <bool CONJ>
+  __device__ __forceinline__ double2 cell(int a, int b) const {
+    return v[a][b];
+  }
+};
+
 template <typename T, bool CONJ, bool ORDER4>
-__device__ __forceinline__ void warp_cells(const typename Cplx<T>::Q* q, int ta, int tb,
-                                           typename Cplx<T>::C (&acc)[8][4]) {
+__device__ __forceinline__ void warp_cells(const typename Cplx<T>::C* q, int sr, int sc, int sg, int sp, int ta,
+                                           int tb, Acc<T>& acc) {
+  using L = UnitLayout<T>;
+  constexpr int per = sizeof(T) == 4 ? 2 : 1;
   if constexpr (sizeof(T) == 4)
-    cells_f32<CONJ, ORDER4>(reinterpret_cast<const float4*>(q), reinterpret_cast<const float4*>(q + 32),
-                            reinterpret_cast<const float4*>(q + 64), reinterpret_cast<const float4*>(q + 127), ta, tb,
-                            acc);
+    cells_f32<ORDER4>(q + per * L::rows + sr, q + per * L::cols + sc, q + per * L::g + sg, q + per * L::plane + sp,
+                      ta, tb, acc.r, acc.i);
   else
-    cells_f64<CONJ, ORDER4>(reinterpret_cast<const double2*>(q), reinterpret_cast<const double2*>(q + 32),
-                            reinterpret_cast<const double2*>(q + 64), reinterpret_cast<const double2*>(q + 127), ta,
-                            tb, acc);
+    cells_f64<CONJ, ORDER4>(q + L::rows, q + L::cols, q + L::g, q + L::plane, ta, tb, acc.v);
 }
 
 template <typename T, bool CONJ, bool ORDER4>
-__global__ void __launch_bounds__(128, sizeof(T) == 4 ? 3 : 2) k_triple_w(const __grid_constant__ TripleArgs a) {
-  using Q = typename Cplx<T>::Q;
+__global__ void __launch_bounds__(128, 2) k_triple_w(const __grid_constant__ TripleArgs a) {
   using C = typename Cplx<T>::C;
+  constexpr int UC = Cplx<T>::kUnitChunks;
+  constexpr int per = sizeof(T) == 4 ? 2 : 1;  // elements per 16-byte chunk
+  constexpr int NCH = (UC + 31) / 32;           // chunk slots per lane
   extern __shared__ __align__(128) unsigned char smraw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ta = lane >> 3, tb = lane & 7;
@@ -701,46 +421,55 @@ __global__ void __launch_bounds__(128, sizeof(T) == 4 ? 3 : 2) k_triple_w(const 
   const int64_t W = (int64_t)a.nregions * nseg;
   const int64_t u0 = gw * W / Nw, u1 = (gw + 1) * W / Nw;
   if (u0 >= u1) return;
-  const Q* E = (const Q*)a.E + ((int64_t)series * a.K + a.seg_begin) * a.Lp;
+  const C* E = (const C*)a.E + ((int64_t)series * a.K + a.seg_begin) * a.Lp;
   C* Pbase = (C*)a.part + (int64_t)series * a.maxslots * a.ncells;
-  const Q* ring = reinterpret_cast<const Q*>(smraw) + warp * (2 * kWarpPairs * kUnitQuads);
+  const C* ring = reinterpret_cast<const C*>(smraw) + warp * (2 * kWarpPairs * UC * per);
   const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring) + 16u * lane;
   const int Lp = a.Lp, f_lo = a.f_lo;
   const int total = (int)(u1 - u0);
   asm volatile("griddepcontrol.wait;" ::: "memory");  // E is written by the previous kernel
 
-  // producer: stages the warp's (region, segment) units two at a time, kWarpPairs-1 pairs ahead
+  // producer: stages the warp's (region, segment) units two at a time, kWarpPairs-1 pairs ahead;
+  // lane l copies chunks l, l+32, ... of each unit from p_seg + p_off[chunk slot]
   int p_todo = total;
   int p_r = (int)(u0 / nseg);
-  int p_left = 0;  // units left in the producer's current region
-  const Q *p_row = nullptr, *p_col = nullptr, *p_g = nullptr, *p_pl = nullptr;
-  int p_slot = 0;  // pair slot
+  int p_left = 0;                  // units left in the producer's current region
+  const char* p_seg = nullptr;     // E row of the next segment to stage
+  unsigned p_off[NCH];             // byte offsets of the lane's chunks in a segment row
+  int p_slot = 0;                  // pair slot
+  const size_t row_bytes = (size_t)Lp * sizeof(C);
   auto p_enter = [&](int r, int seg) {
     const Region g = a.regions[r];
-    const Q* base = E + (int64_t)seg * Lp;
-    p_row = base + (g.row_freq0 - f_lo) + lane;
-    p_col = base + (g.col0 - f_lo) + lane;
-    p_g = base + (g.plane_freq + g.row_freq0 + g.col0 - f_lo) + lane;
-    p_pl = base + (g.plane_freq - f_lo);
-    p_left = nseg - seg;
+    p_seg = reinterpret_cast<const char*>(E + (int64_t)seg * Lp);
+#pragma unroll
+    for (int s = 0; s < NCH; s++)
+      p_off[s] = (unsigned)sizeof(C) * chunk_src<T>(lane + 32 * s, g.row_freq0 - f_lo, g.col0 - f_lo,
+                                                   g.plane_freq + g.row_freq0 + g.col0 - f_lo, g.plane_freq - f_lo);
+    p_left = min(nseg - seg, p_todo);
   };
   p_enter(p_r, (int)(u0 - (int64_t)p_r * nseg));
-  auto stage_unit = [&](unsigned d) {
-    cp_async16_cg(d, p_row);
-    cp_async16_cg(d + 16u * 32, p_col);
-    cp_async16_cg(d + 16u * 64, p_g);
-    if (lane < 31) cp_async16_cg(d + 16u * 96, p_g + 32);
-    if (ORDER4 && lane == 31) cp_async16_cg(d + 16u * (127 - 31), p_pl);
-    p_row += Lp;
-    p_col += Lp;
-    p_g += Lp;
-    p_pl += Lp;
-    if (--p_todo > 0 && --p_left == 0) p_enter(++p_r, 0);
+  auto copy_unit = [&](unsigned d) {
+#pragma unroll
+    for (int s = 0; s < NCH; s++)
+      if (chunk_valid<T, ORDER4>(lane + 32 * s)) cp_async16_cg(d + 16u * 32 * s, p_seg + p_off[s]);
+    p_seg += row_bytes;
   };
   auto stage_pair = [&]() {
-    const unsigned d = ring_s + 16u * (2 * kUnitQuads) * p_slot;
-    if (p_todo > 0) stage_unit(d);
-    if (p_todo > 0) stage_unit(d + 16u * kUnitQuads);
+    const unsigned d = ring_s + 16u * (2 * UC) * p_slot;
+    if (p_left >= 2) {  // both units in the current region
+      copy_unit(d);
+      copy_unit(d + 16u * UC);
+      p_left -= 2;
+      p_todo -= 2;
+    } else {
+      for (int t = 0; t < 2 && p_todo > 0; t++) {
+        if (p_left == 0) p_enter(++p_r, 0);
+        copy_unit(d + 16u * UC * t);
+        p_left--;
+        p_todo--;
+      }
+    }
+    if (p_left == 0 && p_todo > 0) p_enter(++p_r, 0);
     p_slot = p_slot + 1 == kWarpPairs ? 0 : p_slot + 1;
     asm volatile("cp.async.commit_group;" ::: "memory");  // always commit: uniform group counting
   };
@@ -750,13 +479,20 @@ __global__ void __launch_bounds__(128, sizeof(T) == 4 ? 3 : 2) k_triple_w(const 
   int r = (int)(u0 / nseg);
   int left = min(total, nseg - (int)(u0 - (int64_t)r * nseg));  // this warp's units in region r
   int c0 = 0, line0 = 0, nrows = 0;
+  int sr = 0, sc = 0, sg = 0, sp = 0;  // fp32: element shift of each operand in its staged copy
   bool active = false, warp_active = false;
-  C acc[8][4];
+  Acc<T> acc;
   auto enter = [&]() {
     const Region rg = a.regions[r];
     c0 = rg.col0 + tb;
     line0 = rg.line0;
     nrows = rg.nrows;
+    if (sizeof(T) == 4) {
+      sr = (rg.row_freq0 - f_lo) & 1;
+      sc = (rg.col0 - f_lo) & 1;
+      sg = (rg.plane_freq + rg.row_freq0 + rg.col0 - f_lo) & 1;
+      sp = (rg.plane_freq - f_lo) & 1;
+    }
     active = false;
 #pragma unroll
     for (int i = 0; i < 8; i++) {
@@ -764,10 +500,7 @@ __global__ void __launch_bounds__(128, sizeof(T) == 4 ? 3 : 2) k_triple_w(const 
       if (rr < nrows && __ldg(a.line_cmax + line0 + rr) >= c0) active = true;
     }
     warp_active = __any_sync(0xffffffffu, active);
-#pragma unroll
-    for (int i = 0; i < 8; i++)
-#pragma unroll
-      for (int j = 0; j < 4; j++) acc[i][j] = C{0, 0};
+    acc.zero();
   };
   auto finalize = [&]() {  // this warp's partial slot of region r
     if (!active) return;
@@ -783,11 +516,12 @@ __global__ void __launch_bounds__(128, sizeof(T) == 4 ? 3 : 2) k_triple_w(const 
 #pragma unroll
       for (int j = 0; j < 4; j++)
         if (c0 + 8 * j <= cm) {
+          const C cv = acc.template cell<CONJ>(i, j);
           if (a.accumulate) {
             const C v = dst[c0 + 8 * j];
-            dst[c0 + 8 * j] = C{v.x + acc[i][j].x, v.y + acc[i][j].y};
+            dst[c0 + 8 * j] = C{v.x + cv.x, v.y + cv.y};
           } else {
-            dst[c0 + 8 * j] = acc[i][j];
+            dst[c0 + 8 * j] = cv;
           }
         }
     }
@@ -799,12 +533,12 @@ __global__ void __launch_bounds__(128, sizeof(T) == 4 ? 3 : 2) k_triple_w(const 
     stage_pair();
     asm volatile("cp.async.wait_group %0;" ::"n"(kWarpPairs - 1) : "memory");
     __syncwarp();  // the pair's data, copied by all lanes, is visible
-    const Q* q = ring + c_slot * (2 * kUnitQuads);
+    const C* q = ring + c_slot * (2 * UC * per);
     const int cnt = min(2, total - pos);
     if (cnt == 2 && left >= 2) {  // fast path: both units in region r, one straight-line block
       if (warp_active) {
-        warp_cells<T, CONJ, ORDER4>(q, ta, tb, acc);
-        warp_cells<T, CONJ, ORDER4>(q + kUnitQuads, ta, tb, acc);
+        warp_cells<T, CONJ, ORDER4>(q, sr, sc, sg, sp, ta, tb, acc);
+        warp_cells<T, CONJ, ORDER4>(q + UC * per, sr, sc, sg, sp, ta, tb, acc);
       }
       left -= 2;
     } else {
@@ -815,7 +549,7 @@ __global__ void __launch_bounds__(128, sizeof(T) == 4 ? 3 : 2) k_triple_w(const 
           left = min(total - pos - t, nseg);
           enter();
         }
-        if (warp_active) warp_cells<T, CONJ, ORDER4>(q + t * kUnitQuads, ta, tb, acc);
+        if (warp_active) warp_cells<T, CONJ, ORDER4>(q + t * UC * per, sr, sc, sg, sp, ta, tb, acc);
         left--;
       }
     }
@@ -836,26 +570,14 @@ static cudaError_t set_smem(K kernel, size_t bytes) {
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-int triple_warp_kernel() {
-  static int v = -1;
-  if (v < 0) {
-    const char* env = std::getenv("HOS_K2");
-    v = (env && std::string(env) == "tma") ? 0 : 1;
-  }
-  return v;
-}
-
 template <typename T>
 static cudaError_t configure_all() {
+  constexpr size_t sm = warp_triple_smem<T>();
   cudaError_t e;
-  if ((e = set_smem(k_triple_w<T, true, false>, kWarpTripleSmem)) != cudaSuccess) return e;
-  if ((e = set_smem(k_triple_w<T, false, false>, kWarpTripleSmem)) != cudaSuccess) return e;
-  if ((e = set_smem(k_triple_w<T, true, true>, kWarpTripleSmem)) != cudaSuccess) return e;
-  if ((e = set_smem(k_triple_w<T, false, true>, kWarpTripleSmem)) != cudaSuccess) return e;
-  if ((e = set_smem(k_triple<T, true, false>, kTripleSmem)) != cudaSuccess) return e;
-  if ((e = set_smem(k_triple<T, false, false>, kTripleSmem)) != cudaSuccess) return e;
-  if ((e = set_smem(k_triple<T, true, true>, kTripleSmem)) != cudaSuccess) return e;
-  return set_smem(k_triple<T, false, true>, kTripleSmem);
+  if ((e = set_smem(k_triple_w<T, true, false>, sm)) != cudaSuccess) return e;
+  if ((e = set_smem(k_triple_w<T, false, false>, sm)) != cudaSuccess) return e;
+  if ((e = set_smem(k_triple_w<T, true, true>, sm)) != cudaSuccess) return e;
+  return set_smem(k_triple_w<T, false, true>, sm);
 }
 
 static cudaError_t configure() {
@@ -871,39 +593,33 @@ static cudaError_t configure() {
 int triple_occupancy(int precision) {
   if (configure() != cudaSuccess) return 1;
   int n = 1;
-  if (triple_warp_kernel()) {
-    if (precision == 32)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_triple_w<float, true, false>, 128, kWarpTripleSmem);
-    else
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_triple_w<double, true, false>, 128, kWarpTripleSmem);
-  } else if (precision == 32)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_triple<float, true, false>, 128, kTripleSmem);
+  if (precision == 32)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_triple_w<float, true, false>, 128, warp_triple_smem<float>());
   else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_triple<double, true, false>, 128, kTripleSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_triple_w<double, true, false>, 128,
+                                                  warp_triple_smem<double>());
   return n < 1 ? 1 : n;
 }
 
 template <typename T, bool CONJ, bool ORDER4>
 static cudaError_t launch_pdl(const TripleArgs& a, cudaStream_t st) {
   cudaLaunchConfig_t cfg = {};
-  const bool warpk = triple_warp_kernel();
-  cfg.gridDim = dim3(warpk ? (unsigned)((a.nwarps + kTripleWarps - 1) / kTripleWarps) : a.nctas, a.batch);
-  cfg.blockDim = dim3(128);
-  cfg.dynamicSmemBytes = warpk ? kWarpTripleSmem : kTripleSmem;
+  cfg.gridDim = dim3((unsigned)((a.nwarps + kTripleWarps - 1) / kTripleWarps), a.batch);
+  cfg.blockDim = dim3(32 * kTripleWarps);
+  cfg.dynamicSmemBytes = warp_triple_smem<T>();
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (warpk) return cudaLaunchKernelEx(&cfg, k_triple_w<T, CONJ, ORDER4>, a);
-  return cudaLaunchKernelEx(&cfg, k_triple<T, CONJ, ORDER4>, a);
+  return cudaLaunchKernelEx(&cfg, k_triple_w<T, CONJ, ORDER4>, a);
 }
 
 cudaError_t launch_triple(const TripleArgs& a, int precision, cudaStream_t st) {
   cudaError_t e = configure();
   if (e != cudaSuccess) return e;
-  if (a.ntasks == 0 || a.nctas == 0 || a.seg_end <= a.seg_begin) return cudaSuccess;
+  if (a.nregions == 0 || a.nwarps == 0 || a.seg_end <= a.seg_begin) return cudaSuccess;
   const bool o4 = a.order == 4;
   if (precision == 32) {
     if (a.conj && !o4) e = launch_pdl<float, true, false>(a, st);
@@ -934,8 +650,7 @@ constexpr int kScanThreads = 256;
 __device__ __forceinline__ int cell_slots(const SlotInfo& si, int nparts, int64_t l, int64_t col) {
   if (si.line_region0 == nullptr) return nparts;
   const int r = si.line_region0[l] + (int)(col / kRegionCols);
-  if (si.region_task == nullptr) return region_slots(r, si.nseg, (int64_t)si.nregions * si.nseg, si.nwarps);
-  return task_slots(si.region_task[r], si.nseg, (int64_t)si.ntasks * si.nseg, si.nctas);
+  return region_slots(r, si.nseg, (int64_t)si.nregions * si.nseg, si.nwarps);
 }
 
 template <typename P2>

@@ -3,9 +3,7 @@
 //   K0 prep     segment + demean (+ Hann) + cast        hospectra/series.py:159-165
 //   (cuFFT)     batched R2C / D2Z per segment            hospectra/dft.py:36-41
 //   K1 extend   conjugate-symmetric extension of the half spectrum onto the
-//               frequency window [f_lo, f_hi] the triple product reads, in the
-//               "quad" layout (re, im, -im, re) so every operand form the FFMA2
-//               complex arithmetic needs is a free register swizzle
+//               frequency window [f_lo, f_hi] the triple product reads
 //   K2 triple   R(line, c) = sum_i F_i(row) F_i(c) G_i(row + c [+ a])  over D_h,
 //               per segment chunk (hospectra/spectra.py:227-263)
 //   K4a scan    per-line prefix sums of the chunk-summed raw cells (fp64,
@@ -13,7 +11,6 @@
 //   K4b box     window sums as prefix differences, scale 1/(M K w^(d)), write
 //               lexicographic principal-domain values   hospectra/spectra.py:405-415
 #pragma once
-#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdint>
 
@@ -54,22 +51,12 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // launch wrappers (hos_kernels.cu)
 
 struct TripleArgs {
-  // 2-D tensor maps over the extended spectra viewed as [rows=batch*K][2 Lp x 8 bytes]
-  // (one 16-byte spectrum element = 2 x 8 bytes; fp32 quads or fp64 complex),
-  // boxes of kSegsPerSlot segments x (2 x width) 8-byte elements:
-  CUtensorMap map_rows;      // 32 elements        (row factors of a band)
-  CUtensorMap map_cols[3];   // 32k elements       (column factors of k regions)
-  CUtensorMap map_g[3];      // 31 + 32k elements  (last factors G(row+col[+a]))
-  CUtensorMap map_plane;     // 1 element          (order 4: F(a))
-  const void* E;              // [series][K][Lp] 16-byte elements (warp-independent kernel)
-  int Lp;
+  const void* E;              // [series][K][Lp] float2 (fp32) / double2 (fp64) spectrum elements
+  int Lp;                     // row pitch in elements (even: rows stay 16-byte aligned)
   int f_lo;                   // frequency of element 0
   int K;                      // segments per series (E rows per series)
   int seg_begin, seg_end;     // segment range reduced by this launch
-  const Task* tasks;
-  int ntasks;
-  int nctas;                  // CTAs per series splitting the work (<= work units)
-  const Region* regions;      // warp-independent kernel: flat region list
+  const Region* regions;      // flat region list (32 x 32 cells each)
   int nregions;
   int64_t nwarps;             // warps splitting the region x segment work (<= units)
   const int32_t* line_cmax;
@@ -81,30 +68,21 @@ struct TripleArgs {
   int order;
   int conj;
   int batch;
-  unsigned long long* trace;  // optional: per CTA {start, first data, end, smid} (globaltimer ns)
   int accumulate;             // add into the partial slots (chunked launches after the first)
 };
 
-#ifndef HOS_K2_SEGS
-#define HOS_K2_SEGS 4
-#endif
-constexpr int kSegsPerSlot = HOS_K2_SEGS;  // segments per TMA box / ring slot
-
-constexpr int kTripleWarps = 4;   // warps per CTA of the triple-product kernels
+constexpr int kTripleWarps = 4;   // warps per CTA of the triple-product kernel
 
 // Where the partial slots of a K2 launch are (for the K4a / reduce readers).
 struct SlotInfo {
   const int32_t* line_region0;  // nullptr: plain buffer with `nparts` parts
-  const int32_t* region_task;   // TMA kernel: slots are per task; nullptr: per region (warp kernel)
-  int ntasks, nseg, nctas;
+  int nseg;
   int nregions;
   int64_t nwarps;
 };
 
 // occupancy (CTAs / SM) of the triple-product kernel
 int triple_occupancy(int precision);
-// 1: the warp-independent cp.async kernel (default), 0: the CTA-shared TMA kernel
-int triple_warp_kernel();
 
 cudaError_t launch_prep(const void* x, int x_dtype, int64_t x_stride, int m, int seg_begin, int nseg,
                         int batch, int taper, const double* taper_tab, int precision, void* seg_out,
