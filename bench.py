@@ -269,8 +269,8 @@ def run_ours(args):
     if dist is not None:
         dist.barrier()
     sampler.stop()
-    # per-stage device times on the launching stream: each stage launched R
-    # times back to back between two CUDA events (mean per launch; the inputs
+    # per-stage device times on the launching stream: each stage's R launches
+    # replayed as one CUDA graph between two CUDA events (mean per launch; the inputs
     # of every stage are the ones the last estimate left in HBM / L2, as in
     # the pipeline, where each stage reads what the previous one just wrote)
     tri, stages = [], {}
@@ -342,7 +342,7 @@ def run_ours(args):
                     "kernel": "k_triple_f32 (FFMA2 triple product)", "kernel_ms": round(t_tri, 5),
                     "kernel_share_of_step": round(t_tri / ms_per_step, 3),
                     "stage_us": {k_: round(statistics.median(v_) * 1e3, 2) for k_, v_ in stages.items()},
-                    "stage_timing": f"mean of {STAGE_REPS} back-to-back launches per stage, median of 3",
+                    "stage_timing": f"mean of {STAGE_REPS} launches per stage replayed as one CUDA graph, median of 3",
                     "peak_source": f"live FFMA2 outer-product microbenchmark (hos_peak_fp32) at {probe_mhz:.0f} MHz; "
                                    "MEASURED_PEAKS.json has no FP32 figure",
                     "tiling_efficiency": round(plan.units / plan.issued, 4)}

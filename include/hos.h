@@ -171,10 +171,11 @@ int hos_plan_set_timing(hos_plan* plan, int enable);
 /* Diagnostics: K2 CTAs per series (4 warps each). */
 int hos_plan_nctas(const hos_plan* plan);
 /* Diagnostics: mean per-launch device time (ms) of each stage {prep, fft,
- * extend, triple, scan, box}, each launched `reps` times back to back between
- * two events on `stream` after one full estimate of x_dev (same arguments as
- * hos_estimate).  Resolves sub-microsecond changes that single event pairs
- * (~1 us granularity) cannot. */
+ * extend, triple, scan, box}: `reps` launches of the stage captured into one
+ * CUDA graph, replayed between two events on `stream` after one full estimate
+ * of x_dev (same arguments as hos_estimate).  Resolves sub-microsecond changes
+ * that single event pairs (~1 us granularity) cannot; with the fused front
+ * end (power-of-two m) "prep" is the fused kernel and fft/extend read 0. */
 int hos_plan_time_stages(hos_plan* plan, const void* x_dev, int x_dtype, int64_t x_stride, void* out_dev, int reps,
                          double* ms6, void* stream);
 int hos_plan_kernel_ms(const hos_plan* plan, double* triple_ms, double* total_ms);

@@ -63,6 +63,8 @@ struct hos_plan {
   int64_t* d_pair_base = nullptr;
   int32_t* d_line_of_ab = nullptr;
   double* d_taper = nullptr;
+  void* d_tw = nullptr;     // fused front end: m twiddles exp(-2 pi i t/m), compute precision
+  bool fused = false;       // K0+FFT+K1 as one kernel (power-of-two m <= hos::kFrontMaxM)
   // work buffers
   void* d_seg = nullptr;   // batch*k*m real
   void* d_half = nullptr;  // batch*k*hstride complex
@@ -308,9 +310,26 @@ int check_dtype_x(int x_dtype) {
   return HOS_OK;
 }
 
+// Fused front end over segments [seg_begin, seg_begin+nseg) of `batch` series -> E rows.
+int fused_front(hos_plan* p, const void* x_dev, int x_dtype, int64_t x_stride, int seg_begin, int nseg, int batch,
+                cudaStream_t st) {
+  const char* xs = (const char*)x_dev + (size_t)seg_begin * p->m * (x_dtype == HOS_F32 ? 4 : 8);
+  void* E = (char*)p->d_E + (size_t)seg_begin * p->Lp * csize(p->precision);
+  CUDA_TRY(hos::launch_front(xs, x_dtype, x_stride, p->m, nseg, p->k, batch, p->taper, p->d_taper, p->d_tw,
+                             p->precision, p->geo.f_lo, p->L, p->Lp, E, st));
+  return HOS_OK;
+}
+
 // K0 + FFT + K1 for all batch*k segments.
 int run_front(hos_plan* p, const void* x_dev, int x_dtype, int64_t x_stride, cudaStream_t st) {
   const int rows = p->batch * p->k;
+  if (p->fused) {
+    int rc = fused_front(p, x_dev, x_dtype, x_stride, 0, p->k, p->batch, st);
+    if (rc) return rc;
+    if (p->timing)
+      for (int i = 1; i <= 3; i++) CUDA_TRY(cudaEventRecord(p->ev[i], st));
+    return HOS_OK;
+  }
   CUDA_TRY(hos::launch_prep(x_dev, x_dtype, x_stride, p->m, 0, p->k, p->batch, p->taper, p->d_taper, p->precision,
                             p->d_seg, st));
   if (p->timing) CUDA_TRY(cudaEventRecord(p->ev[1], st));
@@ -455,6 +474,28 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
     for (int u = 0; u < m; u++) tab[u] = 0.5 - 0.5 * std::cos(2.0 * M_PI * u / m);
     if ((rc = upload(p, &p->d_taper, tab))) return bail(rc);
   }
+  {
+    const char* env = std::getenv("HOS_FRONT");  // "cufft": K0 -> cuFFT -> K1 even for power-of-two m
+    p->fused = (m & (m - 1)) == 0 && m <= hos::kFrontMaxM && !(env && std::string(env) == "cufft");
+    if (p->fused) {
+      const int h = m;  // full circle: radix-4 stages read w^(j p s) for j <= 3
+      if (precision == 32) {
+        std::vector<float> tw(2 * h);
+        for (int t = 0; t < h; t++) {
+          tw[2 * t] = (float)std::cos(2.0 * M_PI * t / m);
+          tw[2 * t + 1] = (float)-std::sin(2.0 * M_PI * t / m);
+        }
+        if ((rc = upload(p, (float**)&p->d_tw, tw))) return bail(rc);
+      } else {
+        std::vector<double> tw(2 * h);
+        for (int t = 0; t < h; t++) {
+          tw[2 * t] = std::cos(2.0 * M_PI * t / m);
+          tw[2 * t + 1] = -std::sin(2.0 * M_PI * t / m);
+        }
+        if ((rc = upload(p, (double**)&p->d_tw, tw))) return bail(rc);
+      }
+    }
+  }
   const size_t rows = (size_t)batch * k;
   if ((rc = alloc(p, &p->d_seg, rows * m * rsize(precision)))) return bail(rc);
   if ((rc = alloc(p, &p->d_half, rows * p->hstride * csize(precision)))) return bail(rc);
@@ -490,7 +531,7 @@ void hos_plan_destroy(hos_plan* p) {
   for (auto e : p->chunk_ev) cudaEventDestroy(e);
   for (auto& kv : p->ffts) cufftDestroy(kv.second);
   void* bufs[] = {p->d_regions, p->d_line_region0, p->d_line_cmax, p->d_line_start, p->d_row_off, p->d_pair_k1, p->d_pair_k2,
-                  p->d_pair_base, p->d_line_of_ab, p->d_taper, p->d_seg, p->d_half, p->d_E, p->d_part,
+                  p->d_pair_base, p->d_line_of_ab, p->d_taper, p->d_tw, p->d_seg, p->d_half, p->d_E, p->d_part,
                   p->d_S, p->d_xin, p->d_out};
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -662,11 +703,16 @@ int hos_estimate_host(hos_plan* p, const void* x_host, int x_dtype, int64_t x_st
       void* seg = (char*)p->d_seg + (size_t)sb * p->m * rs;
       void* half = (char*)p->d_half + (size_t)sb * p->hstride * cs;
       void* E = (char*)p->d_E + (size_t)sb * p->Lp * csize(p->precision);
-      CUDA_TRY(hos::launch_prep(p->d_xin, x_dtype, 0, p->m, sb, kc, 1, p->taper, p->d_taper, p->precision, seg, s));
-      int r = run_fft(p, kc, seg, half, s);
-      if (r) return r;
-      CUDA_TRY(hos::launch_extend_half(half, p->m, p->hstride, kc, nullptr, p->geo.f_lo, p->L, p->Lp, p->precision,
-                                       E, s));
+      if (p->fused) {
+        int r = fused_front(p, p->d_xin, x_dtype, 0, sb, kc, 1, s);
+        if (r) return r;
+      } else {
+        CUDA_TRY(hos::launch_prep(p->d_xin, x_dtype, 0, p->m, sb, kc, 1, p->taper, p->d_taper, p->precision, seg, s));
+        int r = run_fft(p, kc, seg, half, s);
+        if (r) return r;
+        CUDA_TRY(hos::launch_extend_half(half, p->m, p->hstride, kc, nullptr, p->geo.f_lo, p->L, p->Lp, p->precision,
+                                         E, s));
+      }
       mark(6 + 4 * j, s);
       hos::TripleArgs ta = triple_args(p, sb, sb + kc, p->nctas_chunk, 1);
       ta.accumulate = j > 0;
@@ -739,10 +785,15 @@ int hos_partial_raw(hos_plan* p, const void* x_dev, int x_dtype, int seg_begin, 
   void* seg = (char*)p->d_seg + (size_t)seg_begin * p->m * rs;
   void* half = (char*)p->d_half + (size_t)seg_begin * p->hstride * csize(p->precision);
   void* E = (char*)p->d_E + (size_t)seg_begin * p->Lp * csize(p->precision);
-  CUDA_TRY(hos::launch_prep(x_dev, x_dtype, 0, p->m, seg_begin, nseg, 1, p->taper, p->d_taper, p->precision, seg, st));
-  if ((rc = run_fft(p, nseg, seg, half, st))) return rc;
-  CUDA_TRY(hos::launch_extend_half(half, p->m, p->hstride, nseg, nullptr, p->geo.f_lo, p->L, p->Lp, p->precision, E,
-                                   st));
+  if (p->fused) {
+    if ((rc = fused_front(p, x_dev, x_dtype, 0, seg_begin, nseg, 1, st))) return rc;
+  } else {
+    CUDA_TRY(hos::launch_prep(x_dev, x_dtype, 0, p->m, seg_begin, nseg, 1, p->taper, p->d_taper, p->precision, seg,
+                              st));
+    if ((rc = run_fft(p, nseg, seg, half, st))) return rc;
+    CUDA_TRY(hos::launch_extend_half(half, p->m, p->hstride, nseg, nullptr, p->geo.f_lo, p->L, p->Lp, p->precision,
+                                     E, st));
+  }
   int n = nctas_for(p, nseg, 1);
   while (n > 1 && slots_needed(p, nseg, n) > p->maxslots) n--;
   const hos::TripleArgs ta = triple_args(p, seg_begin, seg_end, n, 1);
@@ -914,37 +965,65 @@ int hos_plan_time_stages(hos_plan* p, const void* x_dev, int x_dtype, int64_t x_
   cudaEvent_t e0, e1;
   CUDA_TRY(cudaEventCreate(&e0));
   CUDA_TRY(cudaEventCreate(&e1));
-  for (int s = 0; s < 6 && !rc; s++) {
-    CUDA_TRY(cudaEventRecord(e0, st));
-    for (int r = 0; r < reps && !rc; r++) {
-      cudaError_t e = cudaSuccess;
-      switch (s) {
-        case 0:
+  // each stage: `reps` launches captured into one CUDA graph (device-paced, as
+  // in the estimate graph; back-to-back host launches would measure the
+  // host's launch rate for the short stages), one warm replay, one timed replay
+  auto launch_stage = [&](int s, cudaStream_t cs) -> int {
+    cudaError_t e = cudaSuccess;
+    int r2 = HOS_OK;
+    switch (s) {
+      case 0:
+        if (p->fused)
+          r2 = fused_front(p, x_dev, x_dtype, x_stride, 0, p->k, p->batch, cs);
+        else
           e = hos::launch_prep(x_dev, x_dtype, x_stride, p->m, 0, p->k, p->batch, p->taper, p->d_taper, p->precision,
-                               p->d_seg, st);
-          break;
-        case 1:
-          rc = run_fft(p, rows, p->d_seg, p->d_half, st);
-          break;
-        case 2:
+                               p->d_seg, cs);
+        break;
+      case 1:
+        if (!p->fused) r2 = run_fft(p, rows, p->d_seg, p->d_half, cs);
+        break;
+      case 2:
+        if (!p->fused)
           e = hos::launch_extend_half(p->d_half, p->m, p->hstride, rows, nullptr, p->geo.f_lo, p->L, p->Lp,
-                                      p->precision, p->d_E, st);
-          break;
-        case 3:
-          e = hos::launch_triple(ta, p->precision, st);
-          break;
-        case 4:
-          e = hos::launch_line_scan(p->d_part, p->maxslots, p->geo.ncells, slot_info(p, p->k, p->nctas),
-                                    p->precision, p->d_line_start, 0, p->geo.nlines, p->geo.ncells, p->batch, p->d_S,
-                                    st);
-          break;
-        default:
-          rc = run_box(p, out_dev, st);
-      }
-      if (e != cudaSuccess) rc = fail(HOS_ECUDA, std::string("CUDA error: ") + cudaGetErrorString(e));
+                                      p->precision, p->d_E, cs);
+        break;
+      case 3:
+        e = hos::launch_triple(ta, p->precision, cs);
+        break;
+      case 4:
+        e = hos::launch_line_scan(p->d_part, p->maxslots, p->geo.ncells, slot_info(p, p->k, p->nctas), p->precision,
+                                  p->d_line_start, 0, p->geo.nlines, p->geo.ncells, p->batch, p->d_S, cs);
+        break;
+      default:
+        r2 = run_box(p, out_dev, cs);
     }
+    if (e != cudaSuccess) return fail(HOS_ECUDA, std::string("CUDA error: ") + cudaGetErrorString(e));
+    return r2;
+  };
+  for (int s = 0; s < 6 && !rc; s++) {
+    if (p->fused && (s == 1 || s == 2)) {
+      ms6[s] = 0.0;
+      continue;
+    }
+    cudaGraph_t graph = nullptr;
+    CUDA_TRY(cudaStreamBeginCapture(p->cap, cudaStreamCaptureModeThreadLocal));
+    for (int r = 0; r < reps && !rc; r++) rc = launch_stage(s, p->cap);
+    cudaError_t ce = cudaStreamEndCapture(p->cap, &graph);
+    if (rc) {
+      if (graph) cudaGraphDestroy(graph);
+      break;
+    }
+    CUDA_TRY(ce);
+    cudaGraphExec_t exec = nullptr;
+    ce = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    CUDA_TRY(ce);
+    CUDA_TRY(cudaGraphLaunch(exec, st));
+    CUDA_TRY(cudaEventRecord(e0, st));
+    CUDA_TRY(cudaGraphLaunch(exec, st));
     CUDA_TRY(cudaEventRecord(e1, st));
     CUDA_TRY(cudaEventSynchronize(e1));
+    cudaGraphExecDestroy(exec);
     float ms = 0;
     CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
     ms6[s] = ms / reps;

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <cstdlib>
 #include <string>
+#include <type_traits>
 
 namespace hos {
 
@@ -14,6 +15,25 @@ inline unsigned grid_for(int64_t n, int threads, int64_t cap = 148 * 64) {
   if (g < 1) g = 1;
   if (g > cap) g = cap;
   return (unsigned)g;
+}
+
+// Launch with programmatic stream serialization: the kernel may be scheduled
+// while its predecessor drains; it must griddepcontrol.wait before reading the
+// predecessor's output (every kernel launched this way does).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl_kernel(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -69,6 +89,218 @@ cudaError_t launch_prep(const void* x, int x_dtype, int64_t x_stride, int m, int
   else
     k_prep<double, double><<<grid, th, 0, st>>>((const double*)x, x_stride, m, seg_begin, nseg, taper, tab, (double*)seg_out);
   return cudaGetLastError();
+}
+
+// ===========================================================================
+// K0+1 (power-of-two m): fused segment + demean (+ taper) + FFT + extension.
+// One CTA per (segment pair, series): the fp64 means exactly as K0, the
+// demeaned (tapered) samples rounded to the compute precision as K0 stores
+// them, packed two segments per complex sequence (z = x_a + i x_b), a
+// radix-4 Stockham FFT in shared memory (natural-order output, twiddles
+// exp(-2 pi i t/m) rounded from fp64), and the extended-spectrum row
+// E[f - f_lo] = F[f mod m] written straight from shared memory -- one launch
+// and one HBM pass instead of K0 -> cuFFT -> K1.
+
+template <typename T>
+struct C2;
+template <>
+struct C2<float> {
+  using t = float2;
+};
+template <>
+struct C2<double> {
+  using t = double2;
+};
+
+// threads of the fused front end for m = 2^LOG2M: m/8 (8 samples, two radix-4
+// butterflies per stage each), clamped to [32, 256]
+template <int LOG2M>
+__host__ __device__ constexpr int front_threads() {
+  return (1 << LOG2M) / 8 >= 256 ? 256 : ((1 << LOG2M) / 8 >= 32 ? (1 << LOG2M) / 8 : 32);
+}
+
+template <typename Tin, typename T, int LOG2M>
+__global__ void __launch_bounds__(front_threads<LOG2M>()) k_front(const Tin* __restrict__ x, int64_t x_stride,
+                                                                  int nseg, int krows, int taper,
+                                                                  const double* __restrict__ tab,
+                                                                  const typename C2<T>::t* __restrict__ tw, int f_lo,
+                                                                  int L, int Lp, typename C2<T>::t* __restrict__ E) {
+  using CT = typename C2<T>::t;
+  constexpr int M = 1 << LOG2M;
+  constexpr int TH = front_threads<LOG2M>();
+  constexpr int VPT = (M + TH - 1) / TH;        // samples per thread and segment
+  constexpr int BPT = (M / 4 + TH - 1) / TH;    // radix-4 butterflies per thread and stage
+  extern __shared__ __align__(16) unsigned char fsm[];
+  CT* bufA = reinterpret_cast<CT*>(fsm);
+  CT* bufB = bufA + M;
+  CT* tws = bufB + M;  // twiddle table staged in shared memory
+  __shared__ double2 red[TH / 32];
+  const int tid = threadIdx.x;
+  // two real segments per CTA, packed as one complex sequence z = x_a + i x_b
+  const int sa = 2 * blockIdx.x, b = blockIdx.y;
+  const bool has_b = sa + 1 < nseg;
+  const Tin* src = x + (int64_t)b * x_stride + (int64_t)sa * M;
+  // samples and taper weights stay in registers between the means and the store
+  Tin xa[VPT], xb[VPT];
+  double wv[VPT];
+  double s_a = 0.0, s_b = 0.0;
+#pragma unroll
+  for (int i = 0; i < VPT; i++) {
+    const int u = tid + i * TH;
+    if (M % TH == 0 || u < M) {
+      xa[i] = src[u];
+      xb[i] = has_b ? src[u + M] : Tin(0);
+      wv[i] = taper ? tab[u] : 1.0;
+      s_a += (double)xa[i];
+      s_b += (double)xb[i];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < VPT; i++) {
+    const int t = tid + i * TH;
+    if (M % TH == 0 || t < M) tws[t] = tw[t];
+  }
+  s_a = warp_sum(s_a);
+  s_b = warp_sum(s_b);
+  if ((tid & 31) == 0) red[tid >> 5] = make_double2(s_a, s_b);
+  __syncthreads();
+  double ta = 0.0, tb = 0.0;
+#pragma unroll
+  for (int w = 0; w < TH / 32; w++) {
+    ta += red[w].x;
+    tb += red[w].y;
+  }
+  const double mean_a = ta / (double)M, mean_b = tb / (double)M;
+#pragma unroll
+  for (int i = 0; i < VPT; i++) {
+    const int u = tid + i * TH;
+    if (M % TH == 0 || u < M) {
+      double va = (double)xa[i] - mean_a, vb = (double)xb[i] - mean_b;
+      if (taper) {
+        va *= wv[i];
+        vb *= wv[i];
+      }
+      bufA[u] = CT{(T)va, (T)vb};
+    }
+  }
+  __syncthreads();
+  // Stockham (self-sorting, decimation in frequency) radix-4 stages, then one
+  // radix-2 stage when log2 m is odd.  Stage with current length n and stride
+  // s = m / n, butterfly (p < n/4, q < s):
+  //   a_j = x[q + s(p + j n/4)],  b = DFT4(a),  y[q + s(4p + j)] = b_j w^(j p s)
+  // with w = exp(-2 pi i / m) (table tw[t], t < m).
+  CT* xin = bufA;
+  CT* yout = bufB;
+#ifndef HOS_FRONT_NOFFT
+#pragma unroll
+  for (int ls = 0; ls + 2 <= LOG2M; ls += 2) {
+    const int qn = (M >> ls) >> 2;  // n / 4 (compile-time after unrolling)
+#pragma unroll
+    for (int r = 0; r < BPT; r++) {
+      const int bf = tid + r * TH;
+      if (M / 4 % TH == 0 || bf < M / 4) {
+        const int p = bf >> ls, q = bf & ((1 << ls) - 1);
+        const CT a0 = xin[q + (p << ls)];
+        const CT a1 = xin[q + ((p + qn) << ls)];
+        const CT a2 = xin[q + ((p + 2 * qn) << ls)];
+        const CT a3 = xin[q + ((p + 3 * qn) << ls)];
+        const T t0r = a0.x + a2.x, t0i = a0.y + a2.y, t1r = a0.x - a2.x, t1i = a0.y - a2.y;
+        const T t2r = a1.x + a3.x, t2i = a1.y + a3.y;
+        const T t3r = a1.y - a3.y, t3i = a3.x - a1.x;  // -i (a1 - a3)
+        const int t = p << ls;
+        CT* y = yout + q + ((4 * p) << ls);
+        y[0] = CT{t0r + t2r, t0i + t2i};
+        const T b1r = t1r + t3r, b1i = t1i + t3i, b2r = t0r - t2r, b2i = t0i - t2i, b3r = t1r - t3r,
+                b3i = t1i - t3i;
+        if (ls + 2 == LOG2M) {  // last radix-4 stage: p = 0, all twiddles 1
+          y[1 << ls] = CT{b1r, b1i};
+          y[2 << ls] = CT{b2r, b2i};
+          y[3 << ls] = CT{b3r, b3i};
+        } else {
+          const CT w1 = tws[t], w2 = tws[2 * t], w3 = tws[3 * t];
+          y[1 << ls] = CT{b1r * w1.x - b1i * w1.y, b1r * w1.y + b1i * w1.x};
+          y[2 << ls] = CT{b2r * w2.x - b2i * w2.y, b2r * w2.y + b2i * w2.x};
+          y[3 << ls] = CT{b3r * w3.x - b3i * w3.y, b3r * w3.y + b3i * w3.x};
+        }
+      }
+    }
+    __syncthreads();
+    CT* tsw = xin;
+    xin = yout;
+    yout = tsw;
+  }
+  if (LOG2M & 1) {  // last radix-2 stage: p = 0, twiddle 1
+#pragma unroll
+    for (int r = 0; r < (M / 2 + TH - 1) / TH; r++) {
+      const int q = tid + r * TH;
+      if (M / 2 % TH == 0 || q < M / 2) {
+        const CT a = xin[q], c = xin[q + M / 2];
+        yout[q] = CT{a.x + c.x, a.y + c.y};
+        yout[q + M / 2] = CT{a.x - c.x, a.y - c.y};
+      }
+    }
+    __syncthreads();
+    xin = yout;
+  }
+#endif
+  if (tid == 0) asm volatile("griddepcontrol.launch_dependents;");
+  // X_a(f) = (Z(f) + conj Z(-f)) / 2,  X_b(f) = (Z(f) - conj Z(-f)) / 2i
+  CT* row = E + ((int64_t)b * krows + sa) * Lp;
+  for (int j = tid; j < L; j += TH) {
+    const int f = (f_lo + j) & (M - 1);
+    const CT z = xin[f], zn = xin[(M - f) & (M - 1)];
+    row[j] = CT{(T)0.5 * (z.x + zn.x), (T)0.5 * (z.y - zn.y)};
+    if (has_b) row[Lp + j] = CT{(T)0.5 * (z.y + zn.y), (T)0.5 * (zn.x - z.x)};
+  }
+}
+
+template <int LOG2M, typename Tin, typename T>
+static void front_go(const Tin* x, int64_t x_stride, int nseg, int krows, int batch, int taper, const double* tab,
+                     const typename C2<T>::t* tw, int f_lo, int L, int Lp, typename C2<T>::t* E, cudaStream_t st) {
+  const size_t smem = 3 * (size_t)(1 << LOG2M) * sizeof(typename C2<T>::t);
+  auto kern = k_front<Tin, T, LOG2M>;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = true;
+  }
+  kern<<<dim3((nseg + 1) / 2, batch), front_threads<LOG2M>(), smem, st>>>(x, x_stride, nseg, krows, taper, tab, tw,
+                                                                          f_lo, L, Lp, E);
+}
+
+template <typename Tin, typename T>
+static cudaError_t front_dispatch(int log2m, const Tin* x, int64_t x_stride, int nseg, int krows, int batch,
+                                  int taper, const double* tab, const typename C2<T>::t* tw, int f_lo, int L, int Lp,
+                                  typename C2<T>::t* E, cudaStream_t st) {
+#define HOS_FRONT_CASE(LG) \
+  case LG: front_go<LG, Tin, T>(x, x_stride, nseg, krows, batch, taper, tab, tw, f_lo, L, Lp, E, st); break;
+  switch (log2m) {
+    HOS_FRONT_CASE(2) HOS_FRONT_CASE(3) HOS_FRONT_CASE(4) HOS_FRONT_CASE(5) HOS_FRONT_CASE(6) HOS_FRONT_CASE(7)
+    HOS_FRONT_CASE(8) HOS_FRONT_CASE(9) HOS_FRONT_CASE(10) HOS_FRONT_CASE(11) HOS_FRONT_CASE(12)
+    default: return cudaErrorInvalidValue;
+  }
+#undef HOS_FRONT_CASE
+  return cudaGetLastError();
+}
+
+cudaError_t launch_front(const void* x, int x_dtype, int64_t x_stride, int m, int nseg, int krows, int batch,
+                         int taper, const double* tab, const void* tw, int precision, int f_lo, int L, int Lp, void* E,
+                         cudaStream_t st) {
+  int log2m = 0;
+  while ((1 << log2m) < m) log2m++;
+  if ((1 << log2m) != m || m > kFrontMaxM || m < 4) return cudaErrorInvalidValue;
+  if (precision == 32) {
+    if (x_dtype == 0)
+      return front_dispatch<float, float>(log2m, (const float*)x, x_stride, nseg, krows, batch, taper, tab,
+                                          (const float2*)tw, f_lo, L, Lp, (float2*)E, st);
+    return front_dispatch<double, float>(log2m, (const double*)x, x_stride, nseg, krows, batch, taper, tab,
+                                         (const float2*)tw, f_lo, L, Lp, (float2*)E, st);
+  }
+  if (x_dtype == 0)
+    return front_dispatch<float, double>(log2m, (const float*)x, x_stride, nseg, krows, batch, taper, tab,
+                                         (const double2*)tw, f_lo, L, Lp, (double2*)E, st);
+  return front_dispatch<double, double>(log2m, (const double*)x, x_stride, nseg, krows, batch, taper, tab,
+                                        (const double2*)tw, f_lo, L, Lp, (double2*)E, st);
 }
 
 // ===========================================================================
@@ -428,6 +660,7 @@ __global__ void __launch_bounds__(128, 2) k_triple_w(const __grid_constant__ Tri
   const int Lp = a.Lp, f_lo = a.f_lo;
   const int total = (int)(u1 - u0);
   asm volatile("griddepcontrol.wait;" ::: "memory");  // E is written by the previous kernel
+  asm volatile("griddepcontrol.launch_dependents;");   // K4a may be scheduled as K2 CTAs retire
 
   // producer: stages the warp's (region, segment) units two at a time, kWarpPairs-1 pairs ahead;
   // lane l copies chunks l, l+32, ... of each unit from p_seg + p_off[chunk slot]
@@ -679,6 +912,8 @@ __global__ void __launch_bounds__(kScanThreads) k_line_scan(const P2* __restrict
                                                             int64_t part_series_stride, SlotInfo si,
                                                             const int64_t* __restrict__ line_start, int64_t line_begin,
                                                             int64_t s_series_stride, double2* __restrict__ S) {
+  asm volatile("griddepcontrol.launch_dependents;");  // K4b may be scheduled as we retire
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // partial slots come from K2
   __shared__ double2 wsum[kScanThreads / 32];
   const int64_t l = line_begin + blockIdx.x;
   const int series = blockIdx.y;
@@ -722,11 +957,11 @@ cudaError_t launch_line_scan(const void* part, int nparts, int64_t part_stride, 
   dim3 grid((unsigned)nlines, batch);
   const int64_t pss = part_stride * nparts;
   if (precision == 32)
-    k_line_scan<float2><<<grid, kScanThreads, 0, st>>>((const float2*)part, nparts, part_stride, pss, si, line_start,
-                                                       line_begin, ncells_series, (double2*)S);
+    return launch_pdl_kernel(k_line_scan<float2>, grid, dim3(kScanThreads), 0, st, (const float2*)part, nparts,
+                             part_stride, pss, si, line_start, line_begin, ncells_series, (double2*)S);
   else
-    k_line_scan<double2><<<grid, kScanThreads, 0, st>>>((const double2*)part, nparts, part_stride, pss, si, line_start,
-                                                        line_begin, ncells_series, (double2*)S);
+    return launch_pdl_kernel(k_line_scan<double2>, grid, dim3(kScanThreads), 0, st, (const double2*)part, nparts,
+                             part_stride, pss, si, line_start, line_begin, ncells_series, (double2*)S);
   return cudaGetLastError();
 }
 
@@ -739,6 +974,7 @@ cudaError_t launch_line_scan(const void* part, int nparts, int64_t part_stride, 
 
 template <typename OUT>
 __global__ void __launch_bounds__(128) k_box3(BoxArgs a, int row0) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // prefix sums come from K4a
   const int k1 = row0 + blockIdx.y;
   const int k2 = blockIdx.x * blockDim.x + threadIdx.x;
   const int series = blockIdx.z;
@@ -765,6 +1001,7 @@ __global__ void __launch_bounds__(128) k_box3(BoxArgs a, int row0) {
 
 template <typename OUT>
 __global__ void __launch_bounds__(64) k_box4(BoxArgs a, int pair0) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // prefix sums come from K4a
   const int pair = pair0 + blockIdx.x;
   const int series = blockIdx.y;
   const int k1 = __ldg(a.pair_k1 + pair), k2 = __ldg(a.pair_k2 + pair);
@@ -801,13 +1038,13 @@ cudaError_t launch_box(const BoxArgs& a, cudaStream_t st) {
     int mx = 1;
     for (int r = a.row_begin; r < a.row_end; r++) mx = max(mx, p3_len(a.m, r));
     dim3 grid((mx + 127) / 128, a.row_end - a.row_begin, a.batch);
-    if (a.precision == 32) k_box3<float2><<<grid, 128, 0, st>>>(a, a.row_begin);
-    else k_box3<double2><<<grid, 128, 0, st>>>(a, a.row_begin);
+    return a.precision == 32 ? launch_pdl_kernel(k_box3<float2>, grid, dim3(128), 0, st, a, a.row_begin)
+                             : launch_pdl_kernel(k_box3<double2>, grid, dim3(128), 0, st, a, a.row_begin);
   } else {
     if (a.pair_end <= a.pair_begin) return cudaSuccess;
     dim3 grid(a.pair_end - a.pair_begin, a.batch);
-    if (a.precision == 32) k_box4<float2><<<grid, 64, 0, st>>>(a, a.pair_begin);
-    else k_box4<double2><<<grid, 64, 0, st>>>(a, a.pair_begin);
+    return a.precision == 32 ? launch_pdl_kernel(k_box4<float2>, grid, dim3(64), 0, st, a, a.pair_begin)
+                             : launch_pdl_kernel(k_box4<double2>, grid, dim3(64), 0, st, a, a.pair_begin);
   }
   return cudaGetLastError();
 }

@@ -2,6 +2,7 @@
 //
 //   K0 prep     segment + demean (+ Hann) + cast        hospectra/series.py:159-165
 //   (cuFFT)     batched R2C / D2Z per segment            hospectra/dft.py:36-41
+//   K0+1 front  fused segment + demean + taper + shared-memory FFT + extension (power-of-two m)
 //   K1 extend   conjugate-symmetric extension of the half spectrum onto the
 //               frequency window [f_lo, f_hi] the triple product reads
 //   K2 triple   R(line, c) = sum_i F_i(row) F_i(c) G_i(row + c [+ a])  over D_h,
@@ -87,6 +88,13 @@ int triple_occupancy(int precision);
 cudaError_t launch_prep(const void* x, int x_dtype, int64_t x_stride, int m, int seg_begin, int nseg,
                         int batch, int taper, const double* taper_tab, int precision, void* seg_out,
                         cudaStream_t st);
+// fused K0 + FFT + K1 for power-of-two m <= kFrontMaxM (tw: m twiddles exp(-2 pi i t/m) in the
+// compute precision); returns cudaErrorInvalidValue for other m
+constexpr int kFrontMaxM = 4096;
+// x: first segment of series 0 (series b at x + b*x_stride); segment s of series b -> E row b*krows + s
+cudaError_t launch_front(const void* x, int x_dtype, int64_t x_stride, int m, int nseg, int krows, int batch,
+                         int taper, const double* taper_tab, const void* tw, int precision, int f_lo, int L, int Lp,
+                         void* E, cudaStream_t st);
 cudaError_t launch_extend_half(const void* H, int m, int hstride, int rows, const void* /*unused*/,
                                int f_lo, int L, int Lp, int precision, void* E, cudaStream_t st);
 cudaError_t launch_extend_full(const void* S, int spec_dtype, int m, int rows, int f_lo, int L, int Lp,
