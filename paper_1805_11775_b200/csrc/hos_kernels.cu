@@ -886,24 +886,23 @@ __device__ __forceinline__ int cell_slots(const SlotInfo& si, int nparts, int64_
   return region_slots(r, si.nseg, (int64_t)si.nregions * si.nseg, si.nwarps);
 }
 
+// sum of the ns partial slots of one cell in slot order (fp64); the loads of
+// a 16-slot chunk are all issued before the adds (one L2 round trip per chunk)
 template <typename P2>
 __device__ __forceinline__ void sum_slots(const P2* __restrict__ src, int ns, int64_t stride, int64_t idx, double& vr,
                                           double& vi) {
-  int p = 0;
-  for (; p + 4 <= ns; p += 4) {
-    const P2 v0 = src[(p + 0) * stride + idx];
-    const P2 v1 = src[(p + 1) * stride + idx];
-    const P2 v2 = src[(p + 2) * stride + idx];
-    const P2 v3 = src[(p + 3) * stride + idx];
-    vr += (double)v0.x; vi += (double)v0.y;
-    vr += (double)v1.x; vi += (double)v1.y;
-    vr += (double)v2.x; vi += (double)v2.y;
-    vr += (double)v3.x; vi += (double)v3.y;
-  }
-  for (; p < ns; p++) {
-    const P2 v = src[p * stride + idx];
-    vr += (double)v.x;
-    vi += (double)v.y;
+  constexpr int kChunk = 16;
+  for (int p0 = 0; p0 < ns; p0 += kChunk) {
+    P2 v[kChunk];
+#pragma unroll
+    for (int t = 0; t < kChunk; t++)
+      if (p0 + t < ns) v[t] = src[(int64_t)(p0 + t) * stride + idx];
+#pragma unroll
+    for (int t = 0; t < kChunk; t++)
+      if (p0 + t < ns) {
+        vr += (double)v[t].x;
+        vi += (double)v[t].y;
+      }
   }
 }
 
@@ -981,16 +980,25 @@ __global__ void __launch_bounds__(128) k_box3(BoxArgs a, int row0) {
   if (k2 >= p3_len(a.m, k1)) return;
   const double2* S = (const double2*)a.S + series * a.s_series_stride;
   double sr = 0.0, si = 0.0;
-  for (int u = a.lo; u <= a.hi; u++) {
-    const int64_t line = (int64_t)(k1 + u - a.lo);
-    const int64_t cb = __ldg(a.line_start + line) - a.cell_base;
-    const double2 s1 = S[cb + k2 + a.m3 - 1];
-    sr += s1.x;
-    si += s1.y;
-    if (k2 >= 1) {
-      const double2 s0 = S[cb + k2 - 1];
-      sr -= s0.x;
-      si -= s0.y;
+  // window lines in chunks of 8, every load of a chunk issued before the adds
+  for (int u0 = 0; u0 < a.m3; u0 += 8) {
+    double2 s1[8], s0[8];
+#pragma unroll
+    for (int t = 0; t < 8; t++) {
+      if (u0 + t < a.m3) {
+        const int64_t cb = __ldg(a.line_start + (int64_t)(k1 + u0 + t)) - a.cell_base;
+        s1[t] = S[cb + k2 + a.m3 - 1];
+        s0[t] = k2 >= 1 ? S[cb + k2 - 1] : make_double2(0.0, 0.0);
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < 8; t++) {
+      if (u0 + t < a.m3) {
+        sr += s1[t].x;
+        si += s1[t].y;
+        sr -= s0[t].x;
+        si -= s0[t].y;
+      }
     }
   }
   const int64_t p = __ldg(a.row_off + k1) + k2;
