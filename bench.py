@@ -363,9 +363,11 @@ def run_ours(args):
                     if world == 1 else "pinned H2D + distributed_estimate + rank-0 D2H"},
             "roofline": roof,
             "clocks": clocks,
-            "gpu_launches": 5 * args.steps if world == 1 else None,
-            "gpu_launches_note": "per step: k_prep, k_extend_half_f32, k_triple_f32, k_line_scan, k_box "
-                                 "(+ cuFFT's own kernels, not counted)",
+            "gpu_launches": lib.hos_plan_launches(plan.handle) * args.steps if world == 1 else None,
+            "gpu_launches_note": ("per step: k_front (fused demean+Hann+FFT+extension), k_triple_w, k_line_scan, "
+                                  "k_box3" if lib.hos_plan_launches(plan.handle) == 4 else
+                                  "per step: k_prep, k_extend_half, k_triple_w, k_line_scan, k_box3 "
+                                  "(+ cuFFT's own kernels, not counted)"),
         }
         if not args.no_cpu_baseline and world == 1:
             cb = cpu_baseline(args.config, steps=1, warmup=1, segments=args.cpu_segments)

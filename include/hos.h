@@ -99,7 +99,8 @@ int64_t hos_plan_units(const hos_plan* plan);
 int64_t hos_plan_issued(const hos_plan* plan);
 /* Device bytes the plan holds. */
 size_t hos_plan_device_bytes(const hos_plan* plan);
-/* Number of kernels one hos_estimate launches (cuFFT counted as 1). */
+/* Number of this library's kernels one hos_estimate launches: 4 with the fused
+ * front end (power-of-two m), else 5 plus cuFFT's own kernels. */
 int hos_plan_launches(const hos_plan* plan);
 
 /* ---- the hot path -----------------------------------------------------------

@@ -545,7 +545,11 @@ int64_t hos_plan_cells(const hos_plan* p) { return p ? p->geo.ncells : -1; }
 int64_t hos_plan_units(const hos_plan* p) { return p ? p->geo.ncells * (int64_t)p->k : -1; }
 int64_t hos_plan_issued(const hos_plan* p) { return p ? p->geo.issued_cells * (int64_t)p->k : -1; }
 size_t hos_plan_device_bytes(const hos_plan* p) { return p ? p->bytes : 0; }
-int hos_plan_launches(const hos_plan* p) { return p ? 6 : -1; }
+int hos_plan_launches(const hos_plan* p) {
+  // kernels of this library per hos_estimate: fused front | K2 | K4a | K4b, or
+  // K0 | K1 | K2 | K4a | K4b around cuFFT's own kernels (general m)
+  return p ? (p->fused ? 4 : 5) : -1;
+}
 int64_t hos_plan_lines(const hos_plan* p) { return p ? p->geo.nlines : -1; }
 
 int hos_plan_line_starts(const hos_plan* p, int64_t* ls) {

@@ -31,7 +31,7 @@ def main(path, kernel_filter=None):
                   if h[i].startswith("smsp__average_warps_issue_stalled_") and h[i].endswith("_per_issue_active.ratio")
                   and v[i] not in ("", "n/a")]
         stalls.sort(key=lambda t: -t[1])
-        print("  stalls/issue:", ", ".join(f"{n[34:-29]}={x:.2f}" for n, x in stalls[:8]))
+        print("  stalls/issue:", ", ".join(f"{n[34:-23]}={x:.2f}" for n, x in stalls[:8]))
 
 
 if __name__ == "__main__":
