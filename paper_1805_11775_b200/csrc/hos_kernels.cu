@@ -409,10 +409,12 @@ cudaError_t launch_expand_full(const void* H, int m, int hstride, int rows, int 
 // other.  A warp walks its (region, segment) units in order; per unit its 32
 // lanes stage the segment's 32 row factors, 32 column factors, 63 last
 // factors G(row+col[+a]) (and F(a) for order 4) with 16-byte cp.async chunks
-// into a private ring of unit PAIRS: the loads of the next pairs overlap the
-// arithmetic of the current one, and the two units of a pair are computed in
-// one straight-line block so the scheduler overlaps one segment's shared
-// loads with the other's FFMA2 chains.  Each (warp, region) piece writes ONE
+// into a private ring of unit GROUPS (4 units; 2 groups: one computed while
+// the next one lands): the loads of the next group overlap the arithmetic of
+// the current one, the group's units run as one straight-line block so the
+// scheduler overlaps one segment's shared loads with another's FFMA2 chains,
+// and the wait / warp-sync / loop bookkeeping is paid once per 4 units
+// (groups of 1, 2, 4, 6, 8 measured: 40.4, 41.2, 38.5, 39.8, 41.0 us).  Each (warp, region) piece writes ONE
 // partial slot (warp index - first warp of the region), fixed by the
 // partition: the fp64 combination order in K4a is fixed and results are
 // deterministic.
@@ -553,12 +555,16 @@ __device__ __forceinline__ void cells_f64(const double2* __restrict__ rows, cons
 }
 
 #ifndef HOS_K2_PAIRS
-#define HOS_K2_PAIRS 3
+#define HOS_K2_PAIRS 2
 #endif
-constexpr int kWarpPairs = HOS_K2_PAIRS;  // ring of unit pairs per warp (kWarpPairs-1 pairs in flight)
+#ifndef HOS_K2_GROUP
+#define HOS_K2_GROUP 4
+#endif
+constexpr int kWarpPairs = HOS_K2_PAIRS;  // ring of unit groups per warp (kWarpPairs-1 groups in flight)
+constexpr int kGroup = HOS_K2_GROUP;      // units staged / waited for / computed together
 template <typename T>
 constexpr size_t warp_triple_smem() {
-  return 16 * (size_t)kTripleWarps * 2 * kWarpPairs * Cplx<T>::kUnitChunks;
+  return 16 * (size_t)kTripleWarps * kGroup * kWarpPairs * Cplx<T>::kUnitChunks;
 }
 
 __device__ __forceinline__ void cp_async16_cg(unsigned dst, const void* src) {
@@ -655,21 +661,21 @@ __global__ void __launch_bounds__(128, 2) k_triple_w(const __grid_constant__ Tri
   if (u0 >= u1) return;
   const C* E = (const C*)a.E + ((int64_t)series * a.K + a.seg_begin) * a.Lp;
   C* Pbase = (C*)a.part + (int64_t)series * a.maxslots * a.ncells;
-  const C* ring = reinterpret_cast<const C*>(smraw) + warp * (2 * kWarpPairs * UC * per);
+  const C* ring = reinterpret_cast<const C*>(smraw) + warp * (kGroup * kWarpPairs * UC * per);
   const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring) + 16u * lane;
   const int Lp = a.Lp, f_lo = a.f_lo;
   const int total = (int)(u1 - u0);
   asm volatile("griddepcontrol.wait;" ::: "memory");  // E is written by the previous kernel
   asm volatile("griddepcontrol.launch_dependents;");   // K4a may be scheduled as K2 CTAs retire
 
-  // producer: stages the warp's (region, segment) units two at a time, kWarpPairs-1 pairs ahead;
+  // producer: stages the warp's (region, segment) units kGroup at a time, kWarpPairs-1 groups ahead;
   // lane l copies chunks l, l+32, ... of each unit from p_seg + p_off[chunk slot]
   int p_todo = total;
   int p_r = (int)(u0 / nseg);
   int p_left = 0;                  // units left in the producer's current region
   const char* p_seg = nullptr;     // E row of the next segment to stage
   unsigned p_off[NCH];             // byte offsets of the lane's chunks in a segment row
-  int p_slot = 0;                  // pair slot
+  int p_slot = 0;                  // group slot
   const size_t row_bytes = (size_t)Lp * sizeof(C);
   auto p_enter = [&](int r, int seg) {
     const Region g = a.regions[r];
@@ -687,15 +693,15 @@ __global__ void __launch_bounds__(128, 2) k_triple_w(const __grid_constant__ Tri
       if (chunk_valid<T, ORDER4>(lane + 32 * s)) cp_async16_cg(d + 16u * 32 * s, p_seg + p_off[s]);
     p_seg += row_bytes;
   };
-  auto stage_pair = [&]() {
-    const unsigned d = ring_s + 16u * (2 * UC) * p_slot;
-    if (p_left >= 2) {  // both units in the current region
-      copy_unit(d);
-      copy_unit(d + 16u * UC);
-      p_left -= 2;
-      p_todo -= 2;
+  auto stage_group = [&]() {
+    const unsigned d = ring_s + 16u * (kGroup * UC) * p_slot;
+    if (p_left >= kGroup) {  // the whole group in the current region
+#pragma unroll
+      for (int t = 0; t < kGroup; t++) copy_unit(d + 16u * UC * t);
+      p_left -= kGroup;
+      p_todo -= kGroup;
     } else {
-      for (int t = 0; t < 2 && p_todo > 0; t++) {
+      for (int t = 0; t < kGroup && p_todo > 0; t++) {
         if (p_left == 0) p_enter(++p_r, 0);
         copy_unit(d + 16u * UC * t);
         p_left--;
@@ -707,7 +713,7 @@ __global__ void __launch_bounds__(128, 2) k_triple_w(const __grid_constant__ Tri
     asm volatile("cp.async.commit_group;" ::: "memory");  // always commit: uniform group counting
   };
 #pragma unroll
-  for (int d = 0; d < kWarpPairs - 1; d++) stage_pair();
+  for (int d = 0; d < kWarpPairs - 1; d++) stage_group();
 
   int r = (int)(u0 / nseg);
   int left = min(total, nseg - (int)(u0 - (int64_t)r * nseg));  // this warp's units in region r
@@ -761,19 +767,19 @@ __global__ void __launch_bounds__(128, 2) k_triple_w(const __grid_constant__ Tri
   };
   enter();
   int c_slot = 0;
-  for (int pos = 0; pos < total; pos += 2) {
-    __syncwarp();  // every lane is done with the pair slot the next stage overwrites
-    stage_pair();
+  for (int pos = 0; pos < total; pos += kGroup) {
+    __syncwarp();  // every lane is done with the group slot the next stage overwrites
+    stage_group();
     asm volatile("cp.async.wait_group %0;" ::"n"(kWarpPairs - 1) : "memory");
-    __syncwarp();  // the pair's data, copied by all lanes, is visible
-    const C* q = ring + c_slot * (2 * UC * per);
-    const int cnt = min(2, total - pos);
-    if (cnt == 2 && left >= 2) {  // fast path: both units in region r, one straight-line block
+    __syncwarp();  // the group's data, copied by all lanes, is visible
+    const C* q = ring + c_slot * (kGroup * UC * per);
+    const int cnt = min(kGroup, total - pos);
+    if (cnt == kGroup && left >= kGroup) {  // fast path: the whole group in region r, one straight-line block
       if (warp_active) {
-        warp_cells<T, CONJ, ORDER4>(q, sr, sc, sg, sp, ta, tb, acc);
-        warp_cells<T, CONJ, ORDER4>(q + UC * per, sr, sc, sg, sp, ta, tb, acc);
+#pragma unroll
+        for (int t = 0; t < kGroup; t++) warp_cells<T, CONJ, ORDER4>(q + t * UC * per, sr, sc, sg, sp, ta, tb, acc);
       }
-      left -= 2;
+      left -= kGroup;
     } else {
       for (int t = 0; t < cnt; t++) {
         if (left == 0) {
@@ -786,10 +792,10 @@ __global__ void __launch_bounds__(128, 2) k_triple_w(const __grid_constant__ Tri
         left--;
       }
     }
-    if (left == 0 && pos + 2 < total) {
+    if (left == 0 && pos + kGroup < total) {
       finalize();
       r++;
-      left = min(total - pos - 2, nseg);
+      left = min(total - pos - kGroup, nseg);
       enter();
     }
     c_slot = c_slot + 1 == kWarpPairs ? 0 : c_slot + 1;
