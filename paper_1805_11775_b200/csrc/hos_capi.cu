@@ -54,7 +54,7 @@ struct hos_plan {
   int L = 0, Lp = 0; // extended-spectrum length / pitch (complex elements)
   // device tables
   hos::Region* d_regions = nullptr;
-  int32_t* d_line_region0 = nullptr;
+  int32_t* d_line_tile0 = nullptr;
   int32_t* d_line_cmax = nullptr;
   int64_t* d_line_start = nullptr;
   int64_t* d_row_off = nullptr;
@@ -191,7 +191,7 @@ int slots_needed(const hos_plan* p, int nseg, int n) {
 
 hos::SlotInfo slot_info(const hos_plan* p, int nseg, int n) {
   hos::SlotInfo si{};
-  si.line_region0 = p->d_line_region0;
+  si.line_tile0 = p->d_line_tile0;
   si.nseg = nseg;
   si.nregions = (int)p->geo.regions.size();
   si.nwarps = nwarps_for(p, nseg, n);
@@ -459,7 +459,7 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
 
   std::vector<int32_t> cmax(g.line_cmax.begin(), g.line_cmax.end());
   if ((rc = upload(p, &p->d_regions, g.regions))) return bail(rc);
-  if ((rc = upload(p, &p->d_line_region0, g.line_region0))) return bail(rc);
+  if ((rc = upload(p, &p->d_line_tile0, g.line_tile0))) return bail(rc);
   if ((rc = upload(p, &p->d_line_cmax, cmax))) return bail(rc);
   if ((rc = upload(p, &p->d_line_start, g.line_start))) return bail(rc);
   if ((rc = upload(p, &p->d_row_off, g.row_off))) return bail(rc);
@@ -530,7 +530,7 @@ void hos_plan_destroy(hos_plan* p) {
   if (p->cap2) cudaStreamDestroy(p->cap2);
   for (auto e : p->chunk_ev) cudaEventDestroy(e);
   for (auto& kv : p->ffts) cufftDestroy(kv.second);
-  void* bufs[] = {p->d_regions, p->d_line_region0, p->d_line_cmax, p->d_line_start, p->d_row_off, p->d_pair_k1, p->d_pair_k2,
+  void* bufs[] = {p->d_regions, p->d_line_tile0, p->d_line_cmax, p->d_line_start, p->d_row_off, p->d_pair_k1, p->d_pair_k2,
                   p->d_pair_base, p->d_line_of_ab, p->d_taper, p->d_tw, p->d_seg, p->d_half, p->d_E, p->d_part,
                   p->d_S, p->d_xin, p->d_out};
   for (void* b : bufs)

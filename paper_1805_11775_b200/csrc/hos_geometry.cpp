@@ -59,12 +59,12 @@ struct RegionRec {
   int line0, nrows, row_freq0, plane_freq, col0;
 };
 
-void add_band_regions(std::vector<RegionRec>& regs, std::vector<int32_t>& line_region0, int line0, int nrows,
+void add_band_regions(std::vector<RegionRec>& regs, std::vector<int32_t>& line_tile0, int line0, int nrows,
                       int row_freq0, int plane_freq, int lo, int cmax_band) {
   const int ncols = cmax_band - lo + 1;
-  const int nr = (ncols + kRegionCols - 1) / kRegionCols;
-  for (int l = line0; l < line0 + nrows; l++) line_region0[l] = (int32_t)regs.size();
-  for (int r = 0; r < nr; r++) regs.push_back({line0, nrows, row_freq0, plane_freq, lo + r * kRegionCols});
+  const int nr = (ncols + kTileCols - 1) / kTileCols;
+  for (int l = line0; l < line0 + nrows; l++) line_tile0[l] = (int32_t)regs.size();
+  for (int r = 0; r < nr; r++) regs.push_back({line0, nrows, row_freq0, plane_freq, lo + r * kTileCols});
 }
 
 }  // namespace
@@ -122,7 +122,7 @@ std::string Geometry::build(int order_, int m_, int m3_) {
   }
 
   line_a.clear(); line_b.clear(); line_cmax.clear(); line_start.clear();
-  line_region0.clear();
+  line_tile0.clear();
   issued_cells = 0;
   std::vector<RegionRec> regs;
   if (order == 3) {
@@ -135,12 +135,12 @@ std::string Geometry::build(int order_, int m_, int m3_) {
       line_start.push_back(line_start.back() + (cmax3[l] - lo + 1));
     }
     ncells = line_start.back();
-    line_region0.assign(n3lines, 0);
+    line_tile0.assign(n3lines, 0);
     for (int l0 = 0; l0 < n3lines; l0 += kBandRows) {
       const int nr = std::min(kBandRows, n3lines - l0);
       int cb = lo;
       for (int l = l0; l < l0 + nr; l++) cb = std::max(cb, (int)cmax3[l]);
-      add_band_regions(regs, line_region0, l0, nr, lo + l0, 0, lo, cb);
+      add_band_regions(regs, line_tile0, l0, nr, lo + l0, 0, lo, cb);
     }
   } else {
     // lines = raw pairs (a,b) of the order-3 dilation; cols c in [lo, cmax4(a,b)]
@@ -168,35 +168,43 @@ std::string Geometry::build(int order_, int m_, int m3_) {
         line_start.push_back(line_start.back() + (best + hi - lo + 1));
       }
       const int nl = (int)line_a.size() - first_line;
-      line_region0.resize(line_a.size(), 0);
+      line_tile0.resize(line_a.size(), 0);
       for (int l0 = 0; l0 < nl; l0 += kBandRows) {
         const int nr = std::min(kBandRows, nl - l0);
         int cb = lo;
         for (int l = first_line + l0; l < first_line + l0 + nr; l++) cb = std::max(cb, (int)line_cmax[l]);
-        add_band_regions(regs, line_region0, first_line + l0, nr, line_b[first_line + l0], a, lo, cb);
+        add_band_regions(regs, line_tile0, first_line + l0, nr, line_b[first_line + l0], a, lo, cb);
       }
     }
     nlines = (int64_t)line_a.size();
     ncells = line_start.back();
   }
 
+  // tiles -> regions (consecutive pairs; an odd last tile gets an empty partner
+  // that mirrors it, so its staged loads stay in range)
   regions.clear();
+  ntiles = (int)regs.size();
   f_lo = order == 3 ? 2 * lo : 3 * lo;
   f_hi = 0;
-  for (const RegionRec& r : regs) {
+  for (size_t i = 0; i < regs.size(); i += 2) {
     Region g{};
-    g.line0 = r.line0;
-    g.nrows = r.nrows;
-    g.row_freq0 = r.row_freq0;
-    g.plane_freq = r.plane_freq;
-    g.col0 = r.col0;
+    for (int h = 0; h < 2; h++) {
+      const bool real = i + h < regs.size();
+      const RegionRec& r = regs[real ? i + h : i];
+      Tile& t = g.t[h];
+      t.line0 = r.line0;
+      t.nrows = real ? r.nrows : 0;
+      t.row_freq0 = r.row_freq0;
+      t.plane_freq = r.plane_freq;
+      t.col0 = r.col0;
+      // frequencies the tile's staged operands cover
+      const int rmax = r.row_freq0 + kBandRows - 1, cmax = r.col0 + kTileCols - 1;
+      f_hi = std::max({f_hi, r.plane_freq + rmax + cmax, rmax, cmax, r.plane_freq});
+      f_lo = std::min({f_lo, r.plane_freq + r.row_freq0 + r.col0, r.row_freq0, r.col0, r.plane_freq});
+    }
     regions.push_back(g);
-    // frequencies the region's staged operands cover
-    const int rmax = r.row_freq0 + kBandRows - 1, cmax = r.col0 + kRegionCols - 1;
-    f_hi = std::max({f_hi, r.plane_freq + rmax + cmax, rmax, cmax, r.plane_freq});
-    f_lo = std::min({f_lo, r.plane_freq + r.row_freq0 + r.col0, r.row_freq0, r.col0, r.plane_freq});
   }
-  issued_cells = (int64_t)regions.size() * kBandRows * kRegionCols;
+  issued_cells = (int64_t)regions.size() * kRegionCells;
   return "";
 }
 

@@ -1,7 +1,7 @@
 // Host-side geometry of the direct-method estimator: the principal domain
 // P (hospectra/spectra.py:133-168), its window dilation D_h (the raw cells
 // the smoothing reads, SURVEY §8 notation) laid out as CSR "lines", and
-// the 32 x 32 regions that tile D_h for the K2 kernel.
+// the 16 x 32 tiles (paired into K2 regions) that cover D_h.
 #pragma once
 #include <cstdint>
 #include <string>
@@ -41,19 +41,27 @@ int64_t domain_size(int order, int m);
 // rows [start, stop) of the lexicographic domain into out ((stop-start) x (order-1))
 void domain_rows(int order, int m, int64_t start, int64_t stop, int32_t* out);
 
-// K2 work decomposition.  D_h is cut into regions of up to kBandRows
-// consecutive lines (a "band" of one plane) x kRegionCols columns; a warp
-// owns one region at a time (K2 splits regions x segments across warps).
-constexpr int kBandRows = 32;    // lines per band (4 lane rows x 8 rows)
-constexpr int kRegionCols = 32;  // columns per region (8 lanes x 4)
+// K2 work decomposition.  D_h is cut into TILES of up to kBandRows
+// consecutive lines (a "band" of one plane) x kTileCols columns, listed band
+// after band; consecutive tiles are paired into REGIONS (a warp's unit of
+// work: 2 tiles x 16 lines x 32 columns = 1024 cells).  16-line bands halve
+// the staircase waste along D_h's sloped edges; pairing tiles (possibly of
+// different bands) keeps a warp's tile of 32 cells per lane.
+constexpr int kBandRows = 16;    // lines per band / tile (2 lane rows x 8 rows)
+constexpr int kTileCols = 32;    // columns per tile (8 lanes x 4)
+constexpr int kRegionCells = 2 * kBandRows * kTileCols;
 
-struct Region {
+struct Tile {
   int32_t line0;      // first line of the band
-  int32_t nrows;      // lines in the band (<= kBandRows)
+  int32_t nrows;      // lines in the band (<= kBandRows; 0: empty second tile)
   int32_t row_freq0;  // frequency of line0's row factor (order 3: a, order 4: b)
   int32_t plane_freq; // order 4: a of the plane; order 3: 0
-  int32_t col0;       // first column of the region
-  int32_t pad[3];
+  int32_t col0;       // first column of the tile
+};
+
+struct Region {
+  Tile t[2];
+  int32_t pad[2];
 };
 
 struct Geometry {
@@ -78,10 +86,11 @@ struct Geometry {
   // order 3: line index = a - lo; lines of output row k1 start at k1
   // frequencies any region reads (inclusive), for the extended spectrum
   int f_lo = 0, f_hi = 0;
-  // K2 regions
-  std::vector<Region> regions;        // flat region list (band after band)
-  std::vector<int32_t> line_region0;  // per line: index of the region holding its first column
-  int64_t issued_cells = 0;           // cells computed by K2 (regions x 32 x 32)
+  // K2 tiles and regions
+  std::vector<Region> regions;        // tile pairs (tile 2r and 2r+1 of the band-major tile list)
+  int ntiles = 0;
+  std::vector<int32_t> line_tile0;    // per line: index of the tile holding its first column
+  int64_t issued_cells = 0;           // cells computed by K2 (regions x 1024)
 
   std::string build(int order, int m, int m3);  // returns "" or an error message
 };

@@ -403,68 +403,63 @@ cudaError_t launch_expand_full(const void* H, int m, int hstride, int rows, int 
 // ===========================================================================
 // K2: triple / quadruple product over D_h (hospectra/spectra.py:227-263).
 //
-// Work = nregions x nseg units (a region is 32 x 32 cells of D_h: 32 lines x
-// 32 columns); the nwarps warps of the launch take equal contiguous unit
-// ranges, so every warp does the same work and warps never wait for each
-// other.  A warp walks its (region, segment) units in order; per unit its 32
-// lanes stage the segment's 32 row factors, 32 column factors, 63 last
-// factors G(row+col[+a]) (and F(a) for order 4) with 16-byte cp.async chunks
-// into a private ring of unit GROUPS (4 units; 2 groups: one computed while
-// the next one lands): the loads of the next group overlap the arithmetic of
-// the current one, the group's units run as one straight-line block so the
+// Work = nregions x nseg units; a region is a pair of D_h tiles (16 lines x
+// 32 columns each, hos_geometry.h), a unit one region in one segment.  The
+// nwarps warps of the launch take equal contiguous unit ranges, so every
+// warp does the same work and warps never wait for each other.  A warp walks
+// its units in order; per unit its 32 lanes stage, for each tile, the
+// segment's 16 row factors, 32 column factors, 47 last factors
+// G(row+col[+a]) (and F(a) for order 4) with 16-byte cp.async chunks into a
+// private ring of unit GROUPS (4 units; 2 groups: one computed while the next
+// one lands): the loads of the next group overlap the arithmetic of the
+// current one, the group's units run as one straight-line block so the
 // scheduler overlaps one segment's shared loads with another's FFMA2 chains,
 // and the wait / warp-sync / loop bookkeeping is paid once per 4 units
-// (groups of 1, 2, 4, 6, 8 measured: 40.4, 41.2, 38.5, 39.8, 41.0 us).  Each (warp, region) piece writes ONE
-// partial slot (warp index - first warp of the region), fixed by the
-// partition: the fp64 combination order in K4a is fixed and results are
-// deterministic.
+// (groups of 1, 2, 4, 6, 8 measured: 40.4, 41.2, 38.5, 39.8, 41.0 us).  Each
+// (warp, region) piece writes ONE partial slot (warp index - first warp of
+// the region), fixed by the partition: the fp64 combination order in K4a is
+// fixed and results are deterministic.
 //
-// Lane (ta, tb) owns rows ta+4i (i<8) and columns tb+8j (j<4) of its region:
-// 8 row + 4 column + 14 G values per segment (cell (i,j) reads G at 4(i+2j));
-// every shared load is a broadcast over <= 11 consecutive 8-byte values.
-// fp32 spectra are plain float2 (8 bytes): a 16-byte "quad" layout would
-// double the shared-memory wavefronts, which bound this kernel (ncu r01:
-// LSU data pipe 71% busy at 46% FMA).  The operand forms the complex FFMA2
-// products need are built in registers, once per column / G value:
-//   p    = fa.re * fb + fa.im * (-fb.im, fb.re)           (FMUL2 + FFMA2)
-//   acc += p.re * conj(g) + p.im * (g.im, g.re)           (2 FFMA2, CONJ)
-//   acc += p.re * g       + p.im * (-g.im, g.re)          (2 FFMA2, !CONJ)
-// fp64: same mapping, scalar DFMA on double2 spectra.
+// Lane 16h + 4u + v works on tile h of the region, rows u + 4i (i<4) and
+// columns v + 4j (j<8): both progressions have step 4, so cell (i,j) reads G
+// at u + v + 4(i+j) and a lane needs 4 row + 8 column + 11 G values per
+// segment; every shared load reads <= 7 consecutive 8-byte values per tile,
+// and the tiles' staged copies sit 8 elements apart modulo the bank width, so
+// no load has a bank conflict (an 8x4 lane tile with step-2 columns had
+// 3.2M conflicts per launch).  fp32 spectra are plain float2 (8 bytes): a 16-byte "quad"
+// layout would double the shared-memory wavefronts, which bounded an earlier
+// version (LSU data pipe 71% busy at 46% FMA).  Two accumulators per cell (see
+// cells_f32).  fp64: same mapping, scalar DFMA on double2 spectra.
 
 template <typename T>
 struct Cplx;
 template <>
 struct Cplx<float> {
   using C = float2;  // spectrum element / accumulator / partial
-  static constexpr int kUnitChunks = 68;  // rows 17 | cols 17 | G 32 | plane 1 (+1 pad) 16-byte chunks
+  static constexpr int kUnitChunks = 104;  // 2 tiles x (rows 9 | cols 17 | G 24 | plane 1 | pad 1) 16-byte chunks
 };
 template <>
 struct Cplx<double> {
   using C = double2;
-  static constexpr int kUnitChunks = 128;  // rows 32 | cols 32 | G 63 | plane 1
+  static constexpr int kUnitChunks = 200;  // 2 tiles x (rows 16 | cols 32 | G 47 | plane 1 | pad 4)
 };
 
-// chunk offsets of the operands inside a staged unit
+// chunk offsets of the operands of one tile inside a staged unit (tile h at h * half)
 template <typename T>
 struct UnitLayout;
 template <>
 struct UnitLayout<float> {
-  static constexpr int rows = 0, cols = 17, g = 34, plane = 66;
-  static constexpr int row_chunks = 17, col_chunks = 17, g_chunks = 32;
+  static constexpr int rows = 0, cols = 9, g = 26, plane = 50, half = 52;  // tile 1 at +104 elements (= 8 mod 16)
 };
 template <>
 struct UnitLayout<double> {
-  static constexpr int rows = 0, cols = 32, g = 64, plane = 127;
-  static constexpr int row_chunks = 32, col_chunks = 32, g_chunks = 63;
+  static constexpr int rows = 0, cols = 16, g = 48, plane = 95, half = 100;  // tile 1 at +100 elements (= 4 mod 8)
 };
 
-__device__ __forceinline__ float2 neg_swap(float2 v) {  // (-v.im, v.re) = i v
-  return make_float2(__int_as_float(__float_as_int(v.y) ^ 0x80000000), v.x);
-}
 // conj(*p) from its own shared load: the negation happens in place in the
 // loaded register pair, and FFMA2's free operand swap turns (re, -im) into
 // (-im, re) = i * value -- no register copies (ptxas duplicates pairs built
-// with neg_swap on values that stay live).
+// from values that stay live).
 __device__ __forceinline__ float2 lds_conj(const float2* p) {
   float2 v;
   asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];"
@@ -474,41 +469,46 @@ __device__ __forceinline__ float2 lds_conj(const float2* p) {
   return v;
 }
 
-// one segment of a lane's 8x4 micro-tile: rows/cols/g point at the segment's
-// staged factors.  Two accumulators per cell, aR += g.re p and aI += g.im p
-// (p = F(row) F(col) [F(a)]): the last factor enters only as broadcast
-// scalars, so no operand form of it has to be built, and the two updates of
-// a cell are independent FFMA2s.  The cell value is aR -+ i aI (CONJ: -).
+// one segment of a lane's 4x8 micro-tile: rows/cols/gs point at the lane's
+// first row / column / G factor of the segment (steps of 4).  p = F(row)
+// F(col) [F(a)] as fb.re * fa + fb.im * (i fa), the i fa operand from a second
+// shared load of the row negated in place (free FFMA2 swap); two
+// accumulators per cell, aR += g.re p and aI += g.im p: the last factor
+// enters only as broadcast scalars, so no operand form of it has to be built,
+// and the two updates of a cell are independent FFMA2s.  The cell value is
+// aR -+ i aI (CONJ: -).
 template <bool ORDER4>
 __device__ __forceinline__ void cells_f32(const float2* __restrict__ rows, const float2* __restrict__ cols,
-                                          const float2* __restrict__ gs, const float2* __restrict__ plane, int ta,
-                                          int tb, float2 (&aR)[8][4], float2 (&aI)[8][4]) {
-  float2 fa[8], fb[4], fbc[4];
-#pragma unroll
-  for (int i = 0; i < 8; i++) fa[i] = rows[ta + 4 * i];
+                                          const float2* __restrict__ gs, const float2* __restrict__ plane,
+                                          float2 (&aR)[4][8], float2 (&aI)[4][8]) {
+  float2 fa[4], fac[4], fb[8];
   if (ORDER4) {
     const float2 pa = *plane, pac = lds_conj(plane);
 #pragma unroll
-    for (int i = 0; i < 8; i++) {
-      const float2 t = fmul2(make_float2(fa[i].x, fa[i].x), pa);
-      fa[i] = ffma2(make_float2(fa[i].y, fa[i].y), make_float2(pac.y, pac.x), t);
+    for (int i = 0; i < 4; i++) {
+      const float2 r = rows[4 * i];
+      const float2 t = fmul2(make_float2(r.x, r.x), pa);
+      fa[i] = ffma2(make_float2(r.y, r.y), make_float2(pac.y, pac.x), t);
+      fac[i] = make_float2(fa[i].x, -fa[i].y);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      fa[i] = rows[4 * i];
+      fac[i] = lds_conj(rows + 4 * i);
     }
   }
 #pragma unroll
-  for (int j = 0; j < 4; j++) {
-    fb[j] = cols[tb + 8 * j];
-    fbc[j] = lds_conj(cols + tb + 8 * j);
-  }
-  const float2* gq = gs + ta + tb;
+  for (int j = 0; j < 8; j++) fb[j] = cols[4 * j];
 #pragma unroll
-  for (int q = 0; q < 14; q++) {
-    const float2 g = gq[4 * q];
+  for (int q = 0; q < 11; q++) {
+    const float2 g = gs[4 * q];
 #pragma unroll
-    for (int j = 0; j < 4; j++) {
-      const int i = q - 2 * j;
-      if (i < 0 || i > 7) continue;
-      float2 p = fmul2(make_float2(fa[i].x, fa[i].x), fb[j]);
-      p = ffma2(make_float2(fa[i].y, fa[i].y), make_float2(fbc[j].y, fbc[j].x), p);
+    for (int i = 0; i < 4; i++) {
+      const int j = q - i;
+      if (j < 0 || j > 7) continue;
+      float2 p = fmul2(make_float2(fb[j].x, fb[j].x), fa[i]);
+      p = ffma2(make_float2(fb[j].y, fb[j].y), make_float2(fac[i].y, fac[i].x), p);
       aR[i][j] = ffma2(make_float2(g.x, g.x), p, aR[i][j]);
       aI[i][j] = ffma2(make_float2(g.y, g.y), p, aI[i][j]);
     }
@@ -517,30 +517,29 @@ __device__ __forceinline__ void cells_f32(const float2* __restrict__ rows, const
 
 template <bool CONJ, bool ORDER4>
 __device__ __forceinline__ void cells_f64(const double2* __restrict__ rows, const double2* __restrict__ cols,
-                                          const double2* __restrict__ gs, const double2* __restrict__ plane, int ta,
-                                          int tb, double2 (&acc)[8][4]) {
-  double2 fa[8], fb[4];
+                                          const double2* __restrict__ gs, const double2* __restrict__ plane,
+                                          double2 (&acc)[4][8]) {
+  double2 fa[4], fb[8];
 #pragma unroll
-  for (int i = 0; i < 8; i++) fa[i] = rows[ta + 4 * i];
+  for (int i = 0; i < 4; i++) fa[i] = rows[4 * i];
   if (ORDER4) {
     const double2 pa = *plane;
 #pragma unroll
-    for (int i = 0; i < 8; i++) {
+    for (int i = 0; i < 4; i++) {
       const double re = fa[i].x * pa.x - fa[i].y * pa.y;
       const double im = fa[i].x * pa.y + fa[i].y * pa.x;
       fa[i] = make_double2(re, im);
     }
   }
 #pragma unroll
-  for (int j = 0; j < 4; j++) fb[j] = cols[tb + 8 * j];
-  const double2* gq = gs + ta + tb;
+  for (int j = 0; j < 8; j++) fb[j] = cols[4 * j];
 #pragma unroll
-  for (int q = 0; q < 14; q++) {
-    const double2 g = gq[4 * q];
+  for (int q = 0; q < 11; q++) {
+    const double2 g = gs[4 * q];
 #pragma unroll
-    for (int j = 0; j < 4; j++) {
-      const int i = q - 2 * j;
-      if (i < 0 || i > 7) continue;
+    for (int i = 0; i < 4; i++) {
+      const int j = q - i;
+      if (j < 0 || j > 7) continue;
       const double pr = fma(-fa[i].y, fb[j].y, fa[i].x * fb[j].x);
       const double pi = fma(fa[i].y, fb[j].x, fa[i].x * fb[j].y);
       if (CONJ) {
@@ -581,20 +580,24 @@ __device__ __forceinline__ int region_slots(int r, int nseg, int64_t W, int64_t 
 // chunks of a staged unit that are copied (the rest is padding)
 template <typename T, bool ORDER4>
 __device__ __forceinline__ bool chunk_valid(int c) {
-  return c < UnitLayout<T>::plane + (ORDER4 ? 1 : 0);
+  using L = UnitLayout<T>;
+  return c < 2 * L::half && c % L::half < L::plane + (ORDER4 ? 1 : 0);
 }
 // Source of (valid) chunk c of a staged unit, as an element offset from the
 // segment's E row.  fp32 operands are copied from the 16-byte-aligned element
 // at or below their start; the consumer adds the operand's shift (0 or 1).
 template <typename T>
-__device__ __forceinline__ int chunk_src(int c, int o_row, int o_col, int o_g, int o_pl) {
+__device__ __forceinline__ int chunk_src(int c, const Region* __restrict__ rg, int f_lo) {
   using L = UnitLayout<T>;
   constexpr int per = sizeof(T) == 4 ? 2 : 1;  // elements per chunk
   auto floor_al = [](int o) { return sizeof(T) == 4 ? (o & ~1) : o; };
-  if (c < L::cols) return floor_al(o_row) + per * (c - L::rows);
-  if (c < L::g) return floor_al(o_col) + per * (c - L::cols);
-  if (c < L::plane) return floor_al(o_g) + per * (c - L::g);
-  return floor_al(o_pl);
+  const int h = c >= L::half;
+  const int cc = c - h * L::half;
+  const Tile& t = rg->t[h];
+  if (cc < L::cols) return floor_al(t.row_freq0 - f_lo) + per * (cc - L::rows);
+  if (cc < L::g) return floor_al(t.col0 - f_lo) + per * (cc - L::cols);
+  if (cc < L::plane) return floor_al(t.plane_freq + t.row_freq0 + t.col0 - f_lo) + per * (cc - L::g);
+  return floor_al(t.plane_freq - f_lo);
 }
 
 // per-lane accumulators of a region: fp32 keeps aR / aI (see cells_f32), fp64 the cell value
@@ -602,12 +605,12 @@ template <typename T>
 struct Acc;
 template <>
 struct Acc<float> {
-  float2 r[8][4], i[8][4];
+  float2 r[4][8], i[4][8];
   __device__ __forceinline__ void zero() {
 #pragma unroll
-    for (int a = 0; a < 8; a++)
+    for (int a = 0; a < 4; a++)
 #pragma unroll
-      for (int b = 0; b < 4; b++) r[a][b] = i[a][b] = make_float2(0.f, 0.f);
+      for (int b = 0; b < 8; b++) r[a][b] = i[a][b] = make_float2(0.f, 0.f);
   }
   template <bool CONJ>
   __device__ __forceinline__ float2 cell(int a, int b) const {
@@ -617,12 +620,12 @@ struct Acc<float> {
 };
 template <>
 struct Acc<double> {
-  double2 v[8][4];
+  double2 v[4][8];
   __device__ __forceinline__ void zero() {
 #pragma unroll
-    for (int a = 0; a < 8; a++)
+    for (int a = 0; a < 4; a++)
 #pragma unroll
-      for (int b = 0; b < 4; b++) v[a][b] = make_double2(0.0, 0.0);
+      for (int b = 0; b < 8; b++) v[a][b] = make_double2(0.0, 0.0);
   }
   template <bool CONJ>
   __device__ __forceinline__ double2 cell(int a, int b) const {
@@ -630,16 +633,18 @@ struct Acc<double> {
   }
 };
 
+// lane's operand positions (elements) inside a staged unit: tile base + the
+// tile operand's alignment shift + the lane's first row / column / G offset
+struct LaneOps {
+  int rows, cols, g, plane;
+};
+
 template <typename T, bool CONJ, bool ORDER4>
-__device__ __forceinline__ void warp_cells(const typename Cplx<T>::C* q, int sr, int sc, int sg, int sp, int ta,
-                                           int tb, Acc<T>& acc) {
-  using L = UnitLayout<T>;
-  constexpr int per = sizeof(T) == 4 ? 2 : 1;
+__device__ __forceinline__ void warp_cells(const typename Cplx<T>::C* q, const LaneOps& o, Acc<T>& acc) {
   if constexpr (sizeof(T) == 4)
-    cells_f32<ORDER4>(q + per * L::rows + sr, q + per * L::cols + sc, q + per * L::g + sg, q + per * L::plane + sp,
-                      ta, tb, acc.r, acc.i);
+    cells_f32<ORDER4>(q + o.rows, q + o.cols, q + o.g, q + o.plane, acc.r, acc.i);
   else
-    cells_f64<CONJ, ORDER4>(q + L::rows, q + L::cols, q + L::g, q + L::plane, ta, tb, acc.v);
+    cells_f64<CONJ, ORDER4>(q + o.rows, q + o.cols, q + o.g, q + o.plane, acc.v);
 }
 
 template <typename T, bool CONJ, bool ORDER4>
@@ -650,7 +655,6 @@ __global__ void __launch_bounds__(128, 2) k_triple_w(const __grid_constant__ Tri
   constexpr int NCH = (UC + 31) / 32;           // chunk slots per lane
   extern __shared__ __align__(128) unsigned char smraw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ta = lane >> 3, tb = lane & 7;
   const int series = blockIdx.y;
   const int64_t Nw = a.nwarps;
   const int64_t gw = (int64_t)blockIdx.x * kTripleWarps + warp;
@@ -678,12 +682,9 @@ __global__ void __launch_bounds__(128, 2) k_triple_w(const __grid_constant__ Tri
   int p_slot = 0;                  // group slot
   const size_t row_bytes = (size_t)Lp * sizeof(C);
   auto p_enter = [&](int r, int seg) {
-    const Region g = a.regions[r];
     p_seg = reinterpret_cast<const char*>(E + (int64_t)seg * Lp);
 #pragma unroll
-    for (int s = 0; s < NCH; s++)
-      p_off[s] = (unsigned)sizeof(C) * chunk_src<T>(lane + 32 * s, g.row_freq0 - f_lo, g.col0 - f_lo,
-                                                   g.plane_freq + g.row_freq0 + g.col0 - f_lo, g.plane_freq - f_lo);
+    for (int s = 0; s < NCH; s++) p_off[s] = (unsigned)sizeof(C) * chunk_src<T>(lane + 32 * s, a.regions + r, f_lo);
     p_left = min(nseg - seg, p_todo);
   };
   p_enter(p_r, (int)(u0 - (int64_t)p_r * nseg));
@@ -717,27 +718,28 @@ __global__ void __launch_bounds__(128, 2) k_triple_w(const __grid_constant__ Tri
 
   int r = (int)(u0 / nseg);
   int left = min(total, nseg - (int)(u0 - (int64_t)r * nseg));  // this warp's units in region r
+  // the lane's tile of the region and its rows ra + 4i, columns cb + 4j
+  const int h = lane >> 4, ra = (lane >> 2) & 3, cb = lane & 3;
   int c0 = 0, line0 = 0, nrows = 0;
-  int sr = 0, sc = 0, sg = 0, sp = 0;  // fp32: element shift of each operand in its staged copy
+  LaneOps ops{};
   bool active = false, warp_active = false;
   Acc<T> acc;
   auto enter = [&]() {
-    const Region rg = a.regions[r];
-    c0 = rg.col0 + tb;
-    line0 = rg.line0;
-    nrows = rg.nrows;
-    if (sizeof(T) == 4) {
-      sr = (rg.row_freq0 - f_lo) & 1;
-      sc = (rg.col0 - f_lo) & 1;
-      sg = (rg.plane_freq + rg.row_freq0 + rg.col0 - f_lo) & 1;
-      sp = (rg.plane_freq - f_lo) & 1;
-    }
+    const Tile t = a.regions[r].t[h];
+    using L = UnitLayout<T>;
+    c0 = t.col0 + cb;
+    line0 = t.line0 + ra;
+    nrows = t.nrows - ra;  // lane rows 4i < nrows
+    const int base = h * L::half * per;
+    const int mask = sizeof(T) == 4 ? 1 : 0;  // fp32: operands staged from the aligned element below
+    ops.rows = base + L::rows * per + ((t.row_freq0 - f_lo) & mask) + ra;
+    ops.cols = base + L::cols * per + ((t.col0 - f_lo) & mask) + cb;
+    ops.g = base + L::g * per + ((t.plane_freq + t.row_freq0 + t.col0 - f_lo) & mask) + ra + cb;
+    ops.plane = base + L::plane * per + ((t.plane_freq - f_lo) & mask);
     active = false;
 #pragma unroll
-    for (int i = 0; i < 8; i++) {
-      const int rr = ta + 4 * i;
-      if (rr < nrows && __ldg(a.line_cmax + line0 + rr) >= c0) active = true;
-    }
+    for (int i = 0; i < 4; i++)
+      if (4 * i < nrows && __ldg(a.line_cmax + line0 + 4 * i) >= c0) active = true;
     warp_active = __any_sync(0xffffffffu, active);
     acc.zero();
   };
@@ -746,21 +748,20 @@ __global__ void __launch_bounds__(128, 2) k_triple_w(const __grid_constant__ Tri
     const int pslot = (int)(gw - warp_of_unit((int64_t)r * nseg, W, Nw));
     C* P = Pbase + (int64_t)pslot * a.ncells;
 #pragma unroll
-    for (int i = 0; i < 8; i++) {
-      const int rr = ta + 4 * i;
-      if (rr >= nrows) continue;
-      const int line = line0 + rr;
+    for (int i = 0; i < 4; i++) {
+      if (4 * i >= nrows) continue;
+      const int line = line0 + 4 * i;
       const int cm = __ldg(a.line_cmax + line);
       C* dst = P + (__ldg(a.line_start + line) - a.lo);
 #pragma unroll
-      for (int j = 0; j < 4; j++)
-        if (c0 + 8 * j <= cm) {
+      for (int j = 0; j < 8; j++)
+        if (c0 + 4 * j <= cm) {
           const C cv = acc.template cell<CONJ>(i, j);
           if (a.accumulate) {
-            const C v = dst[c0 + 8 * j];
-            dst[c0 + 8 * j] = C{v.x + cv.x, v.y + cv.y};
+            const C v = dst[c0 + 4 * j];
+            dst[c0 + 4 * j] = C{v.x + cv.x, v.y + cv.y};
           } else {
-            dst[c0 + 8 * j] = cv;
+            dst[c0 + 4 * j] = cv;
           }
         }
     }
@@ -777,7 +778,7 @@ __global__ void __launch_bounds__(128, 2) k_triple_w(const __grid_constant__ Tri
     if (cnt == kGroup && left >= kGroup) {  // fast path: the whole group in region r, one straight-line block
       if (warp_active) {
 #pragma unroll
-        for (int t = 0; t < kGroup; t++) warp_cells<T, CONJ, ORDER4>(q + t * UC * per, sr, sc, sg, sp, ta, tb, acc);
+        for (int t = 0; t < kGroup; t++) warp_cells<T, CONJ, ORDER4>(q + t * UC * per, ops, acc);
       }
       left -= kGroup;
     } else {
@@ -788,7 +789,7 @@ __global__ void __launch_bounds__(128, 2) k_triple_w(const __grid_constant__ Tri
           left = min(total - pos - t, nseg);
           enter();
         }
-        if (warp_active) warp_cells<T, CONJ, ORDER4>(q + t * UC * per, sr, sc, sg, sp, ta, tb, acc);
+        if (warp_active) warp_cells<T, CONJ, ORDER4>(q + t * UC * per, ops, acc);
         left--;
       }
     }
@@ -887,8 +888,8 @@ constexpr int kScanThreads = 256;
 
 // number of partial slots holding cell `idx` (absolute cell of line l)
 __device__ __forceinline__ int cell_slots(const SlotInfo& si, int nparts, int64_t l, int64_t col) {
-  if (si.line_region0 == nullptr) return nparts;
-  const int r = si.line_region0[l] + (int)(col / kRegionCols);
+  if (si.line_tile0 == nullptr) return nparts;
+  const int r = (si.line_tile0[l] + (int)(col / kTileCols)) >> 1;  // tile -> region (tile pair)
   return region_slots(r, si.nseg, (int64_t)si.nregions * si.nseg, si.nwarps);
 }
 

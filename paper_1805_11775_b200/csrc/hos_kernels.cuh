@@ -57,7 +57,7 @@ struct TripleArgs {
   int f_lo;                   // frequency of element 0
   int K;                      // segments per series (E rows per series)
   int seg_begin, seg_end;     // segment range reduced by this launch
-  const Region* regions;      // flat region list (32 x 32 cells each)
+  const Region* regions;      // tile pairs (2 x 16 x 32 cells each)
   int nregions;
   int64_t nwarps;             // warps splitting the region x segment work (<= units)
   const int32_t* line_cmax;
@@ -76,7 +76,7 @@ constexpr int kTripleWarps = 4;   // warps per CTA of the triple-product kernel
 
 // Where the partial slots of a K2 launch are (for the K4a / reduce readers).
 struct SlotInfo {
-  const int32_t* line_region0;  // nullptr: plain buffer with `nparts` parts
+  const int32_t* line_tile0;    // nullptr: plain buffer with `nparts` parts
   int nseg;
   int nregions;
   int64_t nwarps;
