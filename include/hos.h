@@ -171,6 +171,10 @@ int hos_peak_fp32(double* tflops, double* sm_mhz, void* stream);
 int hos_plan_set_timing(hos_plan* plan, int enable);
 /* Diagnostics: K2 CTAs per series (4 warps each). */
 int hos_plan_nctas(const hos_plan* plan);
+/* Diagnostics: a device buffer of 4 x (4 nctas) x batch uint64 that K2 fills
+ * per warp with {start, first staged data, end (globaltimer ns), smid};
+ * NULL disables.  Traced calls run without graph replay. */
+int hos_plan_set_trace(hos_plan* plan, void* trace_dev);
 /* Diagnostics: mean per-launch device time (ms) of each stage {prep, fft,
  * extend, triple, scan, box}: `reps` launches of the stage captured into one
  * CUDA graph, replayed between two events on `stream` after one full estimate

@@ -59,6 +59,7 @@ EXPORTED_SYMBOLS = {
     "hos_plan_nctas": (_i, [_p]),
     "hos_plan_kernel_ms": (_i, [_p, _p, _p]),
     "hos_plan_stage_ms": (_i, [_p, _p]),
+    "hos_plan_set_trace": (_i, [_p, _p]),
     "hos_plan_time_stages": (_i, [_p, _p, _i, _i64, _p, _i, _p, _p]),
 }
 

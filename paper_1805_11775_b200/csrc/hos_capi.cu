@@ -50,6 +50,7 @@ struct hos_plan {
   int maxslots = 1;   // partial slots allocated per series
   int occupancy = 1;  // K2 CTAs per SM
   int sms = 148;
+  int split_wa = 1, split_wb = 1;  // K2 WarpSplit weights for two-CTA-per-SM launches
   int hstride = 0;   // complex elements per half-spectrum row
   int L = 0, Lp = 0; // extended-spectrum length / pitch (complex elements)
   // device tables
@@ -74,6 +75,7 @@ struct hos_plan {
   void* d_xin = nullptr;   // host path staging (batch*k*m*8 bytes)
   void* d_out = nullptr;   // host path staging
   size_t bytes = 0;
+  unsigned long long* trace = nullptr;  // K2 per-warp trace (diagnostics; 4 x nwarps x batch)
   std::map<int, cufftHandle> ffts;  // rows -> plan
   // CUDA graphs of the whole stream-ordered pipeline, one per buffer binding
   struct GraphKey {
@@ -178,14 +180,26 @@ int64_t nwarps_for(const hos_plan* p, int nseg, int n) {
   return std::max<int64_t>(1, std::min<int64_t>((int64_t)n * hos::kTripleWarps, work_items(p) * nseg));
 }
 
-int slots_needed(const hos_plan* p, int nseg, int n) {
-  const int64_t T = work_items(p), W = T * nseg;
-  if (W <= 0) return 1;
+// WarpSplit weights for an n-CTA launch: skewed towards the first wave of
+// CTAs only when every SM holds exactly two CTAs of one series and each warp
+// keeps >= 16 units (so no range can be empty)
+hos::WarpSplit warp_split(const hos_plan* p, int nseg, int n, int batch) {
+  const int64_t W = work_items(p) * nseg, Nw = nwarps_for(p, nseg, n);
+  hos::WarpSplit sp{W, Nw, Nw / 2, 1, 1};
+  if (batch == 1 && n == 2 * p->sms && p->occupancy == 2 && W >= 16 * Nw) {
+    sp.wa = p->split_wa;
+    sp.wb = p->split_wb;
+  }
+  return sp;
+}
+
+int slots_needed(const hos_plan* p, int nseg, int n, int batch) {
+  const int64_t T = work_items(p);
+  if (T * nseg <= 0) return 1;
   // partial slots the worst region needs (same arithmetic as the kernel)
-  const int64_t parts = nwarps_for(p, nseg, n);
-  auto warp = [&](int64_t u) { return ((u + 1) * parts - 1) / W; };
+  const hos::WarpSplit sp = warp_split(p, nseg, n, batch);
   int best = 1;
-  for (int64_t t = 0; t < T; t++) best = std::max(best, (int)(warp((t + 1) * nseg - 1) - warp(t * nseg) + 1));
+  for (int64_t t = 0; t < T; t++) best = std::max(best, sp.region_slots((int)t, nseg));
   return best;
 }
 
@@ -195,6 +209,9 @@ hos::SlotInfo slot_info(const hos_plan* p, int nseg, int n) {
   si.nseg = nseg;
   si.nregions = (int)p->geo.regions.size();
   si.nwarps = nwarps_for(p, nseg, n);
+  const hos::WarpSplit sp = warp_split(p, nseg, n, p->batch);
+  si.split_wa = sp.wa;
+  si.split_wb = sp.wb;
   return si;
 }
 
@@ -210,6 +227,11 @@ hos::TripleArgs triple_args(const hos_plan* p, int seg_begin, int seg_end, int n
   x.regions = p->d_regions;
   x.nregions = (int)p->geo.regions.size();
   x.nwarps = nwarps_for(p, seg_end - seg_begin, n);
+  {
+    const hos::WarpSplit sp = warp_split(p, seg_end - seg_begin, n, batch);
+    x.split_wa = sp.wa;
+    x.split_wb = sp.wb;
+  }
   x.line_cmax = p->d_line_cmax;
   x.line_start = p->d_line_start;
   x.lo = p->geo.win.lo;
@@ -220,6 +242,7 @@ hos::TripleArgs triple_args(const hos_plan* p, int seg_begin, int seg_end, int n
   x.conj = p->conj;
   x.batch = batch;
   x.accumulate = 0;
+  x.trace = p->trace;
   return x;
 }
 
@@ -442,8 +465,15 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
   p->Lp = (p->L + 4 + 1) & ~1;
   cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, device);
   p->occupancy = hos::triple_occupancy(precision);
+  if (const char* env = std::getenv("HOS_K2_SPLIT")) {  // "wa:wb"
+    int wa = 0, wb = 0;
+    if (std::sscanf(env, "%d:%d", &wa, &wb) == 2 && wa > 0 && wb > 0) {
+      p->split_wa = wa;
+      p->split_wb = wb;
+    }
+  }
   p->nctas = nctas_for(p, k, batch);
-  p->maxslots = slots_needed(p, k, p->nctas);
+  p->maxslots = slots_needed(p, k, p->nctas, batch);
   // pipelined host path: equal segment chunks so every chunk launch owns the same slots
   {
     // off by default: each K2 launch still carries ~4 us of prologue + a tail, which
@@ -454,7 +484,7 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
     while (c > 1 && (k % c != 0 || batch != 1)) c--;
     p->e2e_chunks = c;
     p->nctas_chunk = nctas_for(p, k / c, batch);
-    p->maxslots = std::max(p->maxslots, slots_needed(p, k / c, p->nctas_chunk));
+    p->maxslots = std::max(p->maxslots, slots_needed(p, k / c, p->nctas_chunk, batch));
   }
 
   std::vector<int32_t> cmax(g.line_cmax.begin(), g.line_cmax.end());
@@ -569,7 +599,7 @@ int hos_estimate(hos_plan* p, const void* x_dev, int x_dtype, int64_t x_stride, 
     return fail(HOS_EPARAM, "series stride " + std::to_string(x_stride) + " shorter than k*m = " +
                                 std::to_string((int64_t)p->k * p->m));
   cudaStream_t st = (cudaStream_t)stream;
-  if (p->timing || !p->use_graphs) {
+  if (p->timing || p->trace || !p->use_graphs) {
     if (p->timing) CUDA_TRY(cudaEventRecord(p->ev[0], st));
     if ((rc = run_front(p, x_dev, x_dtype, x_stride, st))) return rc;
     return run_back(p, out_dev, st);
@@ -596,7 +626,7 @@ int hos_estimate_from_spectra(hos_plan* p, const void* spec_dev, int spec_dtype,
       for (int i = 1; i <= 3; i++) CUDA_TRY(cudaEventRecord(p->ev[i], s));
     return run_back(p, out_dev, s);
   };
-  if (p->timing || !p->use_graphs) return body(st);
+  if (p->timing || p->trace || !p->use_graphs) return body(st);
   const hos_plan::GraphKey key{1, spec_dev, spec_dtype, 0, out_dev};
   return run_graph(p, key, st, body);
 }
@@ -753,7 +783,7 @@ int hos_estimate_host(hos_plan* p, const void* x_host, int x_dtype, int64_t x_st
     return HOS_OK;
   }
   for (auto e : dev) cudaEventDestroy(e);
-  if (pinned && p->use_graphs && !p->timing) {
+  if (pinned && p->use_graphs && !p->timing && !p->trace) {
     const hos_plan::GraphKey key{2, x_host, x_dtype, x_stride, out_host};
     if (p->e2e_chunks > 1 && p->batch == 1) {
       if ((rc = run_graph(p, key, st, chunked))) return rc;
@@ -799,7 +829,7 @@ int hos_partial_raw(hos_plan* p, const void* x_dev, int x_dtype, int seg_begin, 
                                      E, st));
   }
   int n = nctas_for(p, nseg, 1);
-  while (n > 1 && slots_needed(p, nseg, n) > p->maxslots) n--;
+  while (n > 1 && slots_needed(p, nseg, n, 1) > p->maxslots) n--;
   const hos::TripleArgs ta = triple_args(p, seg_begin, seg_end, n, 1);
   CUDA_TRY(hos::launch_triple(ta, p->precision, st));
   CUDA_TRY(hos::launch_reduce_parts(p->d_part, p->geo.ncells, slot_info(p, nseg, n), p->d_line_start, p->geo.nlines,
@@ -930,6 +960,13 @@ int hos_peak_fp32(double* tflops, double* sm_mhz, void* stream) {
 }
 
 int hos_plan_nctas(const hos_plan* p) { return p ? p->nctas : -1; }
+
+int hos_plan_set_trace(hos_plan* p, void* trace_dev) {
+  int rc = check_plan(p);
+  if (rc) return rc;
+  p->trace = (unsigned long long*)trace_dev;
+  return HOS_OK;
+}
 
 int hos_plan_set_timing(hos_plan* p, int enable) {
   int rc = check_plan(p);

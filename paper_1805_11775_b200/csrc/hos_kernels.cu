@@ -570,12 +570,6 @@ __device__ __forceinline__ void cp_async16_cg(unsigned dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
 
-// warp owning work unit u of a W-unit range split into N equal parts
-__device__ __forceinline__ int64_t warp_of_unit(int64_t u, int64_t W, int64_t N) { return ((u + 1) * N - 1) / W; }
-
-__device__ __forceinline__ int region_slots(int r, int nseg, int64_t W, int64_t N) {
-  return (int)(warp_of_unit((int64_t)(r + 1) * nseg - 1, W, N) - warp_of_unit((int64_t)r * nseg, W, N) + 1);
-}
 
 // chunks of a staged unit that are copied (the rest is padding)
 template <typename T, bool ORDER4>
@@ -648,7 +642,7 @@ __device__ __forceinline__ void warp_cells(const typename Cplx<T>::C* q, const L
 }
 
 template <typename T, bool CONJ, bool ORDER4>
-__global__ void __launch_bounds__(128, 2) k_triple_w(const __grid_constant__ TripleArgs a) {
+__global__ void __launch_bounds__(32 * kTripleWarps, 8 / kTripleWarps) k_triple_w(const __grid_constant__ TripleArgs a) {
   using C = typename Cplx<T>::C;
   constexpr int UC = Cplx<T>::kUnitChunks;
   constexpr int per = sizeof(T) == 4 ? 2 : 1;  // elements per 16-byte chunk
@@ -661,7 +655,8 @@ __global__ void __launch_bounds__(128, 2) k_triple_w(const __grid_constant__ Tri
   if (gw >= Nw) return;
   const int nseg = a.seg_end - a.seg_begin;
   const int64_t W = (int64_t)a.nregions * nseg;
-  const int64_t u0 = gw * W / Nw, u1 = (gw + 1) * W / Nw;
+  const WarpSplit split{W, Nw, Nw / 2, a.split_wa, a.split_wb};
+  const int64_t u0 = split.begin(gw), u1 = split.begin(gw + 1);
   if (u0 >= u1) return;
   const C* E = (const C*)a.E + ((int64_t)series * a.K + a.seg_begin) * a.Lp;
   C* Pbase = (C*)a.part + (int64_t)series * a.maxslots * a.ncells;
@@ -669,6 +664,14 @@ __global__ void __launch_bounds__(128, 2) k_triple_w(const __grid_constant__ Tri
   const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring) + 16u * lane;
   const int Lp = a.Lp, f_lo = a.f_lo;
   const int total = (int)(u1 - u0);
+  unsigned long long* tr = a.trace ? a.trace + 4 * ((int64_t)series * Nw + gw) : nullptr;
+  if (tr && lane == 0) {
+    unsigned long long t0, sm;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    asm volatile("{ .reg .u32 r; mov.u32 r, %%smid; cvt.u64.u32 %0, r; }" : "=l"(sm));
+    tr[0] = t0;
+    tr[3] = sm;
+  }
   asm volatile("griddepcontrol.wait;" ::: "memory");  // E is written by the previous kernel
   asm volatile("griddepcontrol.launch_dependents;");   // K4a may be scheduled as K2 CTAs retire
 
@@ -745,7 +748,7 @@ __global__ void __launch_bounds__(128, 2) k_triple_w(const __grid_constant__ Tri
   };
   auto finalize = [&]() {  // this warp's partial slot of region r
     if (!active) return;
-    const int pslot = (int)(gw - warp_of_unit((int64_t)r * nseg, W, Nw));
+    const int pslot = (int)(gw - split.warp_of((int64_t)r * nseg));
     C* P = Pbase + (int64_t)pslot * a.ncells;
 #pragma unroll
     for (int i = 0; i < 4; i++) {
@@ -773,6 +776,11 @@ __global__ void __launch_bounds__(128, 2) k_triple_w(const __grid_constant__ Tri
     stage_group();
     asm volatile("cp.async.wait_group %0;" ::"n"(kWarpPairs - 1) : "memory");
     __syncwarp();  // the group's data, copied by all lanes, is visible
+    if (tr && pos == 0 && lane == 0) {
+      unsigned long long t1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      tr[1] = t1;
+    }
     const C* q = ring + c_slot * (kGroup * UC * per);
     const int cnt = min(kGroup, total - pos);
     if (cnt == kGroup && left >= kGroup) {  // fast path: the whole group in region r, one straight-line block
@@ -803,6 +811,11 @@ __global__ void __launch_bounds__(128, 2) k_triple_w(const __grid_constant__ Tri
   }
   finalize();
   asm volatile("cp.async.wait_group 0;" ::: "memory");
+  if (tr && lane == 0) {
+    unsigned long long t2;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2));
+    tr[2] = t2;
+  }
 }
 
 template <typename K>
@@ -834,9 +847,9 @@ int triple_occupancy(int precision) {
   if (configure() != cudaSuccess) return 1;
   int n = 1;
   if (precision == 32)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_triple_w<float, true, false>, 128, warp_triple_smem<float>());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_triple_w<float, true, false>, 32 * kTripleWarps, warp_triple_smem<float>());
   else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_triple_w<double, true, false>, 128,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_triple_w<double, true, false>, 32 * kTripleWarps,
                                                   warp_triple_smem<double>());
   return n < 1 ? 1 : n;
 }
@@ -890,7 +903,8 @@ constexpr int kScanThreads = 256;
 __device__ __forceinline__ int cell_slots(const SlotInfo& si, int nparts, int64_t l, int64_t col) {
   if (si.line_tile0 == nullptr) return nparts;
   const int r = (si.line_tile0[l] + (int)(col / kTileCols)) >> 1;  // tile -> region (tile pair)
-  return region_slots(r, si.nseg, (int64_t)si.nregions * si.nseg, si.nwarps);
+  const WarpSplit split{(int64_t)si.nregions * si.nseg, si.nwarps, si.nwarps / 2, si.split_wa, si.split_wb};
+  return split.region_slots(r, si.nseg);
 }
 
 // sum of the ns partial slots of one cell in slot order (fp64); the loads of

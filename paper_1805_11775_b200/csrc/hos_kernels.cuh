@@ -51,6 +51,29 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // ---------------------------------------------------------------------------
 // launch wrappers (hos_kernels.cu)
 
+// K2's static split of W (region, segment) units over Nw warps: the first H
+// warps weigh wa, the rest wb (wa == wb: equal contiguous ranges).  The
+// hardware favours the older of the two CTAs on an SM (measured: 25.9 vs
+// 35.1 us for equal work, tools/k2_trace.py), so giving the first wave of
+// CTAs more units makes both finish together.  Fixed by the launch shape, so
+// partial-slot numbering and results stay deterministic.
+struct WarpSplit {
+  int64_t W, Nw, H;
+  int wa, wb;
+  HOS_HD int64_t cum(int64_t g) const { return wa * (g < H ? g : H) + wb * (g > H ? g - H : 0); }
+  HOS_HD int64_t begin(int64_t g) const { return W * cum(g) / cum(Nw); }
+  // the warp whose range holds unit u (the last one when ranges coincide)
+  HOS_HD int64_t warp_of(int64_t u) const {
+    const int64_t X = ((u + 1) * cum(Nw) - 1) / W;
+    const int64_t g = X < wa * H ? X / wa : H + (X - wa * H) / wb;
+    return g < Nw - 1 ? g : Nw - 1;
+  }
+  // partial slots of region r (warps whose range touches it)
+  HOS_HD int region_slots(int r, int nseg) const {
+    return (int)(warp_of((int64_t)(r + 1) * nseg - 1) - warp_of((int64_t)r * nseg) + 1);
+  }
+};
+
 struct TripleArgs {
   const void* E;              // [series][K][Lp] float2 (fp32) / double2 (fp64) spectrum elements
   int Lp;                     // row pitch in elements (even: rows stay 16-byte aligned)
@@ -60,6 +83,7 @@ struct TripleArgs {
   const Region* regions;      // tile pairs (2 x 16 x 32 cells each)
   int nregions;
   int64_t nwarps;             // warps splitting the region x segment work (<= units)
+  int split_wa, split_wb;     // WarpSplit weights (first half / second half of the warps)
   const int32_t* line_cmax;
   const int64_t* line_start;
   int lo;
@@ -70,9 +94,13 @@ struct TripleArgs {
   int conj;
   int batch;
   int accumulate;             // add into the partial slots (chunked launches after the first)
+  unsigned long long* trace;  // diagnostics (nullptr: off): per warp {start, first data, end, smid} globaltimer ns
 };
 
-constexpr int kTripleWarps = 4;   // warps per CTA of the triple-product kernel
+#ifndef HOS_K2_WARPS
+#define HOS_K2_WARPS 4
+#endif
+constexpr int kTripleWarps = HOS_K2_WARPS;  // warps per CTA of the triple-product kernel
 
 // Where the partial slots of a K2 launch are (for the K4a / reduce readers).
 struct SlotInfo {
@@ -80,6 +108,7 @@ struct SlotInfo {
   int nseg;
   int nregions;
   int64_t nwarps;
+  int split_wa, split_wb;
 };
 
 // occupancy (CTAs / SM) of the triple-product kernel
