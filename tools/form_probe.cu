@@ -112,6 +112,58 @@ __global__ void __launch_bounds__(128, MINB) k_flat(float2* out, int reps) {
   out[blockIdx.x * 128 + threadIdx.x] = s;
 }
 
+__device__ __forceinline__ float2 lds_conj(const float2* p) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"((unsigned)__cvta_generic_to_shared(p)));
+  v.y = -v.y;
+  return v;
+}
+
+// the production K2 cell code (4x8 lane tile, rows/cols/G step 4, conj rows from a second load)
+__device__ __forceinline__ void cells_48(const float2* __restrict__ rows, const float2* __restrict__ cols,
+                                         const float2* __restrict__ gs, float2 (&aR)[4][8], float2 (&aI)[4][8]) {
+  float2 fa[4], fac[4], fb[8];
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    fa[i] = rows[4 * i];
+    fac[i] = lds_conj(rows + 4 * i);
+  }
+#pragma unroll
+  for (int j = 0; j < 8; j++) fb[j] = cols[4 * j];
+#pragma unroll
+  for (int q = 0; q < 11; q++) {
+    const float2 g = gs[4 * q];
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      const int j = q - i;
+      if (j < 0 || j > 7) continue;
+      float2 p = fmul2(make_float2(fb[j].x, fb[j].x), fa[i]);
+      p = ffma2(make_float2(fb[j].y, fb[j].y), make_float2(fac[i].y, fac[i].x), p);
+      aR[i][j] = ffma2(make_float2(g.x, g.x), p, aR[i][j]);
+      aI[i][j] = ffma2(make_float2(g.y, g.y), p, aI[i][j]);
+    }
+  }
+}
+
+template <int MINB, int NSEG>
+__global__ void __launch_bounds__(128, MINB) k_48(float2* out, int reps) {
+  __shared__ float2 sm[NSEG * 208];
+  for (int i = threadIdx.x; i < NSEG * 208; i += 128) sm[i] = make_float2(1e-3f * i, 1.f);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, h = lane >> 4, ra = (lane >> 2) & 3, cb = lane & 3;
+  float2 aR[4][8], aI[4][8];
+  for (int i = 0; i < 4; i++) for (int j = 0; j < 8; j++) aR[i][j] = aI[i][j] = make_float2(0.f, 0.f);
+  for (int r = 0; r < reps * 4 / NSEG; r++)
+#pragma unroll
+    for (int q = 0; q < NSEG; q++) {
+      const float2* u = sm + q * 208 + h * 104;
+      cells_48(u + ra, u + 18 + cb, u + 52 + ra + cb, aR, aI);
+    }
+  float2 s = make_float2(0, 0);
+  for (int i = 0; i < 4; i++) for (int j = 0; j < 8; j++) { s.x += aR[i][j].x + aI[i][j].y; s.y += aR[i][j].y - aI[i][j].x; }
+  out[blockIdx.x * 128 + threadIdx.x] = s;
+}
+
 template <int MINB>
 __global__ void __launch_bounds__(128, MINB) k_q(float2* out, int reps) {
   __shared__ float4 sm[4 * 320];
@@ -166,6 +218,8 @@ void run(const char* name, K kern, int cells_per_lane, int sms, float2* buf) {
 int main() {
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   float2* buf; cudaMalloc(&buf, sms * 16 * 128 * sizeof(float2));
+  run("C48x4", k_48<2, 4>, 32, sms, buf);
+  run("C48x1", k_48<2, 1>, 32, sms, buf);
   run("FLAT", k_flat<3>, 32, sms, buf);
   run("QREG", k_qreg<3>, 32, sms, buf);
   run("Q", k_q<3>, 32, sms, buf);
