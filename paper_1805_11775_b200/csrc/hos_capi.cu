@@ -90,11 +90,7 @@ struct hos_plan {
   };
   std::map<GraphKey, cudaGraphExec_t> graphs;
   cudaStream_t cap = nullptr;   // capture stream
-  cudaStream_t cap2 = nullptr;  // copy stream forked inside captures
   bool use_graphs = true;
-  int e2e_chunks = 1;           // segment chunks of the pipelined host path (divides k)
-  int nctas_chunk = 1;          // K2 CTAs of one chunk launch
-  std::vector<cudaEvent_t> chunk_ev;
   // timing
   int timing = 0;
   // stage events: 0 start | 1 prep | 2 fft | 3 extend | 4 triple | 5 scan | 6 box
@@ -474,18 +470,7 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
   }
   p->nctas = nctas_for(p, k, batch);
   p->maxslots = slots_needed(p, k, p->nctas, batch);
-  // pipelined host path: equal segment chunks so every chunk launch owns the same slots
-  {
-    // off by default: each K2 launch still carries ~4 us of prologue + a tail, which
-    // costs more than the copy overlap saves at cfg2 (tools/e2e_timeline.py)
-    int want = 1;
-    if (const char* env = std::getenv("HOS_E2E_CHUNKS")) want = std::max(1, std::atoi(env));
-    int c = std::min(want, k);
-    while (c > 1 && (k % c != 0 || batch != 1)) c--;
-    p->e2e_chunks = c;
-    p->nctas_chunk = nctas_for(p, k / c, batch);
-    p->maxslots = std::max(p->maxslots, slots_needed(p, k / c, p->nctas_chunk, batch));
-  }
+
 
   std::vector<int32_t> cmax(g.line_cmax.begin(), g.line_cmax.end());
   if ((rc = upload(p, &p->d_regions, g.regions))) return bail(rc);
@@ -538,16 +523,10 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
   if ((rc = alloc(p, &p->d_out, (size_t)batch * g.npoints * csize(precision)))) return bail(rc);
   cufftHandle h;
   if ((rc = get_fft(p, (int)rows, &h))) return bail(rc);
-  if (p->e2e_chunks > 1 && (rc = get_fft(p, k / p->e2e_chunks, &h))) return bail(rc);  // no allocation in captures
   for (auto& e : p->ev)
     if (cudaEventCreate(&e) != cudaSuccess) return bail(fail(HOS_ECUDA, "cudaEventCreate failed"));
-  if (cudaStreamCreateWithFlags(&p->cap, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&p->cap2, cudaStreamNonBlocking) != cudaSuccess)
+  if (cudaStreamCreateWithFlags(&p->cap, cudaStreamNonBlocking) != cudaSuccess)
     return bail(fail(HOS_ECUDA, "cudaStreamCreate failed"));
-  p->chunk_ev.resize(p->e2e_chunks + 1);
-  for (auto& e : p->chunk_ev)
-    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
-      return bail(fail(HOS_ECUDA, "cudaEventCreate failed"));
   if (const char* env = std::getenv("HOS_NO_GRAPH")) p->use_graphs = std::atoi(env) == 0;
   *out = p;
   return HOS_OK;
@@ -557,8 +536,6 @@ void hos_plan_destroy(hos_plan* p) {
   if (!p) return;
   for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);
   if (p->cap) cudaStreamDestroy(p->cap);
-  if (p->cap2) cudaStreamDestroy(p->cap2);
-  for (auto e : p->chunk_ev) cudaEventDestroy(e);
   for (auto& kv : p->ffts) cufftDestroy(kv.second);
   void* bufs[] = {p->d_regions, p->d_line_tile0, p->d_line_cmax, p->d_line_start, p->d_row_off, p->d_pair_k1, p->d_pair_k2,
                   p->d_pair_base, p->d_line_of_ab, p->d_taper, p->d_tw, p->d_seg, p->d_half, p->d_E, p->d_part,
@@ -695,6 +672,7 @@ int hos_estimate_host(hos_plan* p, const void* x_host, int x_dtype, int64_t x_st
   cudaStream_t st = (cudaStream_t)stream;
   const size_t es = x_dtype == HOS_F32 ? 4 : 8;
   const size_t km = (size_t)p->k * p->m;
+  // copy path: H2D into the plan's staging buffer, the device pipeline, D2H
   auto body = [&](cudaStream_t s) -> int {
     if (p->batch == 1 || x_stride == (int64_t)km) {
       CUDA_TRY(cudaMemcpyAsync(p->d_xin, x_host, km * p->batch * es, cudaMemcpyHostToDevice, s));
@@ -709,87 +687,30 @@ int hos_estimate_host(hos_plan* p, const void* x_host, int x_dtype, int64_t x_st
                              cudaMemcpyDeviceToHost, s));
     return HOS_OK;
   };
-  // pipelined variant (batch 1, pinned): chunk j's copy overlaps chunk j-1's front end + K2;
-  // K2 chunk launches j > 0 add into the slots chunk 0 wrote (same ownership: equal chunks)
-  const bool dbg = std::getenv("HOS_E2E_TRACE") != nullptr;
-  std::vector<cudaEvent_t> dev(dbg ? 4 * p->e2e_chunks + 4 : 0);
-  for (auto& e : dev) cudaEventCreate(&e);
-  auto mark = [&](int i, cudaStream_t s) {
-    if (dbg) cudaEventRecord(dev[i], s);
-  };
-  auto chunked = [&](cudaStream_t s) -> int {
-    const int C = p->e2e_chunks, kc = p->k / C;
-    const size_t rs = rsize(p->precision), cs = csize(p->precision);
-    mark(0, s);
-    CUDA_TRY(cudaEventRecord(p->chunk_ev[C], s));
-    CUDA_TRY(cudaStreamWaitEvent(p->cap2, p->chunk_ev[C], 0));
-    for (int j = 0; j < C; j++) {
-      const size_t off = (size_t)j * kc * p->m;
-      CUDA_TRY(cudaMemcpyAsync((char*)p->d_xin + off * es, (const char*)x_host + off * es, (size_t)kc * p->m * es,
-                               cudaMemcpyHostToDevice, p->cap2));
-      CUDA_TRY(cudaEventRecord(p->chunk_ev[j], p->cap2));
-      mark(4 + 4 * j, p->cap2);
-    }
-    for (int j = 0; j < C; j++) {
-      const int sb = j * kc;
-      CUDA_TRY(cudaStreamWaitEvent(s, p->chunk_ev[j], 0));
-      mark(5 + 4 * j, s);
-      void* seg = (char*)p->d_seg + (size_t)sb * p->m * rs;
-      void* half = (char*)p->d_half + (size_t)sb * p->hstride * cs;
-      void* E = (char*)p->d_E + (size_t)sb * p->Lp * csize(p->precision);
-      if (p->fused) {
-        int r = fused_front(p, p->d_xin, x_dtype, 0, sb, kc, 1, s);
-        if (r) return r;
-      } else {
-        CUDA_TRY(hos::launch_prep(p->d_xin, x_dtype, 0, p->m, sb, kc, 1, p->taper, p->d_taper, p->precision, seg, s));
-        int r = run_fft(p, kc, seg, half, s);
-        if (r) return r;
-        CUDA_TRY(hos::launch_extend_half(half, p->m, p->hstride, kc, nullptr, p->geo.f_lo, p->L, p->Lp, p->precision,
-                                         E, s));
-      }
-      mark(6 + 4 * j, s);
-      hos::TripleArgs ta = triple_args(p, sb, sb + kc, p->nctas_chunk, 1);
-      ta.accumulate = j > 0;
-      CUDA_TRY(hos::launch_triple(ta, p->precision, s));
-      mark(7 + 4 * j, s);
-    }
-    CUDA_TRY(hos::launch_line_scan(p->d_part, p->maxslots, p->geo.ncells, slot_info(p, kc, p->nctas_chunk),
-                                   p->precision, p->d_line_start, 0, p->geo.nlines, p->geo.ncells, 1, p->d_S, s));
-    int r = run_box(p, p->d_out, s);
-    if (r) return r;
-    mark(1, s);
-    CUDA_TRY(cudaMemcpyAsync(out_host, p->d_out, (size_t)p->geo.npoints * cs, cudaMemcpyDeviceToHost, s));
-    mark(2, s);
-    return HOS_OK;
-  };
-  // graphs only with page-locked host buffers (pageable copies are not capturable)
+  // page-locked host buffers are mapped into the device address space (UVA):
+  // the fused front end then reads the series straight over PCIe and K4b
+  // writes the values straight into host memory -- the transfers happen inside
+  // the kernels that consume / produce them, with no copy-engine hop (a copy
+  // overlapped with the kernels slows both, tools/dma_interference.py)
   cudaPointerAttributes ai{}, ao{};
   const bool pinned = cudaPointerGetAttributes(&ai, x_host) == cudaSuccess && ai.type == cudaMemoryTypeHost &&
                       cudaPointerGetAttributes(&ao, out_host) == cudaSuccess && ao.type == cudaMemoryTypeHost;
   cudaGetLastError();
-  if (dbg && p->e2e_chunks > 1) {
-    if ((rc = chunked(st))) return rc;
-    CUDA_TRY(cudaStreamSynchronize(st));
-    auto at = [&](int i) {
-      float t = 0;
-      cudaEventElapsedTime(&t, dev[0], dev[i]);
-      return t * 1e3f;
-    };
-    for (int j = 0; j < p->e2e_chunks; j++)
-      std::fprintf(stderr, "chunk %d: copied %.1f  start %.1f  front done %.1f  K2 done %.1f us\n", j, at(4 + 4 * j),
-                   at(5 + 4 * j), at(6 + 4 * j), at(7 + 4 * j));
-    std::fprintf(stderr, "smooth done %.1f  D2H done %.1f us\n", at(1), at(2));
-    for (auto e : dev) cudaEventDestroy(e);
-    return HOS_OK;
-  }
-  for (auto e : dev) cudaEventDestroy(e);
+  const char* zc_env = std::getenv("HOS_ZEROCOPY");
+  const bool zero_copy = pinned && p->fused && ai.devicePointer && ao.devicePointer && !(zc_env && zc_env[0] == '0');
+  auto zc_body = [&](cudaStream_t s) -> int {
+    if (p->timing) CUDA_TRY(cudaEventRecord(p->ev[0], s));
+    int r = fused_front(p, ai.devicePointer, x_dtype, x_stride, 0, p->k, p->batch, s);
+    if (r) return r;
+    if (p->timing)
+      for (int i = 1; i <= 3; i++) CUDA_TRY(cudaEventRecord(p->ev[i], s));
+    return run_back(p, ao.devicePointer, s);
+  };
   if (pinned && p->use_graphs && !p->timing && !p->trace) {
-    const hos_plan::GraphKey key{2, x_host, x_dtype, x_stride, out_host};
-    if (p->e2e_chunks > 1 && p->batch == 1) {
-      if ((rc = run_graph(p, key, st, chunked))) return rc;
-    } else if ((rc = run_graph(p, key, st, body))) {
-      return rc;
-    }
+    const hos_plan::GraphKey key{zero_copy ? 3 : 2, x_host, x_dtype, x_stride, out_host};
+    if ((rc = zero_copy ? run_graph(p, key, st, zc_body) : run_graph(p, key, st, body))) return rc;
+  } else if (zero_copy) {
+    if ((rc = zc_body(st))) return rc;
   } else {
     if (p->timing) CUDA_TRY(cudaEventRecord(p->ev[0], st));
     if ((rc = body(st))) return rc;
