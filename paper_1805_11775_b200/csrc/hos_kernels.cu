@@ -141,45 +141,16 @@ __global__ void __launch_bounds__(front_threads<LOG2M>()) k_front(const Tin* __r
   const int sa = 2 * blockIdx.x, b = blockIdx.y;
   const bool has_b = sa + 1 < nseg;
   const Tin* src = x + (int64_t)b * x_stride + (int64_t)sa * M;
-  // samples and taper weights stay in registers between the means and the store.
-  // 16-byte loads when the segment is aligned (4x fewer requests -- the series
-  // may be host memory read over PCIe, hos_estimate_host): slot i of a thread
-  // then holds sample (tid + (i / VEC) TH) VEC + i % VEC
-  constexpr int VEC = 16 / (int)sizeof(Tin);
-  constexpr bool kCanVec = VPT % VEC == 0 && M % (VEC * TH) == 0;
-  const bool vec = kCanVec && (reinterpret_cast<uintptr_t>(src) & 15) == 0;
-  auto uidx = [&](int i) { return vec ? (tid + (i / VEC) * TH) * VEC + i % VEC : tid + i * TH; };
+  // samples and taper weights stay in registers between the means and the store
   Tin xa[VPT], xb[VPT];
   double wv[VPT];
-  if (kCanVec && vec) {
-    using V = std::conditional_t<sizeof(Tin) == 4, float4, double2>;
-#pragma unroll
-    for (int k = 0; k < VPT / VEC; k++) {
-      const V va = *reinterpret_cast<const V*>(src + (tid + k * TH) * VEC);
-      const V vb = has_b ? *reinterpret_cast<const V*>(src + M + (tid + k * TH) * VEC) : V{};
-      const Tin* pa = reinterpret_cast<const Tin*>(&va);
-      const Tin* pb = reinterpret_cast<const Tin*>(&vb);
-#pragma unroll
-      for (int c = 0; c < VEC; c++) {
-        xa[k * VEC + c] = pa[c];
-        xb[k * VEC + c] = pb[c];
-      }
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < VPT; i++) {
-      const int u = tid + i * TH;
-      if (M % TH == 0 || u < M) {
-        xa[i] = src[u];
-        xb[i] = has_b ? src[u + M] : Tin(0);
-      }
-    }
-  }
   double s_a = 0.0, s_b = 0.0;
 #pragma unroll
   for (int i = 0; i < VPT; i++) {
-    const int u = uidx(i);
+    const int u = tid + i * TH;
     if (M % TH == 0 || u < M) {
+      xa[i] = src[u];
+      xb[i] = has_b ? src[u + M] : Tin(0);
       wv[i] = taper ? tab[u] : 1.0;
       s_a += (double)xa[i];
       s_b += (double)xb[i];
@@ -203,7 +174,7 @@ __global__ void __launch_bounds__(front_threads<LOG2M>()) k_front(const Tin* __r
   const double mean_a = ta / (double)M, mean_b = tb / (double)M;
 #pragma unroll
   for (int i = 0; i < VPT; i++) {
-    const int u = uidx(i);
+    const int u = tid + i * TH;
     if (M % TH == 0 || u < M) {
       double va = (double)xa[i] - mean_a, vb = (double)xb[i] - mean_b;
       if (taper) {
@@ -942,7 +913,10 @@ __device__ __forceinline__ int cell_slots(const SlotInfo& si, int nparts, int64_
 template <typename P2>
 __device__ __forceinline__ void sum_slots(const P2* __restrict__ src, int ns, int64_t stride, int64_t idx, double& vr,
                                           double& vi) {
-  constexpr int kChunk = 16;
+#ifndef HOS_SCAN_CHUNK
+#define HOS_SCAN_CHUNK 16
+#endif
+  constexpr int kChunk = HOS_SCAN_CHUNK;
   for (int p0 = 0; p0 < ns; p0 += kChunk) {
     P2 v[kChunk];
 #pragma unroll
