@@ -366,10 +366,10 @@ def run_ours(args):
             "roofline": roof,
             "clocks": clocks,
             "gpu_launches": lib.hos_plan_launches(plan.handle) * args.steps if world == 1 else None,
-            "gpu_launches_note": ("per step: k_front (fused demean+Hann+FFT+extension), k_triple_w, k_line_scan, "
-                                  "k_box3" if lib.hos_plan_launches(plan.handle) == 4 else
-                                  "per step: k_prep, k_extend_half, k_triple_w, k_line_scan, k_box3 "
-                                  "(+ cuFFT's own kernels, not counted)"),
+            "gpu_launches_note": "per step: front end (k_front: fused demean+Hann+FFT+extension; or k_prep + "
+                                 "cuFFT + k_extend_half for non-power-of-two M, cuFFT not counted), k_triple_w, "
+                                 "smoothing (k_line_scan + k_box3/k_box4, or k_smooth_series3 for grids that fit in "
+                                 "shared memory)",
         }
         if not args.no_cpu_baseline and world == 1:
             cb = cpu_baseline(args.config, steps=1, warmup=1, segments=args.cpu_segments)

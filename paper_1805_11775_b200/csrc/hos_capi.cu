@@ -50,12 +50,15 @@ struct hos_plan {
   int maxslots = 1;   // partial slots allocated per series
   int occupancy = 1;  // K2 CTAs per SM
   int sms = 148;
+  int max_line = 0;  // longest D_h line (cells)
+  bool series_k4 = false;  // K4 as one CTA per series with the grid in shared memory
   int split_wa = 1, split_wb = 1;  // K2 WarpSplit weights for two-CTA-per-SM launches
   int hstride = 0;   // complex elements per half-spectrum row
   int L = 0, Lp = 0; // extended-spectrum length / pitch (complex elements)
   // device tables
   hos::Region* d_regions = nullptr;
   int32_t* d_line_tile0 = nullptr;
+  int32_t* d_region_slots = nullptr;  // slots per region of the full-K launch (K4 lookups)
   int32_t* d_line_cmax = nullptr;
   int64_t* d_line_start = nullptr;
   int64_t* d_row_off = nullptr;
@@ -201,6 +204,7 @@ int slots_needed(const hos_plan* p, int nseg, int n, int batch) {
 
 hos::SlotInfo slot_info(const hos_plan* p, int nseg, int n) {
   hos::SlotInfo si{};
+  if (nseg == p->k && n == p->nctas) si.region_slots = p->d_region_slots;  // the plan's main launch
   si.line_tile0 = p->d_line_tile0;
   si.nseg = nseg;
   si.nregions = (int)p->geo.regions.size();
@@ -242,8 +246,8 @@ hos::TripleArgs triple_args(const hos_plan* p, int seg_begin, int seg_end, int n
   return x;
 }
 
-// K2 + K4a + K4b over the extended spectra already in p->d_E.
-int run_box(hos_plan* p, void* out_dev, cudaStream_t st) {
+// K4b arguments for the whole grid of every series of the plan
+hos::BoxArgs box_args(const hos_plan* p, void* out_dev) {
   hos::BoxArgs b{};
   b.S = p->d_S;
   b.s_series_stride = p->geo.ncells;
@@ -274,49 +278,41 @@ int run_box(hos_plan* p, void* out_dev, cudaStream_t st) {
   b.out_series_stride = p->geo.npoints;
   b.precision = p->precision;
   b.batch = p->batch;
-  CUDA_TRY(hos::launch_box(b, st));
+  return b;
+}
+
+int run_box(hos_plan* p, void* out_dev, cudaStream_t st) {
+  CUDA_TRY(hos::launch_box(box_args(p, out_dev), st));
   return HOS_OK;
 }
 
+// K4 of the whole grid: one CTA per series in shared memory when the grid is
+// small (order 3), else line scans + box sums
+int run_smooth(hos_plan* p, void* out_dev, cudaStream_t st, int stage = -1) {
+  const hos::SlotInfo si = slot_info(p, p->k, p->nctas);
+  if (p->series_k4) {
+    if (stage != 5)
+      CUDA_TRY(hos::launch_smooth_series3(p->d_part, p->maxslots, p->geo.ncells, si, p->precision,
+                                          box_args(p, out_dev), p->geo.nlines, st));
+    return HOS_OK;
+  }
+  if (stage != 5)
+    CUDA_TRY(hos::launch_line_scan(p->d_part, p->maxslots, p->geo.ncells, si, p->precision, p->d_line_start, 0,
+                                   p->geo.nlines, p->geo.ncells, p->batch, p->d_S, st, p->max_line));
+  if (p->timing && stage < 0) CUDA_TRY(cudaEventRecord(p->ev[5], st));
+  if (stage != 4) return run_box(p, out_dev, st);
+  return HOS_OK;
+}
+
+// K2 + K4 over the extended spectra already in p->d_E.
 int run_back(hos_plan* p, void* out_dev, cudaStream_t st) {
   const hos::TripleArgs ta = triple_args(p, 0, p->k, p->nctas, p->batch);
   CUDA_TRY(hos::launch_triple(ta, p->precision, st));
   if (p->timing) CUDA_TRY(cudaEventRecord(p->ev[4], st));
-  CUDA_TRY(hos::launch_line_scan(p->d_part, p->maxslots, p->geo.ncells, slot_info(p, p->k, p->nctas), p->precision,
-                                 p->d_line_start, 0, p->geo.nlines, p->geo.ncells, p->batch, p->d_S, st));
-  if (p->timing) CUDA_TRY(cudaEventRecord(p->ev[5], st));
-  hos::BoxArgs b{};
-  b.S = p->d_S;
-  b.s_series_stride = p->geo.ncells;
-  b.line_base = 0;
-  b.line_start = p->d_line_start;
-  b.cell_base = 0;
-  b.row_off = p->d_row_off;
-  b.rows = p->geo.rows;
-  b.pair_k1 = p->d_pair_k1;
-  b.pair_k2 = p->d_pair_k2;
-  b.pair_base = p->d_pair_base;
-  b.npairs = (int)p->geo.pair_k1.size();
-  b.line_of_ab = p->d_line_of_ab;
-  b.b_count = p->geo.b_count;
-  b.lo = p->geo.win.lo;
-  b.hi = p->geo.win.hi;
-  b.m3 = p->m3;
-  b.order = p->order;
-  b.m = p->m;
-  b.row_begin = 0;
-  b.row_end = p->geo.rows;
-  b.pair_begin = 0;
-  b.pair_end = (int)p->geo.pair_k1.size();
-  b.p_begin = 0;
-  b.p_end = p->geo.npoints;
-  b.scale = 1.0 / ((double)p->m * (double)p->k * std::pow((double)p->m3, p->order - 1));
-  b.out = out_dev;
-  b.out_series_stride = p->geo.npoints;
-  b.precision = p->precision;
-  b.batch = p->batch;
-  CUDA_TRY(hos::launch_box(b, st));
+  int rc = run_smooth(p, out_dev, st);
+  if (rc) return rc;
   if (p->timing) {
+    if (p->series_k4) CUDA_TRY(cudaEventRecord(p->ev[5], st));
     CUDA_TRY(cudaEventRecord(p->ev[6], st));
     p->timed = true;
   }
@@ -455,6 +451,13 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
   const hos::Geometry& g = p->geo;
   p->hstride = m / 2 + 1;
   p->L = g.f_hi - g.f_lo + 1;
+  for (size_t l = 0; l + 1 < g.line_start.size(); l++)
+    p->max_line = std::max<int>(p->max_line, (int)(g.line_start[l + 1] - g.line_start[l]));
+  {
+    const char* env = std::getenv("HOS_K4_SERIES");  // "0": always line scans + box sums
+    p->series_k4 = order == 3 && hos::smooth_series3_smem(g.ncells, g.nlines, g.rows, (int)g.regions.size(), g.npoints) <= 200 * 1024 &&
+                   !(env && env[0] == '0');
+  }
   // +4 elements: fp32 operands are staged from the 16-byte-aligned element at
   // or below their start, in whole 16-byte chunks (K2), so a copy may read up
   // to 3 elements past the last frequency; even pitch keeps rows 16-byte aligned
@@ -475,6 +478,12 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
   std::vector<int32_t> cmax(g.line_cmax.begin(), g.line_cmax.end());
   if ((rc = upload(p, &p->d_regions, g.regions))) return bail(rc);
   if ((rc = upload(p, &p->d_line_tile0, g.line_tile0))) return bail(rc);
+  {
+    const hos::WarpSplit sp = warp_split(p, k, p->nctas, batch);
+    std::vector<int32_t> rs(g.regions.size());
+    for (size_t r = 0; r < rs.size(); r++) rs[r] = sp.region_slots((int)r, k);
+    if ((rc = upload(p, &p->d_region_slots, rs))) return bail(rc);
+  }
   if ((rc = upload(p, &p->d_line_cmax, cmax))) return bail(rc);
   if ((rc = upload(p, &p->d_line_start, g.line_start))) return bail(rc);
   if ((rc = upload(p, &p->d_row_off, g.row_off))) return bail(rc);
@@ -537,7 +546,7 @@ void hos_plan_destroy(hos_plan* p) {
   for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);
   if (p->cap) cudaStreamDestroy(p->cap);
   for (auto& kv : p->ffts) cufftDestroy(kv.second);
-  void* bufs[] = {p->d_regions, p->d_line_tile0, p->d_line_cmax, p->d_line_start, p->d_row_off, p->d_pair_k1, p->d_pair_k2,
+  void* bufs[] = {p->d_regions, p->d_line_tile0, p->d_region_slots, p->d_line_cmax, p->d_line_start, p->d_row_off, p->d_pair_k1, p->d_pair_k2,
                   p->d_pair_base, p->d_line_of_ab, p->d_taper, p->d_tw, p->d_seg, p->d_half, p->d_E, p->d_part,
                   p->d_S, p->d_xin, p->d_out};
   for (void* b : bufs)
@@ -553,9 +562,9 @@ int64_t hos_plan_units(const hos_plan* p) { return p ? p->geo.ncells * (int64_t)
 int64_t hos_plan_issued(const hos_plan* p) { return p ? p->geo.issued_cells * (int64_t)p->k : -1; }
 size_t hos_plan_device_bytes(const hos_plan* p) { return p ? p->bytes : 0; }
 int hos_plan_launches(const hos_plan* p) {
-  // kernels of this library per hos_estimate: fused front | K2 | K4a | K4b, or
-  // K0 | K1 | K2 | K4a | K4b around cuFFT's own kernels (general m)
-  return p ? (p->fused ? 4 : 5) : -1;
+  // kernels of this library per hos_estimate: [fused front | K0, K1 around
+  // cuFFT's own kernels] + K2 + [per-series K4 | K4a, K4b]
+  return p ? (p->fused ? 1 : 2) + 1 + (p->series_k4 ? 1 : 2) : -1;
 }
 int64_t hos_plan_lines(const hos_plan* p) { return p ? p->geo.nlines : -1; }
 
@@ -777,7 +786,8 @@ int hos_smooth_raw(hos_plan* p, const void* raw_dev, int64_t line_begin, int row
   const char* raw_lb = (const char*)raw_dev + (size_t)(g.line_start[lb] - cell0) * csize(p->precision);
   double* S = p->d_S;  // scratch: cells of lines [lb, le)
   hos::SlotInfo plain{};
-  CUDA_TRY(hos::launch_line_scan(raw_lb, 1, 0, plain, p->precision, p->d_line_start, lb, le - lb, 0, 1, S, st));
+  CUDA_TRY(hos::launch_line_scan(raw_lb, 1, 0, plain, p->precision, p->d_line_start, lb, le - lb, 0, 1, S, st,
+                                 p->max_line));
   hos::BoxArgs b{};
   b.S = S;
   b.s_series_stride = 0;
@@ -953,17 +963,16 @@ int hos_plan_time_stages(hos_plan* p, const void* x_dev, int x_dtype, int64_t x_
         e = hos::launch_triple(ta, p->precision, cs);
         break;
       case 4:
-        e = hos::launch_line_scan(p->d_part, p->maxslots, p->geo.ncells, slot_info(p, p->k, p->nctas), p->precision,
-                                  p->d_line_start, 0, p->geo.nlines, p->geo.ncells, p->batch, p->d_S, cs);
+        r2 = run_smooth(p, out_dev, cs, 4);
         break;
       default:
-        r2 = run_box(p, out_dev, cs);
+        r2 = run_smooth(p, out_dev, cs, 5);
     }
     if (e != cudaSuccess) return fail(HOS_ECUDA, std::string("CUDA error: ") + cudaGetErrorString(e));
     return r2;
   };
   for (int s = 0; s < 6 && !rc; s++) {
-    if (p->fused && (s == 1 || s == 2)) {
+    if ((p->fused && (s == 1 || s == 2)) || (s == 5 && p->series_k4)) {
       ms6[s] = 0.0;
       continue;
     }

@@ -899,24 +899,25 @@ cudaError_t launch_triple(const TripleArgs& a, int precision, cudaStream_t st) {
 // relative (a global fp32 summed-area table would fail 1e-5).
 
 constexpr int kScanThreads = 256;
+constexpr int kWarpScanMaxLine = 96;  // lines up to this many cells: one warp per line
 
 // number of partial slots holding cell `idx` (absolute cell of line l)
 __device__ __forceinline__ int cell_slots(const SlotInfo& si, int nparts, int64_t l, int64_t col) {
   if (si.line_tile0 == nullptr) return nparts;
   const int r = (si.line_tile0[l] + (int)(col / kTileCols)) >> 1;  // tile -> region (tile pair)
+  if (si.region_slots) return __ldg(si.region_slots + r);
   const WarpSplit split{(int64_t)si.nregions * si.nseg, si.nwarps, si.nwarps / 2, si.split_wa, si.split_wb};
   return split.region_slots(r, si.nseg);
 }
 
 // sum of the ns partial slots of one cell in slot order (fp64); the loads of
 // a 16-slot chunk are all issued before the adds (one L2 round trip per chunk)
-template <typename P2>
-__device__ __forceinline__ void sum_slots(const P2* __restrict__ src, int ns, int64_t stride, int64_t idx, double& vr,
-                                          double& vi) {
 #ifndef HOS_SCAN_CHUNK
 #define HOS_SCAN_CHUNK 16
 #endif
-  constexpr int kChunk = HOS_SCAN_CHUNK;
+template <typename P2, int kChunk = HOS_SCAN_CHUNK>
+__device__ __forceinline__ void sum_slots(const P2* __restrict__ src, int ns, int64_t stride, int64_t idx, double& vr,
+                                          double& vi) {
   for (int p0 = 0; p0 < ns; p0 += kChunk) {
     P2 v[kChunk];
 #pragma unroll
@@ -974,12 +975,56 @@ __global__ void __launch_bounds__(kScanThreads) k_line_scan(const P2* __restrict
   }
 }
 
+// Short lines (small M, batched series): one WARP per (line, series), 32
+// cells per step with a warp-shuffle scan and a running carry -- a CTA per
+// line would leave most of its threads idle and make the grid CTA-bound.
+template <typename P2>
+__global__ void __launch_bounds__(256, 4) k_line_scan_w(const P2* __restrict__ part, int nparts, int64_t part_stride,
+                                                     int64_t part_series_stride, SlotInfo si,
+                                                     const int64_t* __restrict__ line_start, int64_t line_begin,
+                                                     int64_t nlines, int64_t s_series_stride, double2* __restrict__ S) {
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= nlines) return;
+  const int64_t l = line_begin + w;
+  const int series = blockIdx.y;
+  const int64_t base = line_start[line_begin];
+  const int64_t c0 = line_start[l] - base, c1 = line_start[l + 1] - base;
+  const P2* src = part + series * part_series_stride;
+  double2* dst = S + series * s_series_stride;
+  double cr = 0.0, ci = 0.0;
+  for (int64_t c = c0; c < c1; c += 32) {
+    const int64_t idx = c + lane;
+    double vr = 0.0, vi = 0.0;
+    if (idx < c1) sum_slots<P2, 4>(src, cell_slots(si, nparts, l, idx - c0), part_stride, idx, vr, vi);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double ur = __shfl_up_sync(0xffffffffu, vr, o);
+      const double ui = __shfl_up_sync(0xffffffffu, vi, o);
+      if (lane >= o) { vr += ur; vi += ui; }
+    }
+    if (idx < c1) dst[idx] = make_double2(vr + cr, vi + ci);
+    cr += __shfl_sync(0xffffffffu, vr, 31);
+    ci += __shfl_sync(0xffffffffu, vi, 31);
+  }
+}
+
 cudaError_t launch_line_scan(const void* part, int nparts, int64_t part_stride, const SlotInfo& si, int precision,
                              const int64_t* line_start, int64_t line_begin, int64_t nlines, int64_t ncells_series,
-                             int batch, double* S, cudaStream_t st) {
+                             int batch, double* S, cudaStream_t st, int max_line) {
   if (nlines <= 0 || batch <= 0) return cudaSuccess;
-  dim3 grid((unsigned)nlines, batch);
   const int64_t pss = part_stride * nparts;
+  if (max_line <= kWarpScanMaxLine) {
+    dim3 g((unsigned)((nlines + 7) / 8), batch);
+    if (precision == 32)
+      return launch_pdl_kernel(k_line_scan_w<float2>, g, dim3(256), 0, st, (const float2*)part, nparts, part_stride,
+                               pss, si, line_start, line_begin, nlines, ncells_series, (double2*)S);
+    return launch_pdl_kernel(k_line_scan_w<double2>, g, dim3(256), 0, st, (const double2*)part, nparts, part_stride,
+                             pss, si, line_start, line_begin, nlines, ncells_series, (double2*)S);
+  }
+  dim3 grid((unsigned)nlines, batch);
   if (precision == 32)
     return launch_pdl_kernel(k_line_scan<float2>, grid, dim3(kScanThreads), 0, st, (const float2*)part, nparts,
                              part_stride, pss, si, line_start, line_begin, ncells_series, (double2*)S);
@@ -997,13 +1042,47 @@ cudaError_t launch_line_scan(const void* part, int nparts, int64_t part_stride, 
 // Order 4: grid (pairs, series), one thread per k3.
 
 template <typename OUT>
+__device__ __forceinline__ void box3_point(const BoxArgs& a, const double2* __restrict__ S, int k1, int k2,
+                                           OUT* __restrict__ out);
+
+// Order 3, short rows (small M, batched series): one thread per output point
+// of a flat [p_begin, p_end) range, its row found by binary search over the
+// rows' point offsets staged in shared memory.
+template <typename OUT>
+__global__ void __launch_bounds__(256, 4) k_box3_flat(BoxArgs a) {
+  extern __shared__ int64_t roff[];  // row_off[row_begin .. row_end]
+  const int nr = a.row_end - a.row_begin;
+  for (int i = threadIdx.x; i <= nr; i += blockDim.x) roff[i] = __ldg(a.row_off + a.row_begin + i);
+  __syncthreads();
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // prefix sums come from K4a
+  const int64_t p = a.p_begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= a.p_end) return;
+  int lo = 0, hi = nr;  // largest r with roff[r] <= p
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (roff[mid] <= p) lo = mid;
+    else hi = mid;
+  }
+  const int series = blockIdx.y;
+  box3_point<OUT>(a, (const double2*)a.S + series * a.s_series_stride, a.row_begin + lo,
+                         (int)(p - roff[lo]), (OUT*)a.out + series * a.out_series_stride);
+}
+
+template <typename OUT>
 __global__ void __launch_bounds__(128) k_box3(BoxArgs a, int row0) {
   asm volatile("griddepcontrol.wait;" ::: "memory");  // prefix sums come from K4a
   const int k1 = row0 + blockIdx.y;
   const int k2 = blockIdx.x * blockDim.x + threadIdx.x;
   const int series = blockIdx.z;
   if (k2 >= p3_len(a.m, k1)) return;
-  const double2* S = (const double2*)a.S + series * a.s_series_stride;
+  box3_point<OUT>(a, (const double2*)a.S + series * a.s_series_stride, k1, k2,
+                  (OUT*)a.out + series * a.out_series_stride);
+}
+
+// output point (k1, k2) of an order-3 grid from the line prefix sums S
+template <typename OUT>
+__device__ __forceinline__ void box3_point(const BoxArgs& a, const double2* __restrict__ S, int k1, int k2,
+                                           OUT* __restrict__ out) {
   double sr = 0.0, si = 0.0;
   // window lines in chunks of 8, every load of a chunk issued before the adds
   for (int u0 = 0; u0 < a.m3; u0 += 8) {
@@ -1027,7 +1106,6 @@ __global__ void __launch_bounds__(128) k_box3(BoxArgs a, int row0) {
     }
   }
   const int64_t p = __ldg(a.row_off + k1) + k2;
-  OUT* out = (OUT*)a.out + series * a.out_series_stride;
   out[p - a.p_begin].x = sr * a.scale;
   out[p - a.p_begin].y = si * a.scale;
 }
@@ -1064,12 +1142,152 @@ __global__ void __launch_bounds__(64) k_box4(BoxArgs a, int pair0) {
   }
 }
 
+// K4 for SMALL order-3 grids (batched series, small M): one CTA per series
+// holds its whole D_h in shared memory -- raw cells (partial slots summed in
+// slot order, fp64), per-line inclusive prefixes (one warp per line), then
+// every output point boxed from shared memory.  HBM sees only the partial
+// slots and the values (the two-kernel path round-trips S through HBM once
+// the batch's S outgrows L2).
+template <typename P2, typename OUT>
+__global__ void __launch_bounds__(512) k_smooth_series3(const P2* __restrict__ part, int nparts, int64_t part_stride,
+                                                        int64_t part_series_stride, SlotInfo si, BoxArgs a,
+                                                        int nlines) {
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  const int ncells = (int)a.s_series_stride;
+  double2* S = reinterpret_cast<double2*>(sm_raw);            // ncells raw cells, then line prefixes
+  int* ls = reinterpret_cast<int*>(S + ncells);               // nlines + 1 line starts
+  int* ro = ls + nlines + 1;                                  // rows + 1 point offsets
+  int* lt0 = ro + a.rows + 1;                                 // nlines: first tile of each line
+  int* rsl = lt0 + nlines;                                    // nregions: partial slots per region
+  unsigned short* cline = reinterpret_cast<unsigned short*>(rsl + si.nregions);  // ncells: line of each cell
+  unsigned short* prow = cline + ncells;                       // npoints: row of each point
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int series = blockIdx.x;
+  for (int i = tid; i <= nlines; i += blockDim.x) ls[i] = (int)__ldg(a.line_start + i);
+  for (int i = tid; i <= a.rows; i += blockDim.x) ro[i] = (int)__ldg(a.row_off + i);
+  for (int i = tid; i < nlines; i += blockDim.x) lt0[i] = __ldg(si.line_tile0 + i);
+  for (int i = tid; i < si.nregions; i += blockDim.x) rsl[i] = __ldg(si.region_slots + i);
+  __syncthreads();
+  for (int l = warp; l < nlines; l += nw)
+    for (int c = ls[l] + lane; c < ls[l + 1]; c += 32) cline[c] = (unsigned short)l;
+  for (int r = warp; r < a.rows; r += nw)
+    for (int q = ro[r] + lane; q < ro[r + 1]; q += 32) prow[q] = (unsigned short)r;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // partial slots come from K2
+  __syncthreads();
+  // raw cells: partial slots summed in slot order (fp64); four cells per
+  // thread per step with all their loads issued first
+  const P2* src = part + series * part_series_stride;
+  constexpr int U = 4;
+  for (int base = 0; base < ncells; base += U * blockDim.x) {
+    P2 v[U][2];
+    int ns[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int idx = base + u * blockDim.x + tid;
+      ns[u] = 0;
+      if (idx < ncells) {
+        const int l = cline[idx];
+        ns[u] = rsl[(lt0[l] + (idx - ls[l]) / kTileCols) >> 1];
+#pragma unroll
+        for (int t = 0; t < 2; t++)
+          if (t < ns[u]) v[u][t] = src[(int64_t)t * part_stride + idx];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int idx = base + u * blockDim.x + tid;
+      if (idx >= ncells) continue;
+      double vr = 0.0, vi = 0.0;
+#pragma unroll
+      for (int t = 0; t < 2; t++)
+        if (t < ns[u]) {
+          vr += (double)v[u][t].x;
+          vi += (double)v[u][t].y;
+        }
+      for (int t = 2; t < ns[u]; t++) {  // more than two slots: rest in order
+        const P2 w = src[(int64_t)t * part_stride + idx];
+        vr += (double)w.x;
+        vi += (double)w.y;
+      }
+      S[idx] = make_double2(vr, vi);
+    }
+  }
+  __syncthreads();
+  for (int l = warp; l < nlines; l += nw) {  // inclusive prefix of each line
+    double cr = 0.0, ci = 0.0;
+    for (int c = ls[l]; c < ls[l + 1]; c += 32) {
+      const int idx = c + lane;
+      double vr = 0.0, vi = 0.0;
+      if (idx < ls[l + 1]) {
+        vr = S[idx].x;
+        vi = S[idx].y;
+      }
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double ur = __shfl_up_sync(0xffffffffu, vr, o);
+        const double ui = __shfl_up_sync(0xffffffffu, vi, o);
+        if (lane >= o) { vr += ur; vi += ui; }
+      }
+      if (idx < ls[l + 1]) S[idx] = make_double2(vr + cr, vi + ci);
+      cr += __shfl_sync(0xffffffffu, vr, 31);
+      ci += __shfl_sync(0xffffffffu, vi, 31);
+    }
+  }
+  __syncthreads();
+  OUT* out = (OUT*)a.out + series * a.out_series_stride;
+  const int npts = ro[a.rows];
+  for (int p = tid; p < npts; p += blockDim.x) {
+    const int k1 = prow[p], k2 = p - ro[k1];
+    double sr = 0.0, si_ = 0.0;
+    for (int u = 0; u < a.m3; u++) {  // window lines k1 .. k1 + w - 1, same order as k_box3
+      const int cb = ls[k1 + u];
+      const double2 s1 = S[cb + k2 + a.m3 - 1];
+      sr += s1.x;
+      si_ += s1.y;
+      if (k2 >= 1) {
+        const double2 s0 = S[cb + k2 - 1];
+        sr -= s0.x;
+        si_ -= s0.y;
+      }
+    }
+    out[p].x = sr * a.scale;
+    out[p].y = si_ * a.scale;
+  }
+}
+
+size_t smooth_series3_smem(int64_t ncells, int64_t nlines, int rows, int nregions, int64_t npoints) {
+  if (nlines > 65535 || rows > 65535) return ~(size_t)0;  // 16-bit line / row tables
+  return (size_t)ncells * sizeof(double2) + (size_t)(nlines + 1 + rows + 1 + nlines + nregions) * sizeof(int) +
+         (size_t)(ncells + npoints) * sizeof(unsigned short);
+}
+
+cudaError_t launch_smooth_series3(const void* part, int nparts, int64_t part_stride, const SlotInfo& si, int precision,
+                                  const BoxArgs& a, int64_t nlines, cudaStream_t st) {
+  if (!si.line_tile0 || !si.region_slots) return cudaErrorInvalidValue;  // needs the plan's slot table
+  const size_t sm = smooth_series3_smem(a.s_series_stride, nlines, a.rows, si.nregions, a.p_end - a.p_begin);
+  const int64_t pss = part_stride * nparts;
+  if (precision == 32) {
+    cudaFuncSetAttribute(k_smooth_series3<float2, float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    return launch_pdl_kernel(k_smooth_series3<float2, float2>, dim3(a.batch), dim3(512), sm, st, (const float2*)part,
+                             nparts, part_stride, pss, si, a, (int)nlines);
+  }
+  cudaFuncSetAttribute(k_smooth_series3<double2, double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  return launch_pdl_kernel(k_smooth_series3<double2, double2>, dim3(a.batch), dim3(512), sm, st,
+                           (const double2*)part, nparts, part_stride, pss, si, a, (int)nlines);
+}
+
 cudaError_t launch_box(const BoxArgs& a, cudaStream_t st) {
   if (a.p_end <= a.p_begin || a.batch <= 0) return cudaSuccess;
   if (a.order == 3) {
     if (a.row_end <= a.row_begin) return cudaSuccess;
     int mx = 1;
     for (int r = a.row_begin; r < a.row_end; r++) mx = max(mx, p3_len(a.m, r));
+    if (mx <= 64) {  // short rows: flat point grid
+      dim3 g((unsigned)((a.p_end - a.p_begin + 255) / 256), a.batch);
+      const size_t sm = (size_t)(a.row_end - a.row_begin + 1) * sizeof(int64_t);
+      return a.precision == 32 ? launch_pdl_kernel(k_box3_flat<float2>, g, dim3(256), sm, st, a)
+                               : launch_pdl_kernel(k_box3_flat<double2>, g, dim3(256), sm, st, a);
+    }
     dim3 grid((mx + 127) / 128, a.row_end - a.row_begin, a.batch);
     return a.precision == 32 ? launch_pdl_kernel(k_box3<float2>, grid, dim3(128), 0, st, a, a.row_begin)
                              : launch_pdl_kernel(k_box3<double2>, grid, dim3(128), 0, st, a, a.row_begin);

@@ -109,6 +109,7 @@ struct SlotInfo {
   int nregions;
   int64_t nwarps;
   int split_wa, split_wb;
+  const int32_t* region_slots;  // optional host-precomputed slots per region (same values), nullptr: compute
 };
 
 // occupancy (CTAs / SM) of the triple-product kernel
@@ -131,9 +132,10 @@ cudaError_t launch_extend_full(const void* S, int spec_dtype, int m, int rows, i
 cudaError_t launch_expand_full(const void* H, int m, int hstride, int rows, int precision, void* out,
                                cudaStream_t st);
 cudaError_t launch_triple(const TripleArgs& a, int precision, cudaStream_t st);
+// max_line: longest line (cells) of the range -- short lines get one warp per line
 cudaError_t launch_line_scan(const void* part, int nparts, int64_t part_stride, const SlotInfo& si, int precision,
                              const int64_t* line_start, int64_t line_begin, int64_t nlines,
-                             int64_t ncells_series, int batch, double* S, cudaStream_t st);
+                             int64_t ncells_series, int batch, double* S, cudaStream_t st, int max_line);
 struct BoxArgs {
   const double* S;          // prefix sums [series][ncells] (cells of lines from line_base)
   int64_t s_series_stride;
@@ -159,6 +161,11 @@ struct BoxArgs {
   int batch;
 };
 cudaError_t launch_box(const BoxArgs& a, cudaStream_t st);
+// K4a + K4b for a small order-3 grid, one CTA per series with the whole grid
+// in shared memory (smooth_series3_smem bytes; the caller checks it fits)
+size_t smooth_series3_smem(int64_t ncells, int64_t nlines, int rows, int nregions, int64_t npoints);
+cudaError_t launch_smooth_series3(const void* part, int nparts, int64_t part_stride, const SlotInfo& si, int precision,
+                                  const BoxArgs& a, int64_t nlines, cudaStream_t st);
 // raw[c] = sum_p part[p][c] (fp64 sum, stored in the compute precision)
 cudaError_t launch_reduce_parts(const void* part, int64_t part_stride, const SlotInfo& si, const int64_t* line_start,
                                 int64_t nlines, int lo, int precision, void* raw, cudaStream_t st);
