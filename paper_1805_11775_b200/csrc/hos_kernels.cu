@@ -119,9 +119,16 @@ template <int LOG2M>
 __host__ __device__ constexpr int front_threads() {
   return (1 << LOG2M) / 8 >= 256 ? 256 : ((1 << LOG2M) / 8 >= 32 ? (1 << LOG2M) / 8 : 32);
 }
+// segment pairs per CTA: one-warp transforms (m <= 256) run four per CTA,
+// each warp on its own pair with warp-level barriers (a CTA per pair made the
+// small-m grids CTA-bound: cfg5 has 160K pairs)
+template <int LOG2M>
+__host__ __device__ constexpr int front_pairs() {
+  return front_threads<LOG2M>() == 32 ? 4 : 1;
+}
 
 template <typename Tin, typename T, int LOG2M>
-__global__ void __launch_bounds__(front_threads<LOG2M>()) k_front(const Tin* __restrict__ x, int64_t x_stride,
+__global__ void __launch_bounds__(front_threads<LOG2M>() * front_pairs<LOG2M>()) k_front(const Tin* __restrict__ x, int64_t x_stride,
                                                                   int nseg, int krows, int taper,
                                                                   const double* __restrict__ tab,
                                                                   const typename C2<T>::t* __restrict__ tw, int f_lo,
@@ -129,16 +136,24 @@ __global__ void __launch_bounds__(front_threads<LOG2M>()) k_front(const Tin* __r
   using CT = typename C2<T>::t;
   constexpr int M = 1 << LOG2M;
   constexpr int TH = front_threads<LOG2M>();
+  constexpr int PPC = front_pairs<LOG2M>();
   constexpr int VPT = (M + TH - 1) / TH;        // samples per thread and segment
   constexpr int BPT = (M / 4 + TH - 1) / TH;    // radix-4 butterflies per thread and stage
   extern __shared__ __align__(16) unsigned char fsm[];
-  CT* bufA = reinterpret_cast<CT*>(fsm);
+  const int grp = threadIdx.x / TH;             // pair of this thread group inside the CTA
+  CT* bufA = reinterpret_cast<CT*>(fsm) + grp * 3 * M;
   CT* bufB = bufA + M;
   CT* tws = bufB + M;  // twiddle table staged in shared memory
-  __shared__ double2 red[TH / 32];
-  const int tid = threadIdx.x;
-  // two real segments per CTA, packed as one complex sequence z = x_a + i x_b
-  const int sa = 2 * blockIdx.x, b = blockIdx.y;
+  __shared__ double2 red_all[PPC][TH / 32];
+  double2* red = red_all[grp];
+  const int tid = threadIdx.x % TH;
+  auto sync = [] {
+    if constexpr (PPC > 1) __syncwarp();
+    else __syncthreads();
+  };
+  // two real segments per thread group, packed as one complex sequence z = x_a + i x_b
+  const int sa = 2 * (blockIdx.x * PPC + grp), b = blockIdx.y;
+  if (sa >= nseg) return;  // whole group (a warp when PPC > 1)
   const bool has_b = sa + 1 < nseg;
   const Tin* src = x + (int64_t)b * x_stride + (int64_t)sa * M;
   // samples and taper weights stay in registers between the means and the store
@@ -164,7 +179,7 @@ __global__ void __launch_bounds__(front_threads<LOG2M>()) k_front(const Tin* __r
   s_a = warp_sum(s_a);
   s_b = warp_sum(s_b);
   if ((tid & 31) == 0) red[tid >> 5] = make_double2(s_a, s_b);
-  __syncthreads();
+  sync();
   double ta = 0.0, tb = 0.0;
 #pragma unroll
   for (int w = 0; w < TH / 32; w++) {
@@ -184,7 +199,7 @@ __global__ void __launch_bounds__(front_threads<LOG2M>()) k_front(const Tin* __r
       bufA[u] = CT{(T)va, (T)vb};
     }
   }
-  __syncthreads();
+  sync();
   // Stockham (self-sorting, decimation in frequency) radix-4 stages, then one
   // radix-2 stage when log2 m is odd.  Stage with current length n and stride
   // s = m / n, butterfly (p < n/4, q < s):
@@ -225,7 +240,7 @@ __global__ void __launch_bounds__(front_threads<LOG2M>()) k_front(const Tin* __r
         }
       }
     }
-    __syncthreads();
+    sync();
     CT* tsw = xin;
     xin = yout;
     yout = tsw;
@@ -240,11 +255,11 @@ __global__ void __launch_bounds__(front_threads<LOG2M>()) k_front(const Tin* __r
         yout[q + M / 2] = CT{a.x - c.x, a.y - c.y};
       }
     }
-    __syncthreads();
+    sync();
     xin = yout;
   }
 #endif
-  if (tid == 0) asm volatile("griddepcontrol.launch_dependents;");
+  if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;");
   // X_a(f) = (Z(f) + conj Z(-f)) / 2,  X_b(f) = (Z(f) - conj Z(-f)) / 2i
   CT* row = E + ((int64_t)b * krows + sa) * Lp;
   for (int j = tid; j < L; j += TH) {
@@ -258,15 +273,17 @@ __global__ void __launch_bounds__(front_threads<LOG2M>()) k_front(const Tin* __r
 template <int LOG2M, typename Tin, typename T>
 static void front_go(const Tin* x, int64_t x_stride, int nseg, int krows, int batch, int taper, const double* tab,
                      const typename C2<T>::t* tw, int f_lo, int L, int Lp, typename C2<T>::t* E, cudaStream_t st) {
-  const size_t smem = 3 * (size_t)(1 << LOG2M) * sizeof(typename C2<T>::t);
+  const size_t smem = 3 * (size_t)(1 << LOG2M) * sizeof(typename C2<T>::t) * front_pairs<LOG2M>();
   auto kern = k_front<Tin, T, LOG2M>;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = true;
   }
-  kern<<<dim3((nseg + 1) / 2, batch), front_threads<LOG2M>(), smem, st>>>(x, x_stride, nseg, krows, taper, tab, tw,
-                                                                          f_lo, L, Lp, E);
+  constexpr int PPC = front_pairs<LOG2M>();
+  const int pairs = (nseg + 1) / 2;
+  kern<<<dim3((pairs + PPC - 1) / PPC, batch), front_threads<LOG2M>() * PPC, smem, st>>>(
+      x, x_stride, nseg, krows, taper, tab, tw, f_lo, L, Lp, E);
 }
 
 template <typename Tin, typename T>
