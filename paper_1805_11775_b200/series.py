@@ -15,7 +15,7 @@ import numpy as np
 
 from .errors import DataError, ParameterError
 
-__all__ = ["TimeSeries", "SegmentConfig", "SegmentSet", "segment_and_demean"]
+__all__ = ["TimeSeries", "SegmentConfig", "SegmentSet", "segment_and_demean", "load_series"]
 
 
 @dataclass(frozen=True)
@@ -80,3 +80,45 @@ def segment_and_demean(series: TimeSeries, cfg: SegmentConfig) -> SegmentSet:
     rows = series.samples[: cfg.k * cfg.m].reshape(cfg.k, cfg.m).copy()
     rows -= rows.mean(axis=1, keepdims=True)
     return SegmentSet(segments=rows, means_removed=True)
+
+
+def load_series(path, fmt: str = "csv") -> TimeSeries:
+    """Read a series file in the reference's interchange formats
+    (hospectra/series.py:95-140): ``csv`` = one decimal value per line, blank
+    lines skipped, an optional single non-numeric header line; ``raw64`` =
+    consecutive little-endian IEEE-754 float64 values.  Unreadable, empty,
+    malformed or non-finite input raises DataError (with file:line for csv)."""
+    path = str(path)
+    if fmt not in ("csv", "raw64"):
+        raise ParameterError(f"unknown series format {fmt!r} (csv or raw64)")
+    try:
+        data = open(path, "rb").read()
+    except OSError as exc:
+        raise DataError(f"cannot read {path}: {exc}") from exc
+    if fmt == "raw64":
+        if len(data) % 8:
+            raise DataError(f"{path}: raw64 size {len(data)} is not a multiple of 8 bytes")
+        vals = np.frombuffer(data, dtype="<f8").astype(np.float64)
+        if vals.size == 0:
+            raise DataError(f"{path}: empty input")
+        bad = ~np.isfinite(vals)
+        if bad.any():
+            raise DataError(f"{path}: non-finite value at index {int(np.argmax(bad))}")
+        return TimeSeries(vals, source=path)
+    out = []
+    for no, raw in enumerate(data.decode("utf-8").splitlines(), start=1):
+        tok = raw.strip()
+        if not tok:
+            continue
+        try:
+            v = float(tok)
+        except ValueError:
+            if no == 1:
+                continue  # header
+            raise DataError(f"{path}:{no}: non-numeric value {tok!r}") from None
+        if not np.isfinite(v):
+            raise DataError(f"{path}:{no}: non-finite value {tok!r}")
+        out.append(v)
+    if not out:
+        raise DataError(f"{path}: empty input")
+    return TimeSeries(np.asarray(out, dtype=np.float64), source=path)
