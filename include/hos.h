@@ -169,6 +169,25 @@ int hos_peak_fp32(double* tflops, double* sm_mhz, void* stream);
  * hos_estimate* call on this plan when timing was enabled (events recorded on
  * the launching stream). */
 int hos_plan_set_timing(hos_plan* plan, int enable);
+/* ---- multi-GPU ----------------------------------------------
+ * One process (or thread) per GPU.  The caller creates an NCCL communicator
+ * (ncclCommInitRank; libnccl.so.2 is resolved at attach time, no link-time
+ * dependency) and attaches it to a batch-1 plan on that rank's device.
+ * hos_estimate_distributed then runs the segment-sharded estimate of ONE
+ * series: every rank passes the full series (device memory, it reads only its
+ * own segments), computes partial raw sums over D_h for its segment shard,
+ * the partials are reduce-scattered by line blocks (ncclReduceScatter), the
+ * halo lines are exchanged (ncclAllGather), each rank smooths its own output
+ * rows and the lexicographic slices are all-gathered: out_dev receives the
+ * full grid on every rank.  Replaces the reference's process fan-out
+ * (hospectra/parallel.py:120-162) with a GPU-per-rank split of the K-sum. */
+int hos_comm_attach(hos_plan* plan, void* nccl_comm, int rank, int nranks);
+int hos_estimate_distributed(hos_plan* plan, const void* x_dev, int x_dtype, void* out_dev, void* stream);
+/* The sharded layout (host only, no device): per rank {seg0, seg1, row0,
+ * row1, own_l0, own_l1, need_l0, need_l1, own_c0, own_c1, need_c0, need_c1,
+ * p0, p1}, then {block, halo, halo_in_next}: 14 * nranks + 3 int64. */
+int hos_shard_layout(int order, int m, int k, int m3, int nranks, int64_t* out);
+
 /* Diagnostics: K2 CTAs per series (4 warps each). */
 int hos_plan_nctas(const hos_plan* plan);
 /* Diagnostics: a device buffer of 4 x (4 nctas) x batch uint64 that K2 fills

@@ -60,6 +60,9 @@ EXPORTED_SYMBOLS = {
     "hos_plan_kernel_ms": (_i, [_p, _p, _p]),
     "hos_plan_stage_ms": (_i, [_p, _p]),
     "hos_plan_set_trace": (_i, [_p, _p]),
+    "hos_comm_attach": (_i, [_p, _p, _i, _i]),
+    "hos_estimate_distributed": (_i, [_p, _p, _i, _p, _p]),
+    "hos_shard_layout": (_i, [_i, _i, _i, _i, _i, _p]),
     "hos_plan_time_stages": (_i, [_p, _p, _i, _i64, _p, _i, _p, _p]),
 }
 
@@ -276,10 +279,34 @@ class Plan:
                                              ctypes.c_void_p(out.data_ptr()), reps, res, self._stream()))
         return dict(zip(("prep", "fft", "extend", "triple", "scan", "box"), list(res)))
 
+    def comm_attach(self, nccl_comm: int, rank: int, nranks: int):
+        """Attach an NCCL communicator (ncclComm_t as an int) of `nranks` ranks."""
+        raise_for(lib().hos_comm_attach(self.handle, ctypes.c_void_p(nccl_comm), rank, nranks))
+
+    def estimate_distributed(self, x, out=None):
+        """Segment-sharded estimate of one series over the attached
+        communicator; x: the full series (CUDA tensor) on every rank."""
+        torch = _torch()
+        if out is None:
+            out = self.empty_out()
+        dt = HOS_F32 if x.dtype == torch.float32 else HOS_F64
+        raise_for(lib().hos_estimate_distributed(self.handle, ctypes.c_void_p(x.data_ptr()), dt,
+                                                 ctypes.c_void_p(out.data_ptr()), self._stream()))
+        return out
+
     def kernel_ms(self):
         t, tot = ctypes.c_double(), ctypes.c_double()
         raise_for(lib().hos_plan_kernel_ms(self.handle, ctypes.byref(t), ctypes.byref(tot)))
         return float(t.value), float(tot.value)
+
+
+def shard_layout_native(order: int, m: int, k: int, m3: int, nranks: int):
+    """hos_shard_layout as (per-rank rows of 14, (block, halo, in_next))."""
+    import numpy as np
+
+    out = np.zeros(14 * nranks + 3, dtype=np.int64)
+    raise_for(lib().hos_shard_layout(order, m, k, m3, nranks, out.ctypes.data_as(ctypes.c_void_p)))
+    return out[:14 * nranks].reshape(nranks, 14), tuple(int(v) for v in out[14 * nranks:])
 
 
 def dft_rows(x, m: int, precision: int = 64):

@@ -2,7 +2,10 @@
 // K0 -> cuFFT -> K1 -> K2 -> K4a -> K4b on one stream, error mapping.
 #include <cuda_runtime.h>
 #include <cufft.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -79,6 +82,17 @@ struct hos_plan {
   void* d_out = nullptr;   // host path staging
   size_t bytes = 0;
   unsigned long long* trace = nullptr;  // K2 per-warp trace (diagnostics; 4 x nwarps x batch)
+  // multi-GPU (hos_comm_attach): NCCL communicator and the segment-sharded layout's buffers
+  void* comm = nullptr;
+  int rank = 0, nranks = 1;
+  std::vector<int64_t> layout;  // hos_shard_layout record of (order, m, k, m3, nranks)
+  void* d_raw = nullptr;        // ncells partial raw sums of this rank's segments
+  void* d_send = nullptr;       // nranks x block reduce-scatter input
+  void* d_mine = nullptr;       // block: this rank's reduced lines
+  void* d_local = nullptr;      // lines this rank smooths (own block + halo)
+  void* d_heads = nullptr;      // nranks x halo (or nranks x block when the halo spans ranks)
+  void* d_vals = nullptr;       // pmax: this rank's values
+  void* d_parts = nullptr;      // nranks x pmax gathered values
   std::map<int, cufftHandle> ffts;  // rows -> plan
   // CUDA graphs of the whole stream-ordered pipeline, one per buffer binding
   struct GraphKey {
@@ -388,6 +402,123 @@ int run_graph(hos_plan* p, const hos_plan::GraphKey& key, cudaStream_t st, F bod
 
 }  // namespace
 
+// lines [lb, le) the output rows [r0, r1) read (order 3: rows r0 .. r1-1+w-1;
+// order 4: the pair lines of planes a in [r0+lo, r1-1+hi])
+void rows_lines(const hos::Geometry& g, int order, int m3, int r0, int r1, int64_t* lb, int64_t* le) {
+  if (order == 3) {
+    *lb = r0;
+    *le = r1 == r0 ? r0 : r1 - 1 + (m3 - 1) + 1;
+    return;
+  }
+  int64_t b = 0, e = 0;
+  const int alo = r0 + g.win.lo, ahi = r1 - 1 + g.win.hi;
+  while (b < g.nlines && g.line_a[b] < alo) b++;
+  e = b;
+  while (e < g.nlines && g.line_a[e] <= ahi) e++;
+  *lb = b;
+  *le = r1 == r0 ? b : e;
+}
+
+// Segment-sharded multi-GPU layout (the C++ twin of parallel.shard_layout):
+// segments split evenly, output rows by whole-row point balance (the
+// reference's row_blocks policy, hospectra/parallel.py:73-80), lines owned
+// from each rank's first needed line, halo = lines past the owned block.
+// Record: per rank {seg0, seg1, row0, row1, own_l0, own_l1, need_l0, need_l1,
+// own_c0, own_c1, need_c0, need_c1, p0, p1}, then {block, halo, in_next}.
+constexpr int kLayoutPerRank = 14;
+std::vector<int64_t> shard_layout(const hos::Geometry& g, int order, int m3, int k, int n) {
+  std::vector<int> rb(n + 1, 0);
+  const int rows = g.rows;
+  const int64_t total = g.row_off[rows];
+  if (n == 1 || total == 0) {
+    for (int r = 1; r <= n; r++) rb[r] = rows;
+  } else {
+    for (int r = 1; r < n; r++) {  // first row whose cumulative point count reaches r / n of the total
+      const double t = (double)r * ((double)total / n);
+      int i = 0;
+      while (i < rows && (double)g.row_off[i + 1] < t) i++;
+      rb[r] = std::min(rows, i + 1);
+    }
+    rb[n] = rows;
+  }
+  std::vector<int64_t> nl0(n), nl1(n), ol0(n), ol1(n);
+  for (int r = 0; r < n; r++) rows_lines(g, order, m3, rb[r], rb[r + 1], &nl0[r], &nl1[r]);
+  int64_t nxt = g.nlines;
+  for (int r = n - 1; r >= 0; r--) {
+    const int64_t l0 = rb[r] < rb[r + 1] ? nl0[r] : nxt;
+    ol0[r] = l0;
+    ol1[r] = nxt;
+    nxt = l0;
+  }
+  ol0[0] = 0;
+  for (int r = 0; r < n; r++)
+    if (!(rb[r] < rb[r + 1])) nl0[r] = nl1[r] = ol0[r];
+  std::vector<int64_t> rec;
+  int64_t block = 1, halo = 1;
+  bool in_next = true;
+  std::vector<int64_t> oc0(n), oc1(n), nc0(n), nc1(n);
+  for (int r = 0; r < n; r++) {
+    oc0[r] = g.line_start[ol0[r]];
+    oc1[r] = g.line_start[ol1[r]];
+    nc0[r] = g.line_start[nl0[r]];
+    nc1[r] = g.line_start[nl1[r]];
+    block = std::max(block, oc1[r] - oc0[r]);
+  }
+  for (int r = 0; r < n; r++) {
+    const int64_t h = std::max<int64_t>(0, nc1[r] - oc1[r]);
+    halo = std::max(halo, h);
+    if (h && !(r + 1 < n && h <= oc1[r + 1] - oc0[r + 1])) in_next = false;
+  }
+  for (int r = 0; r < n; r++) {
+    const int64_t v[kLayoutPerRank] = {(int64_t)r * k / n, (int64_t)(r + 1) * k / n, rb[r], rb[r + 1], ol0[r], ol1[r],
+                                       nl0[r], nl1[r], oc0[r], oc1[r], nc0[r], nc1[r], g.row_off[rb[r]],
+                                       g.row_off[rb[r + 1]]};
+    rec.insert(rec.end(), v, v + kLayoutPerRank);
+  }
+  rec.push_back(block);
+  rec.push_back(halo);
+  rec.push_back(in_next ? 1 : 0);
+  return rec;
+}
+
+// NCCL, resolved at hos_comm_attach (no link-time dependency: the process may
+// already hold another libnccl, e.g. the one PyTorch ships)
+struct NcclApi {
+  decltype(&ncclReduceScatter) reduce_scatter = nullptr;
+  decltype(&ncclAllGather) all_gather = nullptr;
+  decltype(&ncclGetErrorString) error_string = nullptr;
+  decltype(&ncclCommCount) comm_count = nullptr;
+  decltype(&ncclCommUserRank) comm_rank = nullptr;
+};
+const NcclApi* nccl_api(std::string* why) {
+  static NcclApi api;
+  static bool tried = false, ok = false;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);  // already in the process?
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.reduce_scatter = (decltype(api.reduce_scatter))dlsym(h, "ncclReduceScatter");
+      api.all_gather = (decltype(api.all_gather))dlsym(h, "ncclAllGather");
+      api.error_string = (decltype(api.error_string))dlsym(h, "ncclGetErrorString");
+      api.comm_count = (decltype(api.comm_count))dlsym(h, "ncclCommCount");
+      api.comm_rank = (decltype(api.comm_rank))dlsym(h, "ncclCommUserRank");
+      ok = api.reduce_scatter && api.all_gather && api.error_string && api.comm_count && api.comm_rank;
+    }
+  }
+  if (!ok && why) *why = "libnccl.so.2 (ncclReduceScatter, ncclAllGather) is not loadable";
+  return ok ? &api : nullptr;
+}
+
+#define NCCL_TRY(api, expr)                                                                          \
+  do {                                                                                               \
+    ncclResult_t r_ = (expr);                                                                        \
+    if (r_ != ncclSuccess) return fail(HOS_ECUDA, std::string("NCCL error in ") + #expr + ": " +     \
+                                                       (api)->error_string(r_));                     \
+  } while (0)
+
 extern "C" {
 
 const char* hos_version(void) { return "hos_b200 0.1.0 sm_100a"; }
@@ -546,6 +677,8 @@ void hos_plan_destroy(hos_plan* p) {
   for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);
   if (p->cap) cudaStreamDestroy(p->cap);
   for (auto& kv : p->ffts) cufftDestroy(kv.second);
+  for (void* b : {p->d_raw, p->d_send, p->d_mine, p->d_local, p->d_heads, p->d_vals, p->d_parts})
+    if (b) cudaFree(b);
   void* bufs[] = {p->d_regions, p->d_line_tile0, p->d_region_slots, p->d_line_cmax, p->d_line_start, p->d_row_off, p->d_pair_k1, p->d_pair_k2,
                   p->d_pair_base, p->d_line_of_ab, p->d_taper, p->d_tw, p->d_seg, p->d_half, p->d_E, p->d_part,
                   p->d_S, p->d_xin, p->d_out};
@@ -1014,6 +1147,120 @@ int hos_plan_stage_ms(const hos_plan* p, double* ms6) {
     float t = 0;
     CUDA_TRY(cudaEventElapsedTime(&t, p->ev[i], p->ev[i + 1]));
     ms6[i] = t;
+  }
+  return HOS_OK;
+}
+
+int hos_shard_layout(int order, int m, int k, int m3, int nranks, int64_t* out) {
+  if (!out) return fail(HOS_EPARAM, "null output");
+  if (nranks < 1 || k < 1) return fail(HOS_EPARAM, "nranks and k must be positive");
+  hos::Geometry g;
+  const std::string err = g.build(order, m, m3);
+  if (!err.empty()) return fail(HOS_EPARAM, err);
+  const std::vector<int64_t> rec = shard_layout(g, order, m3, k, nranks);
+  std::memcpy(out, rec.data(), rec.size() * sizeof(int64_t));
+  return HOS_OK;
+}
+
+int hos_comm_attach(hos_plan* p, void* nccl_comm, int rank, int nranks) {
+  int rc = check_plan(p);
+  if (rc) return rc;
+  if (p->batch != 1) return fail(HOS_EPARAM, "multi-GPU estimates need a batch-1 plan");
+  std::string why;
+  const NcclApi* api = nccl_api(&why);
+  if (!api) return fail(HOS_ECUDA, why);
+  if (!nccl_comm || nranks < 1 || rank < 0 || rank >= nranks) return fail(HOS_EPARAM, "bad communicator/rank");
+  int cnt = 0, me = 0;
+  NCCL_TRY(api, api->comm_count((ncclComm_t)nccl_comm, &cnt));
+  NCCL_TRY(api, api->comm_rank((ncclComm_t)nccl_comm, &me));
+  if (cnt != nranks || me != rank)
+    return fail(HOS_EPARAM, "communicator has rank " + std::to_string(me) + " of " + std::to_string(cnt) +
+                                ", caller said " + std::to_string(rank) + " of " + std::to_string(nranks));
+  if (cudaSetDevice(p->device) != cudaSuccess) return fail(HOS_ECUDA, "cannot select the plan's device");
+  for (void* b : {p->d_raw, p->d_send, p->d_mine, p->d_local, p->d_heads, p->d_vals, p->d_parts})
+    if (b) cudaFree(b);
+  p->layout = shard_layout(p->geo, p->order, p->m3, p->k, nranks);
+  const int64_t* L = p->layout.data();
+  const int64_t block = L[kLayoutPerRank * nranks], halo = L[kLayoutPerRank * nranks + 1];
+  const bool in_next = L[kLayoutPerRank * nranks + 2] != 0;
+  int64_t pmax = 1, local = 1;
+  for (int r = 0; r < nranks; r++) {
+    const int64_t* R = L + kLayoutPerRank * r;
+    pmax = std::max(pmax, R[13] - R[12]);
+    local = std::max(local, std::max(R[11], R[9]) - R[8]);
+  }
+  const size_t cs = csize(p->precision);
+  const int64_t heads = in_next ? halo : block;
+  if ((rc = alloc(p, &p->d_raw, (size_t)p->geo.ncells * cs)) || (rc = alloc(p, &p->d_send, (size_t)nranks * block * cs)) ||
+      (rc = alloc(p, &p->d_mine, (size_t)block * cs)) || (rc = alloc(p, &p->d_local, (size_t)local * cs)) ||
+      (rc = alloc(p, &p->d_heads, (size_t)nranks * heads * cs)) || (rc = alloc(p, &p->d_vals, (size_t)pmax * cs)) ||
+      (rc = alloc(p, &p->d_parts, (size_t)nranks * pmax * cs)))
+    return rc;
+  p->comm = nccl_comm;
+  p->rank = rank;
+  p->nranks = nranks;
+  return HOS_OK;
+}
+
+int hos_estimate_distributed(hos_plan* p, const void* x_dev, int x_dtype, void* out_dev, void* stream) {
+  int rc = check_plan(p);
+  if (rc) return rc;
+  if (!p->comm) return fail(HOS_EPARAM, "no communicator attached (hos_comm_attach)");
+  if (!x_dev || !out_dev) return fail(HOS_EPARAM, "null buffer");
+  const NcclApi* api = nccl_api(nullptr);
+  cudaStream_t st = (cudaStream_t)stream;
+  ncclComm_t comm = (ncclComm_t)p->comm;
+  const int n = p->nranks, me = p->rank;
+  const int64_t* L = p->layout.data();
+  const int64_t* R = L + kLayoutPerRank * me;
+  const int64_t block = L[kLayoutPerRank * n], halo = L[kLayoutPerRank * n + 1];
+  const bool in_next = L[kLayoutPerRank * n + 2] != 0;
+  const size_t cs = csize(p->precision);
+  const ncclDataType_t dt = p->precision == 32 ? ncclFloat32 : ncclFloat64;  // complex as 2 reals
+  char* raw = (char*)p->d_raw;
+  // 1. partial raw sums of this rank's segments over all of D_h
+  if ((rc = hos_partial_raw(p, x_dev, x_dtype, (int)R[0], (int)R[1], raw, stream))) return rc;
+  // 2. reduce-scatter by owned line blocks (padded to a common block)
+  CUDA_TRY(cudaMemsetAsync(p->d_send, 0, (size_t)n * block * cs, st));
+  for (int r = 0; r < n; r++) {
+    const int64_t* Q = L + kLayoutPerRank * r;
+    if (Q[9] > Q[8])
+      CUDA_TRY(cudaMemcpyAsync((char*)p->d_send + (size_t)r * block * cs, raw + (size_t)Q[8] * cs,
+                               (size_t)(Q[9] - Q[8]) * cs, cudaMemcpyDeviceToDevice, st));
+  }
+  NCCL_TRY(api, api->reduce_scatter(p->d_send, p->d_mine, (size_t)block * 2, dt, ncclSum, comm, st));
+  // 3. local lines = own block + the halo past it (held by the following rank(s))
+  const int64_t oc0 = R[8], oc1 = R[9], nc1 = R[11];
+  char* local = (char*)p->d_local;
+  if (oc1 > oc0) CUDA_TRY(cudaMemcpyAsync(local, p->d_mine, (size_t)(oc1 - oc0) * cs, cudaMemcpyDeviceToDevice, st));
+  const int64_t need = std::max<int64_t>(0, nc1 - oc1);
+  if (in_next) {
+    NCCL_TRY(api, api->all_gather(p->d_mine, p->d_heads, (size_t)halo * 2, dt, comm, st));  // block heads
+    if (need)
+      CUDA_TRY(cudaMemcpyAsync(local + (size_t)(oc1 - oc0) * cs, (char*)p->d_heads + (size_t)(me + 1) * halo * cs,
+                               (size_t)need * cs, cudaMemcpyDeviceToDevice, st));
+  } else {
+    NCCL_TRY(api, api->all_gather(p->d_mine, p->d_heads, (size_t)block * 2, dt, comm, st));
+    for (int r = me + 1; r < n; r++) {
+      const int64_t* Q = L + kLayoutPerRank * r;
+      const int64_t lo = std::max(Q[8], oc1), hi = std::min(Q[9], nc1);
+      if (lo < hi)
+        CUDA_TRY(cudaMemcpyAsync(local + (size_t)(lo - oc0) * cs, (char*)p->d_heads + ((size_t)r * block + lo - Q[8]) * cs,
+                                 (size_t)(hi - lo) * cs, cudaMemcpyDeviceToDevice, st));
+    }
+  }
+  // 4. smooth this rank's output rows, 5. all-gather the lexicographic slices
+  int64_t pmax = 1;
+  for (int r = 0; r < n; r++) pmax = std::max(pmax, L[kLayoutPerRank * r + 13] - L[kLayoutPerRank * r + 12]);
+  if (R[3] > R[2]) {
+    if ((rc = hos_smooth_raw(p, local, R[4], (int)R[2], (int)R[3], p->d_vals, stream))) return rc;
+  }
+  NCCL_TRY(api, api->all_gather(p->d_vals, p->d_parts, (size_t)pmax * 2, dt, comm, st));
+  for (int r = 0; r < n; r++) {
+    const int64_t* Q = L + kLayoutPerRank * r;
+    if (Q[13] > Q[12])
+      CUDA_TRY(cudaMemcpyAsync((char*)out_dev + (size_t)Q[12] * cs, (char*)p->d_parts + (size_t)r * pmax * cs,
+                               (size_t)(Q[13] - Q[12]) * cs, cudaMemcpyDeviceToDevice, st));
   }
   return HOS_OK;
 }

@@ -205,3 +205,26 @@ def test_shard_layout_invariants(m, w, k, n):
             assert lay.need_cells[r][1] - lay.own_cells[r][1] <= lay.halo or lay.halo_in_next is False
     assert lay.block >= max(c1 - c0 for c0, c1 in lay.own_cells)
     assert row_blocks(row_off, 1) == [0, rows]
+
+
+@pytest.mark.parametrize("m,w,k,n", [(64, 5, 12, 2), (128, 9, 7, 3), (256, 4, 16, 8), (32, 3, 5, 4),
+                                     (1024, 9, 1024, 8), (1024, 9, 1024, 3), (4096, 17, 2250, 8)])
+def test_native_shard_layout_matches_python(m, w, k, n):
+    """hos_shard_layout (the C-ABI multi-GPU path's layout) == parallel.shard_layout."""
+    import __graft_entry__
+
+    __graft_entry__.build()
+    from paper_1805_11775_b200 import _native
+
+    rows, lo, hi, cmax, line_start, row_off = _geom3(m, w)
+    rlr = lambda r0, r1: (r0, r1 - 1 + (w - 1) + 1) if r1 > r0 else (r0, r0)
+    lay = shard_layout(k, row_off, line_start, rlr, n)
+    rec, (block, halo, in_next) = _native.shard_layout_native(3, m, k, w, n)
+    assert list(rec[:, 0]) + [rec[-1, 1]] == lay.seg_bounds
+    assert list(rec[:, 2]) + [rec[-1, 3]] == lay.row_bounds
+    assert [tuple(v) for v in rec[:, 4:6]] == [tuple(v) for v in lay.own_lines]
+    assert [tuple(v) for v in rec[:, 6:8]] == [tuple(v) for v in lay.need_lines]
+    assert [tuple(v) for v in rec[:, 8:10]] == [tuple(v) for v in lay.own_cells]
+    assert [tuple(v) for v in rec[:, 10:12]] == [tuple(v) for v in lay.need_cells]
+    assert list(rec[:, 12]) + [rec[-1, 13]] == lay.point_bounds
+    assert (block, halo, bool(in_next)) == (lay.block, lay.halo, lay.halo_in_next)

@@ -334,3 +334,46 @@ def test_distributed_gpu_engine_gloo(cuda, world):
         tol = TOL_FP64 if prec == "fp64" else TOL_FP32
         for r in range(world):
             assert max_rel_dev(out[r][i], ref) <= tol, (world, r, i)
+
+
+def _nccl_single_rank_comm():
+    """A 1-rank NCCL communicator on the current device (ctypes on the
+    libnccl.so.2 the process uses)."""
+    import ctypes
+
+    nccl = ctypes.CDLL("libnccl.so.2")
+
+    class UniqueId(ctypes.Structure):
+        _fields_ = [("internal", ctypes.c_byte * 128)]
+
+    uid = UniqueId()
+    assert nccl.ncclGetUniqueId(ctypes.byref(uid)) == 0
+    comm = ctypes.c_void_p()
+    assert nccl.ncclCommInitRank(ctypes.byref(comm), 1, uid, 0) == 0
+    return nccl, comm
+
+
+@pytest.mark.parametrize("order,m,k,w,prec", [(3, 256, 13, 9, "fp64"), (4, 64, 7, 5, "fp64"), (3, 1024, 64, 9, "fp32")])
+def test_capi_distributed_nccl_single_rank(cuda, order, m, k, w, prec):
+    """hos_comm_attach + hos_estimate_distributed (NCCL reduce-scatter / all-gather
+    inside the library) on a 1-rank communicator match the oracle and the
+    single-GPU path; the multi-rank layout is the one pinned against
+    parallel.shard_layout in test_api.py."""
+    import torch
+
+    from paper_1805_11775_b200 import _native
+
+    nccl, comm = _nccl_single_rank_comm()
+    try:
+        x = np.random.default_rng(order * 1000 + m).standard_normal(m * k)
+        plan = _native.Plan(order, m, k, w, True, 64 if prec == "fp64" else 32, "hann", 1, 0)
+        plan.comm_attach(comm.value, 0, 1)
+        xd = torch.from_numpy(x).cuda()
+        got = plan.estimate_distributed(xd).cpu().numpy()
+        direct = plan.estimate(xd).cpu().numpy()
+        _, ref = O.estimate(x, order, m, k, w, True, "hann")
+        tol = TOL_FP64 if prec == "fp64" else TOL_FP32
+        assert north_star(got, ref) <= tol
+        assert north_star(got, direct) <= tol
+    finally:
+        nccl.ncclCommDestroy(comm)
