@@ -377,3 +377,41 @@ def test_capi_distributed_nccl_single_rank(cuda, order, m, k, w, prec):
         assert north_star(got, direct) <= tol
     finally:
         nccl.ncclCommDestroy(comm)
+
+
+def _sweep_cases():
+    rng = np.random.default_rng(20260601)
+    cases = []
+    for order, ms in ((3, (4, 8, 12, 16, 31, 32, 64, 96, 128, 200, 256, 512)), (4, (8, 16, 24, 32, 50, 64, 128))):
+        for m in ms:
+            wmax = max(1, (m - 1) // 2 - 0)  # 2 m3 < m
+            for _ in range(2):
+                w = int(rng.integers(1, max(2, min(wmax, 12) + 1)))
+                if 2 * w >= m:
+                    w = max(1, (m - 1) // 2)
+                k = int(rng.integers(1, 9))
+                cases.append((order, m, k, w, bool(rng.integers(0, 2)), ["fp64", "fp32"][int(rng.integers(0, 2))],
+                              [None, "hann"][int(rng.integers(0, 2))], int(rng.integers(0, 1 << 30))))
+    return cases
+
+
+@pytest.mark.parametrize("case", _sweep_cases(), ids=lambda c: "o%d_m%d_k%d_w%d_%s_%s_%s" % (
+    c[0], c[1], c[2], c[3], "conj" if c[4] else "noconj", c[5], c[6] or "flat"))
+def test_sweep_small_shapes(cuda, case):
+    """Seeded sweep over small shapes (power-of-two and general M, odd tile
+    counts, k not a multiple of the warp split, w = 1, both orders and
+    precisions, taper on/off) against the oracle."""
+    order, m, k, w, conj, prec, taper, seed = case
+    P = api()
+    x = np.random.default_rng(seed).standard_normal(m * k + 3)
+    cfg = P.EstimationConfig(order, P.SegmentConfig(m=m, k=k), w, conjugate_last=conj, precision=prec, taper=taper)
+    g = P.estimate_spectrum(P.TimeSeries(x), cfg)
+    dom, ref = O.estimate(x, order, m, k, w, conj, taper)
+    assert np.array_equal(g.indices, dom)
+    if np.abs(ref).max() < 1e-12:
+        # identically-zero estimate (e.g. m = 4: every point involves the demeaned
+        # DC bin): the reference's values are rounding noise and max|B| is no
+        # scale -- bound the absolute error by the compute precision instead
+        assert np.abs(g.values).max() <= (1e-12 if prec == "fp64" else 1e-6)
+    else:
+        assert north_star(g.values, ref) <= (TOL_FP64 if prec == "fp64" else TOL_FP32)
