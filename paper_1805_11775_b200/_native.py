@@ -227,8 +227,9 @@ class Plan:
             out_host = np.empty((self.batch, self.npoints) if self.batch > 1 else (self.npoints,), cd)
         dt = HOS_F32 if x_host.dtype == np.float32 else HOS_F64
         stride = x_host.shape[-1]
+        # synchronous: the plan's private stream (no torch stream lookup on this path)
         raise_for(lib().hos_estimate_host(self.handle, x_host.ctypes.data, dt, stride,
-                                          out_host.ctypes.data, self._stream()))
+                                          out_host.ctypes.data, None))
         return out_host
 
     def partial_raw(self, x, seg_begin, seg_end, raw):

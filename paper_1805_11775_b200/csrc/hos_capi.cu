@@ -811,7 +811,8 @@ int hos_estimate_host(hos_plan* p, const void* x_host, int x_dtype, int64_t x_st
   if (rc) return rc;
   if ((rc = check_dtype_x(x_dtype))) return rc;
   if (!x_host || !out_host) return fail(HOS_EPARAM, "null buffer");
-  cudaStream_t st = (cudaStream_t)stream;
+  // synchronous host API: NULL stream = the plan's private stream
+  cudaStream_t st = stream ? (cudaStream_t)stream : p->cap;
   const size_t es = x_dtype == HOS_F32 ? 4 : 8;
   const size_t km = (size_t)p->k * p->m;
   // copy path: H2D into the plan's staging buffer, the device pipeline, D2H
