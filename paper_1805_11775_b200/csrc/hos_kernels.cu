@@ -115,9 +115,13 @@ struct C2<double> {
 
 // threads of the fused front end for m = 2^LOG2M: m/8 (8 samples, two radix-4
 // butterflies per stage each), clamped to [32, 256]
+#ifndef HOS_FRONT_SPT
+#define HOS_FRONT_SPT 8  // samples per thread and segment
+#endif
 template <int LOG2M>
 __host__ __device__ constexpr int front_threads() {
-  return (1 << LOG2M) / 8 >= 256 ? 256 : ((1 << LOG2M) / 8 >= 32 ? (1 << LOG2M) / 8 : 32);
+  return (1 << LOG2M) / HOS_FRONT_SPT >= 256 ? 256
+                                             : ((1 << LOG2M) / HOS_FRONT_SPT >= 32 ? (1 << LOG2M) / HOS_FRONT_SPT : 32);
 }
 // segment pairs per CTA: one-warp transforms (m <= 256) run four per CTA,
 // each warp on its own pair with warp-level barriers (a CTA per pair made the
@@ -207,7 +211,6 @@ __global__ void __launch_bounds__(front_threads<LOG2M>() * front_pairs<LOG2M>())
   // with w = exp(-2 pi i / m) (table tw[t], t < m).
   CT* xin = bufA;
   CT* yout = bufB;
-#ifndef HOS_FRONT_NOFFT
 #pragma unroll
   for (int ls = 0; ls + 2 <= LOG2M; ls += 2) {
     const int qn = (M >> ls) >> 2;  // n / 4 (compile-time after unrolling)
@@ -258,7 +261,6 @@ __global__ void __launch_bounds__(front_threads<LOG2M>() * front_pairs<LOG2M>())
     sync();
     xin = yout;
   }
-#endif
   if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;");
   // X_a(f) = (Z(f) + conj Z(-f)) / 2,  X_b(f) = (Z(f) - conj Z(-f)) / 2i
   CT* row = E + ((int64_t)b * krows + sa) * Lp;
