@@ -59,7 +59,7 @@ struct hos_plan {
   int hstride = 0;   // complex elements per half-spectrum row
   int L = 0, Lp = 0; // extended-spectrum length / pitch (complex elements)
   // device tables
-  hos::Region* d_regions = nullptr;
+  hos::Tile* d_tiles = nullptr;
   int32_t* d_line_tile0 = nullptr;
   int32_t* d_region_slots = nullptr;  // slots per region of the full-K launch (K4 lookups)
   int32_t* d_line_cmax = nullptr;
@@ -165,6 +165,23 @@ int run_fft(hos_plan* p, int rows, const void* in, void* out, cudaStream_t st) {
   return HOS_OK;
 }
 
+// D_h geometry with the K2 tile shape for this M: 8 x 16 tiles (lane step 2)
+// only when the 16 x 32 tiles would issue >= 1.8x more cells, else 16 x 32.
+// An 8 x 16 region stages 2.5x the chunks of a 16 x 32 one and measured
+// 1.79x slower per issued cell (cfg3), so even cfg4 (1.55x fewer cells)
+// loses with it (K2 106 vs 101 us).  HOS_K2_TILE=2|4 forces the step.
+std::string build_geometry(hos::Geometry& g, int order, int m, int m3) {
+  int forced = 0;
+  if (const char* env = std::getenv("HOS_K2_TILE")) forced = std::atoi(env);
+  if (forced == 2 || forced == 4) return g.build(order, m, m3, forced);
+  std::string err = g.build(order, m, m3, 4);
+  if (!err.empty()) return err;
+  hos::Geometry g2;
+  if (!g2.build(order, m, m3, 2).empty()) return "";
+  if ((double)g.issued_cells >= 1.8 * (double)g2.issued_cells) g = std::move(g2);
+  return "";
+}
+
 int check_plan(const hos_plan* p) {
   if (!p) return fail(HOS_EPARAM, "null plan");
   return HOS_OK;
@@ -173,7 +190,7 @@ int check_plan(const hos_plan* p) {
 // CTAs splitting a launch over nseg segments of `batch` series: one wave of
 // SMs x occupancy CTAs in total, at least 16 work units per CTA (and never
 // more CTAs than units, so every CTA's range is non-empty).
-int64_t work_items(const hos_plan* p) { return (int64_t)p->geo.regions.size(); }
+int64_t work_items(const hos_plan* p) { return (int64_t)p->geo.nregions; }
 
 int nctas_for(const hos_plan* p, int nseg, int batch) {
   const int64_t work = work_items(p) * nseg;
@@ -221,7 +238,9 @@ hos::SlotInfo slot_info(const hos_plan* p, int nseg, int n) {
   if (nseg == p->k && n == p->nctas) si.region_slots = p->d_region_slots;  // the plan's main launch
   si.line_tile0 = p->d_line_tile0;
   si.nseg = nseg;
-  si.nregions = (int)p->geo.regions.size();
+  si.nregions = p->geo.nregions;
+  si.tile_cols = p->geo.tile_cols;
+  si.tiles_per_region = p->geo.tiles_per_region;
   si.nwarps = nwarps_for(p, nseg, n);
   const hos::WarpSplit sp = warp_split(p, nseg, n, p->batch);
   si.split_wa = sp.wa;
@@ -238,8 +257,9 @@ hos::TripleArgs triple_args(const hos_plan* p, int seg_begin, int seg_end, int n
   x.seg_end = seg_end;
   x.E = p->d_E;
   x.Lp = p->Lp;
-  x.regions = p->d_regions;
-  x.nregions = (int)p->geo.regions.size();
+  x.tiles = p->d_tiles;
+  x.nregions = p->geo.nregions;
+  x.tile_step = p->geo.tile_step;
   x.nwarps = nwarps_for(p, seg_end - seg_begin, n);
   {
     const hos::WarpSplit sp = warp_split(p, seg_end - seg_begin, n, batch);
@@ -565,7 +585,7 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
   p->taper = taper;
   p->batch = batch;
   p->device = device;
-  std::string err = p->geo.build(order, m, m3);
+  std::string err = build_geometry(p->geo, order, m, m3);
   if (!err.empty()) {
     delete p;
     return fail(HOS_EPARAM, err);
@@ -586,7 +606,7 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
     p->max_line = std::max<int>(p->max_line, (int)(g.line_start[l + 1] - g.line_start[l]));
   {
     const char* env = std::getenv("HOS_K4_SERIES");  // "0": always line scans + box sums
-    p->series_k4 = order == 3 && hos::smooth_series3_smem(g.ncells, g.nlines, g.rows, (int)g.regions.size(), g.npoints) <= 200 * 1024 &&
+    p->series_k4 = order == 3 && hos::smooth_series3_smem(g.ncells, g.nlines, g.rows, g.nregions, g.npoints) <= 200 * 1024 &&
                    !(env && env[0] == '0');
   }
   // +4 elements: fp32 operands are staged from the 16-byte-aligned element at
@@ -594,7 +614,7 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
   // to 3 elements past the last frequency; even pitch keeps rows 16-byte aligned
   p->Lp = (p->L + 4 + 1) & ~1;
   cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, device);
-  p->occupancy = hos::triple_occupancy(precision);
+  p->occupancy = hos::triple_occupancy(precision, g.tile_step);
   if (const char* env = std::getenv("HOS_K2_SPLIT")) {  // "wa:wb"
     int wa = 0, wb = 0;
     if (std::sscanf(env, "%d:%d", &wa, &wb) == 2 && wa > 0 && wb > 0) {
@@ -607,11 +627,11 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
 
 
   std::vector<int32_t> cmax(g.line_cmax.begin(), g.line_cmax.end());
-  if ((rc = upload(p, &p->d_regions, g.regions))) return bail(rc);
+  if ((rc = upload(p, &p->d_tiles, g.tiles))) return bail(rc);
   if ((rc = upload(p, &p->d_line_tile0, g.line_tile0))) return bail(rc);
   {
     const hos::WarpSplit sp = warp_split(p, k, p->nctas, batch);
-    std::vector<int32_t> rs(g.regions.size());
+    std::vector<int32_t> rs(g.nregions);
     for (size_t r = 0; r < rs.size(); r++) rs[r] = sp.region_slots((int)r, k);
     if ((rc = upload(p, &p->d_region_slots, rs))) return bail(rc);
   }
@@ -679,7 +699,7 @@ void hos_plan_destroy(hos_plan* p) {
   for (auto& kv : p->ffts) cufftDestroy(kv.second);
   for (void* b : {p->d_raw, p->d_send, p->d_mine, p->d_local, p->d_heads, p->d_vals, p->d_parts})
     if (b) cudaFree(b);
-  void* bufs[] = {p->d_regions, p->d_line_tile0, p->d_region_slots, p->d_line_cmax, p->d_line_start, p->d_row_off, p->d_pair_k1, p->d_pair_k2,
+  void* bufs[] = {p->d_tiles, p->d_line_tile0, p->d_region_slots, p->d_line_cmax, p->d_line_start, p->d_row_off, p->d_pair_k1, p->d_pair_k2,
                   p->d_pair_base, p->d_line_of_ab, p->d_taper, p->d_tw, p->d_seg, p->d_half, p->d_E, p->d_part,
                   p->d_S, p->d_xin, p->d_out};
   for (void* b : bufs)

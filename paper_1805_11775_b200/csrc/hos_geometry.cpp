@@ -60,16 +60,16 @@ struct RegionRec {
 };
 
 void add_band_regions(std::vector<RegionRec>& regs, std::vector<int32_t>& line_tile0, int line0, int nrows,
-                      int row_freq0, int plane_freq, int lo, int cmax_band) {
+                      int row_freq0, int plane_freq, int lo, int cmax_band, int tile_cols) {
   const int ncols = cmax_band - lo + 1;
-  const int nr = (ncols + kTileCols - 1) / kTileCols;
+  const int nr = (ncols + tile_cols - 1) / tile_cols;
   for (int l = line0; l < line0 + nrows; l++) line_tile0[l] = (int32_t)regs.size();
-  for (int r = 0; r < nr; r++) regs.push_back({line0, nrows, row_freq0, plane_freq, lo + r * kTileCols});
+  for (int r = 0; r < nr; r++) regs.push_back({line0, nrows, row_freq0, plane_freq, lo + r * tile_cols});
 }
 
 }  // namespace
 
-std::string Geometry::build(int order_, int m_, int m3_) {
+std::string Geometry::build(int order_, int m_, int m3_, int tile_step_) {
   order = order_;
   m = m_;
   m3 = m3_;
@@ -77,6 +77,11 @@ std::string Geometry::build(int order_, int m_, int m3_) {
   if (order != 3 && order != 4) return "order must be 3 or 4, got " + std::to_string(order);
   if (m < 2) return "segment length must be >= 2, got " + std::to_string(m);
   if (m3 < 1) return "smoothing window must be >= 1, got " + std::to_string(m3);
+  if (tile_step_ != 2 && tile_step_ != 4) return "tile step must be 2 or 4";
+  tile_step = tile_step_;
+  tile_rows = 4 * tile_step;
+  tile_cols = 8 * tile_step;
+  tiles_per_region = 32 / (tile_step * tile_step);
   if (2 * m3 >= m)
     return "smoothing window " + std::to_string(m3) + " must satisfy m3 < m/2 (segment length m = " +
            std::to_string(m) + ")";
@@ -136,11 +141,11 @@ std::string Geometry::build(int order_, int m_, int m3_) {
     }
     ncells = line_start.back();
     line_tile0.assign(n3lines, 0);
-    for (int l0 = 0; l0 < n3lines; l0 += kBandRows) {
-      const int nr = std::min(kBandRows, n3lines - l0);
+    for (int l0 = 0; l0 < n3lines; l0 += tile_rows) {
+      const int nr = std::min(tile_rows, n3lines - l0);
       int cb = lo;
       for (int l = l0; l < l0 + nr; l++) cb = std::max(cb, (int)cmax3[l]);
-      add_band_regions(regs, line_tile0, l0, nr, lo + l0, 0, lo, cb);
+      add_band_regions(regs, line_tile0, l0, nr, lo + l0, 0, lo, cb, tile_cols);
     }
   } else {
     // lines = raw pairs (a,b) of the order-3 dilation; cols c in [lo, cmax4(a,b)]
@@ -169,42 +174,40 @@ std::string Geometry::build(int order_, int m_, int m3_) {
       }
       const int nl = (int)line_a.size() - first_line;
       line_tile0.resize(line_a.size(), 0);
-      for (int l0 = 0; l0 < nl; l0 += kBandRows) {
-        const int nr = std::min(kBandRows, nl - l0);
+      for (int l0 = 0; l0 < nl; l0 += tile_rows) {
+        const int nr = std::min(tile_rows, nl - l0);
         int cb = lo;
         for (int l = first_line + l0; l < first_line + l0 + nr; l++) cb = std::max(cb, (int)line_cmax[l]);
-        add_band_regions(regs, line_tile0, first_line + l0, nr, line_b[first_line + l0], a, lo, cb);
+        add_band_regions(regs, line_tile0, first_line + l0, nr, line_b[first_line + l0], a, lo, cb, tile_cols);
       }
     }
     nlines = (int64_t)line_a.size();
     ncells = line_start.back();
   }
 
-  // tiles -> regions (consecutive pairs; an odd last tile gets an empty partner
-  // that mirrors it, so its staged loads stay in range)
-  regions.clear();
+  // tiles, padded to whole regions with empty copies of the last real tile
+  // (their staged loads stay in range; nrows 0 keeps them out of the results)
   ntiles = (int)regs.size();
+  nregions = (ntiles + tiles_per_region - 1) / tiles_per_region;
+  tiles.clear();
   f_lo = order == 3 ? 2 * lo : 3 * lo;
   f_hi = 0;
-  for (size_t i = 0; i < regs.size(); i += 2) {
-    Region g{};
-    for (int h = 0; h < 2; h++) {
-      const bool real = i + h < regs.size();
-      const RegionRec& r = regs[real ? i + h : i];
-      Tile& t = g.t[h];
-      t.line0 = r.line0;
-      t.nrows = real ? r.nrows : 0;
-      t.row_freq0 = r.row_freq0;
-      t.plane_freq = r.plane_freq;
-      t.col0 = r.col0;
-      // frequencies the tile's staged operands cover
-      const int rmax = r.row_freq0 + kBandRows - 1, cmax = r.col0 + kTileCols - 1;
-      f_hi = std::max({f_hi, r.plane_freq + rmax + cmax, rmax, cmax, r.plane_freq});
-      f_lo = std::min({f_lo, r.plane_freq + r.row_freq0 + r.col0, r.row_freq0, r.col0, r.plane_freq});
-    }
-    regions.push_back(g);
+  for (int i = 0; i < nregions * tiles_per_region; i++) {
+    const bool real = i < ntiles;
+    const RegionRec& r = regs[real ? i : ntiles - 1];
+    Tile t{};
+    t.line0 = r.line0;
+    t.nrows = real ? r.nrows : 0;
+    t.row_freq0 = r.row_freq0;
+    t.plane_freq = r.plane_freq;
+    t.col0 = r.col0;
+    tiles.push_back(t);
+    // frequencies the tile's staged operands cover
+    const int rmax = r.row_freq0 + tile_rows - 1, cmax = r.col0 + tile_cols - 1;
+    f_hi = std::max({f_hi, r.plane_freq + rmax + cmax, rmax, cmax, r.plane_freq});
+    f_lo = std::min({f_lo, r.plane_freq + r.row_freq0 + r.col0, r.row_freq0, r.col0, r.plane_freq});
   }
-  issued_cells = (int64_t)regions.size() * kRegionCells;
+  issued_cells = (int64_t)nregions * kRegionCells;
   return "";
 }
 

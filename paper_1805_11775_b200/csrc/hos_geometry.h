@@ -41,27 +41,23 @@ int64_t domain_size(int order, int m);
 // rows [start, stop) of the lexicographic domain into out ((stop-start) x (order-1))
 void domain_rows(int order, int m, int64_t start, int64_t stop, int32_t* out);
 
-// K2 work decomposition.  D_h is cut into TILES of up to kBandRows
-// consecutive lines (a "band" of one plane) x kTileCols columns, listed band
-// after band; consecutive tiles are paired into REGIONS (a warp's unit of
-// work: 2 tiles x 16 lines x 32 columns = 1024 cells).  16-line bands halve
-// the staircase waste along D_h's sloped edges; pairing tiles (possibly of
-// different bands) keeps a warp's tile of 32 cells per lane.
-constexpr int kBandRows = 16;    // lines per band / tile (2 lane rows x 8 rows)
-constexpr int kTileCols = 32;    // columns per tile (8 lanes x 4)
-constexpr int kRegionCells = 2 * kBandRows * kTileCols;
+// K2 work decomposition.  D_h is cut into TILES of up to tile_rows
+// consecutive lines (a "band" of one plane) x tile_cols columns, listed band
+// after band; consecutive tiles are grouped into REGIONS of 1024 cells (a
+// warp's unit of work, 32 cells per lane).  The tile shape follows the K2
+// lane step S (hos_kernels.cu): tiles of 4S lines x 8S columns, 32/S^2 per
+// region -- S = 4: 16 x 32 tiles in pairs (large M), S = 2: 8 x 16 tiles in
+// groups of 8 (small M, where D_h's lines are short and large tiles are
+// mostly empty).  The last region is completed with empty tiles (nrows 0)
+// that mirror its last real tile, so their staged loads stay in range.
+constexpr int kRegionCells = 1024;
 
 struct Tile {
   int32_t line0;      // first line of the band
-  int32_t nrows;      // lines in the band (<= kBandRows; 0: empty second tile)
+  int32_t nrows;      // lines in the band (<= tile_rows; 0: empty filler tile)
   int32_t row_freq0;  // frequency of line0's row factor (order 3: a, order 4: b)
   int32_t plane_freq; // order 4: a of the plane; order 3: 0
   int32_t col0;       // first column of the tile
-};
-
-struct Region {
-  Tile t[2];
-  int32_t pad[2];
 };
 
 struct Geometry {
@@ -87,12 +83,14 @@ struct Geometry {
   // frequencies any region reads (inclusive), for the extended spectrum
   int f_lo = 0, f_hi = 0;
   // K2 tiles and regions
-  std::vector<Region> regions;        // tile pairs (tile 2r and 2r+1 of the band-major tile list)
-  int ntiles = 0;
+  int tile_step = 4, tile_rows = 16, tile_cols = 32, tiles_per_region = 2;
+  std::vector<Tile> tiles;            // band-major, padded to whole regions (region r = tiles r*NT ..)
+  int ntiles = 0;                     // real tiles
+  int nregions = 0;
   std::vector<int32_t> line_tile0;    // per line: index of the tile holding its first column
   int64_t issued_cells = 0;           // cells computed by K2 (regions x 1024)
 
-  std::string build(int order, int m, int m3);  // returns "" or an error message
+  std::string build(int order, int m, int m3, int tile_step = 4);  // returns "" or an error message
 };
 
 }  // namespace hos

@@ -423,8 +423,9 @@ cudaError_t launch_expand_full(const void* H, int m, int hstride, int rows, int 
 // ===========================================================================
 // K2: triple / quadruple product over D_h (hospectra/spectra.py:227-263).
 //
-// Work = nregions x nseg units; a region is a pair of D_h tiles (16 lines x
-// 32 columns each, hos_geometry.h), a unit one region in one segment.  The
+// Work = nregions x nseg units; a region is 1024 cells of D_h in 32/S^2 tiles
+// of 4S lines x 8S columns (hos_geometry.h; S = 4 below unless noted, S = 2
+// for small M), a unit one region in one segment.  The
 // nwarps warps of the launch take equal contiguous unit ranges, so every
 // warp does the same work and warps never wait for each other.  A warp walks
 // its units in order; per unit its 32 lanes stage, for each tile, the
@@ -440,9 +441,9 @@ cudaError_t launch_expand_full(const void* H, int m, int hstride, int rows, int 
 // the region), fixed by the partition: the fp64 combination order in K4a is
 // fixed and results are deterministic.
 //
-// Lane 16h + 4u + v works on tile h of the region, rows u + 4i (i<4) and
-// columns v + 4j (j<8): both progressions have step 4, so cell (i,j) reads G
-// at u + v + 4(i+j) and a lane needs 4 row + 8 column + 11 G values per
+// Lane S^2 h + S u + v works on tile h of the region, rows u + S i (i<4) and
+// columns v + S j (j<8): both progressions have step S, so cell (i,j) reads G
+// at u + v + S(i+j) and a lane needs 4 row + 8 column + 11 G values per
 // segment; every shared load reads <= 7 consecutive 8-byte values per tile,
 // and the tiles' staged copies sit 8 elements apart modulo the bank width, so
 // no load has a bank conflict (an 8x4 lane tile with step-2 columns had
@@ -456,24 +457,33 @@ struct Cplx;
 template <>
 struct Cplx<float> {
   using C = float2;  // spectrum element / accumulator / partial
-  static constexpr int kUnitChunks = 104;  // 2 tiles x (rows 9 | cols 17 | G 24 | plane 1 | pad 1) 16-byte chunks
 };
 template <>
 struct Cplx<double> {
   using C = double2;
-  static constexpr int kUnitChunks = 200;  // 2 tiles x (rows 16 | cols 32 | G 47 | plane 1 | pad 4)
 };
 
-// chunk offsets of the operands of one tile inside a staged unit (tile h at h * half)
-template <typename T>
-struct UnitLayout;
-template <>
-struct UnitLayout<float> {
-  static constexpr int rows = 0, cols = 9, g = 26, plane = 50, half = 52;  // tile 1 at +104 elements (= 8 mod 16)
-};
-template <>
-struct UnitLayout<double> {
-  static constexpr int rows = 0, cols = 16, g = 48, plane = 95, half = 100;  // tile 1 at +100 elements (= 4 mod 8)
+// Staged unit layout for precision T and lane step S (tiles of 4S lines x 8S
+// columns, 32/S^2 tiles per region).  Per tile, in 16-byte chunks: rows
+// (4S [+1 alignment shift] elements), columns (8S [+1]), G (12S-1 [+1]), F(a)
+// for order 4, then padding so consecutive tiles start 1/NT of the bank
+// width apart (tile loads of the warp hit different banks).
+template <typename T, int S>
+struct K2Layout {
+  static constexpr int EPC = sizeof(T) == 4 ? 2 : 1;  // elements per 16-byte chunk
+  static constexpr int SH = EPC == 2 ? 1 : 0;         // fp32: operands start 0/1 element into their copy
+  static constexpr int TR = 4 * S, TC = 8 * S, NT = 32 / (S * S);
+  static constexpr int rows = 0;
+  static constexpr int cols = rows + (TR + SH + EPC - 1) / EPC;
+  static constexpr int g = cols + (TC + SH + EPC - 1) / EPC;
+  static constexpr int plane = g + (TR + TC - 1 + SH + EPC - 1) / EPC;
+  static constexpr int used = plane + 1;
+  static constexpr int slots = EPC == 2 ? 16 : 8;  // 128-byte bank row, in elements
+  static constexpr int target = slots / NT;
+  static constexpr int pad_to(int h) { return (h * EPC) % slots == target % slots ? h : pad_to(h + 1); }
+  static constexpr int half = pad_to(used);  // tile stride (chunks)
+  static constexpr int UC = NT * half;       // chunks per staged unit
+  static constexpr int GROUP = S == 4 ? 4 : 2;  // units staged / waited for / computed together
 };
 
 // conj(*p) from its own shared load: the negation happens in place in the
@@ -497,7 +507,7 @@ __device__ __forceinline__ float2 lds_conj(const float2* p) {
 // enters only as broadcast scalars, so no operand form of it has to be built,
 // and the two updates of a cell are independent FFMA2s.  The cell value is
 // aR -+ i aI (CONJ: -).
-template <bool ORDER4>
+template <bool ORDER4, int RS>
 __device__ __forceinline__ void cells_f32(const float2* __restrict__ rows, const float2* __restrict__ cols,
                                           const float2* __restrict__ gs, const float2* __restrict__ plane,
                                           float2 (&aR)[4][8], float2 (&aI)[4][8]) {
@@ -506,7 +516,7 @@ __device__ __forceinline__ void cells_f32(const float2* __restrict__ rows, const
     const float2 pa = *plane, pac = lds_conj(plane);
 #pragma unroll
     for (int i = 0; i < 4; i++) {
-      const float2 r = rows[4 * i];
+      const float2 r = rows[RS * i];
       const float2 t = fmul2(make_float2(r.x, r.x), pa);
       fa[i] = ffma2(make_float2(r.y, r.y), make_float2(pac.y, pac.x), t);
       fac[i] = make_float2(fa[i].x, -fa[i].y);
@@ -514,15 +524,15 @@ __device__ __forceinline__ void cells_f32(const float2* __restrict__ rows, const
   } else {
 #pragma unroll
     for (int i = 0; i < 4; i++) {
-      fa[i] = rows[4 * i];
-      fac[i] = lds_conj(rows + 4 * i);
+      fa[i] = rows[RS * i];
+      fac[i] = lds_conj(rows + RS * i);
     }
   }
 #pragma unroll
-  for (int j = 0; j < 8; j++) fb[j] = cols[4 * j];
+  for (int j = 0; j < 8; j++) fb[j] = cols[RS * j];
 #pragma unroll
   for (int q = 0; q < 11; q++) {
-    const float2 g = gs[4 * q];
+    const float2 g = gs[RS * q];
 #pragma unroll
     for (int i = 0; i < 4; i++) {
       const int j = q - i;
@@ -535,13 +545,13 @@ __device__ __forceinline__ void cells_f32(const float2* __restrict__ rows, const
   }
 }
 
-template <bool CONJ, bool ORDER4>
+template <bool CONJ, bool ORDER4, int RS>
 __device__ __forceinline__ void cells_f64(const double2* __restrict__ rows, const double2* __restrict__ cols,
                                           const double2* __restrict__ gs, const double2* __restrict__ plane,
                                           double2 (&acc)[4][8]) {
   double2 fa[4], fb[8];
 #pragma unroll
-  for (int i = 0; i < 4; i++) fa[i] = rows[4 * i];
+  for (int i = 0; i < 4; i++) fa[i] = rows[RS * i];
   if (ORDER4) {
     const double2 pa = *plane;
 #pragma unroll
@@ -552,10 +562,10 @@ __device__ __forceinline__ void cells_f64(const double2* __restrict__ rows, cons
     }
   }
 #pragma unroll
-  for (int j = 0; j < 8; j++) fb[j] = cols[4 * j];
+  for (int j = 0; j < 8; j++) fb[j] = cols[RS * j];
 #pragma unroll
   for (int q = 0; q < 11; q++) {
-    const double2 g = gs[4 * q];
+    const double2 g = gs[RS * q];
 #pragma unroll
     for (int i = 0; i < 4; i++) {
       const int j = q - i;
@@ -576,14 +586,11 @@ __device__ __forceinline__ void cells_f64(const double2* __restrict__ rows, cons
 #ifndef HOS_K2_PAIRS
 #define HOS_K2_PAIRS 2
 #endif
-#ifndef HOS_K2_GROUP
-#define HOS_K2_GROUP 4
-#endif
 constexpr int kWarpPairs = HOS_K2_PAIRS;  // ring of unit groups per warp (kWarpPairs-1 groups in flight)
-constexpr int kGroup = HOS_K2_GROUP;      // units staged / waited for / computed together
-template <typename T>
+template <typename T, int S>
 constexpr size_t warp_triple_smem() {
-  return 16 * (size_t)kTripleWarps * kGroup * kWarpPairs * Cplx<T>::kUnitChunks;
+  using L = K2Layout<T, S>;
+  return 16 * (size_t)kTripleWarps * L::GROUP * kWarpPairs * L::UC;
 }
 
 __device__ __forceinline__ void cp_async16_cg(unsigned dst, const void* src) {
@@ -592,22 +599,22 @@ __device__ __forceinline__ void cp_async16_cg(unsigned dst, const void* src) {
 
 
 // chunks of a staged unit that are copied (the rest is padding)
-template <typename T, bool ORDER4>
+template <typename T, int S, bool ORDER4>
 __device__ __forceinline__ bool chunk_valid(int c) {
-  using L = UnitLayout<T>;
-  return c < 2 * L::half && c % L::half < L::plane + (ORDER4 ? 1 : 0);
+  using L = K2Layout<T, S>;
+  return c < L::UC && c % L::half < L::plane + (ORDER4 ? 1 : 0);
 }
 // Source of (valid) chunk c of a staged unit, as an element offset from the
 // segment's E row.  fp32 operands are copied from the 16-byte-aligned element
 // at or below their start; the consumer adds the operand's shift (0 or 1).
-template <typename T>
-__device__ __forceinline__ int chunk_src(int c, const Region* __restrict__ rg, int f_lo) {
-  using L = UnitLayout<T>;
-  constexpr int per = sizeof(T) == 4 ? 2 : 1;  // elements per chunk
+template <typename T, int S>
+__device__ __forceinline__ int chunk_src(int c, const Tile* __restrict__ rt, int f_lo) {
+  using L = K2Layout<T, S>;
+  constexpr int per = L::EPC;
   auto floor_al = [](int o) { return sizeof(T) == 4 ? (o & ~1) : o; };
-  const int h = c >= L::half;
+  const int h = L::NT == 2 ? (c >= L::half) : c / L::half;
   const int cc = c - h * L::half;
-  const Tile& t = rg->t[h];
+  const Tile& t = rt[L::NT == 2 || h < L::NT ? h : 0];
   if (cc < L::cols) return floor_al(t.row_freq0 - f_lo) + per * (cc - L::rows);
   if (cc < L::g) return floor_al(t.col0 - f_lo) + per * (cc - L::cols);
   if (cc < L::plane) return floor_al(t.plane_freq + t.row_freq0 + t.col0 - f_lo) + per * (cc - L::g);
@@ -653,19 +660,21 @@ struct LaneOps {
   int rows, cols, g, plane;
 };
 
-template <typename T, bool CONJ, bool ORDER4>
+template <typename T, bool CONJ, bool ORDER4, int S>
 __device__ __forceinline__ void warp_cells(const typename Cplx<T>::C* q, const LaneOps& o, Acc<T>& acc) {
   if constexpr (sizeof(T) == 4)
-    cells_f32<ORDER4>(q + o.rows, q + o.cols, q + o.g, q + o.plane, acc.r, acc.i);
+    cells_f32<ORDER4, S>(q + o.rows, q + o.cols, q + o.g, q + o.plane, acc.r, acc.i);
   else
-    cells_f64<CONJ, ORDER4>(q + o.rows, q + o.cols, q + o.g, q + o.plane, acc.v);
+    cells_f64<CONJ, ORDER4, S>(q + o.rows, q + o.cols, q + o.g, q + o.plane, acc.v);
 }
 
-template <typename T, bool CONJ, bool ORDER4>
+template <typename T, bool CONJ, bool ORDER4, int S>
 __global__ void __launch_bounds__(32 * kTripleWarps, 8 / kTripleWarps) k_triple_w(const __grid_constant__ TripleArgs a) {
   using C = typename Cplx<T>::C;
-  constexpr int UC = Cplx<T>::kUnitChunks;
-  constexpr int per = sizeof(T) == 4 ? 2 : 1;  // elements per 16-byte chunk
+  using L = K2Layout<T, S>;
+  constexpr int UC = L::UC;
+  constexpr int kGroup = L::GROUP;
+  constexpr int per = L::EPC;                   // elements per 16-byte chunk
   constexpr int NCH = (UC + 31) / 32;           // chunk slots per lane
   extern __shared__ __align__(128) unsigned char smraw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -707,14 +716,14 @@ __global__ void __launch_bounds__(32 * kTripleWarps, 8 / kTripleWarps) k_triple_
   auto p_enter = [&](int r, int seg) {
     p_seg = reinterpret_cast<const char*>(E + (int64_t)seg * Lp);
 #pragma unroll
-    for (int s = 0; s < NCH; s++) p_off[s] = (unsigned)sizeof(C) * chunk_src<T>(lane + 32 * s, a.regions + r, f_lo);
+    for (int s = 0; s < NCH; s++) p_off[s] = (unsigned)sizeof(C) * chunk_src<T, S>(lane + 32 * s, a.tiles + (int64_t)r * L::NT, f_lo);
     p_left = min(nseg - seg, p_todo);
   };
   p_enter(p_r, (int)(u0 - (int64_t)p_r * nseg));
   auto copy_unit = [&](unsigned d) {
 #pragma unroll
     for (int s = 0; s < NCH; s++)
-      if (chunk_valid<T, ORDER4>(lane + 32 * s)) cp_async16_cg(d + 16u * 32 * s, p_seg + p_off[s]);
+      if (chunk_valid<T, S, ORDER4>(lane + 32 * s)) cp_async16_cg(d + 16u * 32 * s, p_seg + p_off[s]);
     p_seg += row_bytes;
   };
   auto stage_group = [&]() {
@@ -741,18 +750,17 @@ __global__ void __launch_bounds__(32 * kTripleWarps, 8 / kTripleWarps) k_triple_
 
   int r = (int)(u0 / nseg);
   int left = min(total, nseg - (int)(u0 - (int64_t)r * nseg));  // this warp's units in region r
-  // the lane's tile of the region and its rows ra + 4i, columns cb + 4j
-  const int h = lane >> 4, ra = (lane >> 2) & 3, cb = lane & 3;
+  // the lane's tile of the region and its rows ra + S i, columns cb + S j
+  const int h = lane / (S * S), ra = (lane / S) % S, cb = lane % S;
   int c0 = 0, line0 = 0, nrows = 0;
   LaneOps ops{};
   bool active = false, warp_active = false;
   Acc<T> acc;
   auto enter = [&]() {
-    const Tile t = a.regions[r].t[h];
-    using L = UnitLayout<T>;
+    const Tile t = a.tiles[(int64_t)r * L::NT + h];
     c0 = t.col0 + cb;
     line0 = t.line0 + ra;
-    nrows = t.nrows - ra;  // lane rows 4i < nrows
+    nrows = t.nrows - ra;  // lane rows S i < nrows
     const int base = h * L::half * per;
     const int mask = sizeof(T) == 4 ? 1 : 0;  // fp32: operands staged from the aligned element below
     ops.rows = base + L::rows * per + ((t.row_freq0 - f_lo) & mask) + ra;
@@ -762,7 +770,7 @@ __global__ void __launch_bounds__(32 * kTripleWarps, 8 / kTripleWarps) k_triple_
     active = false;
 #pragma unroll
     for (int i = 0; i < 4; i++)
-      if (4 * i < nrows && __ldg(a.line_cmax + line0 + 4 * i) >= c0) active = true;
+      if (S * i < nrows && __ldg(a.line_cmax + line0 + S * i) >= c0) active = true;
     warp_active = __any_sync(0xffffffffu, active);
     acc.zero();
   };
@@ -772,19 +780,19 @@ __global__ void __launch_bounds__(32 * kTripleWarps, 8 / kTripleWarps) k_triple_
     C* P = Pbase + (int64_t)pslot * a.ncells;
 #pragma unroll
     for (int i = 0; i < 4; i++) {
-      if (4 * i >= nrows) continue;
-      const int line = line0 + 4 * i;
+      if (S * i >= nrows) continue;
+      const int line = line0 + S * i;
       const int cm = __ldg(a.line_cmax + line);
       C* dst = P + (__ldg(a.line_start + line) - a.lo);
 #pragma unroll
       for (int j = 0; j < 8; j++)
-        if (c0 + 4 * j <= cm) {
+        if (c0 + S * j <= cm) {
           const C cv = acc.template cell<CONJ>(i, j);
           if (a.accumulate) {
-            const C v = dst[c0 + 4 * j];
-            dst[c0 + 4 * j] = C{v.x + cv.x, v.y + cv.y};
+            const C v = dst[c0 + S * j];
+            dst[c0 + S * j] = C{v.x + cv.x, v.y + cv.y};
           } else {
-            dst[c0 + 4 * j] = cv;
+            dst[c0 + S * j] = cv;
           }
         }
     }
@@ -806,7 +814,7 @@ __global__ void __launch_bounds__(32 * kTripleWarps, 8 / kTripleWarps) k_triple_
     if (cnt == kGroup && left >= kGroup) {  // fast path: the whole group in region r, one straight-line block
       if (warp_active) {
 #pragma unroll
-        for (int t = 0; t < kGroup; t++) warp_cells<T, CONJ, ORDER4>(q + t * UC * per, ops, acc);
+        for (int t = 0; t < kGroup; t++) warp_cells<T, CONJ, ORDER4, S>(q + t * UC * per, ops, acc);
       }
       left -= kGroup;
     } else {
@@ -817,7 +825,7 @@ __global__ void __launch_bounds__(32 * kTripleWarps, 8 / kTripleWarps) k_triple_
           left = min(total - pos - t, nseg);
           enter();
         }
-        if (warp_active) warp_cells<T, CONJ, ORDER4>(q + t * UC * per, ops, acc);
+        if (warp_active) warp_cells<T, CONJ, ORDER4, S>(q + t * UC * per, ops, acc);
         left--;
       }
     }
@@ -843,68 +851,75 @@ static cudaError_t set_smem(K kernel, size_t bytes) {
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-template <typename T>
+template <typename T, int S>
 static cudaError_t configure_all() {
-  constexpr size_t sm = warp_triple_smem<T>();
+  constexpr size_t sm = warp_triple_smem<T, S>();
   cudaError_t e;
-  if ((e = set_smem(k_triple_w<T, true, false>, sm)) != cudaSuccess) return e;
-  if ((e = set_smem(k_triple_w<T, false, false>, sm)) != cudaSuccess) return e;
-  if ((e = set_smem(k_triple_w<T, true, true>, sm)) != cudaSuccess) return e;
-  return set_smem(k_triple_w<T, false, true>, sm);
+  if ((e = set_smem(k_triple_w<T, true, false, S>, sm)) != cudaSuccess) return e;
+  if ((e = set_smem(k_triple_w<T, false, false, S>, sm)) != cudaSuccess) return e;
+  if ((e = set_smem(k_triple_w<T, true, true, S>, sm)) != cudaSuccess) return e;
+  return set_smem(k_triple_w<T, false, true, S>, sm);
 }
 
 static cudaError_t configure() {
   static bool done = false;
   if (done) return cudaSuccess;
   cudaError_t e;
-  if ((e = configure_all<float>()) != cudaSuccess) return e;
-  if ((e = configure_all<double>()) != cudaSuccess) return e;
+  if ((e = configure_all<float, 4>()) != cudaSuccess) return e;
+  if ((e = configure_all<double, 4>()) != cudaSuccess) return e;
+  if ((e = configure_all<float, 2>()) != cudaSuccess) return e;
+  if ((e = configure_all<double, 2>()) != cudaSuccess) return e;
   done = true;
   return cudaSuccess;
 }
 
-int triple_occupancy(int precision) {
-  if (configure() != cudaSuccess) return 1;
+template <typename T, int S>
+static int occupancy_of() {
   int n = 1;
-  if (precision == 32)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_triple_w<float, true, false>, 32 * kTripleWarps, warp_triple_smem<float>());
-  else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_triple_w<double, true, false>, 32 * kTripleWarps,
-                                                  warp_triple_smem<double>());
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_triple_w<T, true, false, S>, 32 * kTripleWarps,
+                                                warp_triple_smem<T, S>());
   return n < 1 ? 1 : n;
 }
 
-template <typename T, bool CONJ, bool ORDER4>
+int triple_occupancy(int precision, int tile_step) {
+  if (configure() != cudaSuccess) return 1;
+  if (precision == 32) return tile_step == 2 ? occupancy_of<float, 2>() : occupancy_of<float, 4>();
+  return tile_step == 2 ? occupancy_of<double, 2>() : occupancy_of<double, 4>();
+}
+
+template <typename T, bool CONJ, bool ORDER4, int S>
 static cudaError_t launch_pdl(const TripleArgs& a, cudaStream_t st) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)((a.nwarps + kTripleWarps - 1) / kTripleWarps), a.batch);
   cfg.blockDim = dim3(32 * kTripleWarps);
-  cfg.dynamicSmemBytes = warp_triple_smem<T>();
+  cfg.dynamicSmemBytes = warp_triple_smem<T, S>();
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_triple_w<T, CONJ, ORDER4>, a);
+  return cudaLaunchKernelEx(&cfg, k_triple_w<T, CONJ, ORDER4, S>, a);
+}
+
+template <typename T, int S>
+static cudaError_t launch_variant(const TripleArgs& a, cudaStream_t st) {
+  const bool o4 = a.order == 4;
+  if (a.conj && !o4) return launch_pdl<T, true, false, S>(a, st);
+  if (!a.conj && !o4) return launch_pdl<T, false, false, S>(a, st);
+  if (a.conj) return launch_pdl<T, true, true, S>(a, st);
+  return launch_pdl<T, false, true, S>(a, st);
 }
 
 cudaError_t launch_triple(const TripleArgs& a, int precision, cudaStream_t st) {
   cudaError_t e = configure();
   if (e != cudaSuccess) return e;
   if (a.nregions == 0 || a.nwarps == 0 || a.seg_end <= a.seg_begin) return cudaSuccess;
-  const bool o4 = a.order == 4;
-  if (precision == 32) {
-    if (a.conj && !o4) e = launch_pdl<float, true, false>(a, st);
-    else if (!a.conj && !o4) e = launch_pdl<float, false, false>(a, st);
-    else if (a.conj) e = launch_pdl<float, true, true>(a, st);
-    else e = launch_pdl<float, false, true>(a, st);
-  } else {
-    if (a.conj && !o4) e = launch_pdl<double, true, false>(a, st);
-    else if (!a.conj && !o4) e = launch_pdl<double, false, false>(a, st);
-    else if (a.conj) e = launch_pdl<double, true, true>(a, st);
-    else e = launch_pdl<double, false, true>(a, st);
-  }
+  if (a.tile_step != 2 && a.tile_step != 4) return cudaErrorInvalidValue;
+  if (precision == 32)
+    e = a.tile_step == 2 ? launch_variant<float, 2>(a, st) : launch_variant<float, 4>(a, st);
+  else
+    e = a.tile_step == 2 ? launch_variant<double, 2>(a, st) : launch_variant<double, 4>(a, st);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
@@ -923,7 +938,7 @@ constexpr int kWarpScanMaxLine = 96;  // lines up to this many cells: one warp p
 // number of partial slots holding cell `idx` (absolute cell of line l)
 __device__ __forceinline__ int cell_slots(const SlotInfo& si, int nparts, int64_t l, int64_t col) {
   if (si.line_tile0 == nullptr) return nparts;
-  const int r = (si.line_tile0[l] + (int)(col / kTileCols)) >> 1;  // tile -> region (tile pair)
+  const int r = (si.line_tile0[l] + (int)(col / si.tile_cols)) / si.tiles_per_region;  // tile -> region
   if (si.region_slots) return __ldg(si.region_slots + r);
   const WarpSplit split{(int64_t)si.nregions * si.nseg, si.nwarps, si.nwarps / 2, si.split_wa, si.split_wb};
   return split.region_slots(r, si.nseg);
@@ -1206,7 +1221,7 @@ __global__ void __launch_bounds__(512) k_smooth_series3(const P2* __restrict__ p
       ns[u] = 0;
       if (idx < ncells) {
         const int l = cline[idx];
-        ns[u] = rsl[(lt0[l] + (idx - ls[l]) / kTileCols) >> 1];
+        ns[u] = rsl[(lt0[l] + (int)((idx - ls[l]) / si.tile_cols)) / si.tiles_per_region];
 #pragma unroll
         for (int t = 0; t < 2; t++)
           if (t < ns[u]) v[u][t] = src[(int64_t)t * part_stride + idx];

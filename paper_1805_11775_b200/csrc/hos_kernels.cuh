@@ -80,8 +80,9 @@ struct TripleArgs {
   int f_lo;                   // frequency of element 0
   int K;                      // segments per series (E rows per series)
   int seg_begin, seg_end;     // segment range reduced by this launch
-  const Region* regions;      // tile pairs (2 x 16 x 32 cells each)
+  const Tile* tiles;          // [nregions][tiles_per_region] D_h tiles (4S lines x 8S columns)
   int nregions;
+  int tile_step;              // lane step S (2 or 4): tiles_per_region = 32 / S^2
   int64_t nwarps;             // warps splitting the region x segment work (<= units)
   int split_wa, split_wb;     // WarpSplit weights (first half / second half of the warps)
   const int32_t* line_cmax;
@@ -107,13 +108,14 @@ struct SlotInfo {
   const int32_t* line_tile0;    // nullptr: plain buffer with `nparts` parts
   int nseg;
   int nregions;
+  int tile_cols, tiles_per_region;  // Geometry tile shape (tile -> region map)
   int64_t nwarps;
   int split_wa, split_wb;
   const int32_t* region_slots;  // optional host-precomputed slots per region (same values), nullptr: compute
 };
 
 // occupancy (CTAs / SM) of the triple-product kernel
-int triple_occupancy(int precision);
+int triple_occupancy(int precision, int tile_step);
 
 cudaError_t launch_prep(const void* x, int x_dtype, int64_t x_stride, int m, int seg_begin, int nseg,
                         int batch, int taper, const double* taper_tab, int precision, void* seg_out,

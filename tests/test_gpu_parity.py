@@ -216,6 +216,8 @@ def test_deterministic_repeat(cuda):
 
 @pytest.mark.parametrize("prec", [32, 64])
 def test_host_entry_point_matches_device(cuda, prec):
+    """hos_estimate_host: pageable buffers (copies) are bit-identical to the
+    device path; page-locked ones (zero-copy graph) match it."""
     import torch
 
     from paper_1805_11775_b200._native import get_plan
@@ -227,8 +229,8 @@ def test_host_entry_point_matches_device(cuda, prec):
     dev = plan.estimate(torch.from_numpy(x).to(cuda)).cpu().numpy()
     host = plan.estimate_host(x)  # pageable: same launch sequence as the device path
     assert np.array_equal(dev, host)
-    # pinned buffers: the chunked, copy-overlapped pipeline (segment-chunk partial
-    # sums accumulate in a different fp32 order, so compare with a tolerance)
+    # pinned buffers: zero-copy graph (compare with a tolerance: the host path
+    # may take a different launch configuration)
     xp = torch.from_numpy(x).pin_memory()
     op = torch.empty(plan.npoints, dtype=torch.complex64 if prec == 32 else torch.complex128).pin_memory()
     for _ in range(2):  # capture + replay
@@ -415,3 +417,24 @@ def test_sweep_small_shapes(cuda, case):
         assert np.abs(g.values).max() <= (1e-12 if prec == "fp64" else 1e-6)
     else:
         assert north_star(g.values, ref) <= (TOL_FP64 if prec == "fp64" else TOL_FP32)
+
+
+@pytest.mark.parametrize("order,m,k,w,conj,prec", [(3, 64, 5, 5, True, 64), (3, 256, 9, 9, False, 32),
+                                                   (4, 32, 4, 3, True, 32), (4, 64, 3, 5, False, 64)])
+def test_k2_tile_step2(cuda, monkeypatch, order, m, k, w, conj, prec):
+    """The 8 x 16 K2 tile shape (lane step 2, HOS_K2_TILE=2; auto-selected only
+    for very short lines) matches the oracle and issues fewer cells."""
+    import torch
+
+    from paper_1805_11775_b200 import _native
+
+    x = np.random.default_rng(m + k).standard_normal(m * k)
+    _, ref = O.estimate(x, order, m, k, w, conj, "hann")
+    issued = {}
+    for step in ("2", "4"):
+        monkeypatch.setenv("HOS_K2_TILE", step)
+        plan = _native.Plan(order, m, k, w, conj, prec, "hann")
+        out = plan.estimate(torch.from_numpy(x).cuda())
+        issued[step] = plan.issued
+        assert north_star(out.cpu().numpy(), ref) <= (TOL_FP64 if prec == 64 else TOL_FP32), step
+    assert issued["2"] <= issued["4"]
