@@ -190,8 +190,12 @@ int hos_estimate_distributed(hos_plan* plan, const void* x_dev, int x_dtype, voi
  * p0, p1}, then {block, halo, halo_in_next}: 14 * nranks + 3 int64. */
 int hos_shard_layout(int order, int m, int k, int m3, int nranks, int64_t* out);
 
-/* Diagnostics: K2 CTAs per series (4 warps each). */
+/* Diagnostics: K2 CTAs per series (4 warps each) of the per-warp staged kernel. */
 int hos_plan_nctas(const hos_plan* plan);
+/* Diagnostics: which K2 the plan's full estimate launches: 1 = k_triple_cta
+ * (CTA-shared bulk-copied rows, one CTA per SM), 0 = k_triple_w (per-warp
+ * cp.async staging; also every segment-range launch of hos_partial_raw). */
+int hos_plan_k2_kind(const hos_plan* plan);
 /* Diagnostics: a device buffer of 4 x (4 nctas) x batch uint64 that K2 fills
  * per warp with {start, first staged data, end (globaltimer ns), smid};
  * NULL disables.  Traced calls run without graph replay. */

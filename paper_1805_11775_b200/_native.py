@@ -57,6 +57,7 @@ EXPORTED_SYMBOLS = {
     "hos_peak_fp32": (_i, [_p, _p, _p]),
     "hos_plan_set_timing": (_i, [_p, _i]),
     "hos_plan_nctas": (_i, [_p]),
+    "hos_plan_k2_kind": (_i, [_p]),
     "hos_plan_kernel_ms": (_i, [_p, _p, _p]),
     "hos_plan_stage_ms": (_i, [_p, _p]),
     "hos_plan_set_trace": (_i, [_p, _p]),

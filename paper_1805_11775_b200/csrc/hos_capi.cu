@@ -56,6 +56,14 @@ struct hos_plan {
   int max_line = 0;  // longest D_h line (cells)
   bool series_k4 = false;  // K4 as one CTA per series with the grid in shared memory
   int split_wa = 1, split_wb = 1;  // K2 WarpSplit weights for two-CTA-per-SM launches
+  // K2 as k_triple_cta (CTA-staged full rows, host schedule) for the plan's main launch
+  bool cta = false;
+  int cta_nctas = 0, cta_depth = 0, cta_stage_segs = 4, cta_slot_bytes = 0, cta_copy_b = 0;
+  hos::CtaGroup* d_groups = nullptr;
+  hos::CtaBlock* d_blocks = nullptr;
+  hos::CtaStage* d_stages = nullptr;
+  int32_t* d_cta_stage0 = nullptr;
+  int64_t rs_stride = 0;  // d_region_slots entries per series
   int hstride = 0;   // complex elements per half-spectrum row
   int L = 0, Lp = 0; // extended-spectrum length / pitch (complex elements)
   // device tables
@@ -235,7 +243,7 @@ int slots_needed(const hos_plan* p, int nseg, int n, int batch) {
 
 hos::SlotInfo slot_info(const hos_plan* p, int nseg, int n) {
   hos::SlotInfo si{};
-  if (nseg == p->k && n == p->nctas) si.region_slots = p->d_region_slots;  // the plan's main launch
+  if (!p->cta && nseg == p->k && n == p->nctas) si.region_slots = p->d_region_slots;  // the plan's main launch
   si.line_tile0 = p->d_line_tile0;
   si.nseg = nseg;
   si.nregions = p->geo.nregions;
@@ -278,6 +286,193 @@ hos::TripleArgs triple_args(const hos_plan* p, int seg_begin, int seg_end, int n
   x.accumulate = 0;
   x.trace = p->trace;
   return x;
+}
+
+// partial slots of the plan's main K2 launch (k_triple_cta or k_triple_w)
+hos::SlotInfo main_slot_info(const hos_plan* p) {
+  hos::SlotInfo si = slot_info(p, p->k, p->nctas);
+  si.region_slots = p->d_region_slots;
+  si.rs_stride = p->rs_stride;
+  return si;
+}
+
+hos::CtaTripleArgs cta_args(const hos_plan* p) {
+  hos::CtaTripleArgs a{};
+  a.E = p->d_E;
+  a.Lp = p->Lp;
+  a.f_lo = p->geo.f_lo;
+  a.tiles = p->d_tiles;
+  a.tile_step = p->geo.tile_step;
+  a.groups = p->d_groups;
+  a.blocks = p->d_blocks;
+  a.stages = p->d_stages;
+  a.cta_stage0 = p->d_cta_stage0;
+  a.nctas = p->cta_nctas;
+  a.depth = p->cta_depth;
+  a.stage_segs = p->cta_stage_segs;
+  a.slot_bytes = p->cta_slot_bytes;
+  a.copy_b = p->cta_copy_b;
+  a.line_cmax = p->d_line_cmax;
+  a.line_start = p->d_line_start;
+  a.lo = p->geo.win.lo;
+  a.part = p->d_part;
+  a.ncells = p->geo.ncells;
+  a.maxslots = p->maxslots;
+  a.order = p->order;
+  a.conj = p->conj;
+  a.trace = p->trace;
+  a.trace_cta = p->cta_nctas - 1;
+  if (const char* env = std::getenv("HOS_TRACE_CTA")) a.trace_cta = std::atoi(env);
+  return a;
+}
+
+// K2 over all segments of every series of the plan
+cudaError_t launch_main_triple(const hos_plan* p, cudaStream_t st) {
+  if (p->cta) return hos::launch_triple_cta(cta_args(p), p->precision, st);
+  return hos::launch_triple(triple_args(p, 0, p->k, p->nctas, p->batch), p->precision, st);
+}
+
+// Host schedule of k_triple_cta (see hos_kernels.cuh): regions in groups of
+// kCtaWarps (+ one remainder group), the (series, group, segment) sequence
+// split into one contiguous range per CTA (one CTA per SM) of balanced
+// estimated time at segment granularity, ranges cut into blocks
+// at (series, group) boundaries and blocks into stages of up to 4 segments.
+// Partial slots per (series, region) are counted in CTA order.  Returns
+// false when the plan is not eligible (ring too small for one segment).
+struct CtaSchedule {
+  std::vector<hos::CtaGroup> groups;
+  std::vector<hos::CtaBlock> blocks;
+  std::vector<hos::CtaStage> stages;
+  std::vector<int32_t> cta_stage0;
+  std::vector<int32_t> region_slots;  // batch x nregions
+  int nctas = 0, depth = 0, stage_segs = 4, slot_bytes = 0, copy_b = 0, maxslots = 1;
+};
+
+bool build_cta_schedule(const hos_plan* p, CtaSchedule& cs) {
+  const hos::Geometry& g = p->geo;
+  const int R = g.nregions, K = p->k, B = p->batch;
+  if (R <= 0 || K <= 0) return false;
+  const int64_t row_bytes = (int64_t)p->Lp * (int64_t)csize(p->precision);
+  int segs = 0;
+  for (int s = 4; s >= 1 && !segs; s--) {
+    const int64_t A = (s * row_bytes + 127) / 128 * 128;
+    const int64_t slot = 2 * A + 128;
+    // 3 slots: a deeper ring lets the warp the scheduler favours run further
+    // ahead of its sub-partition partner, which then runs alone (cfg2 K2:
+    // depth 3 33.6 us, 4 33.8, 5 34.4, 6 35.3; 2 cannot hide the copies)
+    int64_t depth = std::min<int64_t>(3, (int64_t)hos::kCtaMaxSmem / slot);
+    if (const char* env = std::getenv("HOS_CTA_DEPTH"))  // diagnostics
+      depth = std::max<int64_t>(2, std::min<int64_t>({(int64_t)hos::kCtaMaxDepth, (int64_t)hos::kCtaMaxSmem / slot,
+                                                       (int64_t)std::atoi(env)}));
+    if (depth >= 3 || (s == 1 && depth >= 2)) {
+      segs = s;
+      cs.depth = (int)depth;
+      cs.slot_bytes = (int)slot;
+      cs.copy_b = (int)(A + 64);
+    }
+  }
+  if (!segs) return false;
+  // full groups of W regions, then the remainder r < W: its regions' tiles
+  // split over two warps when r <= W/2 and its stages over `phases` warps.
+  // A remainder stage takes about 1/phases of a full stage's compute but
+  // still copies the whole stage (copy-bound at ~45% of a full stage, cfg2), so a segment weighs max(W / phases, 4)
+  // where a full group's weighs W.
+  const int W = hos::kCtaWarps;
+  auto both_tiles = [&](int r0, int n) {  // every region of [r0, r0+n) has two real tiles
+    if (g.tiles_per_region != 2) return false;
+    for (int r = r0; r < r0 + n; r++)
+      if (g.tiles[2 * r].nrows == 0 || g.tiles[2 * r + 1].nrows == 0) return false;
+    return true;
+  };
+  for (int r0 = 0; r0 < R; r0 += W) {
+    const int n = std::min(W, R - r0);
+    const int halves = n <= W / 2 && both_tiles(r0, n) ? 2 : 1;
+    const int ph = std::max(1, std::min({segs, W / (n * halves), cs.depth}));
+    cs.groups.push_back({r0, n, ph, halves});
+  }
+  const int ng = (int)cs.groups.size();
+  auto weight = [&](int gi) -> int64_t {
+    const hos::CtaGroup& gr = cs.groups[gi];
+    return gr.n == W ? W : std::max<int64_t>(W / gr.phases, 4);
+  };
+  // (series, group) chunks of K segments each.  The CTA ranges come from
+  // the smallest per-CTA time budget T (bisection) for which a greedy fill
+  // needs <= N CTAs; a CTA's time is its segments' weights plus kSwitch per
+  // block after its first (the block switch -- partial-slot stores, the next
+  // block's geometry loads -- stalls all of the CTA's warps, ~1 stage).
+  const int64_t nchunks = (int64_t)B * ng;
+  const int64_t N = std::max<int64_t>(1, std::min<int64_t>(p->sms, (int64_t)B * ng * K));
+  const int64_t kSwitch = 3 * W;
+  // greedy fill: cuts[c] = start (chunk, seg) of CTA c; returns CTAs used
+  auto fill = [&](int64_t T, std::vector<std::pair<int64_t, int>>* cuts) -> int64_t {
+    int64_t used = 0, ch = 0;
+    int seg = 0;
+    while (ch < nchunks) {
+      if (cuts) cuts->push_back({ch, seg});
+      used++;
+      int64_t cost = 0;
+      bool first = true;
+      while (ch < nchunks) {
+        const int64_t w = weight((int)(ch % ng));
+        const int64_t sw = first ? 0 : kSwitch;
+        const int64_t room = T - cost - sw;
+        const int64_t take = room <= 0 ? 0 : std::min<int64_t>(K - seg, room / w);
+        if (take <= 0) {
+          if (first) {  // T below one segment: take one anyway
+            if (++seg >= K) { ch++; seg = 0; }
+          }
+          break;
+        }
+        cost += sw + take * w;
+        first = false;
+        seg += (int)take;
+        if (seg >= K) {
+          ch++;
+          seg = 0;
+        } else {
+          break;
+        }
+      }
+    }
+    return used;
+  };
+  int64_t lo_t = 1, hi_t = 1;
+  for (int64_t c = 0; c < nchunks; c++) hi_t += weight((int)(c % ng)) * K + kSwitch;
+  while (lo_t < hi_t) {
+    const int64_t mid = lo_t + (hi_t - lo_t) / 2;
+    if (fill(mid, nullptr) <= N) hi_t = mid;
+    else lo_t = mid + 1;
+  }
+  std::vector<std::pair<int64_t, int>> cuts;
+  const int64_t used = fill(lo_t, &cuts);
+  cuts.push_back({nchunks, 0});
+  std::vector<int32_t> slots(nchunks, 0);
+  cs.cta_stage0.push_back(0);
+  for (int64_t c = 0; c < used; c++) {
+    const int64_t ch0 = cuts[c].first, ch1 = cuts[c + 1].first;
+    const int sg0 = cuts[c].second, sg1 = cuts[c + 1].second;
+    for (int64_t ch = ch0; ch <= ch1 && ch < nchunks; ch++) {
+      const int sb = ch == ch0 ? sg0 : 0;
+      const int se = ch == ch1 ? sg1 : K;
+      if (se <= sb) continue;
+      const int b = (int)(ch / ng), gi = (int)(ch % ng);
+      const int blk = (int)cs.blocks.size();
+      cs.blocks.push_back({b * K + sb, b, gi, slots[ch]});
+      slots[ch] += cs.groups[gi].phases;
+      for (int s = sb; s < se; s += segs) cs.stages.push_back({b * K + s, std::min(segs, se - s), blk, 0});
+    }
+    cs.cta_stage0.push_back((int32_t)cs.stages.size());
+  }
+  const int64_t N_used = used;
+  cs.nctas = (int)N_used;
+  cs.region_slots.assign((size_t)B * R, 0);
+  cs.maxslots = 1;
+  for (int64_t ch = 0; ch < nchunks; ch++) {
+    const hos::CtaGroup& gr = cs.groups[ch % ng];
+    for (int r = gr.r0; r < gr.r0 + gr.n; r++) cs.region_slots[(ch / ng) * R + r] = slots[ch];
+    cs.maxslots = std::max(cs.maxslots, slots[ch]);
+  }
+  return true;
 }
 
 // K4b arguments for the whole grid of every series of the plan
@@ -323,7 +518,7 @@ int run_box(hos_plan* p, void* out_dev, cudaStream_t st) {
 // K4 of the whole grid: one CTA per series in shared memory when the grid is
 // small (order 3), else line scans + box sums
 int run_smooth(hos_plan* p, void* out_dev, cudaStream_t st, int stage = -1) {
-  const hos::SlotInfo si = slot_info(p, p->k, p->nctas);
+  const hos::SlotInfo si = main_slot_info(p);
   if (p->series_k4) {
     if (stage != 5)
       CUDA_TRY(hos::launch_smooth_series3(p->d_part, p->maxslots, p->geo.ncells, si, p->precision,
@@ -340,8 +535,7 @@ int run_smooth(hos_plan* p, void* out_dev, cudaStream_t st, int stage = -1) {
 
 // K2 + K4 over the extended spectra already in p->d_E.
 int run_back(hos_plan* p, void* out_dev, cudaStream_t st) {
-  const hos::TripleArgs ta = triple_args(p, 0, p->k, p->nctas, p->batch);
-  CUDA_TRY(hos::launch_triple(ta, p->precision, st));
+  CUDA_TRY(launch_main_triple(p, st));
   if (p->timing) CUDA_TRY(cudaEventRecord(p->ev[4], st));
   int rc = run_smooth(p, out_dev, st);
   if (rc) return rc;
@@ -612,7 +806,9 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
   // +4 elements: fp32 operands are staged from the 16-byte-aligned element at
   // or below their start, in whole 16-byte chunks (K2), so a copy may read up
   // to 3 elements past the last frequency; even pitch keeps rows 16-byte aligned
-  p->Lp = (p->L + 4 + 1) & ~1;
+  // k_triple_cta bulk-copies whole rows: a pitch of 16 elements keeps every
+  // row 128-byte aligned (TMA moves aligned rows at the full rate)
+  p->Lp = (p->L + 4 + 15) & ~15;
   cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, device);
   p->occupancy = hos::triple_occupancy(precision, g.tile_step);
   if (const char* env = std::getenv("HOS_K2_SPLIT")) {  // "wa:wb"
@@ -624,12 +820,33 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
   }
   p->nctas = nctas_for(p, k, batch);
   p->maxslots = slots_needed(p, k, p->nctas, batch);
+  CtaSchedule sched;
+  {
+    const char* env = std::getenv("HOS_K2");  // "warp": per-warp staged k_triple_w for every launch
+    p->cta = !(env && std::string(env) == "warp") && build_cta_schedule(p, sched);
+  }
+  if (p->cta) {
+    p->cta_nctas = sched.nctas;
+    p->cta_depth = sched.depth;
+    p->cta_stage_segs = sched.stage_segs;
+    p->cta_slot_bytes = sched.slot_bytes;
+    p->cta_copy_b = sched.copy_b;
+    // batch-1 plans keep room for the segment-range launches of k_triple_w (multi-GPU shards)
+    p->maxslots = batch == 1 ? std::max(p->maxslots, sched.maxslots) : sched.maxslots;
+    p->rs_stride = g.nregions;
+  }
 
 
   std::vector<int32_t> cmax(g.line_cmax.begin(), g.line_cmax.end());
   if ((rc = upload(p, &p->d_tiles, g.tiles))) return bail(rc);
   if ((rc = upload(p, &p->d_line_tile0, g.line_tile0))) return bail(rc);
-  {
+  if (p->cta) {
+    if ((rc = upload(p, &p->d_region_slots, sched.region_slots))) return bail(rc);
+    if ((rc = upload(p, &p->d_groups, sched.groups))) return bail(rc);
+    if ((rc = upload(p, &p->d_blocks, sched.blocks))) return bail(rc);
+    if ((rc = upload(p, &p->d_stages, sched.stages))) return bail(rc);
+    if ((rc = upload(p, &p->d_cta_stage0, sched.cta_stage0))) return bail(rc);
+  } else {
     const hos::WarpSplit sp = warp_split(p, k, p->nctas, batch);
     std::vector<int32_t> rs(g.nregions);
     for (size_t r = 0; r < rs.size(); r++) rs[r] = sp.region_slots((int)r, k);
@@ -699,7 +916,7 @@ void hos_plan_destroy(hos_plan* p) {
   for (auto& kv : p->ffts) cufftDestroy(kv.second);
   for (void* b : {p->d_raw, p->d_send, p->d_mine, p->d_local, p->d_heads, p->d_vals, p->d_parts})
     if (b) cudaFree(b);
-  void* bufs[] = {p->d_tiles, p->d_line_tile0, p->d_region_slots, p->d_line_cmax, p->d_line_start, p->d_row_off, p->d_pair_k1, p->d_pair_k2,
+  void* bufs[] = {p->d_groups, p->d_blocks, p->d_stages, p->d_cta_stage0, p->d_tiles, p->d_line_tile0, p->d_region_slots, p->d_line_cmax, p->d_line_start, p->d_row_off, p->d_pair_k1, p->d_pair_k2,
                   p->d_pair_base, p->d_line_of_ab, p->d_taper, p->d_tw, p->d_seg, p->d_half, p->d_E, p->d_part,
                   p->d_S, p->d_xin, p->d_out};
   for (void* b : bufs)
@@ -1045,6 +1262,7 @@ int hos_peak_fp32(double* tflops, double* sm_mhz, void* stream) {
 }
 
 int hos_plan_nctas(const hos_plan* p) { return p ? p->nctas : -1; }
+int hos_plan_k2_kind(const hos_plan* p) { return p ? (p->cta ? 1 : 0) : -1; }
 
 int hos_plan_set_trace(hos_plan* p, void* trace_dev) {
   int rc = check_plan(p);
@@ -1087,7 +1305,6 @@ int hos_plan_time_stages(hos_plan* p, const void* x_dev, int x_dtype, int64_t x_
   p->timing = saved;
   if (rc) return rc;
   const int rows = p->batch * p->k;
-  const hos::TripleArgs ta = triple_args(p, 0, p->k, p->nctas, p->batch);
   cudaEvent_t e0, e1;
   CUDA_TRY(cudaEventCreate(&e0));
   CUDA_TRY(cudaEventCreate(&e1));
@@ -1114,7 +1331,7 @@ int hos_plan_time_stages(hos_plan* p, const void* x_dev, int x_dtype, int64_t x_
                                       p->precision, p->d_E, cs);
         break;
       case 3:
-        e = hos::launch_triple(ta, p->precision, cs);
+        e = launch_main_triple(p, cs);
         break;
       case 4:
         r2 = run_smooth(p, out_dev, cs, 4);

@@ -925,6 +925,299 @@ cudaError_t launch_triple(const TripleArgs& a, int precision, cudaStream_t st) {
 }
 
 // ===========================================================================
+// K2 (CTA-staged): one 8-warp CTA per SM.  The CTA walks a host-built list
+// of STAGES (up to 4 consecutive E rows = segments of one series); each stage
+// lands in a ring slot as TWO bulk copies (cp.async.bulk, one elected
+// thread, mbarrier transaction counts) of the same rows, copy B 64 bytes
+// further in the banks.  Every warp owns one region of the CTA's current
+// BLOCK (series, group of <= 8 regions, segment range) and reads its two
+// tiles' operands straight out of the full staged rows, tile h from copy h:
+// all tile origins lie on the 16-line x 32-column lattice, so the two tiles'
+// loads differ by a multiple of 16 elements and the 64-byte shift puts them
+// in disjoint banks (no conflicts, as with the per-warp chunk copies).  The
+// warp that finishes a stage last refills its slot.  All warps consume the
+// same stages, so a warp the scheduler favours can run at most a ring ahead
+// of the others: the CTA finishes as one (the per-warp ranges of k_triple_w
+// leave the less-favoured CTA of an SM a tail).  Compute warps issue no copy
+// instructions at all.  Partial slots: (block slot base + warp phase) of the
+// warp's region, fixed by the host schedule -> deterministic results.
+// Groups with fewer regions than warps give each region several warps
+// ("phases"), each taking every phases-th segment of the block.
+
+template <typename T, bool CONJ, bool ORDER4, int S>
+__global__ void __launch_bounds__(32 * kCtaWarps, 1) k_triple_cta(const __grid_constant__ CtaTripleArgs a) {
+  using C = typename Cplx<T>::C;
+  using L = K2Layout<T, S>;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  __shared__ __align__(8) unsigned long long full[kCtaMaxDepth];
+  __shared__ int cnt[kCtaMaxDepth];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int k0 = __ldg(a.cta_stage0 + blockIdx.x), nst = __ldg(a.cta_stage0 + blockIdx.x + 1) - k0;
+  const int depth = a.depth, Lp = a.Lp;
+  unsigned long long* tr = a.trace ? a.trace + 4 * ((int64_t)blockIdx.x * kCtaWarps + warp) : nullptr;
+  auto stamp = [&](int i) {
+    if (tr && lane == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      tr[i] = t;
+      if (i == 0) {
+        unsigned sm;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        tr[3] = sm;
+      }
+    }
+  };
+  stamp(0);
+  const unsigned ring_s = (unsigned)__cvta_generic_to_shared(smraw);
+  if (threadIdx.x == 0) {
+    for (int d = 0; d < depth; d++) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&full[d])));
+      cnt[d] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const C* E = (const C*)a.E;
+  auto ld_stage = [&](int k) {
+    CtaStage v;
+    const int4 r = __ldg(reinterpret_cast<const int4*>(a.stages + k0 + k));
+    v.row = r.x;
+    v.nseg = r.y;
+    v.block = r.z;
+    v.pad = r.w;
+    return v;
+  };
+  auto issue = [&](const CtaStage& sg, int d) {  // a stage of this CTA into ring slot d (one thread)
+    const unsigned bytes = (unsigned)(sg.nseg * Lp * (int)sizeof(C));
+    const C* src = E + (int64_t)sg.row * Lp;
+    const unsigned dst = ring_s + (unsigned)(d * a.slot_bytes);
+    const unsigned bar = (unsigned)__cvta_generic_to_shared(&full[d]);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(2 * bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     dst + (unsigned)a.copy_b),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+  };
+  const int h = lane / (S * S), ra = (lane / S) % S, cb = lane % S;
+  int cur = -1;                  // current block
+  int region = 0, phase = 0, phases = 1, blk_row0 = 0;
+  bool role = false;             // this warp has (a tile of) a region in the block
+  int c0 = 0, line0 = 0, nrows = 0;
+  C* P = nullptr;                // the warp's partial slot (series + slot applied)
+  LaneOps ops{};
+  bool active = false, warp_active = false;
+  Acc<T> acc;
+  int lcm[4], loff[4];            // the lane's lines: last column, cell offset in the slot
+  auto ld_block = [&](int b) {
+    CtaBlock v;
+    const int4 r = __ldg(reinterpret_cast<const int4*>(a.blocks + b));
+    v.row0 = r.x;
+    v.series = r.y;
+    v.group = r.z;
+    v.slot_base = r.w;
+    return v;
+  };
+  auto enter = [&](const CtaBlock& blk) {
+    const CtaGroup grp = a.groups[blk.group];
+    // warps per region: `halves` (2: each warp computes one tile of the
+    // pair, the other half of its lanes idle) x `phases`
+    phases = grp.phases;
+    const int wpr = grp.halves * grp.phases;
+    role = warp < grp.n * wpr;
+    region = grp.r0 + (role ? warp % grp.n : 0);
+    const int sub = role ? warp / grp.n : 0;
+    phase = sub / grp.halves;
+    const bool my_tile = grp.halves == 1 || (sub % grp.halves) == (h & 1);
+    blk_row0 = blk.row0;
+    P = (C*)a.part + ((int64_t)blk.series * a.maxslots + blk.slot_base + phase) * a.ncells;
+    const Tile t = a.tiles[(int64_t)region * L::NT + h];
+    c0 = t.col0 + cb;
+    line0 = t.line0 + ra;
+    nrows = t.nrows - ra;
+    const int base = (h & 1) ? a.copy_b / (int)sizeof(C) : 0;
+    ops.rows = base + (t.row_freq0 - a.f_lo) + ra;
+    ops.cols = base + (t.col0 - a.f_lo) + cb;
+    ops.g = base + (t.plane_freq + t.row_freq0 + t.col0 - a.f_lo) + ra + cb;
+    ops.plane = base + (t.plane_freq - a.f_lo);
+    active = false;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      lcm[i] = -0x40000000;
+      loff[i] = 0;
+      if (S * i < nrows) {
+        lcm[i] = __ldg(a.line_cmax + line0 + S * i);
+        loff[i] = (int)(__ldg(a.line_start + line0 + S * i) - a.lo);
+      }
+    }
+    if (role && my_tile) {
+#pragma unroll
+      for (int i = 0; i < 4; i++)
+        if (lcm[i] >= c0) active = true;
+    }
+    warp_active = __any_sync(0xffffffffu, active);
+    acc.zero();
+  };
+  auto finalize = [&]() {  // no loads: a block switch stalls every warp of the CTA
+    if (!active) return;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      if (S * i >= nrows) continue;
+      const int cm = lcm[i];
+      C* dst = P + loff[i];
+#pragma unroll
+      for (int j = 0; j < 8; j++)
+        if (c0 + S * j <= cm) dst[c0 + S * j] = acc.template cell<CONJ>(i, j);
+    }
+  };
+  // the stage table is read one stage ahead (and the possible refill's
+  // entry `depth` ahead): the warp that finishes a stage last issues its
+  // refill, and a table load on that path would delay it once per stage
+  CtaStage sg = nst > 0 ? ld_stage(0) : CtaStage{};
+  CtaBlock nb = nst > 0 ? ld_block(sg.block) : CtaBlock{};  // the block of stage k, loaded a stage ahead
+  // Static tables (schedule, tiles, lines) are read before waiting for the
+  // front end: under PDL this prologue overlaps its tail, and after an L2
+  // flush each dependent table load costs a DRAM round trip.
+  if (nst > 0) {
+    cur = sg.block;
+    enter(nb);
+  }
+  CtaStage pre[kCtaMaxDepth];
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int d2 = 1; d2 < kCtaMaxDepth; d2++)
+      if (d2 < depth && d2 < nst) pre[d2] = ld_stage(d2);
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // E is written by the previous kernel
+  asm volatile("griddepcontrol.launch_dependents;");
+  // prefill: stage 0 alone first (all SMs prefilling the whole ring at once
+  // would make the first stage wait for the whole burst), the rest of the
+  // ring once it has landed
+  if (threadIdx.x == 0 && nst > 0) issue(sg, 0);
+  for (int k = 0; k < nst; k++) {
+    const int d = k % depth;
+    const CtaStage sg_next = k + 1 < nst ? ld_stage(k + 1) : sg;
+    const CtaStage refill = k + depth < nst ? ld_stage(k + depth) : sg;
+    if (sg.block != cur) {
+      if (cur >= 0) finalize();
+      cur = sg.block;
+      enter(nb);
+    }
+    if (sg_next.block != sg.block) nb = ld_block(sg_next.block);
+    {
+      // suspend (not spin) until the stage lands: the arbiter issues the
+      // highest warp slot first, so a spinning early warp would take issue
+      // slots from the warps still computing on its SM sub-partition
+      const unsigned bar = (unsigned)__cvta_generic_to_shared(&full[d]);
+      const unsigned par = (unsigned)(k / depth) & 1u;
+      asm volatile(
+          "{\n.reg .pred P1;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n@!P1 bra W_%=;\n}\n" ::"r"(
+              bar),
+          "r"(par), "r"(1000000u)
+          : "memory");
+    }
+    if (tr && blockIdx.x == a.trace_cta && k < 64) {  // per-stage stamps of one CTA (diagnostics)
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (lane == 0) a.trace[4 * gridDim.x * kCtaWarps + 64 * warp + k] = t;
+    }
+    if (k == 0) {
+      stamp(1);
+      if (threadIdx.x == 0) {
+#pragma unroll
+        for (int d2 = 1; d2 < kCtaMaxDepth; d2++)
+          if (d2 < depth && d2 < nst) issue(pre[d2], d2);
+      }
+    }
+    const C* q = reinterpret_cast<const C*>(smraw + (size_t)d * a.slot_bytes);
+    // phases > 1: the warp takes every phases-th STAGE of the block (whole
+    // stages keep the 4-segment straight-line block; a warp running one
+    // segment per stage measured ~40% of the FMA rate)
+    if (warp_active && (phases == 1 || ((sg.row - blk_row0) / a.stage_segs) % phases == phase)) {
+      if (sg.nseg == 4) {
+#pragma unroll
+        for (int t = 0; t < 4; t++) warp_cells<T, CONJ, ORDER4, S>(q + t * Lp, ops, acc);
+      } else {
+        for (int t = 0; t < sg.nseg; t++) warp_cells<T, CONJ, ORDER4, S>(q + t * Lp, ops, acc);
+      }
+    }
+    __syncwarp();
+    if (tr && blockIdx.x == a.trace_cta && k < 64) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (lane == 0) a.trace[4 * gridDim.x * kCtaWarps + 512 + 64 * warp + k] = t;
+    }
+    if (lane == 0) {
+      __threadfence_block();
+      if (atomicAdd(&cnt[d], 1) == kCtaWarps - 1) {
+        atomicExch(&cnt[d], 0);
+        if (k + depth < nst) issue(refill, d);
+      }
+    }
+    sg = sg_next;
+  }
+  if (cur >= 0) finalize();
+  stamp(2);
+}
+
+template <typename T, int S>
+static cudaError_t configure_cta(size_t smem) {
+  cudaError_t e;
+  if ((e = set_smem(k_triple_cta<T, true, false, S>, smem)) != cudaSuccess) return e;
+  if ((e = set_smem(k_triple_cta<T, false, false, S>, smem)) != cudaSuccess) return e;
+  if ((e = set_smem(k_triple_cta<T, true, true, S>, smem)) != cudaSuccess) return e;
+  return set_smem(k_triple_cta<T, false, true, S>, smem);
+}
+
+template <typename T, bool CONJ, bool ORDER4, int S>
+static cudaError_t launch_cta_pdl(const CtaTripleArgs& a, size_t smem, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)a.nctas);
+  cfg.blockDim = dim3(32 * kCtaWarps);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_triple_cta<T, CONJ, ORDER4, S>, a);
+}
+
+template <typename T, int S>
+static cudaError_t launch_cta_variant(const CtaTripleArgs& a, cudaStream_t st) {
+  const size_t smem = (size_t)a.depth * a.slot_bytes;
+  static size_t configured = 0;  // per instantiation: the largest dynamic smem enabled so far
+  if (smem > configured) {
+    cudaError_t e = configure_cta<T, S>(kCtaMaxSmem);
+    if (e != cudaSuccess) return e;
+    configured = kCtaMaxSmem;
+  }
+  const bool o4 = a.order == 4;
+  if (a.conj && !o4) return launch_cta_pdl<T, true, false, S>(a, smem, st);
+  if (!a.conj && !o4) return launch_cta_pdl<T, false, false, S>(a, smem, st);
+  if (a.conj) return launch_cta_pdl<T, true, true, S>(a, smem, st);
+  return launch_cta_pdl<T, false, true, S>(a, smem, st);
+}
+
+cudaError_t launch_triple_cta(const CtaTripleArgs& a, int precision, cudaStream_t st) {
+  if (a.nctas <= 0) return cudaSuccess;
+  if (a.tile_step != 2 && a.tile_step != 4) return cudaErrorInvalidValue;
+  if (a.depth < 1 || a.depth > kCtaMaxDepth || (size_t)a.depth * a.slot_bytes > kCtaMaxSmem)
+    return cudaErrorInvalidValue;
+  cudaError_t e;
+  if (precision == 32)
+    e = a.tile_step == 2 ? launch_cta_variant<float, 2>(a, st) : launch_cta_variant<float, 4>(a, st);
+  else
+    e = a.tile_step == 2 ? launch_cta_variant<double, 2>(a, st) : launch_cta_variant<double, 4>(a, st);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+// ===========================================================================
 // K4a: per-line inclusive prefix sums (fp64) of the chunk-summed raw cells.
 // One CTA per (line, series); each thread sums the segment-chunk partials of
 // one cell (fixed chunk order -> deterministic), then a block scan (warp
@@ -936,10 +1229,10 @@ constexpr int kScanThreads = 256;
 constexpr int kWarpScanMaxLine = 96;  // lines up to this many cells: one warp per line
 
 // number of partial slots holding cell `idx` (absolute cell of line l)
-__device__ __forceinline__ int cell_slots(const SlotInfo& si, int nparts, int64_t l, int64_t col) {
+__device__ __forceinline__ int cell_slots(const SlotInfo& si, int nparts, int64_t l, int64_t col, int series) {
   if (si.line_tile0 == nullptr) return nparts;
   const int r = (si.line_tile0[l] + (int)(col / si.tile_cols)) / si.tiles_per_region;  // tile -> region
-  if (si.region_slots) return __ldg(si.region_slots + r);
+  if (si.region_slots) return __ldg(si.region_slots + series * si.rs_stride + r);
   const WarpSplit split{(int64_t)si.nregions * si.nseg, si.nwarps, si.nwarps / 2, si.split_wa, si.split_wb};
   return split.region_slots(r, si.nseg);
 }
@@ -985,7 +1278,7 @@ __global__ void __launch_bounds__(kScanThreads) k_line_scan(const P2* __restrict
   for (int64_t c = c0; c < c1; c += kScanThreads) {
     const int64_t idx = c + threadIdx.x;
     double vr = 0.0, vi = 0.0;
-    if (idx < c1) sum_slots(src, cell_slots(si, nparts, l, idx - c0), part_stride, idx, vr, vi);
+    if (idx < c1) sum_slots(src, cell_slots(si, nparts, l, idx - c0, series), part_stride, idx, vr, vi);
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const double ur = __shfl_up_sync(0xffffffffu, vr, o);
@@ -1032,7 +1325,7 @@ __global__ void __launch_bounds__(256, 4) k_line_scan_w(const P2* __restrict__ p
   for (int64_t c = c0; c < c1; c += 32) {
     const int64_t idx = c + lane;
     double vr = 0.0, vi = 0.0;
-    if (idx < c1) sum_slots<P2, 4>(src, cell_slots(si, nparts, l, idx - c0), part_stride, idx, vr, vi);
+    if (idx < c1) sum_slots<P2, 4>(src, cell_slots(si, nparts, l, idx - c0, series), part_stride, idx, vr, vi);
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const double ur = __shfl_up_sync(0xffffffffu, vr, o);
@@ -1200,7 +1493,7 @@ __global__ void __launch_bounds__(512) k_smooth_series3(const P2* __restrict__ p
   for (int i = tid; i <= nlines; i += blockDim.x) ls[i] = (int)__ldg(a.line_start + i);
   for (int i = tid; i <= a.rows; i += blockDim.x) ro[i] = (int)__ldg(a.row_off + i);
   for (int i = tid; i < nlines; i += blockDim.x) lt0[i] = __ldg(si.line_tile0 + i);
-  for (int i = tid; i < si.nregions; i += blockDim.x) rsl[i] = __ldg(si.region_slots + i);
+  for (int i = tid; i < si.nregions; i += blockDim.x) rsl[i] = __ldg(si.region_slots + series * si.rs_stride + i);
   __syncthreads();
   for (int l = warp; l < nlines; l += nw)
     for (int c = ls[l] + lane; c < ls[l + 1]; c += 32) cline[c] = (unsigned short)l;
@@ -1344,7 +1637,7 @@ __global__ void __launch_bounds__(256) k_reduce_parts(const P2* __restrict__ par
   const int64_t c0 = line_start[l], c1 = line_start[l + 1];
   for (int64_t idx = c0 + threadIdx.x; idx < c1; idx += blockDim.x) {
     double sr = 0.0, si_ = 0.0;
-    sum_slots(part, cell_slots(si, 1, l, idx - c0), stride, idx, sr, si_);
+    sum_slots(part, cell_slots(si, 1, l, idx - c0, 0), stride, idx, sr, si_);
     raw[idx].x = sr;
     raw[idx].y = si_;
   }

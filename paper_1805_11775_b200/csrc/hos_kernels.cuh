@@ -112,7 +112,59 @@ struct SlotInfo {
   int64_t nwarps;
   int split_wa, split_wb;
   const int32_t* region_slots;  // optional host-precomputed slots per region (same values), nullptr: compute
+  int64_t rs_stride;            // region_slots entries per series (0: one table for every series)
 };
+
+// K2 (CTA-staged, k_triple_cta): host-built schedule.  A GROUP is up to
+// kCtaWarps consecutive regions; with n < kCtaWarps regions each region gets
+// `halves` x `phases` warps: with halves = 2 each warp computes one of the
+// region's two tiles, and each warp takes every phases-th stage.  A BLOCK is one CTA's
+// segment range of one (series, group); its warps write partial slots
+// slot_base + phase.  A STAGE is up to 4 consecutive E rows of one block.
+constexpr int kCtaWarps = 8;
+constexpr int kCtaMaxDepth = 8;
+constexpr size_t kCtaMaxSmem = 220 * 1024;
+struct CtaGroup {
+  int32_t r0, n, phases;
+  int32_t halves;     // 2: a region's two tiles go to different warps (n <= kCtaWarps / 2)
+};
+struct CtaBlock {
+  int32_t row0;       // E row of the block's first segment (series * K + seg)
+  int32_t series;
+  int32_t group;
+  int32_t slot_base;
+};
+struct CtaStage {
+  int32_t row;        // E row of the stage's first segment
+  int32_t nseg;       // 1..4
+  int32_t block;
+  int32_t pad;
+};
+struct CtaTripleArgs {
+  const void* E;
+  int Lp, f_lo;
+  const Tile* tiles;
+  int tile_step;
+  const CtaGroup* groups;
+  const CtaBlock* blocks;
+  const CtaStage* stages;
+  const int32_t* cta_stage0;  // nctas + 1
+  int nctas;
+  int depth;                  // ring slots
+  int stage_segs;             // segments per full stage (block stages start every stage_segs segments)
+  int slot_bytes;             // per ring slot (copy A, copy B)
+  int copy_b;                 // byte offset of copy B in a slot (== 64 mod 128)
+  const int32_t* line_cmax;
+  const int64_t* line_start;
+  int lo;
+  void* part;
+  int64_t ncells;
+  int maxslots;
+  int order, conj;
+  unsigned long long* trace;  // diagnostics (nullptr: off): per warp {start, first data, end, smid}
+  int trace_cta;              // diagnostics: CTA whose per-stage times are traced
+};
+cudaError_t launch_triple_cta(const CtaTripleArgs& a, int precision, cudaStream_t st);
 
 // occupancy (CTAs / SM) of the triple-product kernel
 int triple_occupancy(int precision, int tile_step);
