@@ -173,12 +173,30 @@ int run_fft(hos_plan* p, int rows, const void* in, void* out, cudaStream_t st) {
   return HOS_OK;
 }
 
+// k_triple_cta stages 4 whole E rows per ring slot, twice (two bank
+// offsets), in a ring of 3 slots: it is used when that fits in shared memory
+// (fp32: pitch <= 1152 elements, i.e. M up to ~2048; larger M keeps the
+// per-warp staged k_triple_w, which copies only the windows a tile reads).
+bool cta_allowed() {
+  const char* env = std::getenv("HOS_K2");  // "warp": per-warp staged k_triple_w for every launch
+  return !(env && std::string(env) == "warp");
+}
+int pitch_of(const hos::Geometry& g) { return (g.f_hi - g.f_lo + 1 + 4 + 15) & ~15; }
+bool cta_fits(const hos::Geometry& g, int precision) {
+  const int64_t A = (4 * (int64_t)pitch_of(g) * (int64_t)csize(precision) + 127) / 128 * 128;
+  return 3 * (2 * A + 128) <= (int64_t)hos::kCtaMaxSmem;
+}
+
 // D_h geometry with the K2 tile shape for this M: 8 x 16 tiles (lane step 2)
-// only when the 16 x 32 tiles would issue >= 1.8x more cells, else 16 x 32.
-// An 8 x 16 region stages 2.5x the chunks of a 16 x 32 one and measured
-// 1.79x slower per issued cell (cfg3), so even cfg4 (1.55x fewer cells)
-// loses with it (K2 106 vs 101 us).  HOS_K2_TILE=2|4 forces the step.
-std::string build_geometry(hos::Geometry& g, int order, int m, int m3) {
+// when they issue enough fewer cells than 16 x 32 tiles, else 16 x 32.  With
+// k_triple_cta an 8 x 16 region's eight tiles share two bank offsets (the
+// staged rows' copies A and B), so its loads conflict: it pays from 1.25x
+// fewer cells (cfg4 at 1.54x: 70 vs 117 us; cfg5 at 1.29x: 1012 vs 1407 us;
+// cfg2 at 1.08x: 42 vs 34 us).  With
+// k_triple_w an 8 x 16 region stages 2.5x the chunks of a 16 x 32 one and
+// measured 1.79x slower per issued cell, so it needs 1.8x.  HOS_K2_TILE=2|4
+// forces the step.
+std::string build_geometry(hos::Geometry& g, int order, int m, int m3, int precision) {
   int forced = 0;
   if (const char* env = std::getenv("HOS_K2_TILE")) forced = std::atoi(env);
   if (forced == 2 || forced == 4) return g.build(order, m, m3, forced);
@@ -186,7 +204,8 @@ std::string build_geometry(hos::Geometry& g, int order, int m, int m3) {
   if (!err.empty()) return err;
   hos::Geometry g2;
   if (!g2.build(order, m, m3, 2).empty()) return "";
-  if ((double)g.issued_cells >= 1.8 * (double)g2.issued_cells) g = std::move(g2);
+  const bool cta = cta_allowed() && cta_fits(g2, precision);
+  if ((double)g.issued_cells >= (cta ? 1.25 : 1.8) * (double)g2.issued_cells) g = std::move(g2);
   return "";
 }
 
@@ -353,8 +372,9 @@ bool build_cta_schedule(const hos_plan* p, CtaSchedule& cs) {
   const int R = g.nregions, K = p->k, B = p->batch;
   if (R <= 0 || K <= 0) return false;
   const int64_t row_bytes = (int64_t)p->Lp * (int64_t)csize(p->precision);
+  if (!cta_fits(g, p->precision)) return false;
   int segs = 0;
-  for (int s = 4; s >= 1 && !segs; s--) {
+  for (int s = 4; s >= 4 && !segs; s--) {  // 4-segment stages only (the straight-line compute block)
     const int64_t A = (s * row_bytes + 127) / 128 * 128;
     const int64_t slot = 2 * A + 128;
     // 3 slots: a deeper ring lets the warp the scheduler favours run further
@@ -364,7 +384,7 @@ bool build_cta_schedule(const hos_plan* p, CtaSchedule& cs) {
     if (const char* env = std::getenv("HOS_CTA_DEPTH"))  // diagnostics
       depth = std::max<int64_t>(2, std::min<int64_t>({(int64_t)hos::kCtaMaxDepth, (int64_t)hos::kCtaMaxSmem / slot,
                                                        (int64_t)std::atoi(env)}));
-    if (depth >= 3 || (s == 1 && depth >= 2)) {
+    if (depth >= 2) {
       segs = s;
       cs.depth = (int)depth;
       cs.slot_bytes = (int)slot;
@@ -779,7 +799,7 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
   p->taper = taper;
   p->batch = batch;
   p->device = device;
-  std::string err = build_geometry(p->geo, order, m, m3);
+  std::string err = build_geometry(p->geo, order, m, m3, precision);
   if (!err.empty()) {
     delete p;
     return fail(HOS_EPARAM, err);
@@ -808,7 +828,7 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
   // to 3 elements past the last frequency; even pitch keeps rows 16-byte aligned
   // k_triple_cta bulk-copies whole rows: a pitch of 16 elements keeps every
   // row 128-byte aligned (TMA moves aligned rows at the full rate)
-  p->Lp = (p->L + 4 + 15) & ~15;
+  p->Lp = pitch_of(g);
   cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, device);
   p->occupancy = hos::triple_occupancy(precision, g.tile_step);
   if (const char* env = std::getenv("HOS_K2_SPLIT")) {  // "wa:wb"
@@ -821,10 +841,7 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
   p->nctas = nctas_for(p, k, batch);
   p->maxslots = slots_needed(p, k, p->nctas, batch);
   CtaSchedule sched;
-  {
-    const char* env = std::getenv("HOS_K2");  // "warp": per-warp staged k_triple_w for every launch
-    p->cta = !(env && std::string(env) == "warp") && build_cta_schedule(p, sched);
-  }
+  p->cta = cta_allowed() && build_cta_schedule(p, sched);
   if (p->cta) {
     p->cta_nctas = sched.nctas;
     p->cta_depth = sched.depth;

@@ -19,14 +19,25 @@ __device__ __forceinline__ float2 lds_conj(const float2* p) {
   return v;
 }
 
-template <int NI, int NJ>
+__device__ __forceinline__ float2 lds_conj_x(const float2* p) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"((unsigned)__cvta_generic_to_shared(p)));
+  v.y = __int_as_float(__float_as_int(v.y) ^ 0x80000000);
+  return v;
+}
+
+// MODE 0: conj from a second load + FADD negation (production); 1: second load + sign-bit XOR (ALU pipe);
+// 2: one load, conj built with XOR
+template <int NI, int NJ, int MODE = 0>
 __device__ __forceinline__ void cells2(const float2* __restrict__ rows, const float2* __restrict__ cols,
                                        const float2* __restrict__ gs, float2 (&aR)[NI][NJ], float2 (&aI)[NI][NJ]) {
   float2 fa[NI], fac[NI], fb[NJ];
 #pragma unroll
   for (int i = 0; i < NI; i++) {
     fa[i] = rows[4 * i];
-    fac[i] = lds_conj(rows + 4 * i);
+    if (MODE == 0) fac[i] = lds_conj(rows + 4 * i);
+    if (MODE == 1) fac[i] = lds_conj_x(rows + 4 * i);
+    if (MODE == 2) fac[i] = make_float2(fa[i].x, __int_as_float(__float_as_int(fa[i].y) ^ 0x80000000));
   }
 #pragma unroll
   for (int j = 0; j < NJ; j++) fb[j] = cols[4 * j];
@@ -85,7 +96,7 @@ __device__ __forceinline__ void cells1(const float2* __restrict__ rows, const fl
 constexpr int NSEG = 4;
 constexpr int TS = 104;  // tile stride (float2)
 
-template <int MINB, int NJ>
+template <int MINB, int NJ, int MODE = 0>
 __global__ void __launch_bounds__(128, MINB) k_c2(float2* out, int reps) {
   __shared__ float2 sm[4][NSEG * 2 * TS];  // per warp
   const int warp = threadIdx.x >> 5;
@@ -98,7 +109,7 @@ __global__ void __launch_bounds__(128, MINB) k_c2(float2* out, int reps) {
 #pragma unroll
     for (int q = 0; q < NSEG; q++) {
       const float2* u = sm[warp] + q * 2 * TS + h * TS;
-      cells2<4, NJ>(u + ra, u + 18 + cb, u + 52 + ra + cb, aR, aI);
+      cells2<4, NJ, MODE>(u + ra, u + 18 + cb, u + 52 + ra + cb, aR, aI);
     }
   float2 s = make_float2(0, 0);
   for (int i = 0; i < 4; i++) for (int j = 0; j < NJ; j++) { s.x += aR[i][j].x + aI[i][j].y; s.y += aR[i][j].y - aI[i][j].x; }
@@ -179,10 +190,7 @@ int main() {
   // useful FFMA2-class per lane per rep: 4 per cell, cells per rep = 32 x 4 (C48) ...
   run("FLAT", k_flat<4>, 8 * 4 * 16, sms, buf);
   run("C48", k_c2<2, 8>, 4 * 32 * 4, sms, buf);
-  run("C44", k_c2<4, 4>, 4 * 16 * 4 * 2, sms, buf);
-  run("C44m3", k_c2<3, 4>, 4 * 16 * 4 * 2, sms, buf);
-  run("C48n", k_c1<3, false>, 4 * 32 * 4, sms, buf);
-  run("C48q", k_c1<3, true>, 4 * 32 * 4, sms, buf);
-  run("C48n2", k_c1<2, false>, 4 * 32 * 4, sms, buf);
+  run("C48x", k_c2<2, 8, 1>, 4 * 32 * 4, sms, buf);
+  run("C48s", k_c2<2, 8, 2>, 4 * 32 * 4, sms, buf);
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
 }
