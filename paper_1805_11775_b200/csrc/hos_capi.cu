@@ -64,6 +64,18 @@ struct hos_plan {
   hos::CtaStage* d_stages = nullptr;
   int32_t* d_cta_stage0 = nullptr;
   int64_t rs_stride = 0;  // d_region_slots entries per series
+  // streaming host path (hos_estimate_host, zero-copy): the front end runs on
+  // kStreamFrontCtas SMs reading the series over PCIe while k_triple_cta (an
+  // interleaved schedule on the other SMs) consumes rows as they are published
+  bool stream_ok = false;
+  int s_nctas = 0, s_maxslots = 1;
+  hos::CtaBlock* d_s_blocks = nullptr;
+  hos::CtaStage* d_s_stages = nullptr;
+  int32_t* d_s_cta_stage0 = nullptr;
+  int32_t* d_s_region_slots = nullptr;
+  int* d_ready = nullptr;
+  cudaStream_t side = nullptr;
+  cudaEvent_t e_fork = nullptr, e_join = nullptr;
   int hstride = 0;   // complex elements per half-spectrum row
   int L = 0, Lp = 0; // extended-spectrum length / pitch (complex elements)
   // device tables
@@ -308,14 +320,14 @@ hos::TripleArgs triple_args(const hos_plan* p, int seg_begin, int seg_end, int n
 }
 
 // partial slots of the plan's main K2 launch (k_triple_cta or k_triple_w)
-hos::SlotInfo main_slot_info(const hos_plan* p) {
+hos::SlotInfo main_slot_info(const hos_plan* p, bool streaming = false) {
   hos::SlotInfo si = slot_info(p, p->k, p->nctas);
-  si.region_slots = p->d_region_slots;
-  si.rs_stride = p->rs_stride;
+  si.region_slots = streaming ? p->d_s_region_slots : p->d_region_slots;
+  si.rs_stride = streaming ? 0 : p->rs_stride;
   return si;
 }
 
-hos::CtaTripleArgs cta_args(const hos_plan* p) {
+hos::CtaTripleArgs cta_args(const hos_plan* p, bool streaming = false) {
   hos::CtaTripleArgs a{};
   a.E = p->d_E;
   a.Lp = p->Lp;
@@ -342,6 +354,13 @@ hos::CtaTripleArgs cta_args(const hos_plan* p) {
   a.trace = p->trace;
   a.trace_cta = p->cta_nctas - 1;
   if (const char* env = std::getenv("HOS_TRACE_CTA")) a.trace_cta = std::atoi(env);
+  if (streaming) {
+    a.blocks = p->d_s_blocks;
+    a.stages = p->d_s_stages;
+    a.cta_stage0 = p->d_s_cta_stage0;
+    a.nctas = p->s_nctas;
+    a.ready = p->d_ready;
+  }
   return a;
 }
 
@@ -367,7 +386,12 @@ struct CtaSchedule {
   int nctas = 0, depth = 0, stage_segs = 4, slot_bytes = 0, copy_b = 0, maxslots = 1;
 };
 
-bool build_cta_schedule(const hos_plan* p, CtaSchedule& cs) {
+int stream_front_ctas() {
+  if (const char* env = std::getenv("HOS_STREAM_CTAS")) return std::max(1, std::atoi(env));  // diagnostics
+  return hos::kStreamFrontCtas;
+}
+
+bool build_cta_schedule(const hos_plan* p, CtaSchedule& cs, int interleave_ctas = 0) {
   const hos::Geometry& g = p->geo;
   const int R = g.nregions, K = p->k, B = p->batch;
   if (R <= 0 || K <= 0) return false;
@@ -415,6 +439,51 @@ bool build_cta_schedule(const hos_plan* p, CtaSchedule& cs) {
     const hos::CtaGroup& gr = cs.groups[gi];
     return gr.n == W ? W : std::max<int64_t>(W / gr.phases, 4);
   };
+  if (interleave_ctas > 0) {
+    // Streaming schedule (host path, series arriving over PCIe while K2
+    // runs): each group gets an integer number of CTAs in proportion to its
+    // time, and CTA r of a group takes the group's stages j = r, r + n, ...
+    // so every CTA works through the series in arrival order.  One block per
+    // CTA (slot base r x phases).
+    if (B != 1) return false;
+    const int64_t N = interleave_ctas;
+    const int nst = (K + segs - 1) / segs;
+    std::vector<int64_t> n(ng);
+    int64_t tot = 0, sum = 0;
+    for (int gi = 0; gi < ng; gi++) tot += weight(gi);
+    for (int gi = 0; gi < ng; gi++) {
+      n[gi] = std::max<int64_t>(1, std::min<int64_t>(nst, (N * weight(gi) + tot / 2) / tot));
+      sum += n[gi];
+    }
+    while (sum > N) {  // trim the groups with the most CTAs per unit of time
+      int best = -1;
+      for (int gi = 0; gi < ng; gi++)
+        if (n[gi] > 1 && (best < 0 || n[gi] * weight(best) > n[best] * weight(gi))) best = gi;
+      if (best < 0) return false;
+      n[best]--;
+      sum--;
+    }
+    cs.cta_stage0.push_back(0);
+    std::vector<int32_t> slots(ng, 0);
+    for (int gi = 0; gi < ng; gi++) {
+      for (int64_t r = 0; r < n[gi]; r++) {
+        const int blk = (int)cs.blocks.size();
+        cs.blocks.push_back({0, 0, gi, slots[gi]});
+        slots[gi] += cs.groups[gi].phases;
+        for (int64_t j = r; j < nst; j += n[gi])
+          cs.stages.push_back({(int)(j * segs), std::min(segs, K - (int)(j * segs)), blk, 0});
+        cs.cta_stage0.push_back((int32_t)cs.stages.size());
+      }
+    }
+    cs.nctas = (int)sum;
+    cs.region_slots.assign(R, 0);
+    cs.maxslots = 1;
+    for (int gi = 0; gi < ng; gi++) {
+      for (int r = cs.groups[gi].r0; r < cs.groups[gi].r0 + cs.groups[gi].n; r++) cs.region_slots[r] = slots[gi];
+      cs.maxslots = std::max(cs.maxslots, slots[gi]);
+    }
+    return true;
+  }
   // (series, group) chunks of K segments each.  The CTA ranges come from
   // the smallest per-CTA time budget T (bisection) for which a greedy fill
   // needs <= N CTAs; a CTA's time is its segments' weights plus kSwitch per
@@ -537,8 +606,8 @@ int run_box(hos_plan* p, void* out_dev, cudaStream_t st) {
 
 // K4 of the whole grid: one CTA per series in shared memory when the grid is
 // small (order 3), else line scans + box sums
-int run_smooth(hos_plan* p, void* out_dev, cudaStream_t st, int stage = -1) {
-  const hos::SlotInfo si = main_slot_info(p);
+int run_smooth(hos_plan* p, void* out_dev, cudaStream_t st, int stage = -1, bool streaming = false) {
+  const hos::SlotInfo si = main_slot_info(p, streaming);
   if (p->series_k4) {
     if (stage != 5)
       CUDA_TRY(hos::launch_smooth_series3(p->d_part, p->maxslots, p->geo.ncells, si, p->precision,
@@ -852,11 +921,35 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
     p->maxslots = batch == 1 ? std::max(p->maxslots, sched.maxslots) : sched.maxslots;
     p->rs_stride = g.nregions;
   }
+  CtaSchedule ssched;
+  {
+    // opt-in (HOS_STREAM=1): 1.3x faster host calls on most placements, but
+    // some runs of some SM splits were 2.2x slower
+    const char* env = std::getenv("HOS_STREAM");
+    p->stream_ok = p->cta && batch == 1 && k >= 64 && (m & (m - 1)) == 0 && m <= hos::kFrontMaxM &&
+                   (env && env[0] == '1') &&
+                   build_cta_schedule(p, ssched, std::max(1, p->sms - stream_front_ctas()));
+    if (p->stream_ok) {
+      p->s_nctas = ssched.nctas;
+      p->maxslots = std::max(p->maxslots, ssched.maxslots);
+    }
+  }
 
 
   std::vector<int32_t> cmax(g.line_cmax.begin(), g.line_cmax.end());
   if ((rc = upload(p, &p->d_tiles, g.tiles))) return bail(rc);
   if ((rc = upload(p, &p->d_line_tile0, g.line_tile0))) return bail(rc);
+  if (p->stream_ok) {
+    if ((rc = upload(p, &p->d_s_region_slots, ssched.region_slots))) return bail(rc);
+    if ((rc = upload(p, &p->d_s_blocks, ssched.blocks))) return bail(rc);
+    if ((rc = upload(p, &p->d_s_stages, ssched.stages))) return bail(rc);
+    if ((rc = upload(p, &p->d_s_cta_stage0, ssched.cta_stage0))) return bail(rc);
+    if ((rc = alloc(p, (void**)&p->d_ready, (size_t)k * sizeof(int)))) return bail(rc);
+    if (cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p->e_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p->e_join, cudaEventDisableTiming) != cudaSuccess)
+      return bail(fail(HOS_ECUDA, "cannot create the streaming path's stream/events"));
+  }
   if (p->cta) {
     if ((rc = upload(p, &p->d_region_slots, sched.region_slots))) return bail(rc);
     if ((rc = upload(p, &p->d_groups, sched.groups))) return bail(rc);
@@ -931,6 +1024,12 @@ void hos_plan_destroy(hos_plan* p) {
   for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);
   if (p->cap) cudaStreamDestroy(p->cap);
   for (auto& kv : p->ffts) cufftDestroy(kv.second);
+  if (p->side) cudaStreamDestroy(p->side);
+  if (p->e_fork) cudaEventDestroy(p->e_fork);
+  if (p->e_join) cudaEventDestroy(p->e_join);
+  for (void* b : {(void*)p->d_s_blocks, (void*)p->d_s_stages, (void*)p->d_s_cta_stage0, (void*)p->d_s_region_slots,
+                  (void*)p->d_ready})
+    if (b) cudaFree(b);
   for (void* b : {p->d_raw, p->d_send, p->d_mine, p->d_local, p->d_heads, p->d_vals, p->d_parts})
     if (b) cudaFree(b);
   void* bufs[] = {p->d_groups, p->d_blocks, p->d_stages, p->d_cta_stage0, p->d_tiles, p->d_line_tile0, p->d_region_slots, p->d_line_cmax, p->d_line_start, p->d_row_off, p->d_pair_k1, p->d_pair_k2,
@@ -1097,6 +1196,20 @@ int hos_estimate_host(hos_plan* p, const void* x_host, int x_dtype, int64_t x_st
   const bool zero_copy = pinned && p->fused && ai.devicePointer && ao.devicePointer && !(zc_env && zc_env[0] == '0');
   auto zc_body = [&](cudaStream_t s) -> int {
     if (p->timing) CUDA_TRY(cudaEventRecord(p->ev[0], s));
+    if (p->stream_ok && !p->timing && !p->trace) {
+      // K2 first (its CTAs take one SM each and signal PDL dependents at
+      // once), then the front end as its programmatic dependent: it fills the
+      // SMs K2 left free, reads the series over PCIe and publishes each E row;
+      // K2 consumes rows as their ready flags flip, so the PCIe read overlaps
+      // the triple product.  The memset after them is a full barrier (K4 must
+      // see K2's partial slots, and the front end ran ahead of K2's end).
+      CUDA_TRY(cudaMemsetAsync(p->d_ready, 0, (size_t)p->k * sizeof(int), s));
+      CUDA_TRY(hos::launch_triple_cta(cta_args(p, true), p->precision, s));
+      CUDA_TRY(hos::launch_front(ai.devicePointer, x_dtype, x_stride, p->m, p->k, p->k, 1, p->taper, p->d_taper,
+                                 p->d_tw, p->precision, p->geo.f_lo, p->L, p->Lp, p->d_E, s, 0, p->d_ready));
+      CUDA_TRY(cudaMemsetAsync(p->d_ready, 0, sizeof(int), s));
+      return run_smooth(p, ao.devicePointer, s, -1, true);
+    }
     int r = fused_front(p, ai.devicePointer, x_dtype, x_stride, 0, p->k, p->batch, s);
     if (r) return r;
     if (p->timing)

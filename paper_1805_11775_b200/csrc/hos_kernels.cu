@@ -136,7 +136,8 @@ __global__ void __launch_bounds__(front_threads<LOG2M>() * front_pairs<LOG2M>())
                                                                   int nseg, int krows, int taper,
                                                                   const double* __restrict__ tab,
                                                                   const typename C2<T>::t* __restrict__ tw, int f_lo,
-                                                                  int L, int Lp, typename C2<T>::t* __restrict__ E) {
+                                                                  int L, int Lp, typename C2<T>::t* __restrict__ E,
+                                                                  int* __restrict__ ready) {
   using CT = typename C2<T>::t;
   constexpr int M = 1 << LOG2M;
   constexpr int TH = front_threads<LOG2M>();
@@ -155,30 +156,48 @@ __global__ void __launch_bounds__(front_threads<LOG2M>() * front_pairs<LOG2M>())
     if constexpr (PPC > 1) __syncwarp();
     else __syncthreads();
   };
-  // two real segments per thread group, packed as one complex sequence z = x_a + i x_b
-  const int sa = 2 * (blockIdx.x * PPC + grp), b = blockIdx.y;
-  if (sa >= nseg) return;  // whole group (a warp when PPC > 1)
-  const bool has_b = sa + 1 < nseg;
-  const Tin* src = x + (int64_t)b * x_stride + (int64_t)sa * M;
-  // samples and taper weights stay in registers between the means and the store
+  // two real segments per thread group, packed as one complex sequence z = x_a + i x_b.
+  // A group takes pairs pi, pi + gridDim.x*PPC, ... (one pair when the grid
+  // covers them all; the streaming launch runs few persistent CTAs and loads
+  // the next pair's samples while transforming the current one).
+  const int b = blockIdx.y;
+  const int pstride = gridDim.x * PPC;
+  int pi = blockIdx.x * PPC + grp;
+  if (2 * pi >= nseg) return;  // whole group (a warp when PPC > 1)
   Tin xa[VPT], xb[VPT];
+  auto load = [&](int pair) {
+    const int s0 = 2 * pair;
+    const bool hb = s0 + 1 < nseg;
+    const Tin* src = x + (int64_t)b * x_stride + (int64_t)s0 * M;
+#pragma unroll
+    for (int i = 0; i < VPT; i++) {
+      const int u = tid + i * TH;
+      if (M % TH == 0 || u < M) {
+        xa[i] = src[u];
+        xb[i] = hb ? src[u + M] : Tin(0);
+      }
+    }
+  };
+  load(pi);
+#pragma unroll
+  for (int i = 0; i < VPT; i++) {
+    const int t = tid + i * TH;
+    if (M % TH == 0 || t < M) tws[t] = tw[t];
+  }
+  for (;;) {
+  const int sa = 2 * pi;
+  const bool has_b = sa + 1 < nseg;
+  // samples and taper weights stay in registers between the means and the store
   double wv[VPT];
   double s_a = 0.0, s_b = 0.0;
 #pragma unroll
   for (int i = 0; i < VPT; i++) {
     const int u = tid + i * TH;
     if (M % TH == 0 || u < M) {
-      xa[i] = src[u];
-      xb[i] = has_b ? src[u + M] : Tin(0);
       wv[i] = taper ? tab[u] : 1.0;
       s_a += (double)xa[i];
       s_b += (double)xb[i];
     }
-  }
-#pragma unroll
-  for (int i = 0; i < VPT; i++) {
-    const int t = tid + i * TH;
-    if (M % TH == 0 || t < M) tws[t] = tw[t];
   }
   s_a = warp_sum(s_a);
   s_b = warp_sum(s_b);
@@ -203,6 +222,9 @@ __global__ void __launch_bounds__(front_threads<LOG2M>() * front_pairs<LOG2M>())
       bufA[u] = CT{(T)va, (T)vb};
     }
   }
+  const int pn = pi + pstride;
+  const bool more = 2 * pn < nseg;
+  if (more) load(pn);  // in flight during the transform
   sync();
   // Stockham (self-sorting, decimation in frequency) radix-4 stages, then one
   // radix-2 stage when log2 m is odd.  Stage with current length n and stride
@@ -270,30 +292,54 @@ __global__ void __launch_bounds__(front_threads<LOG2M>() * front_pairs<LOG2M>())
     row[j] = CT{(T)0.5 * (z.x + zn.x), (T)0.5 * (z.y - zn.y)};
     if (has_b) row[Lp + j] = CT{(T)0.5 * (z.y + zn.y), (T)0.5 * (zn.x - z.x)};
   }
+  sync();  // the E rows are written (ready flags) and xin is free (next pair)
+  if (ready && tid == 0) {  // publish the pair's rows to a concurrently running K2
+    __threadfence();
+    int* f = ready + (int64_t)b * krows + sa;
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(f), "r"(1) : "memory");
+    if (has_b) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(f + 1), "r"(1) : "memory");
+  }
+  if (!more) break;
+  pi = pn;
+  }
 }
 
+// stream_ctas > 0: that many persistent CTAs, each padded to more than half
+// an SM's shared memory so they occupy exactly stream_ctas SMs (a concurrent
+// one-CTA-per-SM K2 then always finds the rest), publishing ready flags
 template <int LOG2M, typename Tin, typename T>
 static void front_go(const Tin* x, int64_t x_stride, int nseg, int krows, int batch, int taper, const double* tab,
-                     const typename C2<T>::t* tw, int f_lo, int L, int Lp, typename C2<T>::t* E, cudaStream_t st) {
-  const size_t smem = 3 * (size_t)(1 << LOG2M) * sizeof(typename C2<T>::t) * front_pairs<LOG2M>();
+                     const typename C2<T>::t* tw, int f_lo, int L, int Lp, typename C2<T>::t* E, int stream_ctas,
+                     int* ready, cudaStream_t st) {
+  const size_t base = 3 * (size_t)(1 << LOG2M) * sizeof(typename C2<T>::t) * front_pairs<LOG2M>();
+  const size_t smem = stream_ctas > 0 ? std::max<size_t>(base, kFrontStreamSmem) : base;
   auto kern = k_front<Tin, T, LOG2M>;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)std::max<size_t>(base, kFrontStreamSmem));
     configured = true;
   }
   constexpr int PPC = front_pairs<LOG2M>();
   const int pairs = (nseg + 1) / 2;
-  kern<<<dim3((pairs + PPC - 1) / PPC, batch), front_threads<LOG2M>() * PPC, smem, st>>>(
-      x, x_stride, nseg, krows, taper, tab, tw, f_lo, L, Lp, E);
+  const int grid = stream_ctas > 0 ? std::min(stream_ctas, (pairs + PPC - 1) / PPC) : (pairs + PPC - 1) / PPC;
+  if (ready) {  // streaming: a programmatic dependent of the K2 that consumes its rows (see hos_capi.cu)
+    launch_pdl_kernel(kern, dim3(grid, batch), dim3(front_threads<LOG2M>() * PPC), smem, st, x, x_stride, nseg, krows,
+                      taper, tab, tw, f_lo, L, Lp, E, ready);
+    return;
+  }
+  kern<<<dim3(grid, batch), front_threads<LOG2M>() * PPC, smem, st>>>(x, x_stride, nseg, krows, taper, tab, tw, f_lo,
+                                                                      L, Lp, E, ready);
 }
 
 template <typename Tin, typename T>
 static cudaError_t front_dispatch(int log2m, const Tin* x, int64_t x_stride, int nseg, int krows, int batch,
                                   int taper, const double* tab, const typename C2<T>::t* tw, int f_lo, int L, int Lp,
-                                  typename C2<T>::t* E, cudaStream_t st) {
+                                  typename C2<T>::t* E, int stream_ctas, int* ready, cudaStream_t st) {
 #define HOS_FRONT_CASE(LG) \
-  case LG: front_go<LG, Tin, T>(x, x_stride, nseg, krows, batch, taper, tab, tw, f_lo, L, Lp, E, st); break;
+  case LG:                                                                                                   \
+    front_go<LG, Tin, T>(x, x_stride, nseg, krows, batch, taper, tab, tw, f_lo, L, Lp, E, stream_ctas, ready, st); \
+    break;
   switch (log2m) {
     HOS_FRONT_CASE(2) HOS_FRONT_CASE(3) HOS_FRONT_CASE(4) HOS_FRONT_CASE(5) HOS_FRONT_CASE(6) HOS_FRONT_CASE(7)
     HOS_FRONT_CASE(8) HOS_FRONT_CASE(9) HOS_FRONT_CASE(10) HOS_FRONT_CASE(11) HOS_FRONT_CASE(12)
@@ -305,22 +351,22 @@ static cudaError_t front_dispatch(int log2m, const Tin* x, int64_t x_stride, int
 
 cudaError_t launch_front(const void* x, int x_dtype, int64_t x_stride, int m, int nseg, int krows, int batch,
                          int taper, const double* tab, const void* tw, int precision, int f_lo, int L, int Lp, void* E,
-                         cudaStream_t st) {
+                         cudaStream_t st, int stream_ctas, int* ready) {
   int log2m = 0;
   while ((1 << log2m) < m) log2m++;
   if ((1 << log2m) != m || m > kFrontMaxM || m < 4) return cudaErrorInvalidValue;
   if (precision == 32) {
     if (x_dtype == 0)
       return front_dispatch<float, float>(log2m, (const float*)x, x_stride, nseg, krows, batch, taper, tab,
-                                          (const float2*)tw, f_lo, L, Lp, (float2*)E, st);
+                                          (const float2*)tw, f_lo, L, Lp, (float2*)E, stream_ctas, ready, st);
     return front_dispatch<double, float>(log2m, (const double*)x, x_stride, nseg, krows, batch, taper, tab,
-                                         (const float2*)tw, f_lo, L, Lp, (float2*)E, st);
+                                         (const float2*)tw, f_lo, L, Lp, (float2*)E, stream_ctas, ready, st);
   }
   if (x_dtype == 0)
     return front_dispatch<float, double>(log2m, (const float*)x, x_stride, nseg, krows, batch, taper, tab,
-                                         (const double2*)tw, f_lo, L, Lp, (double2*)E, st);
+                                         (const double2*)tw, f_lo, L, Lp, (double2*)E, stream_ctas, ready, st);
   return front_dispatch<double, double>(log2m, (const double*)x, x_stride, nseg, krows, batch, taper, tab,
-                                        (const double2*)tw, f_lo, L, Lp, (double2*)E, st);
+                                        (const double2*)tw, f_lo, L, Lp, (double2*)E, stream_ctas, ready, st);
 }
 
 // ===========================================================================
@@ -988,6 +1034,21 @@ __global__ void __launch_bounds__(32 * kCtaWarps, 1) k_triple_cta(const __grid_c
     return v;
   };
   auto issue = [&](const CtaStage& sg, int d) {  // a stage of this CTA into ring slot d (one thread)
+    if (a.ready) {  // rows published by a concurrently running front end (streaming host path)
+      for (int r = sg.row; r < sg.row + sg.nseg; r++) {
+        unsigned long long t0, t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        for (;;) {
+          int v;
+          asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(a.ready + r) : "memory");
+          if (v) break;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+          if (t1 - t0 > 200000000ull) break;  // 200 ms: never hang the GPU (the result is then wrong)
+          __nanosleep(200);
+        }
+      }
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // the bulk copy (async proxy) reads them
+    }
     const unsigned bytes = (unsigned)(sg.nseg * Lp * (int)sizeof(C));
     const C* src = E + (int64_t)sg.row * Lp;
     const unsigned dst = ring_s + (unsigned)(d * a.slot_bytes);
@@ -1004,7 +1065,7 @@ __global__ void __launch_bounds__(32 * kCtaWarps, 1) k_triple_cta(const __grid_c
   };
   const int h = lane / (S * S), ra = (lane / S) % S, cb = lane % S;
   int cur = -1;                  // current block
-  int region = 0, phase = 0, phases = 1, blk_row0 = 0;
+  int region = 0, phase = 0, phases = 1, blk_row0 = 0, blk_k0 = 0;
   bool role = false;             // this warp has (a tile of) a region in the block
   int c0 = 0, line0 = 0, nrows = 0;
   C* P = nullptr;                // the warp's partial slot (series + slot applied)
@@ -1021,7 +1082,8 @@ __global__ void __launch_bounds__(32 * kCtaWarps, 1) k_triple_cta(const __grid_c
     v.slot_base = r.w;
     return v;
   };
-  auto enter = [&](const CtaBlock& blk) {
+  auto enter = [&](const CtaBlock& blk, int k_first) {
+    blk_k0 = k_first;  // the block's first stage (phases deal its stages round-robin)
     const CtaGroup grp = a.groups[blk.group];
     // warps per region: `halves` (2: each warp computes one tile of the
     // pair, the other half of its lanes idle) x `phases`
@@ -1083,7 +1145,7 @@ __global__ void __launch_bounds__(32 * kCtaWarps, 1) k_triple_cta(const __grid_c
   // flush each dependent table load costs a DRAM round trip.
   if (nst > 0) {
     cur = sg.block;
-    enter(nb);
+    enter(nb, 0);
   }
   CtaStage pre[kCtaMaxDepth];
   if (threadIdx.x == 0) {
@@ -1104,7 +1166,7 @@ __global__ void __launch_bounds__(32 * kCtaWarps, 1) k_triple_cta(const __grid_c
     if (sg.block != cur) {
       if (cur >= 0) finalize();
       cur = sg.block;
-      enter(nb);
+      enter(nb, k);
     }
     if (sg_next.block != sg.block) nb = ld_block(sg_next.block);
     {
@@ -1136,7 +1198,7 @@ __global__ void __launch_bounds__(32 * kCtaWarps, 1) k_triple_cta(const __grid_c
     // phases > 1: the warp takes every phases-th STAGE of the block (whole
     // stages keep the 4-segment straight-line block; a warp running one
     // segment per stage measured ~40% of the FMA rate)
-    if (warp_active && (phases == 1 || ((sg.row - blk_row0) / a.stage_segs) % phases == phase)) {
+    if (warp_active && (phases == 1 || (k - blk_k0) % phases == phase)) {
       if (sg.nseg == 4) {
 #pragma unroll
         for (int t = 0; t < 4; t++) warp_cells<T, CONJ, ORDER4, S>(q + t * Lp, ops, acc);
