@@ -1551,21 +1551,55 @@ __global__ void __launch_bounds__(512) k_smooth_series3(const P2* __restrict__ p
   unsigned short* cline = reinterpret_cast<unsigned short*>(rsl + si.nregions);  // ncells: line of each cell
   unsigned short* prow = cline + ncells;                       // npoints: row of each point
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  const int series = blockIdx.x;
+  // persistent: the geometry tables are built once per CTA, then the CTA
+  // smooths series blockIdx.x, blockIdx.x + gridDim.x, ...
+  __shared__ int max_slots;
   for (int i = tid; i <= nlines; i += blockDim.x) ls[i] = (int)__ldg(a.line_start + i);
   for (int i = tid; i <= a.rows; i += blockDim.x) ro[i] = (int)__ldg(a.row_off + i);
   for (int i = tid; i < nlines; i += blockDim.x) lt0[i] = __ldg(si.line_tile0 + i);
-  for (int i = tid; i < si.nregions; i += blockDim.x) rsl[i] = __ldg(si.region_slots + series * si.rs_stride + i);
   __syncthreads();
   for (int l = warp; l < nlines; l += nw)
     for (int c = ls[l] + lane; c < ls[l + 1]; c += 32) cline[c] = (unsigned short)l;
   for (int r = warp; r < a.rows; r += nw)
     for (int q = ro[r] + lane; q < ro[r + 1]; q += 32) prow[q] = (unsigned short)r;
   asm volatile("griddepcontrol.wait;" ::: "memory");  // partial slots come from K2
+  for (int series = blockIdx.x; series < a.batch; series += gridDim.x) {
+  __syncthreads();  // the previous series' box reads of S are done
+  if (tid == 0) max_slots = 0;
   __syncthreads();
+  for (int i = tid; i < si.nregions; i += blockDim.x) {
+    rsl[i] = __ldg(si.region_slots + series * si.rs_stride + i);
+    atomicMax(&max_slots, rsl[i]);
+  }
+  __syncthreads();
+  const P2* src = part + series * part_series_stride;
+  if (max_slots == 1) {
+    // every cell in one slot: contiguous loads, two cells (16 / 32 bytes) per thread and step
+    constexpr int U = 4;
+    const int npair = ncells / 2;
+    for (int base = 0; base < npair; base += U * blockDim.x) {
+      P2 v[U][2];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int q = base + u * blockDim.x + tid;
+        if (q < npair) {
+          v[u][0] = src[2 * q];
+          v[u][1] = src[2 * q + 1];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int q = base + u * blockDim.x + tid;
+        if (q < npair) {
+          S[2 * q] = make_double2((double)v[u][0].x, (double)v[u][0].y);
+          S[2 * q + 1] = make_double2((double)v[u][1].x, (double)v[u][1].y);
+        }
+      }
+    }
+    if ((ncells & 1) && tid == 0) S[ncells - 1] = make_double2((double)src[ncells - 1].x, (double)src[ncells - 1].y);
+  } else {
   // raw cells: partial slots summed in slot order (fp64); four cells per
   // thread per step with all their loads issued first
-  const P2* src = part + series * part_series_stride;
   constexpr int U = 4;
   for (int base = 0; base < ncells; base += U * blockDim.x) {
     P2 v[U][2];
@@ -1600,6 +1634,7 @@ __global__ void __launch_bounds__(512) k_smooth_series3(const P2* __restrict__ p
       }
       S[idx] = make_double2(vr, vi);
     }
+  }
   }
   __syncthreads();
   for (int l = warp; l < nlines; l += nw) {  // inclusive prefix of each line
@@ -1642,6 +1677,7 @@ __global__ void __launch_bounds__(512) k_smooth_series3(const P2* __restrict__ p
     out[p].x = sr * a.scale;
     out[p].y = si_ * a.scale;
   }
+  }
 }
 
 size_t smooth_series3_smem(int64_t ncells, int64_t nlines, int rows, int nregions, int64_t npoints) {
@@ -1655,13 +1691,22 @@ cudaError_t launch_smooth_series3(const void* part, int nparts, int64_t part_str
   if (!si.line_tile0 || !si.region_slots) return cudaErrorInvalidValue;  // needs the plan's slot table
   const size_t sm = smooth_series3_smem(a.s_series_stride, nlines, a.rows, si.nregions, a.p_end - a.p_begin);
   const int64_t pss = part_stride * nparts;
+  // persistent CTAs: as many as fit at once (grid capped at the batch)
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int per_sm = 1;
   if (precision == 32) {
     cudaFuncSetAttribute(k_smooth_series3<float2, float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    return launch_pdl_kernel(k_smooth_series3<float2, float2>, dim3(a.batch), dim3(512), sm, st, (const float2*)part,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_smooth_series3<float2, float2>, 512, sm);
+    const int grid = std::max(1, std::min(a.batch, sms * std::max(1, per_sm)));
+    return launch_pdl_kernel(k_smooth_series3<float2, float2>, dim3(grid), dim3(512), sm, st, (const float2*)part,
                              nparts, part_stride, pss, si, a, (int)nlines);
   }
   cudaFuncSetAttribute(k_smooth_series3<double2, double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  return launch_pdl_kernel(k_smooth_series3<double2, double2>, dim3(a.batch), dim3(512), sm, st,
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_smooth_series3<double2, double2>, 512, sm);
+  const int grid = std::max(1, std::min(a.batch, sms * std::max(1, per_sm)));
+  return launch_pdl_kernel(k_smooth_series3<double2, double2>, dim3(grid), dim3(512), sm, st,
                            (const double2*)part, nparts, part_stride, pss, si, a, (int)nlines);
 }
 
