@@ -1196,7 +1196,7 @@ int hos_estimate_host(hos_plan* p, const void* x_host, int x_dtype, int64_t x_st
   const bool zero_copy = pinned && p->fused && ai.devicePointer && ao.devicePointer && !(zc_env && zc_env[0] == '0');
   auto zc_body = [&](cudaStream_t s) -> int {
     if (p->timing) CUDA_TRY(cudaEventRecord(p->ev[0], s));
-    if (p->stream_ok && !p->timing && !p->trace) {
+    if (p->stream_ok && !p->timing) {
       // K2 first (its CTAs take one SM each and signal PDL dependents at
       // once), then the front end as its programmatic dependent: it fills the
       // SMs K2 left free, reads the series over PCIe and publishes each E row;
