@@ -1225,7 +1225,16 @@ int hos_estimate_host(hos_plan* p, const void* x_host, int x_dtype, int64_t x_st
     if (p->timing) CUDA_TRY(cudaEventRecord(p->ev[0], st));
     if ((rc = body(st))) return rc;
   }
-  CUDA_TRY(cudaStreamSynchronize(st));
+  // the call returns the values in host memory: wait by polling (a blocking
+  // synchronize can add a scheduler wake-up to every call's latency)
+  if (std::getenv("HOS_HOST_SYNC_BLOCK")) {
+    CUDA_TRY(cudaStreamSynchronize(st));
+  } else {
+    cudaError_t q;
+    while ((q = cudaStreamQuery(st)) == cudaErrorNotReady) {
+    }
+    CUDA_TRY(q);
+  }
   return HOS_OK;
 }
 
