@@ -1302,7 +1302,7 @@ __device__ __forceinline__ int cell_slots(const SlotInfo& si, int nparts, int64_
 // sum of the ns partial slots of one cell in slot order (fp64); the loads of
 // a 16-slot chunk are all issued before the adds (one L2 round trip per chunk)
 #ifndef HOS_SCAN_CHUNK
-#define HOS_SCAN_CHUNK 16
+#define HOS_SCAN_CHUNK 8
 #endif
 template <typename P2, int kChunk = HOS_SCAN_CHUNK>
 __device__ __forceinline__ void sum_slots(const P2* __restrict__ src, int ns, int64_t stride, int64_t idx, double& vr,
@@ -1322,7 +1322,10 @@ __device__ __forceinline__ void sum_slots(const P2* __restrict__ src, int ns, in
 }
 
 template <typename P2>
-__global__ void __launch_bounds__(kScanThreads) k_line_scan(const P2* __restrict__ part, int nparts, int64_t part_stride,
+#ifndef HOS_SCAN_MINB
+#define HOS_SCAN_MINB 3  // 3 CTAs per SM: the 520-line cfg2 grid in one wave
+#endif
+__global__ void __launch_bounds__(kScanThreads, HOS_SCAN_MINB) k_line_scan(const P2* __restrict__ part, int nparts, int64_t part_stride,
                                                             int64_t part_series_stride, SlotInfo si,
                                                             const int64_t* __restrict__ line_start, int64_t line_begin,
                                                             int64_t s_series_stride, double2* __restrict__ S) {
