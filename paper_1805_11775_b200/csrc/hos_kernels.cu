@@ -1460,8 +1460,11 @@ __global__ void __launch_bounds__(256, 4) k_box3_flat(BoxArgs a) {
                          (int)(p - roff[lo]), (OUT*)a.out + series * a.out_series_stride);
 }
 
+#ifndef HOS_BOX_MINB
+#define HOS_BOX_MINB 1
+#endif
 template <typename OUT>
-__global__ void __launch_bounds__(128) k_box3(BoxArgs a, int row0) {
+__global__ void __launch_bounds__(128, HOS_BOX_MINB) k_box3(BoxArgs a, int row0) {
   asm volatile("griddepcontrol.wait;" ::: "memory");  // prefix sums come from K4a
   const int k1 = row0 + blockIdx.y;
   const int k2 = blockIdx.x * blockDim.x + threadIdx.x;
