@@ -190,6 +190,16 @@ int hos_estimate_distributed(hos_plan* plan, const void* x_dev, int x_dtype, voi
  * p0, p1}, then {block, halo, halo_in_next}: 14 * nranks + 3 int64. */
 int hos_shard_layout(int order, int m, int k, int m3, int nranks, int64_t* out);
 
+/* Host-only check of the k_triple_cta schedule a plan of this shape would
+ * use on a GPU with `sms` SMs (interleave != 0: the streaming host path's
+ * schedule): every (series, region group, segment) covered exactly once,
+ * stages inside their block's series, warp roles within the CTA, partial
+ * slot bases consecutive and counted.  No device needed.  stats (12 int64):
+ * {ctas, stages, max stages per CTA, min, max slots, tile step, ring depth,
+ * groups, regions, blocks, segments per stage, slot bytes}; ctas = 0: the plan would not
+ * use k_triple_cta.  Returns HOS_EDATA with the failed property. */
+int hos_cta_schedule_check(int order, int m, int k, int m3, int precision, int batch, int sms, int interleave,
+                           int64_t* stats);
 /* Diagnostics: K2 CTAs per series (4 warps each) of the per-warp staged kernel. */
 int hos_plan_nctas(const hos_plan* plan);
 /* Diagnostics: which K2 the plan's full estimate launches: 1 = k_triple_cta

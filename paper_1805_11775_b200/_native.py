@@ -64,6 +64,7 @@ EXPORTED_SYMBOLS = {
     "hos_comm_attach": (_i, [_p, _p, _i, _i]),
     "hos_estimate_distributed": (_i, [_p, _p, _i, _p, _p]),
     "hos_shard_layout": (_i, [_i, _i, _i, _i, _i, _p]),
+    "hos_cta_schedule_check": (_i, [_i, _i, _i, _i, _i, _i, _i, _i, _p]),
     "hos_plan_time_stages": (_i, [_p, _p, _i, _i64, _p, _i, _p, _p]),
 }
 

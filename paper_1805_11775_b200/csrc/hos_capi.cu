@@ -1539,6 +1539,92 @@ int hos_shard_layout(int order, int m, int k, int m3, int nranks, int64_t* out) 
   return HOS_OK;
 }
 
+int hos_cta_schedule_check(int order, int m, int k, int m3, int precision, int batch, int sms, int interleave,
+                           int64_t* stats) {
+  if (!stats) return fail(HOS_EPARAM, "null output");
+  if (m < 1 || k < 1 || batch < 1 || sms < 2 || (precision != 32 && precision != 64))
+    return fail(HOS_EPARAM, "bad shape");
+  hos_plan p;  // host fields only: no device resources
+  p.order = order;
+  p.m = m;
+  p.k = k;
+  p.m3 = m3;
+  p.precision = precision;
+  p.batch = batch;
+  p.sms = sms;
+  std::string err = build_geometry(p.geo, order, m, m3, precision);
+  if (!err.empty()) return fail(HOS_EPARAM, err);
+  p.Lp = pitch_of(p.geo);
+  const hos::Geometry& g = p.geo;
+  CtaSchedule cs;
+  const int nf = interleave ? std::max(1, sms - stream_front_ctas()) : 0;
+  for (int i = 0; i < 12; i++) stats[i] = 0;
+  if (!build_cta_schedule(&p, cs, nf)) return HOS_OK;  // not eligible: stats[0] = 0
+  const int R = g.nregions, W = hos::kCtaWarps;
+  auto bad = [&](const std::string& why) { return fail(HOS_EDATA, "schedule check: " + why); };
+  if ((int)cs.cta_stage0.size() != cs.nctas + 1 || cs.cta_stage0.front() != 0 ||
+      cs.cta_stage0.back() != (int)cs.stages.size())
+    return bad("CTA stage ranges");
+  if (cs.nctas > sms) return bad("more CTAs than SMs");
+  // every (series, group, segment) exactly once; stages inside their block's series
+  const int ng = (int)cs.groups.size();
+  std::vector<uint8_t> seen((size_t)batch * ng * k, 0);
+  int64_t smax = 0, smin = INT64_MAX;
+  std::vector<int> blk_cta(cs.blocks.size(), -1);
+  for (int c = 0; c < cs.nctas; c++) {
+    const int64_t n = cs.cta_stage0[c + 1] - cs.cta_stage0[c];
+    smax = std::max(smax, n);
+    smin = std::min(smin, n);
+    for (int j = cs.cta_stage0[c]; j < cs.cta_stage0[c + 1]; j++) {
+      const hos::CtaStage& st = cs.stages[j];
+      if (st.block < 0 || st.block >= (int)cs.blocks.size()) return bad("stage block index");
+      if (blk_cta[st.block] >= 0 && blk_cta[st.block] != c) return bad("block shared by two CTAs");
+      blk_cta[st.block] = c;
+      const hos::CtaBlock& b = cs.blocks[st.block];
+      if (st.nseg < 1 || st.nseg > cs.stage_segs) return bad("stage size");
+      for (int t = 0; t < st.nseg; t++) {
+        const int row = st.row + t;
+        if (row / k != b.series || b.series < 0 || b.series >= batch) return bad("stage outside its series");
+        uint8_t& v = seen[((size_t)b.series * ng + b.group) * k + row % k];
+        if (v) return bad("segment covered twice");
+        v = 1;
+      }
+    }
+  }
+  for (uint8_t v : seen)
+    if (!v) return bad("segment not covered");
+  // roles: n x halves x phases warps; slot ranges of a (series, group) disjoint and counted
+  std::vector<int> used((size_t)batch * ng, 0);
+  for (const hos::CtaBlock& b : cs.blocks) {
+    const hos::CtaGroup& gr = cs.groups[b.group];
+    if (gr.n * gr.halves * gr.phases > W || gr.n < 1) return bad("group roles exceed the CTA's warps");
+    if (gr.halves == 2 && g.tiles_per_region != 2) return bad("halves without tile pairs");
+    int& u = used[(size_t)b.series * ng + b.group];
+    if (b.slot_base != u) return bad("slot bases not consecutive");
+    u += gr.phases;
+  }
+  for (int b = 0; b < batch; b++)
+      for (int gi = 0; gi < ng; gi++)
+        for (int r = cs.groups[gi].r0; r < cs.groups[gi].r0 + cs.groups[gi].n; r++) {
+          const int want = used[(size_t)b * ng + gi];
+          const int have = cs.region_slots[(size_t)(interleave ? 0 : b) * R + r];
+          if (have != want || have > cs.maxslots) return bad("region slot counts");
+        }
+  stats[0] = cs.nctas;
+  stats[1] = (int64_t)cs.stages.size();
+  stats[2] = smax;
+  stats[3] = smin;
+  stats[4] = cs.maxslots;
+  stats[5] = g.tile_step;
+  stats[6] = cs.depth;
+  stats[7] = ng;
+  stats[8] = R;
+  stats[9] = (int64_t)cs.blocks.size();
+  stats[10] = cs.stage_segs;
+  stats[11] = cs.slot_bytes;
+  return HOS_OK;
+}
+
 int hos_comm_attach(hos_plan* p, void* nccl_comm, int rank, int nranks) {
   int rc = check_plan(p);
   if (rc) return rc;

@@ -118,3 +118,47 @@ def test_estimators_fail_loudly_without_gpu(lib):
     with pytest.raises(RuntimeError, match="CUDA device"):
         estimate_spectrum(TimeSeries(np.random.default_rng(0).standard_normal(128)),
                           EstimationConfig(3, SegmentConfig(m=64, k=2), 5))
+
+
+SCHED_SHAPES = [
+    # order, m, k, m3, precision, batch
+    (3, 1024, 1024, 9, 32, 1),   # cfg2
+    (3, 1024, 1024, 9, 64, 1),
+    (3, 128, 16, 5, 32, 1),      # cfg1
+    (3, 256, 78, 7, 32, 4096),   # cfg5
+    (3, 256, 78, 7, 32, 37),     # a batch that does not divide the CTAs
+    (4, 256, 1024, 5, 32, 1),    # cfg4
+    (4, 64, 12, 5, 64, 3),
+    (3, 512, 7, 3, 32, 1),       # fewer segments than a stage per CTA
+    (3, 2048, 300, 11, 32, 1),
+    (3, 4096, 2250, 17, 32, 1),  # cfg3: k_triple_w (not eligible)
+    (3, 100, 50, 5, 32, 2),      # non-power-of-two M
+]
+
+
+@pytest.mark.parametrize("shape", SCHED_SHAPES, ids=lambda s: "o%d_m%d_k%d_w%d_p%d_b%d" % s)
+@pytest.mark.parametrize("sms", [148, 132, 7])
+@pytest.mark.parametrize("interleave", [0, 1])
+def test_cta_schedule_covers_every_segment_once(lib, shape, sms, interleave):
+    """hos_cta_schedule_check builds the k_triple_cta schedule on the host
+    (no GPU) and verifies coverage, stage bounds, warp roles and partial-slot
+    bookkeeping; here also the balance of the per-CTA stage counts."""
+    import ctypes
+
+    order, m, k, m3, prec, batch = shape
+    if interleave and batch != 1:
+        pytest.skip("the streaming schedule is for single series")
+    stats = (ctypes.c_int64 * 12)()
+    rc = lib.hos_cta_schedule_check(order, m, k, m3, prec, batch, sms, interleave, stats)
+    assert rc == 0, lib.hos_last_error().decode()
+    ctas, stages, smax, smin = stats[0], stats[1], stats[2], stats[3]
+    if m == 4096:
+        assert ctas == 0  # four whole rows per ring slot do not fit: per-warp staged kernel
+        return
+    if interleave and sms - 20 < 1:
+        return
+    assert 0 < ctas <= sms
+    assert stats[4] >= 1 and stats[5] in (2, 4) and stats[6] >= 2
+    groups = stats[7]
+    assert stages >= batch * groups * -(-k // stats[10])  # each (series, group) needs ceil(k/4) stages at least
+    assert smin >= 1 and smax >= smin
