@@ -208,14 +208,28 @@ bool cta_fits(const hos::Geometry& g, int precision) {
 // k_triple_w an 8 x 16 region stages 2.5x the chunks of a 16 x 32 one and
 // measured 1.79x slower per issued cell, so it needs 1.8x.  HOS_K2_TILE=2|4
 // forces the step.
+// For order 3 the first band's height (1..tile rows) shifts every later band
+// across D_h's staircase edges: the tiling with the fewest regions is kept
+// (ties: full first band).  E.g. M = 2048, w = 11: 289 instead of 297
+// regions; cfg2 and cfg5 are already minimal.
+std::string build_best_band(hos::Geometry& g, int order, int m, int m3, int step) {
+  std::string err = g.build(order, m, m3, step);
+  if (!err.empty() || order != 3) return err;
+  for (int fb = 1; fb < 4 * step; fb++) {
+    hos::Geometry t;
+    if (t.build(order, m, m3, step, fb).empty() && t.nregions < g.nregions) g = std::move(t);
+  }
+  return "";
+}
+
 std::string build_geometry(hos::Geometry& g, int order, int m, int m3, int precision) {
   int forced = 0;
   if (const char* env = std::getenv("HOS_K2_TILE")) forced = std::atoi(env);
-  if (forced == 2 || forced == 4) return g.build(order, m, m3, forced);
-  std::string err = g.build(order, m, m3, 4);
+  if (forced == 2 || forced == 4) return build_best_band(g, order, m, m3, forced);
+  std::string err = build_best_band(g, order, m, m3, 4);
   if (!err.empty()) return err;
   hos::Geometry g2;
-  if (!g2.build(order, m, m3, 2).empty()) return "";
+  if (!build_best_band(g2, order, m, m3, 2).empty()) return "";
   const bool cta = cta_allowed() && cta_fits(g2, precision);
   if ((double)g.issued_cells >= (cta ? 1.25 : 1.8) * (double)g2.issued_cells) g = std::move(g2);
   return "";

@@ -69,7 +69,7 @@ void add_band_regions(std::vector<RegionRec>& regs, std::vector<int32_t>& line_t
 
 }  // namespace
 
-std::string Geometry::build(int order_, int m_, int m3_, int tile_step_) {
+std::string Geometry::build(int order_, int m_, int m3_, int tile_step_, int first_band) {
   order = order_;
   m = m_;
   m3 = m3_;
@@ -141,8 +141,9 @@ std::string Geometry::build(int order_, int m_, int m3_, int tile_step_) {
     }
     ncells = line_start.back();
     line_tile0.assign(n3lines, 0);
-    for (int l0 = 0; l0 < n3lines; l0 += tile_rows) {
-      const int nr = std::min(tile_rows, n3lines - l0);
+    const int fb = first_band >= 1 && first_band <= tile_rows ? first_band : tile_rows;
+    for (int l0 = 0; l0 < n3lines; l0 += (l0 == 0 ? fb : tile_rows)) {
+      const int nr = std::min(l0 == 0 ? fb : tile_rows, n3lines - l0);
       int cb = lo;
       for (int l = l0; l < l0 + nr; l++) cb = std::max(cb, (int)cmax3[l]);
       add_band_regions(regs, line_tile0, l0, nr, lo + l0, 0, lo, cb, tile_cols);

@@ -90,7 +90,9 @@ struct Geometry {
   std::vector<int32_t> line_tile0;    // per line: index of the tile holding its first column
   int64_t issued_cells = 0;           // cells computed by K2 (regions x 1024)
 
-  std::string build(int order, int m, int m3, int tile_step = 4);  // returns "" or an error message
+  // first_band (order 3): lines in the first band (1..tile_rows; 0 = tile_rows) -- shifts every
+  // later band, which changes how D_h's staircase edges fall into tiles
+  std::string build(int order, int m, int m3, int tile_step = 4, int first_band = 0);  // "" or an error
 };
 
 }  // namespace hos

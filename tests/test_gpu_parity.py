@@ -438,3 +438,17 @@ def test_k2_tile_step2(cuda, monkeypatch, order, m, k, w, conj, prec):
         issued[step] = plan.issued
         assert north_star(out.cpu().numpy(), ref) <= (TOL_FP64 if prec == 64 else TOL_FP32), step
     assert issued["2"] <= issued["4"]
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+@pytest.mark.parametrize("m,k,w", [(384, 10, 3), (384, 9, 11), (256, 12, 5)])
+def test_shifted_band_tilings_vs_oracle(cuda, prec, m, k, w):
+    """Shapes whose best tiling starts with a short band (fewer regions than
+    full 16-line bands): the shifted band lattice against the oracle port."""
+    P = api()
+    x = np.random.default_rng(m * 31 + k * 7 + w).standard_normal(m * k)
+    cfg = P.EstimationConfig(3, P.SegmentConfig(m=m, k=k), w, precision=prec, taper="hann")
+    g = P.estimate_spectrum(P.TimeSeries(x), cfg)
+    dom, ref = O.estimate(x, 3, m, k, w, True, "hann")
+    assert np.array_equal(g.indices, dom)
+    assert O.north_star_error(g.values, ref) <= TOL[prec]
