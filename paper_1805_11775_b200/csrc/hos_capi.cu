@@ -1220,7 +1220,7 @@ int hos_estimate_host(hos_plan* p, const void* x_host, int x_dtype, int64_t x_st
       CUDA_TRY(cudaMemsetAsync(p->d_ready, 0, (size_t)p->k * sizeof(int), s));
       CUDA_TRY(hos::launch_triple_cta(cta_args(p, true), p->precision, s));
       CUDA_TRY(hos::launch_front(ai.devicePointer, x_dtype, x_stride, p->m, p->k, p->k, 1, p->taper, p->d_taper,
-                                 p->d_tw, p->precision, p->geo.f_lo, p->L, p->Lp, p->d_E, s, 0, p->d_ready));
+                                 p->d_tw, p->precision, p->geo.f_lo, p->L, p->Lp, p->d_E, s, p->d_ready));
       CUDA_TRY(cudaMemsetAsync(p->d_ready, 0, sizeof(int), s));
       return run_smooth(p, ao.devicePointer, s, -1, true);
     }

@@ -157,9 +157,9 @@ __global__ void __launch_bounds__(front_threads<LOG2M>() * front_pairs<LOG2M>())
     else __syncthreads();
   };
   // two real segments per thread group, packed as one complex sequence z = x_a + i x_b.
-  // A group takes pairs pi, pi + gridDim.x*PPC, ... (one pair when the grid
-  // covers them all; the streaming launch runs few persistent CTAs and loads
-  // the next pair's samples while transforming the current one).
+  // A group takes pairs pi, pi + gridDim.x*PPC, ... (the launches size the
+  // grid to one pair per group; a smaller, persistent grid would load the
+  // next pair's samples while transforming the current one).
   const int b = blockIdx.y;
   const int pstride = gridDim.x * PPC;
   int pi = blockIdx.x * PPC + grp;
@@ -304,26 +304,24 @@ __global__ void __launch_bounds__(front_threads<LOG2M>() * front_pairs<LOG2M>())
   }
 }
 
-// stream_ctas > 0: that many persistent CTAs, each padded to more than half
-// an SM's shared memory so they occupy exactly stream_ctas SMs (a concurrent
-// one-CTA-per-SM K2 then always finds the rest), publishing ready flags
+// ready != nullptr: streaming launch (see hos_capi.cu): each pair publishes
+// its rows' ready flags, and the kernel is a programmatic (PDL) dependent of
+// the K2 that consumes them
 template <int LOG2M, typename Tin, typename T>
 static void front_go(const Tin* x, int64_t x_stride, int nseg, int krows, int batch, int taper, const double* tab,
-                     const typename C2<T>::t* tw, int f_lo, int L, int Lp, typename C2<T>::t* E, int stream_ctas,
-                     int* ready, cudaStream_t st) {
-  const size_t base = 3 * (size_t)(1 << LOG2M) * sizeof(typename C2<T>::t) * front_pairs<LOG2M>();
-  const size_t smem = stream_ctas > 0 ? std::max<size_t>(base, kFrontStreamSmem) : base;
+                     const typename C2<T>::t* tw, int f_lo, int L, int Lp, typename C2<T>::t* E, int* ready,
+                     cudaStream_t st) {
+  const size_t smem = 3 * (size_t)(1 << LOG2M) * sizeof(typename C2<T>::t) * front_pairs<LOG2M>();
   auto kern = k_front<Tin, T, LOG2M>;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)std::max<size_t>(base, kFrontStreamSmem));
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = true;
   }
   constexpr int PPC = front_pairs<LOG2M>();
   const int pairs = (nseg + 1) / 2;
-  const int grid = stream_ctas > 0 ? std::min(stream_ctas, (pairs + PPC - 1) / PPC) : (pairs + PPC - 1) / PPC;
-  if (ready) {  // streaming: a programmatic dependent of the K2 that consumes its rows (see hos_capi.cu)
+  const int grid = (pairs + PPC - 1) / PPC;
+  if (ready) {
     launch_pdl_kernel(kern, dim3(grid, batch), dim3(front_threads<LOG2M>() * PPC), smem, st, x, x_stride, nseg, krows,
                       taper, tab, tw, f_lo, L, Lp, E, ready);
     return;
@@ -335,10 +333,10 @@ static void front_go(const Tin* x, int64_t x_stride, int nseg, int krows, int ba
 template <typename Tin, typename T>
 static cudaError_t front_dispatch(int log2m, const Tin* x, int64_t x_stride, int nseg, int krows, int batch,
                                   int taper, const double* tab, const typename C2<T>::t* tw, int f_lo, int L, int Lp,
-                                  typename C2<T>::t* E, int stream_ctas, int* ready, cudaStream_t st) {
+                                  typename C2<T>::t* E, int* ready, cudaStream_t st) {
 #define HOS_FRONT_CASE(LG) \
   case LG:                                                                                                   \
-    front_go<LG, Tin, T>(x, x_stride, nseg, krows, batch, taper, tab, tw, f_lo, L, Lp, E, stream_ctas, ready, st); \
+    front_go<LG, Tin, T>(x, x_stride, nseg, krows, batch, taper, tab, tw, f_lo, L, Lp, E, ready, st); \
     break;
   switch (log2m) {
     HOS_FRONT_CASE(2) HOS_FRONT_CASE(3) HOS_FRONT_CASE(4) HOS_FRONT_CASE(5) HOS_FRONT_CASE(6) HOS_FRONT_CASE(7)
@@ -351,22 +349,22 @@ static cudaError_t front_dispatch(int log2m, const Tin* x, int64_t x_stride, int
 
 cudaError_t launch_front(const void* x, int x_dtype, int64_t x_stride, int m, int nseg, int krows, int batch,
                          int taper, const double* tab, const void* tw, int precision, int f_lo, int L, int Lp, void* E,
-                         cudaStream_t st, int stream_ctas, int* ready) {
+                         cudaStream_t st, int* ready) {
   int log2m = 0;
   while ((1 << log2m) < m) log2m++;
   if ((1 << log2m) != m || m > kFrontMaxM || m < 4) return cudaErrorInvalidValue;
   if (precision == 32) {
     if (x_dtype == 0)
       return front_dispatch<float, float>(log2m, (const float*)x, x_stride, nseg, krows, batch, taper, tab,
-                                          (const float2*)tw, f_lo, L, Lp, (float2*)E, stream_ctas, ready, st);
+                                          (const float2*)tw, f_lo, L, Lp, (float2*)E, ready, st);
     return front_dispatch<double, float>(log2m, (const double*)x, x_stride, nseg, krows, batch, taper, tab,
-                                         (const float2*)tw, f_lo, L, Lp, (float2*)E, stream_ctas, ready, st);
+                                         (const float2*)tw, f_lo, L, Lp, (float2*)E, ready, st);
   }
   if (x_dtype == 0)
     return front_dispatch<float, double>(log2m, (const float*)x, x_stride, nseg, krows, batch, taper, tab,
-                                         (const double2*)tw, f_lo, L, Lp, (double2*)E, stream_ctas, ready, st);
+                                         (const double2*)tw, f_lo, L, Lp, (double2*)E, ready, st);
   return front_dispatch<double, double>(log2m, (const double*)x, x_stride, nseg, krows, batch, taper, tab,
-                                        (const double2*)tw, f_lo, L, Lp, (double2*)E, stream_ctas, ready, st);
+                                        (const double2*)tw, f_lo, L, Lp, (double2*)E, ready, st);
 }
 
 // ===========================================================================

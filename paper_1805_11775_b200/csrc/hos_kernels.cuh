@@ -177,13 +177,12 @@ cudaError_t launch_prep(const void* x, int x_dtype, int64_t x_stride, int m, int
 // compute precision); returns cudaErrorInvalidValue for other m
 constexpr int kFrontMaxM = 4096;
 // x: first segment of series 0 (series b at x + b*x_stride); segment s of series b -> E row b*krows + s
-// stream_ctas > 0: streaming launch (that many persistent CTAs, one per SM, each publishing
-// ready[b*krows + s] = 1 with release semantics once E row s is written); 0: one CTA per pair
-constexpr size_t kFrontStreamSmem = 150 * 1024;
+// ready != nullptr: streaming launch (a PDL dependent of the consuming K2), publishing
+// ready[b*krows + s] = 1 with release semantics once E row s is written
 constexpr int kStreamFrontCtas = 20;  // SMs left to the streaming front end (K2 runs on the rest)
 cudaError_t launch_front(const void* x, int x_dtype, int64_t x_stride, int m, int nseg, int krows, int batch,
                          int taper, const double* taper_tab, const void* tw, int precision, int f_lo, int L, int Lp,
-                         void* E, cudaStream_t st, int stream_ctas = 0, int* ready = nullptr);
+                         void* E, cudaStream_t st, int* ready = nullptr);
 cudaError_t launch_extend_half(const void* H, int m, int hstride, int rows, const void* /*unused*/,
                                int f_lo, int L, int Lp, int precision, void* E, cudaStream_t st);
 cudaError_t launch_extend_full(const void* S, int spec_dtype, int m, int rows, int f_lo, int L, int Lp,
