@@ -82,6 +82,22 @@ def segment_and_demean(series: TimeSeries, cfg: SegmentConfig) -> SegmentSet:
     return SegmentSet(segments=rows, means_removed=True)
 
 
+def save_series(series: TimeSeries, path, fmt: str = "csv") -> None:
+    """Write a series in a format ``load_series`` reads back exactly
+    (hospectra/series.py:146-156): csv = one ``%.17g`` value per line, raw64
+    = little-endian float64."""
+    path = str(path)
+    samples = np.asarray(series.samples, dtype=np.float64)
+    if fmt == "csv":
+        with open(path, "w", encoding="utf-8") as fh:
+            for value in samples:
+                fh.write(f"{value:.17g}\n")
+    elif fmt == "raw64":
+        samples.astype("<f8").tofile(path)
+    else:
+        raise ParameterError(f"unknown format {fmt!r}; expected csv or raw64")
+
+
 def load_series(path, fmt: str = "csv") -> TimeSeries:
     """Read a series file in the reference's interchange formats
     (hospectra/series.py:95-140): ``csv`` = one decimal value per line, blank

@@ -3,6 +3,7 @@ vocabulary, partitioning, interchange format and the multi-GPU shard layout.
 Ports of hospectra tests/test_spectra.py, test_parallel.py, test_series.py."""
 
 import csv
+import json
 
 import numpy as np
 import pytest
@@ -228,3 +229,33 @@ def test_native_shard_layout_matches_python(m, w, k, n):
     assert [tuple(v) for v in rec[:, 10:12]] == [tuple(v) for v in lay.need_cells]
     assert list(rec[:, 12]) + [rec[-1, 13]] == lay.point_bounds
     assert (block, halo, bool(in_next)) == (lay.block, lay.halo, lay.halo_in_next)
+
+
+def test_reference_window_and_report_json():
+    """The harness API mirrors hospectra/bench.py: the window ladder and its
+    n^0.622 curve, and BenchReport's JSON schema (round trip)."""
+    import paper_1805_11775_b200 as P
+
+    assert [P.reference_window(n) for n in (128, 256, 1024, 8192)] == [21, 33, 77, 279]
+    # off-ladder sizes follow round(21 (n/128)^0.622) | 1, clamped to (n-1)//2
+    for n in (100, 300, 3000, 20):
+        w = int(round(21.0 * (n / 128.0) ** 0.622)) | 1
+        assert P.reference_window(n) == max(1, min(w, (n - 1) // 2))
+    r = P.BenchReport(plan="EFFICIENT", order=3, n=256, M=256, K=1, M3=33, P=1, wall_seconds=0.5,
+                      peak_extra_bytes=123, peak_rss_bytes=456, checksum=7.25)
+    text = P.reports_to_json([r, r])
+    assert P.reports_from_json(text) == [r, r]
+    assert set(json.loads(text)[0]) == {"plan", "order", "n", "M", "K", "M3", "P", "wall_seconds",
+                                        "peak_extra_bytes", "peak_rss_bytes", "checksum", "status"}
+
+
+def test_save_series_round_trip(tmp_path):
+    import paper_1805_11775_b200 as P
+
+    x = np.random.default_rng(3).standard_normal(257) * 1e3
+    for fmt in ("csv", "raw64"):
+        path = tmp_path / f"s.{fmt}"
+        P.save_series(P.TimeSeries(x), path, fmt=fmt)
+        assert np.array_equal(P.load_series(path, fmt=fmt).samples, x)
+    with pytest.raises(P.ParameterError):
+        P.save_series(P.TimeSeries(x), tmp_path / "s.bin", fmt="bin")

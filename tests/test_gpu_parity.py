@@ -452,3 +452,18 @@ def test_shifted_band_tilings_vs_oracle(cuda, prec, m, k, w):
     dom, ref = O.estimate(x, 3, m, k, w, True, "hann")
     assert np.array_equal(g.indices, dom)
     assert O.north_star_error(g.values, ref) <= TOL[prec]
+
+
+def test_run_benchmarks_checksums_vs_oracle(cuda):
+    """run_benchmarks (the reference harness API on the GPU path): one QPC
+    series of length n as one segment, checksum = sum |B| of the grid, the
+    same as the oracle's grid for that series."""
+    P = api()
+    reps = P.run_benchmarks([3], [128, 256], ["EFFICIENT"], repeats=2, seed=1234)
+    assert [r.status for r in reps] == ["ok", "ok"]
+    for r in reps:
+        x = P.generate_qpc(0.1, 0.15, r.n, 0.5, 1234).samples
+        dom, ref = O.estimate(x, 3, r.n, 1, r.M3, True, None)
+        assert abs(r.checksum - float(np.abs(ref).sum())) <= 1e-9 * float(np.abs(ref).sum())
+        assert r.wall_seconds > 0 and r.peak_extra_bytes > 0
+    assert P.reports_from_json(P.reports_to_json(reps)) == reps
