@@ -342,7 +342,7 @@ def run_ours(args):
             roof = {"bound": "fp32", "achieved": round(achieved, 3), "peak": round(peak_tf, 3), "unit": "TFLOP/s",
                     "frac": round(achieved / peak_tf, 4), "traffic": load_traffic(args.config),
                     "kernel": ("k_triple_cta" if lib.hos_plan_k2_kind(plan.handle) == 1 else "k_triple_w")
-                              + " (fp32 FFMA2 triple product)", "kernel_ms": round(t_tri, 5),
+                              + (" (fp32 FFMA2 triple product)" if prec == 32 else " (fp64 DFMA triple product; peak below is the FP32 one)"), "kernel_ms": round(t_tri, 5),
                     "kernel_share_of_step": round(t_tri / ms_per_step, 3),
                     "stage_us": {k_: round(statistics.median(v_) * 1e3, 2) for k_, v_ in stages.items()},
                     "stage_timing": f"mean of {STAGE_REPS} launches per stage replayed as one CUDA graph, median of 3",
