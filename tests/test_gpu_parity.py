@@ -467,3 +467,21 @@ def test_run_benchmarks_checksums_vs_oracle(cuda):
         assert abs(r.checksum - float(np.abs(ref).sum())) <= 1e-9 * float(np.abs(ref).sum())
         assert r.wall_seconds > 0 and r.peak_extra_bytes > 0
     assert P.reports_from_json(P.reports_to_json(reps)) == reps
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+@pytest.mark.parametrize("batch,m,k,w", [(3, 128, 20, 5), (37, 256, 9, 7), (160, 128, 6, 3)])
+def test_small_batches_vs_oracle(cuda, prec, batch, m, k, w):
+    """Batches that do not fill the GPU with whole series: the K2 schedule
+    cuts CTA ranges across series, so partial-slot counts differ per series."""
+    import torch
+
+    P = api()
+    rng = np.random.default_rng(batch * 1000 + m + k)
+    x = rng.standard_normal((batch, m * k))
+    cfg = P.EstimationConfig(3, P.SegmentConfig(m=m, k=k), w, precision=prec, taper="hann")
+    vals = P.estimate_batch(torch.from_numpy(x).to(cuda), cfg)
+    rows = range(batch) if batch <= 37 else (0, 1, batch // 2, batch - 1)
+    for s in rows:
+        dom, ref = O.estimate(x[s], 3, m, k, w, True, "hann")
+        assert O.north_star_error(np.asarray(vals[s]), ref) <= TOL[prec], s
