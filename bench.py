@@ -229,7 +229,8 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
-    if world > 1:
+    force_dist = os.environ.get("HOS_BENCH_FORCE_DIST") == "1"  # test hook: the multi-GPU code path on 1 rank
+    if world > 1 or force_dist:
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=dev)
@@ -248,10 +249,25 @@ def run_ours(args):
     out = plan.empty_out()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
-    if world == 1:
+    native = False
+    multi = world > 1 or force_dist
+    if not multi:
         step = lambda: plan.estimate(x, out)
     else:
-        step = lambda: P.distributed_estimate(x, cfg, gather=True)
+        # the library's own NCCL path (collectives issued inside the C-ABI);
+        # the torch.distributed restatement if it cannot be set up
+        try:
+            from paper_1805_11775_b200.parallel import native_distributed_plan
+
+            dplan = native_distributed_plan(cfg)
+            dout = dplan.empty_out()
+            dplan.estimate_distributed(x, dout)
+            torch.cuda.synchronize()
+            step = lambda: dplan.estimate_distributed(x, dout)
+            native = True
+        except Exception as exc:  # noqa: BLE001
+            print(f"[bench] native NCCL path unavailable ({exc}); torch.distributed path", file=sys.stderr)
+            step = lambda: P.distributed_estimate(x, cfg, gather=True)
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -293,7 +309,7 @@ def run_ours(args):
 
     # ---- e2e: host buffers through the C-ABI (hos_estimate_host), wall clock
     e2e_ms = []
-    if world == 1:
+    if not multi:
         xp = torch.from_numpy(x_host).pin_memory()
         cd = torch.complex64 if prec == 32 else torch.complex128
         op = torch.empty(out.shape, dtype=cd).pin_memory()
@@ -319,7 +335,7 @@ def run_ours(args):
             dist.barrier()
             t0 = time.perf_counter()
             xd = xp.to(dev, non_blocking=True)
-            vals = P.distributed_estimate(xd, cfg, gather=True)
+            vals = dplan.estimate_distributed(xd, dout) if native else P.distributed_estimate(xd, cfg, gather=True)
             if rank == 0:
                 vals.cpu()
             torch.cuda.synchronize()
@@ -358,7 +374,8 @@ def run_ours(args):
                        "L": c.m3 // 2, "taper": c.taper, "batch": batch, "precision": args.precision,
                        "units_per_step": units, "points_per_step": plan.npoints * batch,
                        "l2": "flushed: 256 MiB device write between timed steps (outside the events)",
-                       "parallelism": f"segments sharded over {world} GPUs (NCCL reduce-scatter + halo)"
+                       "parallelism": f"segments sharded over {world} GPUs (NCCL reduce-scatter + halo"
+                                      + (" inside the C-ABI)" if native else ", torch.distributed)")
                        if world > 1 else "1 GPU"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                     "ms_per_step": statistics.median(e2e_ms),

@@ -1679,11 +1679,27 @@ int hos_comm_attach(hos_plan* p, void* nccl_comm, int rank, int nranks) {
   return HOS_OK;
 }
 
+int estimate_distributed_body(hos_plan* p, const void* x_dev, int x_dtype, void* out_dev, void* stream);
+
 int hos_estimate_distributed(hos_plan* p, const void* x_dev, int x_dtype, void* out_dev, void* stream) {
   int rc = check_plan(p);
   if (rc) return rc;
   if (!p->comm) return fail(HOS_EPARAM, "no communicator attached (hos_comm_attach)");
   if (!x_dev || !out_dev) return fail(HOS_EPARAM, "null buffer");
+  if ((rc = check_dtype_x(x_dtype))) return rc;
+  // the ~20 small copies, kernels and NCCL collectives of a step replay as one
+  // CUDA graph per buffer binding (NCCL operations are capturable)
+  const char* env = std::getenv("HOS_DIST_GRAPH");
+  if (p->use_graphs && !p->timing && !(env && env[0] == '0')) {
+    const hos_plan::GraphKey key{4, x_dev, x_dtype, 0, out_dev};
+    return run_graph(p, key, (cudaStream_t)stream,
+                     [&](cudaStream_t s) { return estimate_distributed_body(p, x_dev, x_dtype, out_dev, s); });
+  }
+  return estimate_distributed_body(p, x_dev, x_dtype, out_dev, stream);
+}
+
+int estimate_distributed_body(hos_plan* p, const void* x_dev, int x_dtype, void* out_dev, void* stream) {
+  int rc = HOS_OK;
   const NcclApi* api = nccl_api(nullptr);
   cudaStream_t st = (cudaStream_t)stream;
   ncclComm_t comm = (ncclComm_t)p->comm;

@@ -214,6 +214,52 @@ def distributed_estimate(x, cfg: EstimationConfig, *, group=None, engine=None, g
     return out
 
 
+_NATIVE = {}
+
+
+def native_distributed_plan(cfg: EstimationConfig, group=None):
+    """The library's own multi-GPU path (hos_comm_attach + hos_estimate_
+    distributed: NCCL reduce-scatter / all-gather issued inside the C-ABI, no
+    per-step Python collectives): a plan of ``cfg`` on the current device with
+    a dedicated NCCL communicator over the ranks of ``group``, built once per
+    (cfg, device, group).  The communicator's unique id travels over
+    ``torch.distributed`` (broadcast from rank 0).  Use ``plan.estimate_
+    distributed(x)`` with the full series on every rank."""
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    from ._native import get_plan
+
+    dev = torch.cuda.current_device()
+    key = (cfg.order, cfg.segment.m, cfg.segment.k, cfg.m3, cfg.conjugate_last, cfg.bits, cfg.taper, dev, id(group))
+    if key in _NATIVE:
+        return _NATIVE[key][0]
+    nccl = ctypes.CDLL("libnccl.so.2")
+
+    class UniqueId(ctypes.Structure):
+        _fields_ = [("internal", ctypes.c_byte * 128)]
+
+    rank, nranks = dist.get_rank(group), dist.get_world_size(group)
+    uid = UniqueId()
+    buf = torch.zeros(128, dtype=torch.uint8, device="cuda")
+    if rank == 0:
+        if nccl.ncclGetUniqueId(ctypes.byref(uid)) != 0:
+            raise RuntimeError("ncclGetUniqueId failed")
+        buf.copy_(torch.frombuffer(bytearray(bytes(uid.internal)), dtype=torch.uint8))
+    dist.broadcast(buf, 0, group=group)
+    ctypes.memmove(ctypes.byref(uid), bytes(buf.cpu().numpy().tobytes()), 128)
+    comm = ctypes.c_void_p()
+    rc = nccl.ncclCommInitRank(ctypes.byref(comm), nranks, uid, rank)
+    if rc != 0:
+        raise RuntimeError(f"ncclCommInitRank failed ({rc})")
+    plan = get_plan(cfg.order, cfg.segment.m, cfg.segment.k, cfg.m3, cfg.conjugate_last, cfg.bits, cfg.taper, 1, dev)
+    plan.comm_attach(comm.value, rank, nranks)
+    _NATIVE[key] = (plan, nccl, comm)
+    return plan
+
+
 def _reduce_scatter(dist, engine, out, inp, group):
     # complex -> real view (NCCL/gloo reduce real dtypes)
     o, i = engine.as_real(out), engine.as_real(inp)
