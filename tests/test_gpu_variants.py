@@ -56,3 +56,38 @@ def test_variant_parity(cuda, env):
     r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env={**os.environ, k: v}, capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0 and "VARIANT-OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
+NATIVE_CHILD = r"""
+import os, sys
+sys.path.insert(0, {root!r})
+sys.path.insert(0, {tests!r})
+import numpy as np, torch, torch.distributed as dist
+os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+os.environ.setdefault("MASTER_PORT", "29561")
+torch.cuda.set_device(0)
+dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+import paper_1805_11775_b200 as P
+from paper_1805_11775_b200.parallel import native_distributed_plan
+from conftest import north_star
+c = P.baseline_config("cfg2")
+x = torch.from_numpy(P.baseline_series(c)).cuda()
+for prec in ("fp32", "fp64"):
+    cfg = P.EstimationConfig(3, P.SegmentConfig(m=c.m, k=c.k), c.m3, precision=prec, taper="hann")
+    plan = native_distributed_plan(cfg)
+    ref = P.estimate_spectrum(x, cfg).values
+    for _ in range(3):  # capture, then replays
+        got = plan.estimate_distributed(x).cpu().numpy()
+        assert north_star(got, ref) <= (1e-6 if prec == "fp32" else 1e-13), prec
+dist.destroy_process_group()
+print("NATIVE-OK")
+"""
+
+
+def test_native_distributed_plan_one_rank(cuda):
+    """parallel.native_distributed_plan (dedicated NCCL communicator, the
+    library's in-C-ABI collectives, graph replay) on a one-rank process group
+    agrees with the single-GPU estimate."""
+    code = NATIVE_CHILD.format(root=ROOT, tests=os.path.join(ROOT, "tests"))
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "NATIVE-OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
