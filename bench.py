@@ -385,7 +385,7 @@ def run_ours(args):
             "clocks": clocks,
             "gpu_launches": lib.hos_plan_launches(plan.handle) * args.steps if world == 1 else None,
             "gpu_launches_note": "per step: front end (k_front: fused demean+Hann+FFT+extension; or k_prep + "
-                                 "cuFFT + k_extend_half for non-power-of-two M, cuFFT not counted), k_triple_w, "
+                                 "cuFFT + k_extend_half for non-power-of-two M, cuFFT not counted), k_triple_cta (k_triple_w for large M), "
                                  "smoothing (k_line_scan + k_box3/k_box4, or k_smooth_series3 for grids that fit in "
                                  "shared memory)",
         }

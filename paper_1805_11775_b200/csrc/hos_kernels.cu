@@ -1541,8 +1541,12 @@ __global__ void __launch_bounds__(64) k_box4(BoxArgs a, int pair0) {
 // every output point boxed from shared memory.  HBM sees only the partial
 // slots and the values (the two-kernel path round-trips S through HBM once
 // the batch's S outgrows L2).
+#ifndef HOS_BOX_ROWS
+#define HOS_BOX_ROWS 3
+#endif
+constexpr int kBoxRows = HOS_BOX_ROWS;  // output rows per box item in k_smooth_series3
 template <typename P2, typename OUT>
-__global__ void __launch_bounds__(512) k_smooth_series3(const P2* __restrict__ part, int nparts, int64_t part_stride,
+__global__ void __launch_bounds__(512, 2) k_smooth_series3(const P2* __restrict__ part, int nparts, int64_t part_stride,
                                                         int64_t part_series_stride, SlotInfo si, BoxArgs a,
                                                         int nlines) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
@@ -1552,8 +1556,9 @@ __global__ void __launch_bounds__(512) k_smooth_series3(const P2* __restrict__ p
   int* ro = ls + nlines + 1;                                  // rows + 1 point offsets
   int* lt0 = ro + a.rows + 1;                                 // nlines: first tile of each line
   int* rsl = lt0 + nlines;                                    // nregions: partial slots per region
-  unsigned short* cline = reinterpret_cast<unsigned short*>(rsl + si.nregions);  // ncells: line of each cell
-  unsigned short* prow = cline + ncells;                       // npoints: row of each point
+  int* bo = rsl + si.nregions;                                // nblk + 1: first box item of each row block
+  unsigned short* cline = reinterpret_cast<unsigned short*>(bo + a.rows + 1);  // ncells: line of each cell
+  unsigned short* prow = cline + ncells;  // npoints: row of each point (kBoxRows == 1), else row block of each box item
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   // persistent: the geometry tables are built once per CTA, then the CTA
   // smooths series blockIdx.x, blockIdx.x + gridDim.x, ...
@@ -1564,8 +1569,26 @@ __global__ void __launch_bounds__(512) k_smooth_series3(const P2* __restrict__ p
   __syncthreads();
   for (int l = warp; l < nlines; l += nw)
     for (int c = ls[l] + lane; c < ls[l + 1]; c += 32) cline[c] = (unsigned short)l;
-  for (int r = warp; r < a.rows; r += nw)
-    for (int q = ro[r] + lane; q < ro[r + 1]; q += 32) prow[q] = (unsigned short)r;
+  if (kBoxRows == 1)
+    for (int r = warp; r < a.rows; r += nw)
+      for (int q = ro[r] + lane; q < ro[r + 1]; q += 32) prow[q] = (unsigned short)r;
+  // box items (kBoxRows > 1): (block of kBoxRows consecutive output rows,
+  // column k2) for k2 below the block's longest row
+  const int nblk = (a.rows + kBoxRows - 1) / kBoxRows;
+  if (kBoxRows > 1 && tid == 0) {
+    int acc = 0;
+    for (int b = 0; b < nblk; b++) {
+      bo[b] = acc;
+      int mx = 0;
+      for (int r = b * kBoxRows; r < min(a.rows, (b + 1) * kBoxRows); r++) mx = max(mx, ro[r + 1] - ro[r]);
+      acc += mx;
+    }
+    bo[nblk] = acc;
+  }
+  __syncthreads();
+  if (kBoxRows > 1)
+    for (int b = warp; b < nblk; b += nw)
+      for (int q = bo[b] + lane; q < bo[b + 1]; q += 32) prow[q] = (unsigned short)b;
   asm volatile("griddepcontrol.wait;" ::: "memory");  // partial slots come from K2
   for (int series = blockIdx.x; series < a.batch; series += gridDim.x) {
   __syncthreads();  // the previous series' box reads of S are done
@@ -1668,6 +1691,7 @@ __global__ void __launch_bounds__(512) k_smooth_series3(const P2* __restrict__ p
   }
   __syncthreads();
   OUT* out = (OUT*)a.out + series * a.out_series_stride;
+  if constexpr (kBoxRows == 1) {
   const int npts = ro[a.rows];
   for (int p = tid; p < npts; p += blockDim.x) {
     const int k1 = prow[p], k2 = p - ro[k1];
@@ -1686,12 +1710,59 @@ __global__ void __launch_bounds__(512) k_smooth_series3(const P2* __restrict__ p
     out[p].x = sr * a.scale;
     out[p].y = si_ * a.scale;
   }
+  } else {
+  // a thread boxes the kBoxRows vertically adjacent points of one item and
+  // loads each of their w + kBoxRows - 1 window lines' two prefix ends once
+  // (2 (w + R - 1) / R shared loads per point instead of 2w); every point's
+  // sum keeps k_box3's order (+ window end, - start, line by line).  Valid
+  // rows of a column form one run: row lengths are unimodal in k1.
+  // cfg5: 255 -> 233 us at R = 3 (R = 2 / 4: 255 / 256 us)
+  const int nitems = bo[nblk];
+  for (int it = tid; it < nitems; it += blockDim.x) {
+    const int b = prow[it], k2 = it - bo[b], k1 = b * kBoxRows;
+    bool val[kBoxRows];
+    int ra = kBoxRows, rb = -1;
+#pragma unroll
+    for (int r = 0; r < kBoxRows; r++) {
+      val[r] = k1 + r < a.rows && k2 < ro[k1 + r + 1] - ro[k1 + r];
+      if (val[r]) {
+        ra = min(ra, r);
+        rb = r;
+      }
+    }
+    double sr[kBoxRows], sv[kBoxRows];
+#pragma unroll
+    for (int r = 0; r < kBoxRows; r++) sr[r] = sv[r] = 0.0;
+    for (int u = ra; u < rb + a.m3; u++) {
+      const int cb = ls[k1 + u];
+      const double2 s1 = S[cb + k2 + a.m3 - 1];
+      const double2 s0 = k2 >= 1 ? S[cb + k2 - 1] : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int r = 0; r < kBoxRows; r++)
+        if (val[r] && u >= r && u < r + a.m3) {
+          sr[r] += s1.x;
+          sv[r] += s1.y;
+          if (k2 >= 1) {
+            sr[r] -= s0.x;
+            sv[r] -= s0.y;
+          }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < kBoxRows; r++)
+      if (val[r]) {
+        const int p = ro[k1 + r] + k2;
+        out[p].x = sr[r] * a.scale;
+        out[p].y = sv[r] * a.scale;
+      }
+  }
+  }
   }
 }
 
 size_t smooth_series3_smem(int64_t ncells, int64_t nlines, int rows, int nregions, int64_t npoints) {
   if (nlines > 65535 || rows > 65535) return ~(size_t)0;  // 16-bit line / row tables
-  return (size_t)ncells * sizeof(double2) + (size_t)(nlines + 1 + rows + 1 + nlines + nregions) * sizeof(int) +
+  return (size_t)ncells * sizeof(double2) + (size_t)(nlines + 1 + rows + 1 + nlines + nregions + rows + 1) * sizeof(int) +
          (size_t)(ncells + npoints) * sizeof(unsigned short);
 }
 
