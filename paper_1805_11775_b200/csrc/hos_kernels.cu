@@ -131,8 +131,12 @@ __host__ __device__ constexpr int front_pairs() {
   return front_threads<LOG2M>() == 32 ? 4 : 1;
 }
 
+#ifndef HOS_FRONT_MINB
+#define HOS_FRONT_MINB 6  // one-warp transforms: 6 CTAs/SM (64 regs; cfg5 front 273 -> 240 us, 8: 267)
+#endif
 template <typename Tin, typename T, int LOG2M>
-__global__ void __launch_bounds__(front_threads<LOG2M>() * front_pairs<LOG2M>()) k_front(const Tin* __restrict__ x, int64_t x_stride,
+__global__ void __launch_bounds__(front_threads<LOG2M>() * front_pairs<LOG2M>(),
+                                  front_pairs<LOG2M>() > 1 ? HOS_FRONT_MINB : 1) k_front(const Tin* __restrict__ x, int64_t x_stride,
                                                                   int nseg, int krows, int taper,
                                                                   const double* __restrict__ tab,
                                                                   const typename C2<T>::t* __restrict__ tw, int f_lo,
@@ -157,9 +161,9 @@ __global__ void __launch_bounds__(front_threads<LOG2M>() * front_pairs<LOG2M>())
     else __syncthreads();
   };
   // two real segments per thread group, packed as one complex sequence z = x_a + i x_b.
-  // A group takes pairs pi, pi + gridDim.x*PPC, ... (the launches size the
-  // grid to one pair per group; a smaller, persistent grid would load the
-  // next pair's samples while transforming the current one).
+  // A group takes pairs pi, pi + gridDim.x*PPC, ... (the launches cap the
+  // grid at HOS_FRONT_PERSIST CTAs per SM, so with many pairs a group loads
+  // its next pair's samples while transforming the current one).
   const int b = blockIdx.y;
   const int pstride = gridDim.x * PPC;
   int pi = blockIdx.x * PPC + grp;
@@ -320,7 +324,19 @@ static void front_go(const Tin* x, int64_t x_stride, int nseg, int krows, int ba
   }
   constexpr int PPC = front_pairs<LOG2M>();
   const int pairs = (nseg + 1) / 2;
-  const int grid = (pairs + PPC - 1) / PPC;
+  int grid = (pairs + PPC - 1) / PPC;
+#ifndef HOS_FRONT_PERSIST
+#define HOS_FRONT_PERSIST 12  // CTAs per SM before the groups turn persistent (cfg5 front 240 -> 230 us)
+#endif
+  {  // persistent groups: each loads its next pair's samples during the current transform
+    static int sms = 0;
+    if (!sms) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    grid = std::min(grid, std::max(1, sms * HOS_FRONT_PERSIST / std::max(1, batch)));
+  }
   if (ready) {
     launch_pdl_kernel(kern, dim3(grid, batch), dim3(front_threads<LOG2M>() * PPC), smem, st, x, x_stride, nseg, krows,
                       taper, tab, tw, f_lo, L, Lp, E, ready);
