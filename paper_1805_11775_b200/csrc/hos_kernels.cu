@@ -132,7 +132,7 @@ __host__ __device__ constexpr int front_pairs() {
 }
 
 #ifndef HOS_FRONT_MINB
-#define HOS_FRONT_MINB 6  // one-warp transforms: 6 CTAs/SM (64 regs; cfg5 front 273 -> 240 us, 8: 267)
+#define HOS_FRONT_MINB 5  // one-warp transforms: 5 CTAs/SM, <= 102 regs (cfg5 front with persistent groups: 3 / 4 / 5 / 6 / 7 -> 232 / 217 / 214 / 230 / 239 us)
 #endif
 template <typename Tin, typename T, int LOG2M>
 __global__ void __launch_bounds__(front_threads<LOG2M>() * front_pairs<LOG2M>(),
@@ -326,7 +326,7 @@ static void front_go(const Tin* x, int64_t x_stride, int nseg, int krows, int ba
   const int pairs = (nseg + 1) / 2;
   int grid = (pairs + PPC - 1) / PPC;
 #ifndef HOS_FRONT_PERSIST
-#define HOS_FRONT_PERSIST 12  // CTAs per SM before the groups turn persistent (cfg5 front 240 -> 230 us)
+#define HOS_FRONT_PERSIST 12  // CTAs per SM before the groups turn persistent (cfg5 front 273 -> 214 us with MINB 5)
 #endif
   {  // persistent groups: each loads its next pair's samples during the current transform
     static int sms = 0;
