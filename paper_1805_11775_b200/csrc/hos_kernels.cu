@@ -113,10 +113,10 @@ struct C2<double> {
   using t = double2;
 };
 
-// threads of the fused front end for m = 2^LOG2M: m/8 (8 samples, two radix-4
+// threads of the fused front end for m = 2^LOG2M: m/HOS_FRONT_SPT (16 samples, four radix-4
 // butterflies per stage each), clamped to [32, 256]
 #ifndef HOS_FRONT_SPT
-#define HOS_FRONT_SPT 8  // samples per thread and segment
+#define HOS_FRONT_SPT 16  // samples per thread and segment (cfg2 front 6.8 -> 5.7 us vs 8; 32 spills)
 #endif
 template <int LOG2M>
 __host__ __device__ constexpr int front_threads() {
