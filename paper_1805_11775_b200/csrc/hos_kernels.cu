@@ -1301,8 +1301,14 @@ cudaError_t launch_triple_cta(const CtaTripleArgs& a, int precision, cudaStream_
 // pieces.  The per-line anchoring keeps the fp64 sums exact to ~1e-16
 // relative (a global fp32 summed-area table would fail 1e-5).
 
-constexpr int kScanThreads = 256;
-constexpr int kWarpScanMaxLine = 96;  // lines up to this many cells: one warp per line
+#ifndef HOS_SCAN_THREADS
+#define HOS_SCAN_THREADS 256
+#endif
+#ifndef HOS_WARP_SCAN_MAX
+#define HOS_WARP_SCAN_MAX 96
+#endif
+constexpr int kScanThreads = HOS_SCAN_THREADS;
+constexpr int kWarpScanMaxLine = HOS_WARP_SCAN_MAX;  // lines up to this many cells: one warp per line
 
 // number of partial slots holding cell `idx` (absolute cell of line l)
 __device__ __forceinline__ int cell_slots(const SlotInfo& si, int nparts, int64_t l, int64_t col, int series) {
@@ -1477,8 +1483,12 @@ __global__ void __launch_bounds__(256, 4) k_box3_flat(BoxArgs a) {
 #ifndef HOS_BOX_MINB
 #define HOS_BOX_MINB 1
 #endif
+#ifndef HOS_BOX_THREADS
+#define HOS_BOX_THREADS 128
+#endif
+constexpr int kBoxThreads = HOS_BOX_THREADS;
 template <typename OUT>
-__global__ void __launch_bounds__(128, HOS_BOX_MINB) k_box3(BoxArgs a, int row0) {
+__global__ void __launch_bounds__(kBoxThreads, HOS_BOX_MINB) k_box3(BoxArgs a, int row0) {
   asm volatile("griddepcontrol.wait;" ::: "memory");  // prefix sums come from K4a
   const int k1 = row0 + blockIdx.y;
   const int k2 = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1818,9 +1828,9 @@ cudaError_t launch_box(const BoxArgs& a, cudaStream_t st) {
       return a.precision == 32 ? launch_pdl_kernel(k_box3_flat<float2>, g, dim3(256), sm, st, a)
                                : launch_pdl_kernel(k_box3_flat<double2>, g, dim3(256), sm, st, a);
     }
-    dim3 grid((mx + 127) / 128, a.row_end - a.row_begin, a.batch);
-    return a.precision == 32 ? launch_pdl_kernel(k_box3<float2>, grid, dim3(128), 0, st, a, a.row_begin)
-                             : launch_pdl_kernel(k_box3<double2>, grid, dim3(128), 0, st, a, a.row_begin);
+    dim3 grid((mx + kBoxThreads - 1) / kBoxThreads, a.row_end - a.row_begin, a.batch);
+    return a.precision == 32 ? launch_pdl_kernel(k_box3<float2>, grid, dim3(kBoxThreads), 0, st, a, a.row_begin)
+                             : launch_pdl_kernel(k_box3<double2>, grid, dim3(kBoxThreads), 0, st, a, a.row_begin);
   } else {
     if (a.pair_end <= a.pair_begin) return cudaSuccess;
     dim3 grid(a.pair_end - a.pair_begin, a.batch);
