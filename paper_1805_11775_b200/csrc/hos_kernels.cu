@@ -1529,9 +1529,9 @@ __device__ __forceinline__ void box3_point(const BoxArgs& a, const double2* __re
   out[p - a.p_begin].y = si * a.scale;
 }
 
+constexpr int kBox4Lines = 64;  // k_box4: windows of up to 8 x 8 pair lines stage their line starts
 template <typename OUT>
 __global__ void __launch_bounds__(64) k_box4(BoxArgs a, int pair0) {
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // prefix sums come from K4a
   const int pair = pair0 + blockIdx.x;
   const int series = blockIdx.y;
   const int k1 = __ldg(a.pair_k1 + pair), k2 = __ldg(a.pair_k2 + pair);
@@ -1539,6 +1539,39 @@ __global__ void __launch_bounds__(64) k_box4(BoxArgs a, int pair0) {
   const int n3 = p4_len(a.m, k1, k2);
   const double2* S = (const double2*)a.S + series * a.s_series_stride;
   OUT* out = (OUT*)a.out + series * a.out_series_stride;
+  const int w = a.hi - a.lo + 1, nw2 = w * w;
+  if (nw2 <= kBox4Lines) {
+    // the w x w window's pair-line starts are the same for every k3 of the
+    // pair and static geometry: staged in shared memory before the PDL wait
+    // (two dependent table loads per window line were on every point's path)
+    __shared__ int64_t cbs[kBox4Lines];
+    for (int i = threadIdx.x; i < nw2; i += blockDim.x) {
+      const int u = i / w, v = i - u * w;
+      const int line = __ldg(a.line_of_ab + (int64_t)(k1 + u) * a.b_count + (k2 + v));
+      cbs[i] = __ldg(a.line_start + line) - a.cell_base;
+    }
+    __syncthreads();
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // prefix sums come from K4a
+    for (int k3 = threadIdx.x; k3 < n3; k3 += blockDim.x) {
+      double sr = 0.0, si = 0.0;  // same order as below: u-major, v-minor
+#pragma unroll 5
+      for (int i = 0; i < nw2; i++) {
+        const int64_t cb = cbs[i];
+        const double2 s1 = S[cb + k3 + a.m3 - 1];
+        sr += s1.x;
+        si += s1.y;
+        if (k3 >= 1) {
+          const double2 s0 = S[cb + k3 - 1];
+          sr -= s0.x;
+          si -= s0.y;
+        }
+      }
+      out[base + k3 - a.p_begin].x = sr * a.scale;
+      out[base + k3 - a.p_begin].y = si * a.scale;
+    }
+    return;
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // prefix sums come from K4a
   for (int k3 = threadIdx.x; k3 < n3; k3 += blockDim.x) {
     double sr = 0.0, si = 0.0;
     for (int u = a.lo; u <= a.hi; u++) {
