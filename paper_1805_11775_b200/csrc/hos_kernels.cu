@@ -1530,8 +1530,12 @@ __device__ __forceinline__ void box3_point(const BoxArgs& a, const double2* __re
 }
 
 constexpr int kBox4Lines = 64;  // k_box4: windows of up to 8 x 8 pair lines stage their line starts
+#ifndef HOS_BOX4_THREADS
+#define HOS_BOX4_THREADS 32  // one warp per pair (cfg4 box 10.4 -> 6.5 us; 128: 12.3)
+#endif
+constexpr int kBox4Threads = HOS_BOX4_THREADS;
 template <typename OUT>
-__global__ void __launch_bounds__(64) k_box4(BoxArgs a, int pair0) {
+__global__ void __launch_bounds__(kBox4Threads) k_box4(BoxArgs a, int pair0) {
   const int pair = pair0 + blockIdx.x;
   const int series = blockIdx.y;
   const int k1 = __ldg(a.pair_k1 + pair), k2 = __ldg(a.pair_k2 + pair);
@@ -1867,8 +1871,8 @@ cudaError_t launch_box(const BoxArgs& a, cudaStream_t st) {
   } else {
     if (a.pair_end <= a.pair_begin) return cudaSuccess;
     dim3 grid(a.pair_end - a.pair_begin, a.batch);
-    return a.precision == 32 ? launch_pdl_kernel(k_box4<float2>, grid, dim3(64), 0, st, a, a.pair_begin)
-                             : launch_pdl_kernel(k_box4<double2>, grid, dim3(64), 0, st, a, a.pair_begin);
+    return a.precision == 32 ? launch_pdl_kernel(k_box4<float2>, grid, dim3(kBox4Threads), 0, st, a, a.pair_begin)
+                             : launch_pdl_kernel(k_box4<double2>, grid, dim3(kBox4Threads), 0, st, a, a.pair_begin);
   }
   return cudaGetLastError();
 }
