@@ -114,14 +114,21 @@ struct C2<double> {
 };
 
 // threads of the fused front end for m = 2^LOG2M: m/HOS_FRONT_SPT (16 samples, four radix-4
-// butterflies per stage each), clamped to [32, 256]
+// butterflies per stage each; HOS_FRONT_SPT_L samples for m >= 4096), clamped to [32, HOS_FRONT_MAXT]
 #ifndef HOS_FRONT_SPT
 #define HOS_FRONT_SPT 16  // samples per thread and segment (cfg2 front 6.8 -> 5.7 us vs 8; 32 spills)
 #endif
+#ifndef HOS_FRONT_SPT_L
+#define HOS_FRONT_SPT_L 8  // samples per thread for m >= 4096 (cfg3 front 45.7 -> 44.4 us; 4: 51.6)
+#endif
+#ifndef HOS_FRONT_MAXT
+#define HOS_FRONT_MAXT 512
+#endif
 template <int LOG2M>
 __host__ __device__ constexpr int front_threads() {
-  return (1 << LOG2M) / HOS_FRONT_SPT >= 256 ? 256
-                                             : ((1 << LOG2M) / HOS_FRONT_SPT >= 32 ? (1 << LOG2M) / HOS_FRONT_SPT : 32);
+  constexpr int spt = LOG2M >= 12 ? HOS_FRONT_SPT_L : HOS_FRONT_SPT;
+  return (1 << LOG2M) / spt >= HOS_FRONT_MAXT ? HOS_FRONT_MAXT
+                                              : ((1 << LOG2M) / spt >= 32 ? (1 << LOG2M) / spt : 32);
 }
 // segment pairs per CTA: one-warp transforms (m <= 256) run four per CTA,
 // each warp on its own pair with warp-level barriers (a CTA per pair made the
