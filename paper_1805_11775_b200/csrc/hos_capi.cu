@@ -418,7 +418,10 @@ bool build_cta_schedule(const hos_plan* p, CtaSchedule& cs, int interleave_ctas 
     // 3 slots: a deeper ring lets the warp the scheduler favours run further
     // ahead of its sub-partition partner, which then runs alone (cfg2 K2:
     // depth 3 33.6 us, 4 33.8, 5 34.4, 6 35.3; 2 cannot hide the copies)
-    int64_t depth = std::min<int64_t>(3, (int64_t)hos::kCtaMaxSmem / slot);
+    // order 4 (short rows, 8 x 16 tiles): 5 slots (cfg4 K2 3 / 4 / 5 / 6:
+    // 72.3 / 70.3 / 69.6 / 69.4 us; cfg5, order 3 at the same M, is flat)
+    int64_t depth = std::min<int64_t>({(int64_t)(p->order == 4 ? 5 : 3), (int64_t)hos::kCtaMaxDepth,
+                                       (int64_t)hos::kCtaMaxSmem / slot});
     if (const char* env = std::getenv("HOS_CTA_DEPTH"))  // diagnostics
       depth = std::max<int64_t>(2, std::min<int64_t>({(int64_t)hos::kCtaMaxDepth, (int64_t)hos::kCtaMaxSmem / slot,
                                                        (int64_t)std::atoi(env)}));
