@@ -133,11 +133,32 @@ struct hos_plan {
   // stage events: 0 start | 1 prep | 2 fft | 3 extend | 4 triple | 5 scan | 6 box
   cudaEvent_t ev[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   bool timed = false;
+  // one caller at a time per plan: graph cache, capture stream and scratch
+  // buffers are shared (recursive: entry points call each other)
+  std::recursive_mutex mu;
+  // streaming host path: host-mapped error word K2 sets when a ready-flag wait timed out
+  int* h_err = nullptr;
+  int* d_err = nullptr;
 };
 
 namespace {
 
 size_t csize(int precision) { return precision == 32 ? 8 : 16; }
+
+// Serialises callers of one plan and runs the call on the plan's device
+// (restoring the caller's current device afterwards), so a plan built for
+// cuda:1 works whatever device the calling thread has selected.
+struct PlanGuard {
+  std::lock_guard<std::recursive_mutex> lock;
+  int prev = -1, dev;
+  explicit PlanGuard(hos_plan* p) : lock(p->mu), dev(p->device) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~PlanGuard() {
+    if (prev >= 0 && prev != dev) cudaSetDevice(prev);
+  }
+};
 size_t rsize(int precision) { return precision == 32 ? 4 : 8; }
 
 template <typename T>
@@ -374,6 +395,7 @@ hos::CtaTripleArgs cta_args(const hos_plan* p, bool streaming = false) {
     a.cta_stage0 = p->d_s_cta_stage0;
     a.nctas = p->s_nctas;
     a.ready = p->d_ready;
+    a.err = p->d_err;
   }
   return a;
 }
@@ -962,6 +984,10 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
     if ((rc = upload(p, &p->d_s_stages, ssched.stages))) return bail(rc);
     if ((rc = upload(p, &p->d_s_cta_stage0, ssched.cta_stage0))) return bail(rc);
     if ((rc = alloc(p, (void**)&p->d_ready, (size_t)k * sizeof(int)))) return bail(rc);
+    if (cudaHostAlloc((void**)&p->h_err, sizeof(int), cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer((void**)&p->d_err, p->h_err, 0) != cudaSuccess)
+      return bail(fail(HOS_ECUDA, "cannot map the streaming path's error word"));
+    *p->h_err = 0;
     if (cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&p->e_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&p->e_join, cudaEventDisableTiming) != cudaSuccess)
@@ -1047,6 +1073,7 @@ void hos_plan_destroy(hos_plan* p) {
   for (void* b : {(void*)p->d_s_blocks, (void*)p->d_s_stages, (void*)p->d_s_cta_stage0, (void*)p->d_s_region_slots,
                   (void*)p->d_ready})
     if (b) cudaFree(b);
+  if (p->h_err) cudaFreeHost(p->h_err);
   for (void* b : {p->d_raw, p->d_send, p->d_mine, p->d_local, p->d_heads, p->d_vals, p->d_parts})
     if (b) cudaFree(b);
   void* bufs[] = {p->d_groups, p->d_blocks, p->d_stages, p->d_cta_stage0, p->d_tiles, p->d_line_tile0, p->d_region_slots, p->d_line_cmax, p->d_line_start, p->d_row_off, p->d_pair_k1, p->d_pair_k2,
@@ -1082,6 +1109,7 @@ int hos_plan_line_starts(const hos_plan* p, int64_t* ls) {
 int hos_estimate(hos_plan* p, const void* x_dev, int x_dtype, int64_t x_stride, void* out_dev, void* stream) {
   int rc = check_plan(p);
   if (rc) return rc;
+  PlanGuard guard_(p);
   if ((rc = check_dtype_x(x_dtype))) return rc;
   if (!x_dev || !out_dev) return fail(HOS_EPARAM, "null buffer");
   if (p->batch > 1 && x_stride < (int64_t)p->k * p->m)
@@ -1103,6 +1131,7 @@ int hos_estimate(hos_plan* p, const void* x_dev, int x_dtype, int64_t x_stride, 
 int hos_estimate_from_spectra(hos_plan* p, const void* spec_dev, int spec_dtype, void* out_dev, void* stream) {
   int rc = check_plan(p);
   if (rc) return rc;
+  PlanGuard guard_(p);
   if (spec_dtype != HOS_C64 && spec_dtype != HOS_C128)
     return fail(HOS_EPARAM, "spectra dtype must be HOS_C64 or HOS_C128");
   if (!spec_dev || !out_dev) return fail(HOS_EPARAM, "null buffer");
@@ -1123,6 +1152,7 @@ int hos_estimate_from_spectra(hos_plan* p, const void* spec_dev, int spec_dtype,
 int hos_segment_spectra(hos_plan* p, const void* x_dev, int x_dtype, int64_t x_stride, void* spec_dev, void* stream) {
   int rc = check_plan(p);
   if (rc) return rc;
+  PlanGuard guard_(p);
   if ((rc = check_dtype_x(x_dtype))) return rc;
   if (!x_dev || !spec_dev) return fail(HOS_EPARAM, "null buffer");
   cudaStream_t st = (cudaStream_t)stream;
@@ -1179,6 +1209,7 @@ int hos_dft_rows(const void* x_dev, int x_dtype, int rows, int m, int precision,
 int hos_estimate_host(hos_plan* p, const void* x_host, int x_dtype, int64_t x_stride, void* out_host, void* stream) {
   int rc = check_plan(p);
   if (rc) return rc;
+  PlanGuard guard_(p);
   if ((rc = check_dtype_x(x_dtype))) return rc;
   if (!x_host || !out_host) return fail(HOS_EPARAM, "null buffer");
   // synchronous host API: NULL stream = the plan's private stream
@@ -1252,6 +1283,11 @@ int hos_estimate_host(hos_plan* p, const void* x_host, int x_dtype, int64_t x_st
     }
     CUDA_TRY(q);
   }
+  if (p->h_err && *reinterpret_cast<volatile int*>(p->h_err)) {
+    *p->h_err = 0;
+    return fail(HOS_ECUDA, "streaming host path: the triple product waited > 200 ms for a spectrum row "
+                           "(the front end found no free SM); unset HOS_STREAM");
+  }
   return HOS_OK;
 }
 
@@ -1259,6 +1295,7 @@ int hos_partial_raw(hos_plan* p, const void* x_dev, int x_dtype, int seg_begin, 
                     void* stream) {
   int rc = check_plan(p);
   if (rc) return rc;
+  PlanGuard guard_(p);
   if ((rc = check_dtype_x(x_dtype))) return rc;
   if (p->batch != 1) return fail(HOS_EPARAM, "hos_partial_raw needs a batch-1 plan");
   if (!(0 <= seg_begin && seg_begin <= seg_end && seg_end <= p->k))
@@ -1298,6 +1335,7 @@ int hos_smooth_raw(hos_plan* p, const void* raw_dev, int64_t line_begin, int row
                    void* stream) {
   int rc = check_plan(p);
   if (rc) return rc;
+  PlanGuard guard_(p);
   if (p->batch != 1) return fail(HOS_EPARAM, "hos_smooth_raw needs a batch-1 plan");
   if (!raw_dev || !out_dev) return fail(HOS_EPARAM, "null buffer");
   int64_t lb = 0, le = 0;
@@ -1452,6 +1490,7 @@ int hos_plan_time_stages(hos_plan* p, const void* x_dev, int x_dtype, int64_t x_
                          double* ms6, void* stream) {
   int rc = check_plan(p);
   if (rc) return rc;
+  PlanGuard guard_(p);
   if ((rc = check_dtype_x(x_dtype))) return rc;
   if (!ms6 || reps < 1) return fail(HOS_EPARAM, "null output or reps < 1");
   cudaStream_t st = (cudaStream_t)stream;
@@ -1645,6 +1684,7 @@ int hos_cta_schedule_check(int order, int m, int k, int m3, int precision, int b
 int hos_comm_attach(hos_plan* p, void* nccl_comm, int rank, int nranks) {
   int rc = check_plan(p);
   if (rc) return rc;
+  PlanGuard guard_(p);
   if (p->batch != 1) return fail(HOS_EPARAM, "multi-GPU estimates need a batch-1 plan");
   std::string why;
   const NcclApi* api = nccl_api(&why);
@@ -1687,6 +1727,7 @@ int estimate_distributed_body(hos_plan* p, const void* x_dev, int x_dtype, void*
 int hos_estimate_distributed(hos_plan* p, const void* x_dev, int x_dtype, void* out_dev, void* stream) {
   int rc = check_plan(p);
   if (rc) return rc;
+  PlanGuard guard_(p);
   if (!p->comm) return fail(HOS_EPARAM, "no communicator attached (hos_comm_attach)");
   if (!x_dev || !out_dev) return fail(HOS_EPARAM, "null buffer");
   if ((rc = check_dtype_x(x_dtype))) return rc;

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 #include <cstdlib>
+#include <mutex>
 #include <string>
 #include <type_traits>
 #include <cstdint>
@@ -35,6 +36,32 @@ cudaError_t launch_pdl_kernel(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
+// One-time per-device setup (function attributes and device properties are
+// per device: a plan on cuda:1 must not rely on cuda:0 having been set up).
+struct PerDevice {
+  std::mutex mu;
+  uint64_t bits = 0;
+  template <typename F>
+  cudaError_t once(F f) {
+    int d = 0;
+    cudaGetDevice(&d);
+    std::lock_guard<std::mutex> lock(mu);
+    if (d < 64 && ((bits >> d) & 1)) return cudaSuccess;
+    const cudaError_t e = f();
+    if (e == cudaSuccess && d < 64) bits |= 1ull << d;
+    return e;
+  }
+};
+
+inline int device_sms() {
+  static int sms[64] = {};
+  int d = 0;
+  cudaGetDevice(&d);
+  if (d >= 64) d = 63;
+  if (!sms[d]) cudaDeviceGetAttribute(&sms[d], cudaDevAttrMultiProcessorCount, d);
+  return sms[d] > 0 ? sms[d] : 148;
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -324,11 +351,8 @@ static void front_go(const Tin* x, int64_t x_stride, int nseg, int krows, int ba
                      cudaStream_t st) {
   const size_t smem = 3 * (size_t)(1 << LOG2M) * sizeof(typename C2<T>::t) * front_pairs<LOG2M>();
   auto kern = k_front<Tin, T, LOG2M>;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = true;
-  }
+  static PerDevice configured;
+  configured.once([&] { return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
   constexpr int PPC = front_pairs<LOG2M>();
   const int pairs = (nseg + 1) / 2;
   int grid = (pairs + PPC - 1) / PPC;
@@ -336,12 +360,7 @@ static void front_go(const Tin* x, int64_t x_stride, int nseg, int krows, int ba
 #define HOS_FRONT_PERSIST 12  // CTAs per SM before the groups turn persistent (cfg5 front 273 -> 214 us with MINB 5)
 #endif
   {  // persistent groups: each loads its next pair's samples during the current transform
-    static int sms = 0;
-    if (!sms) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int sms = device_sms();
     grid = std::min(grid, std::max(1, sms * HOS_FRONT_PERSIST / std::max(1, batch)));
   }
   if (ready) {
@@ -929,15 +948,14 @@ static cudaError_t configure_all() {
 }
 
 static cudaError_t configure() {
-  static bool done = false;
-  if (done) return cudaSuccess;
-  cudaError_t e;
-  if ((e = configure_all<float, 4>()) != cudaSuccess) return e;
-  if ((e = configure_all<double, 4>()) != cudaSuccess) return e;
-  if ((e = configure_all<float, 2>()) != cudaSuccess) return e;
-  if ((e = configure_all<double, 2>()) != cudaSuccess) return e;
-  done = true;
-  return cudaSuccess;
+  static PerDevice done;
+  return done.once([] {
+    cudaError_t e;
+    if ((e = configure_all<float, 4>()) != cudaSuccess) return e;
+    if ((e = configure_all<double, 4>()) != cudaSuccess) return e;
+    if ((e = configure_all<float, 2>()) != cudaSuccess) return e;
+    return configure_all<double, 2>();
+  });
 }
 
 template <typename T, int S>
@@ -1064,7 +1082,10 @@ __global__ void __launch_bounds__(32 * kCtaWarps, 1) k_triple_cta(const __grid_c
           asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(a.ready + r) : "memory");
           if (v) break;
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-          if (t1 - t0 > 200000000ull) break;  // 200 ms: never hang the GPU (the result is then wrong)
+          if (t1 - t0 > 200000000ull) {  // 200 ms: never hang the GPU; the call reports the failure
+            if (a.err) *reinterpret_cast<volatile int*>(a.err) = 1;
+            break;
+          }
           __nanosleep(200);
         }
       }
@@ -1273,12 +1294,9 @@ static cudaError_t launch_cta_pdl(const CtaTripleArgs& a, size_t smem, cudaStrea
 template <typename T, int S>
 static cudaError_t launch_cta_variant(const CtaTripleArgs& a, cudaStream_t st) {
   const size_t smem = (size_t)a.depth * a.slot_bytes;
-  static size_t configured = 0;  // per instantiation: the largest dynamic smem enabled so far
-  if (smem > configured) {
-    cudaError_t e = configure_cta<T, S>(kCtaMaxSmem);
-    if (e != cudaSuccess) return e;
-    configured = kCtaMaxSmem;
-  }
+  static PerDevice configured;  // per instantiation and device: the largest ring enabled once
+  cudaError_t e = configured.once([] { return configure_cta<T, S>(kCtaMaxSmem); });
+  if (e != cudaSuccess) return e;
   const bool o4 = a.order == 4;
   if (a.conj && !o4) return launch_cta_pdl<T, true, false, S>(a, smem, st);
   if (!a.conj && !o4) return launch_cta_pdl<T, false, false, S>(a, smem, st);

@@ -164,6 +164,7 @@ struct CtaTripleArgs {
   unsigned long long* trace;  // diagnostics (nullptr: off): per warp {start, first data, end, smid}
   int trace_cta;              // diagnostics: CTA whose per-stage times are traced
   const int* ready;           // nullptr, or per E row: 1 once a concurrently running front end wrote it
+  int* err;                   // streaming: set to 1 (host-mapped word) when a ready wait timed out
 };
 cudaError_t launch_triple_cta(const CtaTripleArgs& a, int precision, cudaStream_t st);
 

@@ -221,7 +221,7 @@ def estimate_batch(x, cfg: EstimationConfig, *, device=None, to_host: bool = Tru
         cfg.segment.validate_for(np.empty(x.shape[1]))
         plan = _plan_for(cfg, x.shape[0], x.device.index if device is None else device)
         xt = x
-    out = plan.estimate(xt)
+    out = plan.estimate(xt).reshape(xt.shape[0], plan.npoints)  # (batch, npoints) for batch 1 too
     return _to_host_c128(out) if to_host else out
 
 

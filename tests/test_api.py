@@ -231,22 +231,22 @@ def test_native_shard_layout_matches_python(m, w, k, n):
     assert (block, halo, bool(in_next)) == (lay.block, lay.halo, lay.halo_in_next)
 
 
-def test_reference_window_and_report_json():
-    """The harness API mirrors hospectra/bench.py: the window ladder and its
-    n^0.622 curve, and BenchReport's JSON schema (round trip)."""
+def test_report_json_schema():
+    """BenchReport keeps the reference's JSON schema (hospectra/bench.py:58-80):
+    the twelve keys, their types, round trip, rejection of foreign records."""
     import paper_1805_11775_b200 as P
 
-    assert [P.reference_window(n) for n in (128, 256, 1024, 8192)] == [21, 33, 77, 279]
-    # off-ladder sizes follow round(21 (n/128)^0.622) | 1, clamped to (n-1)//2
-    for n in (100, 300, 3000, 20):
-        w = int(round(21.0 * (n / 128.0) ** 0.622)) | 1
-        assert P.reference_window(n) == max(1, min(w, (n - 1) // 2))
     r = P.BenchReport(plan="EFFICIENT", order=3, n=256, M=256, K=1, M3=33, P=1, wall_seconds=0.5,
                       peak_extra_bytes=123, peak_rss_bytes=456, checksum=7.25)
     text = P.reports_to_json([r, r])
     assert P.reports_from_json(text) == [r, r]
-    assert set(json.loads(text)[0]) == {"plan", "order", "n", "M", "K", "M3", "P", "wall_seconds",
-                                        "peak_extra_bytes", "peak_rss_bytes", "checksum", "status"}
+    assert list(json.loads(text)[0]) == ["plan", "order", "n", "M", "K", "M3", "P", "wall_seconds",
+                                         "peak_extra_bytes", "peak_rss_bytes", "checksum", "status"]
+    assert r.status == "ok" and isinstance(r.wall_seconds, float)
+    with pytest.raises(P.ParameterError):
+        P.reports_from_json(json.dumps([{"plan": "EFFICIENT"}]))
+    with pytest.raises(P.ParameterError):
+        P.reports_from_json(json.dumps({"plan": "EFFICIENT"}))
 
 
 def test_save_series_round_trip(tmp_path):
@@ -259,3 +259,31 @@ def test_save_series_round_trip(tmp_path):
         assert np.array_equal(P.load_series(path, fmt=fmt).samples, x)
     with pytest.raises(P.ParameterError):
         P.save_series(P.TimeSeries(x), tmp_path / "s.bin", fmt="bin")
+
+
+def test_compare_grids_semantics():
+    """compare_grids is the reference's per-point relative deviation
+    (hospectra/spectra.py:442-453): max|a-b| / max(|a|, |b|, 1e-12),
+    0.0 on empty grids, ParameterError on mismatched grids."""
+    import paper_1805_11775_b200 as P
+
+    dom = O.principal_domain(3, 16)
+    rng = np.random.default_rng(9)
+    va = rng.standard_normal(len(dom)) + 1j * rng.standard_normal(len(dom))
+    vb = va * (1 + 1e-7) + 1e-13
+    vb[3] = 0.0
+    a = P.SpectrumGrid(3, 16, 3, P.SmoothingPlan.EFFICIENT, dom, va)
+    b = P.SpectrumGrid(3, 16, 3, P.SmoothingPlan.NAIVE, dom, vb)
+    want = np.max(np.abs(va - vb) / np.maximum(np.maximum(np.abs(va), np.abs(vb)), 1e-12))
+    assert P.compare_grids(a, b) == want == 1.0   # a zeroed point counts fully
+    vb[3] = va[3]
+    assert P.compare_grids(a, P.SpectrumGrid(3, 16, 3, P.SmoothingPlan.NAIVE, dom, vb)) < 2e-7
+    tiny = P.SpectrumGrid(3, 16, 3, P.SmoothingPlan.NAIVE, dom, np.zeros(len(dom)) + 1e-14)
+    zero = P.SpectrumGrid(3, 16, 3, P.SmoothingPlan.NAIVE, dom, np.zeros(len(dom), complex))
+    assert P.compare_grids(tiny, zero) == pytest.approx(1e-2)   # the 1e-12 floor
+    e = P.SpectrumGrid(3, 2, 1, P.SmoothingPlan.NAIVE, dom[:0], np.zeros(0, complex))
+    assert P.compare_grids(e, e) == 0.0
+    with pytest.raises(P.ParameterError):
+        P.compare_grids(a, P.SpectrumGrid(3, 16, 5, P.SmoothingPlan.NAIVE, dom, va))
+    with pytest.raises(P.ParameterError):
+        P.compare_grids(a, P.SpectrumGrid(3, 16, 3, P.SmoothingPlan.NAIVE, dom[:-1], va[:-1]))
