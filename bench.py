@@ -16,9 +16,11 @@ ranks.  N > 1 (torchrun): segments sharded across ranks, NCCL reduce-scatter
 of the partial raw sums + halo + gather (distributed_estimate), strong
 scaling of one series.
 
---impl reference: the reference's CPU algorithm (the oracle port of the
-EFFICIENT plan, bit-exact with hospectra; the Python reference cannot travel
-to the GPU box) on all host cores, on a bounded sample of the same workload.
+--impl reference: the reference's own CPU path, the unmodified hospectra
+package installed under baseline/_ref (git-ignored; it travels to the GPU
+box with the snapshot): hospectra.parallel_estimate over all host cores
+(cfg5: a process pool over series), each step a bounded sample of the same
+workload; the oracle port stands in only if baseline/_ref is missing.
 """
 
 from __future__ import annotations
@@ -52,7 +54,6 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-segments", type=int, default=0, help="segments in the CPU sample (0 = auto)")
     return ap.parse_args()
 
 
@@ -125,65 +126,147 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline: the reference algorithm (oracle port) on all host cores
+# CPU baseline / reference arm: the reference's own CPU path on all host cores
+
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
 
-def cpu_baseline(cfg_name: str, steps: int, warmup: int, segments: int = 0, budget_s: float = 0.0):
+def dh_cells(order: int, m: int, m3: int) -> int:
+    """|D_h|: raw cells the window sums of the principal domain read (SURVEY
+    §8(d) recipe: mark every window offset of every domain point, count)."""
     from oracle import hos_oracle as O
+
+    dom = O.principal_domain(order, m)
+    lo, hi = -(m3 // 2), m3 - 1 - m3 // 2
+    offs = range(lo, hi + 1)
+    if order == 3:
+        mask = np.zeros((m, m), dtype=bool)
+        for u in offs:
+            for v in offs:
+                mask[(dom[:, 0] + u) % m, (dom[:, 1] + v) % m] = True
+    else:
+        mask = np.zeros((m, m, m), dtype=bool)
+        for u in offs:
+            for v in offs:
+                for t in offs:
+                    mask[(dom[:, 0] + u) % m, (dom[:, 1] + v) % m, (dom[:, 2] + t) % m] = True
+    return int(mask.sum())
+
+
+def _hospectra():
+    """The unmodified reference package installed under baseline/_ref (None if absent)."""
+    if not os.path.isdir(os.path.join(REF_DIR, "hospectra")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import hospectra
+
+        return hospectra
+    except Exception:
+        return None
+
+
+def _ref_one_series(args):
+    H, (x, order, m, k, m3) = _hospectra(), args
+    cfg = H.EstimationConfig(order, H.SegmentConfig(m=m, k=k), m3, H.SmoothingPlan.EFFICIENT)
+    return H.estimate_spectrum(H.TimeSeries(x), cfg).values.shape[0]
+
+
+def lscpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def cpu_reference(cfg_name: str, steps: int, warmup: int, budget_s: float, step_s: float = 5.0):
+    """Time the reference CPU path on a bounded sample of the config's workload.
+
+    With hospectra installed (baseline/_ref, the unmodified package): one step
+    = ``hospectra.parallel_estimate(TimeSeries, EstimationConfig(..., EFFICIENT),
+    WorkerConfig(p=cores))`` on the first K' segments of the series (K' = K
+    when a full step fits ``step_s``), or for batched configs a process pool
+    mapping ``estimate_spectrum`` over the first S series (SURVEY §8(d) CPU
+    protocol).  Without it, the oracle port (bit-exact with hospectra).  The
+    reference has no taper (SURVEY §0.1 #1): cost-neutral, so it runs untapered."""
     from paper_1805_11775_b200 import signals
 
     c = signals.baseline_config(cfg_name)
-    x = signals.baseline_series(c)
-    if x.ndim == 2:
-        x = x[0]
+    x = signals.baseline_series(c).astype(np.float64)
     cores = os.cpu_count() or 1
-    if segments <= 0:
-        segments = min(c.k, max(64, 8 * cores))
-    spec = O.segment_spectra(x, c.m, segments, c.taper)
-    dom = O.principal_domain(c.order, c.m)
+    dh = dh_cells(c.order, c.m, c.m3)
+    H = _hospectra()
     import multiprocessing as mp
-    from concurrent.futures import ProcessPoolExecutor
 
-    bounds = O._row_block_bounds(dom, cores)
-    parts = [dom[bounds[i]: bounds[i + 1]] for i in range(cores) if bounds[i + 1] > bounds[i]]
-    pool = ProcessPoolExecutor(max_workers=len(parts), mp_context=mp.get_context("spawn"))
-    try:
-        jobs = lambda: list(pool.map(O._worker, [(spec, c.order, c.m3, True, p) for p in parts]))
-        for _ in range(max(1, warmup)):
-            jobs()
-        times = []
-        for i in range(max(1, steps)):
+    if H is not None and c.batch > 1:
+        nser = min(c.batch, 2 * cores)
+        pool = mp.get_context("fork").Pool(cores)
+        job = lambda: pool.map(_ref_one_series, [(x[i], c.order, c.m, c.k, c.m3) for i in range(nser)])
+        units = nser * c.k * dh
+        what = (f"{cfg_name}: first {nser} of {c.batch} series, multiprocessing.Pool({cores}) mapping "
+                f"hospectra.estimate_spectrum (EFFICIENT)")
+        kind, close = "reference", pool.terminate
+    elif H is not None:
+        x1 = x[0] if x.ndim == 2 else x
+
+        def run(kk):
+            cfg = H.EstimationConfig(c.order, H.SegmentConfig(m=c.m, k=kk), c.m3, H.SmoothingPlan.EFFICIENT)
+            return H.parallel_estimate(H.TimeSeries(x1[: kk * c.m]), cfg, H.WorkerConfig(p=cores))
+
+        kk = max(1, min(c.k, 32))  # grow the sample until a step takes ~step_s (or is the full K)
+        for _ in range(4):
             t0 = time.perf_counter()
-            jobs()
+            run(kk)
+            t = time.perf_counter() - t0
+            if kk == c.k or t > step_s / 2:
+                break
+            kk = int(max(1, min(c.k, kk * step_s / max(t, 1e-3))))
+        job = lambda: run(kk)
+        units = kk * dh
+        what = (f"{cfg_name}: first {kk} of {c.k} segments, full principal domain, "
+                f"hospectra.parallel_estimate(WorkerConfig(p={cores})), EFFICIENT plan")
+        kind, close = "reference", (lambda: None)
+    else:
+        from concurrent.futures import ProcessPoolExecutor
+
+        from oracle import hos_oracle as O
+
+        x1 = x[0] if x.ndim == 2 else x
+        kk = min(c.k, max(64, 8 * cores))
+        spec = O.segment_spectra(x1, c.m, kk, None)
+        dom = O.principal_domain(c.order, c.m)
+        bounds = O._row_block_bounds(dom, cores)
+        parts = [dom[bounds[i]: bounds[i + 1]] for i in range(cores) if bounds[i + 1] > bounds[i]]
+        pool = ProcessPoolExecutor(max_workers=len(parts), mp_context=mp.get_context("spawn"))
+        job = lambda: list(pool.map(O._worker, [(spec, c.order, c.m3, True, p) for p in parts]))
+        units = kk * dh
+        what = (f"{cfg_name}: first {kk} of {c.k} segments, EFFICIENT-plan port (oracle/hos_oracle.py, "
+                f"bit-exact with hospectra; baseline/_ref not installed), {len(parts)} processes")
+        kind, close = "port", pool.shutdown
+    try:
+        t_start = time.perf_counter()
+        for _ in range(max(1, warmup)):
+            job()
+            if budget_s and time.perf_counter() - t_start > budget_s / 3:
+                break
+        times = []
+        for _ in range(max(1, steps)):
+            t0 = time.perf_counter()
+            job()
             times.append(time.perf_counter() - t0)
-            if budget_s and sum(times) + times[0] > budget_s:  # keep the whole run within minutes
+            if budget_s and time.perf_counter() - t_start + times[0] > budget_s:
                 break
     finally:
-        pool.shutdown()
-    units = segments * _dh_cells(c)
+        close()
     t = statistics.median(times)
-    return {"value": units / t, "unit": UNIT, "cores": len(parts), "kind": "port",
-            "sample": f"{cfg_name}: first {segments} of {c.k} segments, full principal domain "
-                      f"({len(dom)} points), EFFICIENT-plan port (oracle/hos_oracle.py, bit-exact with "
-                      f"hospectra), {len(parts)} processes over row blocks, median of {len(times)}",
+    return {"value": units / t, "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"{what}; median of {len(times)} steps; host: {lscpu_model()}, os.cpu_count()={cores}",
             "seconds_per_step": t, "units_per_step": units, "steps_timed": len(times)}
-
-
-def _dh_cells(c) -> int:
-    """|D_h| of a config (logical cells of the dilated principal domain),
-    the same count hos_plan_cells reports."""
-    h = c.m3 // 2
-    lo, hi = -h, c.m3 - 1 - h
-    m = c.m
-    rows = (m - 1) // 2 + 1
-    stop = [min(k1, (m - 2 * k1 - 1) // 2) + 1 for k1 in range(rows)]
-    if c.order == 3:
-        total = 0
-        for a in range(lo, rows - 1 + hi + 1):
-            ks = range(max(0, a - hi), min(rows - 1, a - lo) + 1)
-            total += max(stop[k] - 1 for k in ks) + hi - lo + 1
-        return total
-    raise NotImplementedError("order-4 cell count comes from the plan")
 
 
 # ---------------------------------------------------------------------------
@@ -200,6 +283,14 @@ def peak_fp32(lib, stream):
     return tf.value, mhz.value
 
 
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return float(json.load(open(p))["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured)"
+    except Exception:
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
 def load_traffic(cfg_name):
     p = os.path.join(ROOT, "profiles", "ncu_triple_latest.json")
     if os.path.exists(p):
@@ -210,6 +301,43 @@ def load_traffic(cfg_name):
         except Exception:
             return None
     return None
+
+
+STAMP_KINDS = ("front", "prep", "extend", "triple", "scan", "box", "series_smooth", "reduce")
+
+
+def kernel_spans(log):
+    """{kind: median over steps of (last end - first start) in ms} from the
+    per-step stamp records (see hos_plan_set_stamps), plus the step's first
+    start -> last end."""
+    out = {}
+    firsts, lasts = [], []
+    # (steps, 16, SMs): reduce over SMs -> first start (max of ~t), last end
+    log = np.asarray(log).view(np.uint64)  # the device compares unsigned
+    log = np.stack([log[:, 0::2].max(axis=2), log[:, 1::2].max(axis=2)], axis=2).reshape(len(log), 16)
+    for k, name in enumerate(STAMP_KINDS):
+        st = (~log[:, 2 * k]).astype(np.int64)   # ~(~t) = t for the slots that were stamped
+        en = log[:, 2 * k + 1]
+        ok = (log[:, 2 * k] != 0) & (en != 0)
+        if ok.any():
+            out[name] = float(np.median((en[ok].astype(np.int64) - st[ok]) * 1e-6))
+            firsts.append(st[ok])
+            lasts.append(en[ok].astype(np.int64))
+    if firsts:
+        f = np.min(np.stack([np.pad(a, (0, len(log) - len(a)), constant_values=a.max()) for a in firsts]), axis=0)
+        l_ = np.max(np.stack([np.pad(a, (0, len(log) - len(a))) for a in lasts]), axis=0)
+        out["first_start_to_last_end"] = float(np.median((l_ - f) * 1e-6))
+    return out
+
+
+def peak_fp64(lib, stream):
+    import ctypes
+
+    tf, mhz = ctypes.c_double(), ctypes.c_double()
+    rc = lib.hos_peak_fp64(ctypes.byref(tf), ctypes.byref(mhz), stream)
+    if rc:
+        raise RuntimeError(lib.hos_last_error())
+    return tf.value, mhz.value
 
 
 def run_ours(args):
@@ -239,19 +367,23 @@ def run_ours(args):
     x_host = P.baseline_series(c)
     batch = c.batch
     cfg = P.EstimationConfig(c.order, P.SegmentConfig(m=c.m, k=c.k), c.m3, precision=args.precision, taper=c.taper)
-    plan = _native.get_plan(c.order, c.m, c.k, c.m3, True, prec, c.taper, batch, local)
-    units = plan.units * batch
+    multi = world > 1 or force_dist
+    by_series = multi and batch > 1  # north_star: batches shard by series, no collective
+    b0, b1 = (P.series_shard(batch, rank, world) if by_series else (0, batch))
+    plan = _native.get_plan(c.order, c.m, c.k, c.m3, True, prec, c.taper, b1 - b0, local)
+    units = plan.units * batch  # whole job: every rank's series
     stream = torch.cuda.current_stream(dev)
     cstream = ctypes.c_void_p(stream.cuda_stream)
     lib = _native.lib()
 
+    if by_series:
+        x_host = np.ascontiguousarray(x_host[b0:b1])
     x = torch.from_numpy(x_host).to(dev)
     out = plan.empty_out()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     native = False
-    multi = world > 1 or force_dist
-    if not multi:
+    if not multi or by_series:
         step = lambda: plan.estimate(x, out)
     else:
         # the library's own NCCL path (collectives issued inside the C-ABI);
@@ -273,6 +405,12 @@ def run_ours(args):
         step()
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    # in-step kernel spans: every pipeline kernel stamps {~first CTA start after its
+    # PDL wait, last warp end} (globaltimer) into `stamps`; zeroed before and copied
+    # out after each timed step, outside the events, like the L2 flush
+    stamps = torch.zeros((16, 192), dtype=torch.int64, device=dev)
+    stamp_log = torch.zeros((args.steps, 16, 192), dtype=torch.int64, device=dev)
+    plan.set_stamps(stamps)
     sampler = ClockSampler(local)
     if dist is not None:
         dist.barrier()
@@ -280,17 +418,20 @@ def run_ours(args):
     sampler.start()
     for i in range(args.steps):
         flush.fill_(i & 0xFF)
+        stamps.zero_()
         ev[i][0].record(stream)
         step()  # the whole pipeline replays as one CUDA graph
         ev[i][1].record(stream)
+        stamp_log[i].copy_(stamps)
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
     sampler.stop()
+    plan.set_stamps(None)
+    in_step = kernel_spans(stamp_log.cpu().numpy())
     # per-stage device times on the launching stream: each stage's R launches
-    # replayed as one CUDA graph between two CUDA events (mean per launch; the inputs
-    # of every stage are the ones the last estimate left in HBM / L2, as in
-    # the pipeline, where each stage reads what the previous one just wrote)
+    # replayed as one CUDA graph between two CUDA events (warm L2; reported beside
+    # the in-step spans, which are the roofline's numbers)
     tri, stages = [], {}
     if world == 1:
         for _ in range(3):
@@ -309,7 +450,7 @@ def run_ours(args):
 
     # ---- e2e: host buffers through the C-ABI (hos_estimate_host), wall clock
     e2e_ms = []
-    if not multi:
+    if not multi or by_series:
         xp = torch.from_numpy(x_host).pin_memory()
         cd = torch.complex64 if prec == 32 else torch.complex128
         op = torch.empty(out.shape, dtype=cd).pin_memory()
@@ -324,8 +465,12 @@ def run_ours(args):
             t0 = time.perf_counter()
             plan.estimate_host(xn, on)
             e2e_ms.append((time.perf_counter() - t0) * 1e3)
-        h2d = xn.nbytes
-        d2h = on.nbytes
+        h2d = xn.nbytes * (world if by_series else 1)
+        d2h = on.nbytes * (world if by_series else 1)
+        if by_series:  # the job ends when the slowest rank's shard is back on its host
+            t = torch.tensor([statistics.median(e2e_ms)], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = [float(t.item())]
     else:
         shard = (c.k + world - 1) // world * c.m
         xp = torch.from_numpy(x_host).pin_memory()
@@ -350,47 +495,72 @@ def run_ours(args):
     result = None
     if rank == 0:
         clocks = sampler.summary()
-        peak_tf, probe_mhz = peak_fp32(lib, cstream)
+        peak_tf, probe_mhz = (peak_fp32 if prec == 32 else peak_fp64)(lib, cstream)
         roof = None
-        if tri:
-            t_tri = statistics.median(tri)
+        t_tri = in_step.get("triple")
+        if t_tri:
             achieved = FLOPS_PER_UNIT * units / (t_tri * 1e-3) / 1e12
-            roof = {"bound": "fp32", "achieved": round(achieved, 3), "peak": round(peak_tf, 3), "unit": "TFLOP/s",
-                    "frac": round(achieved / peak_tf, 4), "traffic": load_traffic(args.config),
+            t_rep = statistics.median(tri) if tri else None
+            roof = {"bound": "fp32" if prec == 32 else "fp64", "achieved": round(achieved, 3), "peak": round(peak_tf, 3),
+                    "unit": "TFLOP/s", "frac": round(achieved / peak_tf, 4), "traffic": load_traffic(args.config),
                     "kernel": ("k_triple_cta" if lib.hos_plan_k2_kind(plan.handle) == 1 else "k_triple_w")
-                              + (" (fp32 FFMA2 triple product)" if prec == 32 else " (fp64 DFMA triple product; peak below is the FP32 one)"), "kernel_ms": round(t_tri, 5),
+                              + (" (fp32 FFMA2 triple product)" if prec == 32 else " (fp64 DFMA triple product)"),
+                    "kernel_ms": round(t_tri, 5),
+                    "kernel_timing": "in-step: median over the timed steps of the K2 span (first CTA start after its "
+                                     "PDL wait -> last warp end, globaltimer) inside the L2-flushed timed step",
                     "kernel_share_of_step": round(t_tri / ms_per_step, 3),
-                    "stage_us": {k_: round(statistics.median(v_) * 1e3, 2) for k_, v_ in stages.items()},
-                    "stage_timing": f"mean of {STAGE_REPS} launches per stage replayed as one CUDA graph, median of 3",
-                    "peak_source": f"live FFMA2 outer-product microbenchmark (hos_peak_fp32) at {probe_mhz:.0f} MHz; "
-                                   "MEASURED_PEAKS.json has no FP32 figure",
+                    "in_step_us": {k_: round(v_ * 1e3, 2) for k_, v_ in in_step.items()},
+                    "kernel_ms_replay": round(t_rep, 5) if t_rep else None,
+                    "stage_us_replay": {k_: round(statistics.median(v_) * 1e3, 2) for k_, v_ in stages.items()},
+                    "stage_timing_replay": f"mean of {STAGE_REPS} launches per stage replayed as one CUDA graph "
+                                           "(warm L2), median of 3",
+                    "peak_source": f"live {'FFMA2' if prec == 32 else 'DFMA'} microbenchmark "
+                                   f"(hos_peak_fp{prec}) at {probe_mhz:.0f} MHz; MEASURED_PEAKS.json has no "
+                                   "FP32/FP64 figure",
                     "tiling_efficiency": round(plan.units / plan.issued, 4)}
+        smooth_ms = in_step.get("series_smooth") or (
+            (in_step.get("scan") or 0) + (in_step.get("box") or 0)) or None
+        roof_s = None
+        if smooth_ms:
+            hbm = hbm_peak()
+            nbytes = (plan.cells + plan.npoints) * (8 if prec == 32 else 16) * batch
+            roof_s = {"bound": "hbm", "achieved": round(nbytes / (smooth_ms * 1e-3) / 1e9, 1), "peak": hbm[0],
+                      "unit": "GB/s", "frac": round(nbytes / (smooth_ms * 1e-3) / 1e9 / hbm[0], 4),
+                      "algorithmic_bytes": nbytes, "kernel_ms": round(smooth_ms, 5),
+                      "kernels": "k_smooth_series3" if in_step.get("series_smooth") else "k_line_scan + k_box",
+                      "peak_source": hbm[1],
+                      "note": "(|D_h| + |P|) x complex bytes x series / in-step smoothing span; the grid of a "
+                              "single cfg2-4 series is L2-resident, so the HBM gate is cfg5"}
         result = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32" if prec == 32 else "f64",
-            "data": "synthetic (seeded BASELINE cfg2 bilinear process, paper_1805_11775_b200/signals.py)",
+            "data": f"synthetic (seeded BASELINE {c.name} series, paper_1805_11775_b200/signals.py)",
             "config": {"workload": c.name, "order": c.order, "n": c.n, "M": c.m, "K": c.k, "w": c.m3,
                        "L": c.m3 // 2, "taper": c.taper, "batch": batch, "precision": args.precision,
                        "units_per_step": units, "points_per_step": plan.npoints * batch,
                        "l2": "flushed: 256 MiB device write between timed steps (outside the events)",
-                       "parallelism": f"segments sharded over {world} GPUs (NCCL reduce-scatter + halo"
-                                      + (" inside the C-ABI)" if native else ", torch.distributed)")
+                       "parallelism": (f"series sharded over {world} GPUs ({b1 - b0} on rank 0), no collective"
+                                       if by_series else
+                                       f"segments sharded over {world} GPUs (NCCL reduce-scatter + halo"
+                                       + (" inside the C-ABI)" if native else ", torch.distributed)"))
                        if world > 1 else "1 GPU"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                     "ms_per_step": statistics.median(e2e_ms),
                     "path": "hos_estimate_host (C-ABI, pinned host buffers, copies inside the timed call)"
-                    if world == 1 else "pinned H2D + distributed_estimate + rank-0 D2H"},
+                    if world == 1 or by_series else "pinned H2D + distributed_estimate + rank-0 D2H",
+                    "ms_is": "max over ranks" if by_series else "rank 0"},
             "roofline": roof,
+            "roofline_smoothing": roof_s,
             "clocks": clocks,
-            "gpu_launches": lib.hos_plan_launches(plan.handle) * args.steps if world == 1 else None,
+            "gpu_launches": lib.hos_plan_launches(plan.handle) * args.steps if (world == 1 or by_series) else None,
             "gpu_launches_note": "per step: front end (k_front: fused demean+Hann+FFT+extension; or k_prep + "
                                  "cuFFT + k_extend_half for non-power-of-two M, cuFFT not counted), k_triple_cta (k_triple_w for large M), "
                                  "smoothing (k_line_scan + k_box3/k_box4, or k_smooth_series3 for grids that fit in "
                                  "shared memory)",
         }
         if not args.no_cpu_baseline and world == 1:
-            cb = cpu_baseline(args.config, steps=1, warmup=1, segments=args.cpu_segments)
+            cb = cpu_reference(args.config, steps=1, warmup=1, budget_s=60.0)
             result["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
     if dist is not None:
         dist.barrier()
@@ -407,18 +577,18 @@ def run_reference(args):
     from paper_1805_11775_b200 import signals
 
     c = signals.baseline_config(args.config)
-    # every step is one bounded sample of the workload (~60 ms on 16 cores); K and
-    # W as requested, K cut short only if the run would exceed ~150 s
-    cb = cpu_baseline(args.config, steps=max(1, args.steps), warmup=max(1, args.warmup), segments=args.cpu_segments,
-                      budget_s=150.0)
+    # every step is one bounded sample of the workload (<= ~5 s on the box's
+    # cores); K and W as requested, K cut short only if the run would exceed ~200 s
+    cb = cpu_reference(args.config, steps=max(1, args.steps), warmup=max(1, args.warmup), budget_s=200.0)
     steps = cb["steps_timed"]
     line = {
         "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": world,
         "steps": steps, "warmup": max(1, args.warmup), "ms_per_step": cb["seconds_per_step"] * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded BASELINE cfg2 bilinear process)",
+        "data": f"synthetic (seeded BASELINE {c.name} series, paper_1805_11775_b200/signals.py)",
         "config": {"workload": c.name, "order": c.order, "n": c.n, "M": c.m, "K": c.k, "w": c.m3,
-                   "taper": c.taper, "units_per_step": cb["units_per_step"]},
+                   "taper": None, "batch": c.batch, "units_per_step": cb["units_per_step"],
+                   "sample": cb["sample"]},
         "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }

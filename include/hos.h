@@ -36,7 +36,8 @@
  * Ownership: the caller owns every input/output buffer; a plan owns its
  * cuFFT plan, scratch and geometry tables, all allocated at create time so
  * hos_estimate* never allocate (stream-ordered, CUDA-graph capturable).
- * A plan is used by one host thread / stream at a time.
+ * Calls on one plan are serialised by a per-plan lock and run on the
+ * plan's device whatever device the calling thread has selected.
  */
 #ifndef HOS_B200_H
 #define HOS_B200_H
@@ -167,10 +168,21 @@ int hos_rows_line_range(const hos_plan* plan, int row_begin, int row_end, int64_
  * FP32 pipe peak (FFMA2 outer-product microbenchmark, flops counted as 2 per
  * lane FMA) and the SM clock seen meanwhile, on the current device. */
 int hos_peak_fp32(double* tflops, double* sm_mhz, void* stream);
+/* FP64 pipe peak (DFMA chains, 2 flops per FMA) and the SM clock seen meanwhile. */
+int hos_peak_fp64(double* tflops, double* sm_mhz, void* stream);
 /* Mean duration (ms) of the triple-product kernel launches of the last
  * hos_estimate* call on this plan when timing was enabled (events recorded on
  * the launching stream). */
 int hos_plan_set_timing(hos_plan* plan, int enable);
+/* In-step kernel timing: stamps_dev = a zeroed device buffer of 16 x 192
+ * uint64 (NULL: off) on the plan's device.  While set, every pipeline kernel
+ * of every plan on that device records, per SM, ~(globaltimer at its first
+ * CTA's start on that SM, after its PDL wait) into [2 kind][sm] and the
+ * globaltimer of its last warp's end there into [2 kind + 1][sm] (atomicMax);
+ * kind = 0 front end, 1 prep, 2 extend, 3 triple product, 4 line scan, 5 box,
+ * 6 per-series smoothing, 7 slot reduction.  The caller zeroes the buffer
+ * between calls and reduces over SMs.  Works under graph replay. */
+int hos_plan_set_stamps(hos_plan* plan, void* stamps_dev);
 /* ---- multi-GPU ----------------------------------------------
  * One process (or thread) per GPU.  The caller creates an NCCL communicator
  * (ncclCommInitRank; libnccl.so.2 is resolved at attach time, no link-time

@@ -55,7 +55,9 @@ EXPORTED_SYMBOLS = {
     "hos_row_point_offset": (_i64, [_p, _i]),
     "hos_rows_line_range": (_i, [_p, _i, _i, _p, _p]),
     "hos_peak_fp32": (_i, [_p, _p, _p]),
+    "hos_peak_fp64": (_i, [_p, _p, _p]),
     "hos_plan_set_timing": (_i, [_p, _i]),
+    "hos_plan_set_stamps": (_i, [_p, _p]),
     "hos_plan_nctas": (_i, [_p]),
     "hos_plan_k2_kind": (_i, [_p]),
     "hos_plan_kernel_ms": (_i, [_p, _p, _p]),
@@ -262,6 +264,10 @@ class Plan:
 
     def set_timing(self, on: bool):
         raise_for(lib().hos_plan_set_timing(self.handle, int(on)))
+
+    def set_stamps(self, buf):
+        """In-step kernel stamps into a (16, 192) int64 CUDA tensor (None: off)."""
+        raise_for(lib().hos_plan_set_stamps(self.handle, ctypes.c_void_p(buf.data_ptr() if buf is not None else 0)))
 
     def stage_ms(self):
         out = (ctypes.c_double * 6)()

@@ -1414,25 +1414,32 @@ int hos_rows_line_range(const hos_plan* p, int row_begin, int row_end, int64_t* 
   return HOS_OK;
 }
 
-int hos_peak_fp32(double* tflops, double* sm_mhz, void* stream) {
+namespace {
+// FMA-pipe peak microbenchmark on the current device: precision 32 = FFMA2
+// (2 lane FMAs per instruction), 64 = DFMA; flops counted as 2 per FMA
+int peak_probe(int precision, double* tflops, double* sm_mhz, void* stream) {
   if (!tflops || !sm_mhz) return fail(HOS_EPARAM, "null output");
   cudaStream_t st = (cudaStream_t)stream;
   int dev = 0, sms = 148;
   CUDA_TRY(cudaGetDevice(&dev));
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int blocks = sms * 4, iters = 4096;
-  float2* buf = nullptr;
+  const int blocks = sms * 4, iters = precision == 32 ? 4096 : 512;
+  void* buf = nullptr;
   unsigned long long* clk = nullptr;
-  CUDA_TRY(cudaMalloc(&buf, (size_t)blocks * 256 * sizeof(float2)));
+  CUDA_TRY(cudaMalloc(&buf, (size_t)blocks * 256 * 8));
   CUDA_TRY(cudaMalloc(&clk, 16));
+  auto launch = [&]() {
+    return precision == 32 ? hos::launch_peak_fp32((float2*)buf, blocks, iters, st)
+                           : hos::launch_peak_fp64((double*)buf, blocks, iters, st);
+  };
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  CUDA_TRY(hos::launch_peak_fp32(buf, blocks, iters, st));  // warm-up
+  CUDA_TRY(launch());  // warm-up
   float best = 1e30f;
   for (int r = 0; r < 5; r++) {
     cudaEventRecord(a, st);
-    CUDA_TRY(hos::launch_peak_fp32(buf, blocks, iters, st));
+    CUDA_TRY(launch());
     cudaEventRecord(b, st);
     cudaEventSynchronize(b);
     float ms;
@@ -1440,12 +1447,13 @@ int hos_peak_fp32(double* tflops, double* sm_mhz, void* stream) {
     if (ms < best) best = ms;
   }
   // SM clock while the probe kernel is resident alongside a loaded device
-  CUDA_TRY(hos::launch_peak_fp32(buf, blocks, iters, st));
+  CUDA_TRY(launch());
   CUDA_TRY(hos::launch_clock_probe(clk, 20000000, st));
   unsigned long long h[2] = {0, 0};
   CUDA_TRY(cudaMemcpyAsync(h, clk, 16, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
-  const double flops = (double)blocks * 256 * iters * 32 * 2 * 2;
+  const double fmas_per_thread_iter = precision == 32 ? 32 * 2 : 32;
+  const double flops = (double)blocks * 256 * iters * fmas_per_thread_iter * 2;
   *tflops = flops / (best * 1e-3) / 1e12;
   *sm_mhz = h[1] ? (double)h[0] / ((double)h[1] * 1e-3) : 0.0;
   cudaEventDestroy(a);
@@ -1454,6 +1462,10 @@ int hos_peak_fp32(double* tflops, double* sm_mhz, void* stream) {
   cudaFree(clk);
   return HOS_OK;
 }
+}  // namespace
+
+int hos_peak_fp32(double* tflops, double* sm_mhz, void* stream) { return peak_probe(32, tflops, sm_mhz, stream); }
+int hos_peak_fp64(double* tflops, double* sm_mhz, void* stream) { return peak_probe(64, tflops, sm_mhz, stream); }
 
 int hos_plan_nctas(const hos_plan* p) { return p ? p->nctas : -1; }
 int hos_plan_k2_kind(const hos_plan* p) { return p ? (p->cta ? 1 : 0) : -1; }
@@ -1462,6 +1474,14 @@ int hos_plan_set_trace(hos_plan* p, void* trace_dev) {
   int rc = check_plan(p);
   if (rc) return rc;
   p->trace = (unsigned long long*)trace_dev;
+  return HOS_OK;
+}
+
+int hos_plan_set_stamps(hos_plan* p, void* stamps_dev) {
+  int rc = check_plan(p);
+  if (rc) return rc;
+  PlanGuard guard_(p);
+  CUDA_TRY(hos::set_stamp_buffer((unsigned long long*)stamps_dev));
   return HOS_OK;
 }
 

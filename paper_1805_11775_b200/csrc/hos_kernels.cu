@@ -64,6 +64,37 @@ inline int device_sms() {
   return sms[d] > 0 ? sms[d] : 148;
 }
 
+// ---------------------------------------------------------------------------
+// In-step kernel timing (diagnostics, bench.py's roofline): when g_stamps is
+// set (hos_plan_set_stamps), each pipeline kernel records, per SM, the
+// globaltimer of its first CTA's start on that SM (after its PDL wait: the
+// moment its inputs were ready) as ~t (atomicMax of ~t = min t) and of its
+// last warp's end; the host reduces over SMs.  Per-SM slots keep the atomics
+// uncontended (one address for a whole grid serialised ~1000 atomics in L2).
+__device__ unsigned long long* g_stamps = nullptr;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned s;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
+  return s < kStampSms ? s : kStampSms - 1;
+}
+__device__ __forceinline__ void stamp_start(int kind) {
+  unsigned long long* s = g_stamps;
+  if (s && threadIdx.x == 0) atomicMax(s + (2 * kind) * kStampSms + smid(), ~gtimer());
+}
+struct StampEnd {
+  int kind;
+  __device__ explicit StampEnd(int k) : kind(k) {}
+  __device__ ~StampEnd() {
+    unsigned long long* s = g_stamps;
+    if (s && (threadIdx.x & 31) == 0) atomicMax(s + (2 * kind + 1) * kStampSms + smid(), gtimer());
+  }
+};
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -81,6 +112,8 @@ template <typename Tin, typename Tout>
 __global__ void __launch_bounds__(256) k_prep(const Tin* __restrict__ x, int64_t x_stride, int m, int seg_begin,
                                               int nseg, int taper, const double* __restrict__ tab,
                                               Tout* __restrict__ out) {
+  StampEnd stamp_end_(kStampPrep);
+  stamp_start(kStampPrep);
   __shared__ double red[8];
   const int seg = blockIdx.x, b = blockIdx.y;
   const Tin* src = x + (int64_t)b * x_stride + (int64_t)(seg_begin + seg) * m;
@@ -176,6 +209,8 @@ __global__ void __launch_bounds__(front_threads<LOG2M>() * front_pairs<LOG2M>(),
                                                                   const typename C2<T>::t* __restrict__ tw, int f_lo,
                                                                   int L, int Lp, typename C2<T>::t* __restrict__ E,
                                                                   int* __restrict__ ready) {
+  StampEnd stamp_end_(kStampFront);
+  stamp_start(kStampFront);
   using CT = typename C2<T>::t;
   constexpr int M = 1 << LOG2M;
   constexpr int TH = front_threads<LOG2M>();
@@ -430,6 +465,8 @@ __device__ __forceinline__ C half_lookup(const C* __restrict__ H, int m, int f) 
 
 __global__ void k_extend_half_f32(const float2* __restrict__ H, int m, int hstride, int64_t n, int f_lo, int L,
                                   int Lp, float2* __restrict__ E) {
+  StampEnd stamp_end_(kStampExtend);
+  stamp_start(kStampExtend);
   asm volatile("griddepcontrol.launch_dependents;");  // let K2 stage its setup (it waits for our writes)
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = t / L;
@@ -439,6 +476,8 @@ __global__ void k_extend_half_f32(const float2* __restrict__ H, int m, int hstri
 }
 __global__ void k_extend_half_f64(const double2* __restrict__ H, int m, int hstride, int64_t n, int f_lo, int L,
                                   int Lp, double2* __restrict__ E) {
+  StampEnd stamp_end_(kStampExtend);
+  stamp_start(kStampExtend);
   asm volatile("griddepcontrol.launch_dependents;");
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = t / L;
@@ -460,6 +499,8 @@ cudaError_t launch_extend_half(const void* H, int m, int hstride, int rows, cons
 // From caller-supplied full spectra (estimate_from_spectra): no symmetry assumed.
 template <typename Cin, bool F32>
 __global__ void k_extend_full(const Cin* __restrict__ S, int m, int64_t n, int f_lo, int L, int Lp, void* E) {
+  StampEnd stamp_end_(kStampExtend);
+  stamp_start(kStampExtend);
   asm volatile("griddepcontrol.launch_dependents;");
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = t / L;
@@ -756,6 +797,7 @@ __device__ __forceinline__ void warp_cells(const typename Cplx<T>::C* q, const L
 
 template <typename T, bool CONJ, bool ORDER4, int S>
 __global__ void __launch_bounds__(32 * kTripleWarps, 8 / kTripleWarps) k_triple_w(const __grid_constant__ TripleArgs a) {
+  StampEnd stamp_end_(kStampTriple);
   using C = typename Cplx<T>::C;
   using L = K2Layout<T, S>;
   constexpr int UC = L::UC;
@@ -787,7 +829,8 @@ __global__ void __launch_bounds__(32 * kTripleWarps, 8 / kTripleWarps) k_triple_
     tr[0] = t0;
     tr[3] = sm;
   }
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // E is written by the previous kernel
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  stamp_start(kStampTriple);  // E is written by the previous kernel
   asm volatile("griddepcontrol.launch_dependents;");   // K4a may be scheduled as K2 CTAs retire
 
   // producer: stages the warp's (region, segment) units kGroup at a time, kWarpPairs-1 groups ahead;
@@ -1031,6 +1074,7 @@ cudaError_t launch_triple(const TripleArgs& a, int precision, cudaStream_t st) {
 
 template <typename T, bool CONJ, bool ORDER4, int S>
 __global__ void __launch_bounds__(32 * kCtaWarps, 1) k_triple_cta(const __grid_constant__ CtaTripleArgs a) {
+  StampEnd stamp_end_(kStampTriple);
   using C = typename Cplx<T>::C;
   using L = K2Layout<T, S>;
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -1195,7 +1239,8 @@ __global__ void __launch_bounds__(32 * kCtaWarps, 1) k_triple_cta(const __grid_c
     for (int d2 = 1; d2 < kCtaMaxDepth; d2++)
       if (d2 < depth && d2 < nst) pre[d2] = ld_stage(d2);
   }
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // E is written by the previous kernel
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  stamp_start(kStampTriple);  // E is written by the previous kernel
   asm volatile("griddepcontrol.launch_dependents;");
   // prefill: stage 0 alone first (all SMs prefilling the whole ring at once
   // would make the first stage wait for the whole burst), the rest of the
@@ -1374,8 +1419,10 @@ __global__ void __launch_bounds__(kScanThreads, HOS_SCAN_MINB) k_line_scan(const
                                                             int64_t part_series_stride, SlotInfo si,
                                                             const int64_t* __restrict__ line_start, int64_t line_begin,
                                                             int64_t s_series_stride, double2* __restrict__ S) {
+  StampEnd stamp_end_(kStampScan);
   asm volatile("griddepcontrol.launch_dependents;");  // K4b may be scheduled as we retire
-  asm volatile("griddepcontrol.wait;" ::: "memory");   // partial slots come from K2
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  stamp_start(kStampScan);   // partial slots come from K2
   __shared__ double2 wsum[kScanThreads / 32];
   const int64_t l = line_begin + blockIdx.x;
   const int series = blockIdx.y;
@@ -1420,8 +1467,10 @@ __global__ void __launch_bounds__(256, 4) k_line_scan_w(const P2* __restrict__ p
                                                      int64_t part_series_stride, SlotInfo si,
                                                      const int64_t* __restrict__ line_start, int64_t line_begin,
                                                      int64_t nlines, int64_t s_series_stride, double2* __restrict__ S) {
+  StampEnd stamp_end_(kStampScan);
   asm volatile("griddepcontrol.launch_dependents;");
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  stamp_start(kStampScan);
   const int lane = threadIdx.x & 31;
   const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (w >= nlines) return;
@@ -1487,11 +1536,13 @@ __device__ __forceinline__ void box3_point(const BoxArgs& a, const double2* __re
 // rows' point offsets staged in shared memory.
 template <typename OUT>
 __global__ void __launch_bounds__(256, 4) k_box3_flat(BoxArgs a) {
+  StampEnd stamp_end_(kStampBox);
   extern __shared__ int64_t roff[];  // row_off[row_begin .. row_end]
   const int nr = a.row_end - a.row_begin;
   for (int i = threadIdx.x; i <= nr; i += blockDim.x) roff[i] = __ldg(a.row_off + a.row_begin + i);
   __syncthreads();
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // prefix sums come from K4a
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  stamp_start(kStampBox);  // prefix sums come from K4a
   const int64_t p = a.p_begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= a.p_end) return;
   int lo = 0, hi = nr;  // largest r with roff[r] <= p
@@ -1514,7 +1565,9 @@ __global__ void __launch_bounds__(256, 4) k_box3_flat(BoxArgs a) {
 constexpr int kBoxThreads = HOS_BOX_THREADS;
 template <typename OUT>
 __global__ void __launch_bounds__(kBoxThreads, HOS_BOX_MINB) k_box3(BoxArgs a, int row0) {
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // prefix sums come from K4a
+  StampEnd stamp_end_(kStampBox);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  stamp_start(kStampBox);  // prefix sums come from K4a
   const int k1 = row0 + blockIdx.y;
   const int k2 = blockIdx.x * blockDim.x + threadIdx.x;
   const int series = blockIdx.z;
@@ -1561,6 +1614,7 @@ constexpr int kBox4Lines = 64;  // k_box4: windows of up to 8 x 8 pair lines sta
 constexpr int kBox4Threads = HOS_BOX4_THREADS;
 template <typename OUT>
 __global__ void __launch_bounds__(kBox4Threads) k_box4(BoxArgs a, int pair0) {
+  StampEnd stamp_end_(kStampBox);
   const int pair = pair0 + blockIdx.x;
   const int series = blockIdx.y;
   const int k1 = __ldg(a.pair_k1 + pair), k2 = __ldg(a.pair_k2 + pair);
@@ -1580,7 +1634,8 @@ __global__ void __launch_bounds__(kBox4Threads) k_box4(BoxArgs a, int pair0) {
       cbs[i] = __ldg(a.line_start + line) - a.cell_base;
     }
     __syncthreads();
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // prefix sums come from K4a
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  stamp_start(kStampBox);  // prefix sums come from K4a
     for (int k3 = threadIdx.x; k3 < n3; k3 += blockDim.x) {
       double sr = 0.0, si = 0.0;  // same order as below: u-major, v-minor
 #pragma unroll 5
@@ -1600,7 +1655,8 @@ __global__ void __launch_bounds__(kBox4Threads) k_box4(BoxArgs a, int pair0) {
     }
     return;
   }
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // prefix sums come from K4a
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  stamp_start(kStampBox);  // prefix sums come from K4a
   for (int k3 = threadIdx.x; k3 < n3; k3 += blockDim.x) {
     double sr = 0.0, si = 0.0;
     for (int u = a.lo; u <= a.hi; u++) {
@@ -1637,6 +1693,7 @@ template <typename P2, typename OUT>
 __global__ void __launch_bounds__(512, 2) k_smooth_series3(const P2* __restrict__ part, int nparts, int64_t part_stride,
                                                         int64_t part_series_stride, SlotInfo si, BoxArgs a,
                                                         int nlines) {
+  StampEnd stamp_end_(kStampSeries);
   extern __shared__ __align__(16) unsigned char sm_raw[];
   const int ncells = (int)a.s_series_stride;
   double2* S = reinterpret_cast<double2*>(sm_raw);            // ncells raw cells, then line prefixes
@@ -1677,7 +1734,8 @@ __global__ void __launch_bounds__(512, 2) k_smooth_series3(const P2* __restrict_
   if (kBoxRows > 1)
     for (int b = warp; b < nblk; b += nw)
       for (int q = bo[b] + lane; q < bo[b + 1]; q += 32) prow[q] = (unsigned short)b;
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // partial slots come from K2
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  stamp_start(kStampSeries);  // partial slots come from K2
   for (int series = blockIdx.x; series < a.batch; series += gridDim.x) {
   __syncthreads();  // the previous series' box reads of S are done
   if (tid == 0) max_slots = 0;
@@ -1908,6 +1966,8 @@ cudaError_t launch_box(const BoxArgs& a, cudaStream_t st) {
 template <typename P2>
 __global__ void __launch_bounds__(256) k_reduce_parts(const P2* __restrict__ part, int64_t stride, SlotInfo si,
                                                       const int64_t* __restrict__ line_start, P2* __restrict__ raw) {
+  StampEnd stamp_end_(kStampReduce);
+  stamp_start(kStampReduce);
   const int64_t l = blockIdx.x;
   const int64_t c0 = line_start[l], c1 = line_start[l + 1];
   for (int64_t idx = c0 + threadIdx.x; idx < c1; idx += blockDim.x) {
@@ -1977,6 +2037,36 @@ cudaError_t launch_peak_fp32(float2* buf, int blocks, int iters, cudaStream_t st
   return cudaGetLastError();
 }
 
+// DFMA peak probe: 8 x 4 independent fp64 accumulator chains per thread
+__global__ void __launch_bounds__(256) k_peak_fp64(double* out, int iters, double seed) {
+  double a[8], b[4], acc[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; i++) a[i] = seed + i * threadIdx.x;
+#pragma unroll
+  for (int j = 0; j < 4; j++) b[j] = seed * j + 1.0;
+#pragma unroll
+  for (int i = 0; i < 8; i++)
+#pragma unroll
+    for (int j = 0; j < 4; j++) acc[i][j] = 0.0;
+  for (int it = 0; it < iters; it++) {
+#pragma unroll
+    for (int i = 0; i < 8; i++)
+#pragma unroll
+      for (int j = 0; j < 4; j++) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; i++)
+#pragma unroll
+    for (int j = 0; j < 4; j++) s += acc[i][j];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+cudaError_t launch_peak_fp64(double* buf, int blocks, int iters, cudaStream_t st) {
+  k_peak_fp64<<<blocks, 256, 0, st>>>(buf, iters, 1.0001);
+  return cudaGetLastError();
+}
+
 __global__ void k_clock_probe(unsigned long long* o, long long spin) {
   unsigned long long g0, g1;
   const long long c0 = clock64();
@@ -1994,4 +2084,10 @@ cudaError_t launch_clock_probe(unsigned long long* out, long long spin, cudaStre
   return cudaGetLastError();
 }
 
+}  // namespace hos
+
+namespace hos {
+cudaError_t set_stamp_buffer(unsigned long long* dev_buf) {
+  return cudaMemcpyToSymbol(g_stamps, &dev_buf, sizeof(dev_buf));
+}
 }  // namespace hos

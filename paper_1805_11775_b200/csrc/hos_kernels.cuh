@@ -166,6 +166,12 @@ struct CtaTripleArgs {
   const int* ready;           // nullptr, or per E row: 1 once a concurrently running front end wrote it
   int* err;                   // streaming: set to 1 (host-mapped word) when a ready wait timed out
 };
+// in-step kernel timing slots (hos_plan_set_stamps): [kind][~first start | last end][SM]
+enum StampKind { kStampFront = 0, kStampPrep, kStampExtend, kStampTriple, kStampScan, kStampBox, kStampSeries,
+                 kStampReduce, kStampKinds };
+constexpr unsigned kStampSms = 192;  // SM slots per (kind, start|end)
+cudaError_t set_stamp_buffer(unsigned long long* dev_buf);  // on the current device; nullptr: off
+
 cudaError_t launch_triple_cta(const CtaTripleArgs& a, int precision, cudaStream_t st);
 
 // occupancy (CTAs / SM) of the triple-product kernel
@@ -230,6 +236,7 @@ cudaError_t launch_reduce_parts(const void* part, int64_t part_stride, const Slo
                                 int64_t nlines, int lo, int precision, void* raw, cudaStream_t st);
 cudaError_t launch_cast(const void* x, int x_dtype, int64_t n, int precision, void* out, cudaStream_t st);
 cudaError_t launch_peak_fp32(float2* buf, int blocks, int iters, cudaStream_t st);
+cudaError_t launch_peak_fp64(double* buf, int blocks, int iters, cudaStream_t st);
 cudaError_t launch_clock_probe(unsigned long long* out, long long spin, cudaStream_t st);
 
 }  // namespace hos

@@ -31,7 +31,7 @@ from .series import TimeSeries
 from .spectra import EstimationConfig, SpectrumGrid, estimate_spectrum, principal_domain
 
 __all__ = ["WorkerConfig", "partition_domain", "parallel_estimate", "row_blocks", "ShardLayout",
-           "shard_layout", "distributed_estimate"]
+           "shard_layout", "distributed_estimate", "series_shard", "sharded_batch_estimate"]
 
 
 @dataclass(frozen=True)
@@ -75,14 +75,117 @@ def partition_domain(domain, workers: WorkerConfig) -> list:
 
 
 def parallel_estimate(series: TimeSeries, cfg: EstimationConfig, workers: WorkerConfig, *,
-                      device=None) -> SpectrumGrid:
-    """Same contract and values as ``estimate_spectrum`` for every worker
-    count (hospectra/parallel.py:120-162).  One GPU computes the whole
-    domain; the worker count only exists for API compatibility."""
+                      device=None, devices=None) -> SpectrumGrid:
+    """Same contract as ``estimate_spectrum`` for every worker count
+    (hospectra/parallel.py:120-162), with ``workers.p`` mapped to GPUs.
+
+    ``p == 1`` (or one visible GPU): the whole estimate on one device, values
+    identical for every ``WorkerConfig``.  ``p > 1`` with several GPUs: the
+    K-sum is split across ``g = min(p, device_count)`` devices of this process
+    by contiguous segment ranges: every device runs the front
+    end + triple product on its segments (``hos_partial_raw``), the partial
+    raw sums are added on the first device in device order (fixed, so the
+    result is deterministic for a given g), and that device smooths the whole
+    grid (``hos_smooth_raw``).  Across different g the values agree within the
+    precision's parity bar (the segment sum is regrouped).  ``devices``
+    overrides the device list (tests: several shards on one GPU)."""
     if not isinstance(workers, WorkerConfig):
         raise ParameterError("workers must be a WorkerConfig")
     cfg.segment.validate_for(series)
-    return estimate_spectrum(series, cfg, device=device)
+    import torch
+
+    if devices is None:
+        n_dev = torch.cuda.device_count() if torch.cuda.is_available() else 0
+        g = min(workers.p, n_dev)
+        base = 0 if device is None else int(device)
+        devices = [(base + i) % max(n_dev, 1) for i in range(g)]
+    devices = list(devices)
+    if len(devices) <= 1:
+        return estimate_spectrum(series, cfg, device=devices[0] if devices else device)
+    return _segment_split_estimate(series, cfg, devices)
+
+
+def _segment_split_estimate(series: TimeSeries, cfg: EstimationConfig, devices) -> SpectrumGrid:
+    import torch
+
+    from ._native import get_plan
+
+    k, m = cfg.segment.k, cfg.segment.m
+    g = len(devices)
+    segb = [(r * k) // g for r in range(g + 1)]
+    xs = np.ascontiguousarray(series.samples[: k * m])
+    raws = []
+    for r, d in enumerate(devices):  # launches are asynchronous: the devices run concurrently
+        plan = get_plan(cfg.order, m, k, cfg.m3, cfg.conjugate_last, cfg.bits, cfg.taper, 1, d)
+        with torch.cuda.device(d):
+            x = torch.from_numpy(xs).to(f"cuda:{d}")
+            raw = torch.empty(plan.cells, dtype=plan.complex_dtype, device=f"cuda:{d}")
+            raws.append(plan.partial_raw(x, segb[r], segb[r + 1], raw))
+    d0 = devices[0]
+    plan0 = get_plan(cfg.order, m, k, cfg.m3, cfg.conjugate_last, cfg.bits, cfg.taper, 1, d0)
+    with torch.cuda.device(d0):
+        total = raws[0].clone()
+        for raw in raws[1:]:  # fixed device order
+            total += raw.to(f"cuda:{d0}")
+        rows = (m - 1) // 2 + 1
+        out = torch.empty(plan0.npoints, dtype=plan0.complex_dtype, device=f"cuda:{d0}")
+        plan0.smooth_raw(total, 0, 0, rows, out)
+        vals = out.cpu().numpy().astype(np.complex128, copy=False)
+    return SpectrumGrid(order=cfg.order, m=m, m3=cfg.m3, plan=cfg.plan,
+                        indices=principal_domain(cfg.order, m), values=vals)
+
+
+# ---------------------------------------------------------------------------
+# multi-GPU: batches of independent series, sharded by series (no collective)
+
+
+def series_shard(batch: int, rank: int, nranks: int) -> tuple:
+    """Contiguous, balanced series range [b0, b1) of ``rank``."""
+    if not (0 <= rank < nranks):
+        raise ParameterError(f"rank {rank} outside [0, {nranks})")
+    return (rank * batch) // nranks, ((rank + 1) * batch) // nranks
+
+
+def sharded_batch_estimate(x, cfg: EstimationConfig, *, group=None, gather: bool = True, engine=None):
+    """Independent estimates of the rows of ``x`` (batch, n), split by series
+    across the ranks of ``group`` (one process per GPU).  Each rank computes
+    only its own rows [b0, b1) -- there is no collective on the data path
+    (north_star: "multi-series batches shard by series with no collective").
+    ``gather=True`` collects the (batch, npoints) values on every rank (one
+    all-gather of padded shards, the analogue of hospectra/parallel.py:155's
+    shared result buffer); ``gather=False`` returns (values of [b0, b1), (b0, b1)).
+    ``engine(x_rows, cfg)`` computes a shard (default: estimate_batch on the
+    current GPU); the CPU tests inject one."""
+    import torch
+    import torch.distributed as dist
+
+    rank, nranks = dist.get_rank(group), dist.get_world_size(group)
+    batch = x.shape[0]
+    b0, b1 = series_shard(batch, rank, nranks)
+    if engine is None:
+        from .spectra import estimate_batch
+
+        engine = lambda rows, c: estimate_batch(rows, c, to_host=False)
+    vals = engine(x[b0:b1], cfg) if b1 > b0 else None
+    if not gather:
+        return vals, (b0, b1)
+    npts = len(principal_domain(cfg.order, cfg.segment.m))
+    width = max(series_shard(batch, r, nranks)[1] - series_shard(batch, r, nranks)[0] for r in range(nranks))
+    like = vals if vals is not None else torch.zeros(0)
+    dev = like.device if isinstance(like, torch.Tensor) else torch.device("cpu")
+    dt = like.dtype if isinstance(like, torch.Tensor) and like.numel() else torch.complex128
+    pad = torch.zeros((max(width, 1), npts), dtype=dt, device=dev)
+    if vals is not None:
+        pad[: b1 - b0] = torch.as_tensor(vals, device=dev).reshape(b1 - b0, npts)
+    real = torch.view_as_real(pad).reshape(-1)
+    outs = [torch.empty_like(real) for _ in range(nranks)]
+    dist.all_gather(outs, real, group=group)
+    res = torch.empty((batch, npts), dtype=dt, device=dev)
+    for r in range(nranks):
+        a, b = series_shard(batch, r, nranks)
+        if b > a:
+            res[a:b] = torch.view_as_complex(outs[r].reshape(-1, npts, 2))[: b - a]
+    return res
 
 
 # ---------------------------------------------------------------------------

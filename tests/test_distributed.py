@@ -135,3 +135,60 @@ def test_segment_sharded_estimate_gloo(world):
         for (a0, a1, part), (b0, _, _) in zip(slices, slices[1:] + [(len(ref), 0, None)]):
             assert a1 == b0 and len(part) == a1 - a0
             assert np.max(np.abs(part - ref[a0:a1]), initial=0.0) <= 1e-12 * scale
+
+
+def _oracle_rows(rows, cfg):
+    """CPU engine for sharded_batch_estimate: the oracle on each series."""
+    vals = [O.estimate(r, cfg.order, cfg.segment.m, cfg.segment.k, cfg.m3, cfg.conjugate_last, cfg.taper)[1]
+            for r in rows]
+    return torch.from_numpy(np.stack(vals))
+
+
+def _series_worker(rank, world, port, batch, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1805_11775_b200 import EstimationConfig, SegmentConfig, sharded_batch_estimate
+
+        x = np.random.default_rng(77).standard_normal((batch, 64 * 3))
+        cfg = EstimationConfig(3, SegmentConfig(m=64, k=3), 5, taper="hann")
+        calls = []
+        eng = lambda rows, c: (calls.append(len(rows)), _oracle_rows(rows, c))[1]
+        full = sharded_batch_estimate(x, cfg, engine=eng).numpy()
+        part, (b0, b1) = sharded_batch_estimate(x, cfg, engine=eng, gather=False)
+        q.put((rank, full, None if part is None else part.numpy(), b0, b1, calls))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,batch", [(2, 7), (3, 8), (2, 1)])
+def test_series_sharded_batch_gloo(world, batch):
+    """Batched series split by series (north_star: no collective on the data
+    path): every rank computes only its contiguous series range, the ranges
+    tile the batch, and the gathered (batch, npoints) result equals the
+    oracle row by row."""
+    from paper_1805_11775_b200 import series_shard
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_series_worker, args=(r, world, port, batch, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = {r: rest for r, *rest in (q.get(timeout=300) for _ in procs)}
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    x = np.random.default_rng(77).standard_normal((batch, 64 * 3))
+    ref = np.stack([O.estimate(r, 3, 64, 3, 5, True, "hann")[1] for r in x])
+    covered = []
+    for r in range(world):
+        full, part, b0, b1, calls = out[r]
+        assert (b0, b1) == series_shard(batch, r, world)
+        assert np.array_equal(full, ref)
+        assert calls == ([b1 - b0] * 2 if b1 > b0 else [])  # only its own series, never the batch
+        if b1 > b0:
+            assert np.array_equal(part, ref[b0:b1])
+        covered += list(range(b0, b1))
+    assert covered == list(range(batch))

@@ -517,3 +517,18 @@ def test_estimate_batch_of_one_keeps_batch_axis(cuda):
     assert vals.shape == (1, P.principal_domain(3, 64).shape[0])
     dom, ref = O.estimate(x[0], 3, 64, 4, 3)
     assert north_star(vals[0], ref) <= TOL_FP64
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_parallel_estimate_segment_split(cuda, prec):
+    """WorkerConfig.p > 1 maps to a segment split over GPUs; here the shards
+    are placed on one device (devices=[0]*p) so the split-and-sum path runs
+    on a one-GPU box; values match the oracle within the precision's bar."""
+    P = api()
+    x = np.random.default_rng(31).standard_normal(128 * 12)
+    cfg = P.EstimationConfig(3, P.SegmentConfig(m=128, k=12), 5, precision=prec, taper="hann")
+    dom, ref = O.estimate(x, 3, 128, 12, 5, True, "hann")
+    for p in (2, 3, 5):
+        g = P.parallel_estimate(P.TimeSeries(x), cfg, P.WorkerConfig(p=p), devices=[0] * p)
+        assert np.array_equal(g.indices, dom)
+        assert north_star(g.values, ref) <= TOL[prec], p
