@@ -58,7 +58,10 @@ struct hos_plan {
   int split_wa = 1, split_wb = 1;  // K2 WarpSplit weights for two-CTA-per-SM launches
   // K2 as k_triple_cta (CTA-staged full rows, host schedule) for the plan's main launch
   bool cta = false;
+  bool quad = false;  // fp32 k_triple_cta plan: E rows hold quads {re, im, im, im} (16 bytes)
+  int cta_warps = 8;  // warps per k_triple_cta CTA (16 for fp32, 8 for fp64)
   int cta_nctas = 0, cta_depth = 0, cta_stage_segs = 4, cta_slot_bytes = 0, cta_copy_b = 0;
+  int cta_tab_stages = 0, cta_tab_blocks = 0, s_tab_stages = 0, s_tab_blocks = 0;
   hos::CtaGroup* d_groups = nullptr;
   hos::CtaBlock* d_blocks = nullptr;
   hos::CtaStage* d_stages = nullptr;
@@ -215,8 +218,17 @@ bool cta_allowed() {
   return !(env && std::string(env) == "warp");
 }
 int pitch_of(const hos::Geometry& g) { return (g.f_hi - g.f_lo + 1 + 4 + 15) & ~15; }
+// fp32 quad E rows for k_triple_cta (opt-in, HOS_K2_QUAD=1): 16 warps of <= 128
+// registers with one float2 accumulator per cell and no operand-building
+// instructions, but twice the staged bytes; measured slower than the float2
+// kernel on cfg2/cfg4/cfg5, so off by default
+bool want_quad(int precision) {
+  const char* env = std::getenv("HOS_K2_QUAD");
+  return precision == 32 && env && env[0] == '1';
+}
+size_t e_bytes(int precision) { return want_quad(precision) ? 16 : csize(precision); }
 bool cta_fits(const hos::Geometry& g, int precision) {
-  const int64_t A = (4 * (int64_t)pitch_of(g) * (int64_t)csize(precision) + 127) / 128 * 128;
+  const int64_t A = (4 * (int64_t)pitch_of(g) * (int64_t)e_bytes(precision) + 127) / 128 * 128;
   return 3 * (2 * A + 128) <= (int64_t)hos::kCtaMaxSmem;
 }
 
@@ -378,6 +390,9 @@ hos::CtaTripleArgs cta_args(const hos_plan* p, bool streaming = false) {
   a.stage_segs = p->cta_stage_segs;
   a.slot_bytes = p->cta_slot_bytes;
   a.copy_b = p->cta_copy_b;
+  a.quad = p->quad ? 1 : 0;
+  a.tab_stages = p->cta_tab_stages;
+  a.tab_blocks = p->cta_tab_blocks;
   a.line_cmax = p->d_line_cmax;
   a.line_start = p->d_line_start;
   a.lo = p->geo.win.lo;
@@ -394,6 +409,8 @@ hos::CtaTripleArgs cta_args(const hos_plan* p, bool streaming = false) {
     a.stages = p->d_s_stages;
     a.cta_stage0 = p->d_s_cta_stage0;
     a.nctas = p->s_nctas;
+    a.tab_stages = p->s_tab_stages;
+    a.tab_blocks = p->s_tab_blocks;
     a.ready = p->d_ready;
     a.err = p->d_err;
   }
@@ -420,6 +437,19 @@ struct CtaSchedule {
   std::vector<int32_t> cta_stage0;
   std::vector<int32_t> region_slots;  // batch x nregions
   int nctas = 0, depth = 0, stage_segs = 4, slot_bytes = 0, copy_b = 0, maxslots = 1;
+  int tab_stages = 0, tab_blocks = 0;  // most stages / blocks of one CTA (shared-memory tables)
+  // fills tab_* (0: ring + tables exceed the CTA's shared memory, the kernel reads them from global)
+  bool size_tables() {
+    tab_stages = tab_blocks = 0;
+    for (int c = 0; c + 1 < (int)cta_stage0.size(); c++) {
+      const int n = cta_stage0[c + 1] - cta_stage0[c];
+      tab_stages = std::max(tab_stages, n);
+      if (n > 0) tab_blocks = std::max(tab_blocks, stages[cta_stage0[c + 1] - 1].block - stages[cta_stage0[c]].block + 1);
+    }
+    if ((size_t)depth * slot_bytes + 16 * (size_t)(tab_stages + tab_blocks) > hos::kCtaSmemLimit)
+      tab_stages = tab_blocks = 0;  // read from global memory
+    return true;
+  }
 };
 
 int stream_front_ctas() {
@@ -431,12 +461,17 @@ bool build_cta_schedule(const hos_plan* p, CtaSchedule& cs, int interleave_ctas 
   const hos::Geometry& g = p->geo;
   const int R = g.nregions, K = p->k, B = p->batch;
   if (R <= 0 || K <= 0) return false;
-  const int64_t row_bytes = (int64_t)p->Lp * (int64_t)csize(p->precision);
+  const int64_t row_bytes = (int64_t)p->Lp * (int64_t)e_bytes(p->precision);
   if (!cta_fits(g, p->precision)) return false;
   int segs = 0;
-  for (int s = 4; s >= 4 && !segs; s--) {  // 4-segment stages only (the straight-line compute block)
+  // stage shape: 4 segments staged twice (two bank offsets) by default;
+  // HOS_K2_SEGS / HOS_K2_COPIES (diagnostics) try 8-segment single-copy stages
+  int seg_try = 4, copies = 2;
+  if (const char* env = std::getenv("HOS_K2_SEGS")) seg_try = std::max(1, std::min(16, std::atoi(env)));
+  if (const char* env = std::getenv("HOS_K2_COPIES")) copies = std::atoi(env) == 1 ? 1 : 2;
+  for (int s = seg_try; s >= seg_try && !segs; s--) {
     const int64_t A = (s * row_bytes + 127) / 128 * 128;
-    const int64_t slot = 2 * A + 128;
+    const int64_t slot = copies * A + 128;
     // 3 slots: a deeper ring lets the warp the scheduler favours run further
     // ahead of its sub-partition partner, which then runs alone (cfg2 K2:
     // depth 3 33.6 us, 4 33.8, 5 34.4, 6 35.3; 2 cannot hide the copies)
@@ -451,7 +486,8 @@ bool build_cta_schedule(const hos_plan* p, CtaSchedule& cs, int interleave_ctas 
       segs = s;
       cs.depth = (int)depth;
       cs.slot_bytes = (int)slot;
-      cs.copy_b = (int)(A + 64);
+      cs.copy_b = copies == 2 ? (int)(A + 64) : 0;
+      cs.stage_segs = s;
     }
   }
   if (!segs) return false;
@@ -460,7 +496,7 @@ bool build_cta_schedule(const hos_plan* p, CtaSchedule& cs, int interleave_ctas 
   // A remainder stage takes about 1/phases of a full stage's compute but
   // still copies the whole stage (copy-bound at ~45% of a full stage, cfg2), so a segment weighs max(W / phases, 4)
   // where a full group's weighs W.
-  const int W = hos::kCtaWarps;
+  const int W = hos::cta_warps(want_quad(p->precision));
   auto both_tiles = [&](int r0, int n) {  // every region of [r0, r0+n) has two real tiles
     if (g.tiles_per_region != 2) return false;
     for (int r = r0; r < r0 + n; r++)
@@ -521,7 +557,7 @@ bool build_cta_schedule(const hos_plan* p, CtaSchedule& cs, int interleave_ctas 
       for (int r = cs.groups[gi].r0; r < cs.groups[gi].r0 + cs.groups[gi].n; r++) cs.region_slots[r] = slots[gi];
       cs.maxslots = std::max(cs.maxslots, slots[gi]);
     }
-    return true;
+    return cs.size_tables();
   }
   // (series, group) chunks of K segments each.  The CTA ranges come from
   // the smallest per-CTA time budget T (bisection) for which a greedy fill
@@ -600,7 +636,7 @@ bool build_cta_schedule(const hos_plan* p, CtaSchedule& cs, int interleave_ctas 
     for (int r = gr.r0; r < gr.r0 + gr.n; r++) cs.region_slots[(ch / ng) * R + r] = slots[ch];
     cs.maxslots = std::max(cs.maxslots, slots[ch]);
   }
-  return true;
+  return cs.size_tables();
 }
 
 // K4b arguments for the whole grid of every series of the plan
@@ -682,12 +718,14 @@ int check_dtype_x(int x_dtype) {
 }
 
 // Fused front end over segments [seg_begin, seg_begin+nseg) of `batch` series -> E rows.
+// quad: E rows as quads for k_triple_cta (the plan's main launch); the
+// segment-range launches of hos_partial_raw (k_triple_w) write plain rows.
 int fused_front(hos_plan* p, const void* x_dev, int x_dtype, int64_t x_stride, int seg_begin, int nseg, int batch,
-                cudaStream_t st) {
+                cudaStream_t st, bool quad) {
   const char* xs = (const char*)x_dev + (size_t)seg_begin * p->m * (x_dtype == HOS_F32 ? 4 : 8);
-  void* E = (char*)p->d_E + (size_t)seg_begin * p->Lp * csize(p->precision);
+  void* E = (char*)p->d_E + (size_t)seg_begin * p->Lp * (quad ? 16 : csize(p->precision));
   CUDA_TRY(hos::launch_front(xs, x_dtype, x_stride, p->m, nseg, p->k, batch, p->taper, p->d_taper, p->d_tw,
-                             p->precision, p->geo.f_lo, p->L, p->Lp, E, st));
+                             p->precision, p->geo.f_lo, p->L, p->Lp, E, st, quad ? 1 : 0));
   return HOS_OK;
 }
 
@@ -695,7 +733,7 @@ int fused_front(hos_plan* p, const void* x_dev, int x_dtype, int64_t x_stride, i
 int run_front(hos_plan* p, const void* x_dev, int x_dtype, int64_t x_stride, cudaStream_t st) {
   const int rows = p->batch * p->k;
   if (p->fused) {
-    int rc = fused_front(p, x_dev, x_dtype, x_stride, 0, p->k, p->batch, st);
+    int rc = fused_front(p, x_dev, x_dtype, x_stride, 0, p->k, p->batch, st, p->quad);
     if (rc) return rc;
     if (p->timing)
       for (int i = 1; i <= 3; i++) CUDA_TRY(cudaEventRecord(p->ev[i], st));
@@ -708,7 +746,7 @@ int run_front(hos_plan* p, const void* x_dev, int x_dtype, int64_t x_stride, cud
   if (rc) return rc;
   if (p->timing) CUDA_TRY(cudaEventRecord(p->ev[2], st));
   CUDA_TRY(hos::launch_extend_half(p->d_half, p->m, p->hstride, rows, nullptr, p->geo.f_lo, p->L, p->Lp,
-                                   p->precision, p->d_E, st));
+                                   p->precision, p->d_E, st, p->quad));
   if (p->timing) CUDA_TRY(cudaEventRecord(p->ev[3], st));
   return HOS_OK;
 }
@@ -951,11 +989,15 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
   CtaSchedule sched;
   p->cta = cta_allowed() && build_cta_schedule(p, sched);
   if (p->cta) {
+    p->quad = want_quad(precision);
+    p->cta_warps = hos::cta_warps(p->quad);
     p->cta_nctas = sched.nctas;
     p->cta_depth = sched.depth;
     p->cta_stage_segs = sched.stage_segs;
     p->cta_slot_bytes = sched.slot_bytes;
     p->cta_copy_b = sched.copy_b;
+    p->cta_tab_stages = sched.tab_stages;
+    p->cta_tab_blocks = sched.tab_blocks;
     // batch-1 plans keep room for the segment-range launches of k_triple_w (multi-GPU shards)
     p->maxslots = batch == 1 ? std::max(p->maxslots, sched.maxslots) : sched.maxslots;
     p->rs_stride = g.nregions;
@@ -970,6 +1012,8 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
                    build_cta_schedule(p, ssched, std::max(1, p->sms - stream_front_ctas()));
     if (p->stream_ok) {
       p->s_nctas = ssched.nctas;
+      p->s_tab_stages = ssched.tab_stages;
+      p->s_tab_blocks = ssched.tab_blocks;
       p->maxslots = std::max(p->maxslots, ssched.maxslots);
     }
   }
@@ -1044,8 +1088,9 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
   const size_t rows = (size_t)batch * k;
   if ((rc = alloc(p, &p->d_seg, rows * m * rsize(precision)))) return bail(rc);
   if ((rc = alloc(p, &p->d_half, rows * p->hstride * csize(precision)))) return bail(rc);
-  if ((rc = alloc(p, &p->d_E, rows * p->Lp * csize(precision)))) return bail(rc);
-  if (cudaMemset(p->d_E, 0, rows * p->Lp * csize(precision)) != cudaSuccess)  // pad elements stay defined
+  const size_t e_bytes = rows * p->Lp * (p->quad ? 16 : csize(precision));  // plain rows of partial_raw fit too
+  if ((rc = alloc(p, &p->d_E, e_bytes))) return bail(rc);
+  if (cudaMemset(p->d_E, 0, e_bytes) != cudaSuccess)  // pad elements stay defined
     return bail(fail(HOS_ECUDA, "cudaMemset failed"));
   if ((rc = alloc(p, &p->d_part, (size_t)batch * p->maxslots * g.ncells * csize(precision)))) return bail(rc);
   if ((rc = alloc(p, (void**)&p->d_S, (size_t)batch * g.ncells * 16))) return bail(rc);
@@ -1139,7 +1184,7 @@ int hos_estimate_from_spectra(hos_plan* p, const void* spec_dev, int spec_dtype,
   auto body = [&](cudaStream_t s) -> int {
     if (p->timing) CUDA_TRY(cudaEventRecord(p->ev[0], s));
     CUDA_TRY(hos::launch_extend_full(spec_dev, spec_dtype, p->m, p->batch * p->k, p->geo.f_lo, p->L, p->Lp,
-                                     p->precision, p->d_E, s));
+                                     p->precision, p->d_E, s, p->quad));
     if (p->timing)
       for (int i = 1; i <= 3; i++) CUDA_TRY(cudaEventRecord(p->ev[i], s));
     return run_back(p, out_dev, s);
@@ -1254,11 +1299,12 @@ int hos_estimate_host(hos_plan* p, const void* x_host, int x_dtype, int64_t x_st
       CUDA_TRY(cudaMemsetAsync(p->d_ready, 0, (size_t)p->k * sizeof(int), s));
       CUDA_TRY(hos::launch_triple_cta(cta_args(p, true), p->precision, s));
       CUDA_TRY(hos::launch_front(ai.devicePointer, x_dtype, x_stride, p->m, p->k, p->k, 1, p->taper, p->d_taper,
-                                 p->d_tw, p->precision, p->geo.f_lo, p->L, p->Lp, p->d_E, s, p->d_ready));
+                                 p->d_tw, p->precision, p->geo.f_lo, p->L, p->Lp, p->d_E, s, p->quad ? 1 : 0,
+                                 p->d_ready));
       CUDA_TRY(cudaMemsetAsync(p->d_ready, 0, sizeof(int), s));
       return run_smooth(p, ao.devicePointer, s, -1, true);
     }
-    int r = fused_front(p, ai.devicePointer, x_dtype, x_stride, 0, p->k, p->batch, s);
+    int r = fused_front(p, ai.devicePointer, x_dtype, x_stride, 0, p->k, p->batch, s, p->quad);
     if (r) return r;
     if (p->timing)
       for (int i = 1; i <= 3; i++) CUDA_TRY(cudaEventRecord(p->ev[i], s));
@@ -1314,13 +1360,13 @@ int hos_partial_raw(hos_plan* p, const void* x_dev, int x_dtype, int seg_begin, 
   void* half = (char*)p->d_half + (size_t)seg_begin * p->hstride * csize(p->precision);
   void* E = (char*)p->d_E + (size_t)seg_begin * p->Lp * csize(p->precision);
   if (p->fused) {
-    if ((rc = fused_front(p, x_dev, x_dtype, 0, seg_begin, nseg, 1, st))) return rc;
+    if ((rc = fused_front(p, x_dev, x_dtype, 0, seg_begin, nseg, 1, st, false))) return rc;
   } else {
     CUDA_TRY(hos::launch_prep(x_dev, x_dtype, 0, p->m, seg_begin, nseg, 1, p->taper, p->d_taper, p->precision, seg,
                               st));
     if ((rc = run_fft(p, nseg, seg, half, st))) return rc;
     CUDA_TRY(hos::launch_extend_half(half, p->m, p->hstride, nseg, nullptr, p->geo.f_lo, p->L, p->Lp, p->precision,
-                                     E, st));
+                                     E, st, 0));
   }
   int n = nctas_for(p, nseg, 1);
   while (n > 1 && slots_needed(p, nseg, n, 1) > p->maxslots) n--;
@@ -1532,7 +1578,7 @@ int hos_plan_time_stages(hos_plan* p, const void* x_dev, int x_dtype, int64_t x_
     switch (s) {
       case 0:
         if (p->fused)
-          r2 = fused_front(p, x_dev, x_dtype, x_stride, 0, p->k, p->batch, cs);
+          r2 = fused_front(p, x_dev, x_dtype, x_stride, 0, p->k, p->batch, cs, p->quad);
         else
           e = hos::launch_prep(x_dev, x_dtype, x_stride, p->m, 0, p->k, p->batch, p->taper, p->d_taper, p->precision,
                                p->d_seg, cs);
@@ -1543,7 +1589,7 @@ int hos_plan_time_stages(hos_plan* p, const void* x_dev, int x_dtype, int64_t x_
       case 2:
         if (!p->fused)
           e = hos::launch_extend_half(p->d_half, p->m, p->hstride, rows, nullptr, p->geo.f_lo, p->L, p->Lp,
-                                      p->precision, p->d_E, cs);
+                                      p->precision, p->d_E, cs, p->quad);
         break;
       case 3:
         e = launch_main_triple(p, cs);
@@ -1636,7 +1682,7 @@ int hos_cta_schedule_check(int order, int m, int k, int m3, int precision, int b
   const int nf = interleave ? std::max(1, sms - stream_front_ctas()) : 0;
   for (int i = 0; i < 12; i++) stats[i] = 0;
   if (!build_cta_schedule(&p, cs, nf)) return HOS_OK;  // not eligible: stats[0] = 0
-  const int R = g.nregions, W = hos::kCtaWarps;
+  const int R = g.nregions, W = hos::cta_warps(want_quad(precision));
   auto bad = [&](const std::string& why) { return fail(HOS_EDATA, "schedule check: " + why); };
   if ((int)cs.cta_stage0.size() != cs.nctas + 1 || cs.cta_stage0.front() != 0 ||
       cs.cta_stage0.back() != (int)cs.stages.size())

@@ -201,13 +201,26 @@ __host__ __device__ constexpr int front_pairs() {
 #ifndef HOS_FRONT_MINB
 #define HOS_FRONT_MINB 5  // one-warp transforms: 5 CTAs/SM, <= 102 regs (cfg5 front with persistent groups: 3 / 4 / 5 / 6 / 7 -> 232 / 217 / 214 / 230 / 239 us)
 #endif
-template <typename Tin, typename T, int LOG2M>
+// E element of the compute precision: fp32 rows read by k_triple_cta hold
+// quads {re, im, im, im} (Q; see cells_q), other rows plain complex values
+template <typename T, bool Q>
+struct EElem {
+  using t = typename C2<T>::t;
+  __device__ static t make(typename C2<T>::t v) { return v; }
+};
+template <>
+struct EElem<float, true> {
+  using t = float4;
+  __device__ static float4 make(float2 v) { return make_float4(v.x, v.y, v.y, v.y); }
+};
+
+template <typename Tin, typename T, int LOG2M, bool Q>
 __global__ void __launch_bounds__(front_threads<LOG2M>() * front_pairs<LOG2M>(),
                                   front_pairs<LOG2M>() > 1 ? HOS_FRONT_MINB : 1) k_front(const Tin* __restrict__ x, int64_t x_stride,
                                                                   int nseg, int krows, int taper,
                                                                   const double* __restrict__ tab,
                                                                   const typename C2<T>::t* __restrict__ tw, int f_lo,
-                                                                  int L, int Lp, typename C2<T>::t* __restrict__ E,
+                                                                  int L, int Lp, typename EElem<T, Q>::t* __restrict__ E,
                                                                   int* __restrict__ ready) {
   StampEnd stamp_end_(kStampFront);
   stamp_start(kStampFront);
@@ -358,12 +371,13 @@ __global__ void __launch_bounds__(front_threads<LOG2M>() * front_pairs<LOG2M>(),
   }
   if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;");
   // X_a(f) = (Z(f) + conj Z(-f)) / 2,  X_b(f) = (Z(f) - conj Z(-f)) / 2i
-  CT* row = E + ((int64_t)b * krows + sa) * Lp;
+  using EL = EElem<T, Q>;
+  typename EL::t* row = E + ((int64_t)b * krows + sa) * Lp;
   for (int j = tid; j < L; j += TH) {
     const int f = (f_lo + j) & (M - 1);
     const CT z = xin[f], zn = xin[(M - f) & (M - 1)];
-    row[j] = CT{(T)0.5 * (z.x + zn.x), (T)0.5 * (z.y - zn.y)};
-    if (has_b) row[Lp + j] = CT{(T)0.5 * (z.y + zn.y), (T)0.5 * (zn.x - z.x)};
+    row[j] = EL::make(CT{(T)0.5 * (z.x + zn.x), (T)0.5 * (z.y - zn.y)});
+    if (has_b) row[Lp + j] = EL::make(CT{(T)0.5 * (z.y + zn.y), (T)0.5 * (zn.x - z.x)});
   }
   sync();  // the E rows are written (ready flags) and xin is free (next pair)
   if (ready && tid == 0) {  // publish the pair's rows to a concurrently running K2
@@ -380,12 +394,12 @@ __global__ void __launch_bounds__(front_threads<LOG2M>() * front_pairs<LOG2M>(),
 // ready != nullptr: streaming launch (see hos_capi.cu): each pair publishes
 // its rows' ready flags, and the kernel is a programmatic (PDL) dependent of
 // the K2 that consumes them
-template <int LOG2M, typename Tin, typename T>
+template <int LOG2M, typename Tin, typename T, bool Q>
 static void front_go(const Tin* x, int64_t x_stride, int nseg, int krows, int batch, int taper, const double* tab,
-                     const typename C2<T>::t* tw, int f_lo, int L, int Lp, typename C2<T>::t* E, int* ready,
+                     const typename C2<T>::t* tw, int f_lo, int L, int Lp, typename EElem<T, Q>::t* E, int* ready,
                      cudaStream_t st) {
   const size_t smem = 3 * (size_t)(1 << LOG2M) * sizeof(typename C2<T>::t) * front_pairs<LOG2M>();
-  auto kern = k_front<Tin, T, LOG2M>;
+  auto kern = k_front<Tin, T, LOG2M, Q>;
   static PerDevice configured;
   configured.once([&] { return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
   constexpr int PPC = front_pairs<LOG2M>();
@@ -407,13 +421,14 @@ static void front_go(const Tin* x, int64_t x_stride, int nseg, int krows, int ba
                                                                       L, Lp, E, ready);
 }
 
-template <typename Tin, typename T>
+template <typename Tin, typename T, bool Q>
 static cudaError_t front_dispatch(int log2m, const Tin* x, int64_t x_stride, int nseg, int krows, int batch,
                                   int taper, const double* tab, const typename C2<T>::t* tw, int f_lo, int L, int Lp,
-                                  typename C2<T>::t* E, int* ready, cudaStream_t st) {
+                                  void* E, int* ready, cudaStream_t st) {
+  using ET = typename EElem<T, Q>::t;
 #define HOS_FRONT_CASE(LG) \
   case LG:                                                                                                   \
-    front_go<LG, Tin, T>(x, x_stride, nseg, krows, batch, taper, tab, tw, f_lo, L, Lp, E, ready, st); \
+    front_go<LG, Tin, T, Q>(x, x_stride, nseg, krows, batch, taper, tab, tw, f_lo, L, Lp, (ET*)E, ready, st); \
     break;
   switch (log2m) {
     HOS_FRONT_CASE(2) HOS_FRONT_CASE(3) HOS_FRONT_CASE(4) HOS_FRONT_CASE(5) HOS_FRONT_CASE(6) HOS_FRONT_CASE(7)
@@ -426,22 +441,27 @@ static cudaError_t front_dispatch(int log2m, const Tin* x, int64_t x_stride, int
 
 cudaError_t launch_front(const void* x, int x_dtype, int64_t x_stride, int m, int nseg, int krows, int batch,
                          int taper, const double* tab, const void* tw, int precision, int f_lo, int L, int Lp, void* E,
-                         cudaStream_t st, int* ready) {
+                         cudaStream_t st, int quad, int* ready) {
   int log2m = 0;
   while ((1 << log2m) < m) log2m++;
   if ((1 << log2m) != m || m > kFrontMaxM || m < 4) return cudaErrorInvalidValue;
   if (precision == 32) {
+    const float2* t2 = (const float2*)tw;
     if (x_dtype == 0)
-      return front_dispatch<float, float>(log2m, (const float*)x, x_stride, nseg, krows, batch, taper, tab,
-                                          (const float2*)tw, f_lo, L, Lp, (float2*)E, ready, st);
-    return front_dispatch<double, float>(log2m, (const double*)x, x_stride, nseg, krows, batch, taper, tab,
-                                         (const float2*)tw, f_lo, L, Lp, (float2*)E, ready, st);
+      return quad ? front_dispatch<float, float, true>(log2m, (const float*)x, x_stride, nseg, krows, batch, taper,
+                                                       tab, t2, f_lo, L, Lp, E, ready, st)
+                  : front_dispatch<float, float, false>(log2m, (const float*)x, x_stride, nseg, krows, batch, taper,
+                                                        tab, t2, f_lo, L, Lp, E, ready, st);
+    return quad ? front_dispatch<double, float, true>(log2m, (const double*)x, x_stride, nseg, krows, batch, taper,
+                                                      tab, t2, f_lo, L, Lp, E, ready, st)
+                : front_dispatch<double, float, false>(log2m, (const double*)x, x_stride, nseg, krows, batch, taper,
+                                                       tab, t2, f_lo, L, Lp, E, ready, st);
   }
   if (x_dtype == 0)
-    return front_dispatch<float, double>(log2m, (const float*)x, x_stride, nseg, krows, batch, taper, tab,
-                                         (const double2*)tw, f_lo, L, Lp, (double2*)E, ready, st);
-  return front_dispatch<double, double>(log2m, (const double*)x, x_stride, nseg, krows, batch, taper, tab,
-                                        (const double2*)tw, f_lo, L, Lp, (double2*)E, ready, st);
+    return front_dispatch<float, double, false>(log2m, (const float*)x, x_stride, nseg, krows, batch, taper, tab,
+                                                (const double2*)tw, f_lo, L, Lp, E, ready, st);
+  return front_dispatch<double, double, false>(log2m, (const double*)x, x_stride, nseg, krows, batch, taper, tab,
+                                               (const double2*)tw, f_lo, L, Lp, E, ready, st);
 }
 
 // ===========================================================================
@@ -463,15 +483,16 @@ __device__ __forceinline__ C half_lookup(const C* __restrict__ H, int m, int f) 
   return v;
 }
 
+template <bool Q>
 __global__ void k_extend_half_f32(const float2* __restrict__ H, int m, int hstride, int64_t n, int f_lo, int L,
-                                  int Lp, float2* __restrict__ E) {
+                                  int Lp, typename EElem<float, Q>::t* __restrict__ E) {
   StampEnd stamp_end_(kStampExtend);
   stamp_start(kStampExtend);
   asm volatile("griddepcontrol.launch_dependents;");  // let K2 stage its setup (it waits for our writes)
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = t / L;
     const int j = (int)(t - r * L);
-    E[r * Lp + j] = half_lookup(H + r * hstride, m, f_lo + j);
+    E[r * Lp + j] = EElem<float, Q>::make(half_lookup(H + r * hstride, m, f_lo + j));
   }
 }
 __global__ void k_extend_half_f64(const double2* __restrict__ H, int m, int hstride, int64_t n, int f_lo, int L,
@@ -487,10 +508,12 @@ __global__ void k_extend_half_f64(const double2* __restrict__ H, int m, int hstr
 }
 
 cudaError_t launch_extend_half(const void* H, int m, int hstride, int rows, const void*, int f_lo, int L, int Lp,
-                               int precision, void* E, cudaStream_t st) {
+                               int precision, void* E, cudaStream_t st, int quad) {
   const int64_t n = (int64_t)rows * L;
-  if (precision == 32)
-    k_extend_half_f32<<<grid_for(n, 256), 256, 0, st>>>((const float2*)H, m, hstride, n, f_lo, L, Lp, (float2*)E);
+  if (precision == 32 && quad)
+    k_extend_half_f32<true><<<grid_for(n, 256), 256, 0, st>>>((const float2*)H, m, hstride, n, f_lo, L, Lp, (float4*)E);
+  else if (precision == 32)
+    k_extend_half_f32<false><<<grid_for(n, 256), 256, 0, st>>>((const float2*)H, m, hstride, n, f_lo, L, Lp, (float2*)E);
   else
     k_extend_half_f64<<<grid_for(n, 256), 256, 0, st>>>((const double2*)H, m, hstride, n, f_lo, L, Lp, (double2*)E);
   return cudaGetLastError();
@@ -498,7 +521,8 @@ cudaError_t launch_extend_half(const void* H, int m, int hstride, int rows, cons
 
 // From caller-supplied full spectra (estimate_from_spectra): no symmetry assumed.
 template <typename Cin, bool F32>
-__global__ void k_extend_full(const Cin* __restrict__ S, int m, int64_t n, int f_lo, int L, int Lp, void* E) {
+__global__ void k_extend_full(const Cin* __restrict__ S, int m, int64_t n, int f_lo, int L, int Lp, void* E,
+                              int quad) {
   StampEnd stamp_end_(kStampExtend);
   stamp_start(kStampExtend);
   asm volatile("griddepcontrol.launch_dependents;");
@@ -506,7 +530,9 @@ __global__ void k_extend_full(const Cin* __restrict__ S, int m, int64_t n, int f
     const int64_t r = t / L;
     const int j = (int)(t - r * L);
     const Cin v = S[r * m + fmod_pos(f_lo + j, m)];
-    if (F32) {
+    if (F32 && quad) {
+      ((float4*)E)[r * Lp + j] = make_float4((float)v.x, (float)v.y, (float)v.y, (float)v.y);
+    } else if (F32) {
       ((float2*)E)[r * Lp + j] = make_float2((float)v.x, (float)v.y);
     } else {
       ((double2*)E)[r * Lp + j] = make_double2((double)v.x, (double)v.y);
@@ -515,15 +541,15 @@ __global__ void k_extend_full(const Cin* __restrict__ S, int m, int64_t n, int f
 }
 
 cudaError_t launch_extend_full(const void* S, int spec_dtype, int m, int rows, int f_lo, int L, int Lp, int precision,
-                               void* E, cudaStream_t st) {
+                               void* E, cudaStream_t st, int quad) {
   const int64_t n = (int64_t)rows * L;
   const unsigned g = grid_for(n, 256);
   if (spec_dtype == 2) {
-    if (precision == 32) k_extend_full<float2, true><<<g, 256, 0, st>>>((const float2*)S, m, n, f_lo, L, Lp, E);
-    else k_extend_full<float2, false><<<g, 256, 0, st>>>((const float2*)S, m, n, f_lo, L, Lp, E);
+    if (precision == 32) k_extend_full<float2, true><<<g, 256, 0, st>>>((const float2*)S, m, n, f_lo, L, Lp, E, quad);
+    else k_extend_full<float2, false><<<g, 256, 0, st>>>((const float2*)S, m, n, f_lo, L, Lp, E, 0);
   } else {
-    if (precision == 32) k_extend_full<double2, true><<<g, 256, 0, st>>>((const double2*)S, m, n, f_lo, L, Lp, E);
-    else k_extend_full<double2, false><<<g, 256, 0, st>>>((const double2*)S, m, n, f_lo, L, Lp, E);
+    if (precision == 32) k_extend_full<double2, true><<<g, 256, 0, st>>>((const double2*)S, m, n, f_lo, L, Lp, E, quad);
+    else k_extend_full<double2, false><<<g, 256, 0, st>>>((const double2*)S, m, n, f_lo, L, Lp, E, 0);
   }
   return cudaGetLastError();
 }
@@ -709,6 +735,69 @@ __device__ __forceinline__ void cells_f64(const double2* __restrict__ rows, cons
     }
   }
 }
+
+// fp32 cells from QUAD spectra {re, im, im, im} (k_triple_cta).  Every FFMA2
+// operand is a broadcast scalar or a register pair of a staged quad, with
+// the hardware's free operand modifiers (half swap, per-half negation):
+//   p   = F(row) F(col)  = fa.x * fb + (-fa.y, fa.y) * (fb.y, fb.x)
+//   acc += p G            = g.x * p + (-g.y, g.y) * (p.y, p.x)
+//   acc += p conj(G)      = g.x * p + (g.y, -g.y) * (p.y, p.x)
+// 4 FMA-pipe instructions per cell (FMUL2 + 3 FFMA2) with ONE float2
+// accumulator, and no operand-building instructions (a float2 layout needs
+// ~1 MOV per FFMA2 to form the (im, im) pairs; the quad holds them).
+// Order 4: the row factor is F(b) F(a) (plane), formed once per row.
+template <bool CONJ, bool ORDER4, int RS>
+__device__ __forceinline__ void cells_q(const float4* __restrict__ rows, const float4* __restrict__ cols,
+                                        const float4* __restrict__ gs, const float4* __restrict__ plane,
+                                        float2 (&acc)[4][8]) {
+  float4 fa[4];
+  float2 fb[8];
+  if (ORDER4) {
+    const float4 pa = *plane;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      const float4 r = rows[RS * i];
+      float2 t = fmul2(make_float2(r.x, r.x), make_float2(pa.x, pa.y));
+      t = ffma2(make_float2(-r.z, r.w), make_float2(pa.y, pa.x), t);
+      fa[i] = make_float4(t.x, t.y, t.y, t.y);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; i++) fa[i] = rows[RS * i];
+  }
+#pragma unroll
+  for (int j = 0; j < 8; j++) fb[j] = *reinterpret_cast<const float2*>(cols + RS * j);
+#pragma unroll
+  for (int q = 0; q < 11; q++) {
+    const float4 g = gs[RS * q];
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      const int j = q - i;
+      if (j < 0 || j > 7) continue;
+      float2 p = fmul2(make_float2(fa[i].x, fa[i].x), fb[j]);
+      p = ffma2(make_float2(-fa[i].z, fa[i].w), make_float2(fb[j].y, fb[j].x), p);
+      acc[i][j] = ffma2(make_float2(g.x, g.x), p, acc[i][j]);
+      if (CONJ)
+        acc[i][j] = ffma2(make_float2(g.z, -g.w), make_float2(p.y, p.x), acc[i][j]);
+      else
+        acc[i][j] = ffma2(make_float2(-g.z, g.w), make_float2(p.y, p.x), acc[i][j]);
+    }
+  }
+}
+
+struct AccQ {
+  float2 v[4][8];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int a = 0; a < 4; a++)
+#pragma unroll
+      for (int b = 0; b < 8; b++) v[a][b] = make_float2(0.f, 0.f);
+  }
+  template <bool CONJ>
+  __device__ __forceinline__ float2 cell(int a, int b) const {
+    return v[a][b];
+  }
+};
 
 #ifndef HOS_K2_PAIRS
 #define HOS_K2_PAIRS 2
@@ -1072,10 +1161,27 @@ cudaError_t launch_triple(const TripleArgs& a, int precision, cudaStream_t st) {
 // Groups with fewer regions than warps give each region several warps
 // ("phases"), each taking every phases-th segment of the block.
 
-template <typename T, bool CONJ, bool ORDER4, int S>
-__global__ void __launch_bounds__(32 * kCtaWarps, 1) k_triple_cta(const __grid_constant__ CtaTripleArgs a) {
+// cells of one staged segment: fp32 quads (cells_q), fp32 float2 (cells_f32)
+// or fp64 double2 (cells_f64)
+template <typename T, bool CONJ, bool ORDER4, int S, bool Q, typename EL, typename A>
+__device__ __forceinline__ void cta_cells(const EL* q, const LaneOps& o, A& acc) {
+  if constexpr (Q)
+    cells_q<CONJ, ORDER4, S>(q + o.rows, q + o.cols, q + o.g, q + o.plane, acc.v);
+  else if constexpr (sizeof(T) == 4)
+    cells_f32<ORDER4, S>(q + o.rows, q + o.cols, q + o.g, q + o.plane, acc.r, acc.i);
+  else
+    cells_f64<CONJ, ORDER4, S>(q + o.rows, q + o.cols, q + o.g, q + o.plane, acc.v);
+}
+
+template <typename T, bool CONJ, bool ORDER4, int S, bool Q>
+__global__ void __launch_bounds__(32 * (Q ? kCtaWarpsQ : kCtaWarps), 1)
+    k_triple_cta(const __grid_constant__ CtaTripleArgs a) {
   StampEnd stamp_end_(kStampTriple);
-  using C = typename Cplx<T>::C;
+  // Q (fp32 only): quad rows, 16 warps, one float2 accumulator per cell;
+  // else float2 / double2 rows, 8 warps (fp32: two float2 accumulators per cell)
+  constexpr int NW = Q ? kCtaWarpsQ : kCtaWarps;
+  using C = typename Cplx<T>::C;             // partial-slot value
+  using EL = typename std::conditional<Q, float4, C>::type;  // staged row element
   using L = K2Layout<T, S>;
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ __align__(8) unsigned long long full[kCtaMaxDepth];
@@ -1083,7 +1189,7 @@ __global__ void __launch_bounds__(32 * kCtaWarps, 1) k_triple_cta(const __grid_c
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int k0 = __ldg(a.cta_stage0 + blockIdx.x), nst = __ldg(a.cta_stage0 + blockIdx.x + 1) - k0;
   const int depth = a.depth, Lp = a.Lp;
-  unsigned long long* tr = a.trace ? a.trace + 4 * ((int64_t)blockIdx.x * kCtaWarps + warp) : nullptr;
+  unsigned long long* tr = a.trace ? a.trace + 4 * ((int64_t)blockIdx.x * NW + warp) : nullptr;
   auto stamp = [&](int i) {
     if (tr && lane == 0) {
       unsigned long long t;
@@ -1098,6 +1204,24 @@ __global__ void __launch_bounds__(32 * kCtaWarps, 1) k_triple_cta(const __grid_c
   };
   stamp(0);
   const unsigned ring_s = (unsigned)__cvta_generic_to_shared(smraw);
+  // the CTA's stage and block lists are copied to shared memory behind the
+  // ring (static tables: before the PDL wait, overlapping the front end);
+  // the stage loop then reads them with shared loads instead of dependent
+  // global loads on every warp's path
+  // (tab_stages == 0: the tables did not fit next to the ring -- huge batches
+  // on few SMs -- and are read from global memory)
+  const int b0 = nst > 0 ? __ldg(&a.stages[k0].block) : 0;
+  const int nb_cta = nst > 0 ? __ldg(&a.stages[k0 + nst - 1].block) - b0 + 1 : 0;
+  const int4* st_s = reinterpret_cast<const int4*>(a.stages + k0);
+  const int4* bl_s = reinterpret_cast<const int4*>(a.blocks + b0);
+  if (a.tab_stages > 0) {
+    int4* st_w = reinterpret_cast<int4*>(smraw + (size_t)depth * a.slot_bytes);
+    int4* bl_w = st_w + a.tab_stages;
+    for (int i = threadIdx.x; i < nst; i += blockDim.x) st_w[i] = __ldg(st_s + i);
+    for (int i = threadIdx.x; i < nb_cta; i += blockDim.x) bl_w[i] = __ldg(bl_s + i);
+    st_s = st_w;
+    bl_s = bl_w;
+  }
   if (threadIdx.x == 0) {
     for (int d = 0; d < depth; d++) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&full[d])));
@@ -1106,10 +1230,10 @@ __global__ void __launch_bounds__(32 * kCtaWarps, 1) k_triple_cta(const __grid_c
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const C* E = (const C*)a.E;
+  const EL* E = (const EL*)a.E;
   auto ld_stage = [&](int k) {
     CtaStage v;
-    const int4 r = __ldg(reinterpret_cast<const int4*>(a.stages + k0 + k));
+    const int4 r = st_s[k];
     v.row = r.x;
     v.nseg = r.y;
     v.block = r.z;
@@ -1135,19 +1259,22 @@ __global__ void __launch_bounds__(32 * kCtaWarps, 1) k_triple_cta(const __grid_c
       }
       asm volatile("fence.proxy.async.global;" ::: "memory");  // the bulk copy (async proxy) reads them
     }
-    const unsigned bytes = (unsigned)(sg.nseg * Lp * (int)sizeof(C));
-    const C* src = E + (int64_t)sg.row * Lp;
+    const unsigned bytes = (unsigned)(sg.nseg * Lp * (int)sizeof(EL));
+    const EL* src = E + (int64_t)sg.row * Lp;
     const unsigned dst = ring_s + (unsigned)(d * a.slot_bytes);
     const unsigned bar = (unsigned)__cvta_generic_to_shared(&full[d]);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(2 * bytes) : "memory");
+    const bool two = a.copy_b != 0;  // copy_b == 0: one copy (the tiles' loads may conflict)
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(two ? 2 * bytes : bytes)
+                 : "memory");
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                  "l"(src), "r"(bytes), "r"(bar)
                  : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     dst + (unsigned)a.copy_b),
-                 "l"(src), "r"(bytes), "r"(bar)
-                 : "memory");
+    if (two)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       dst + (unsigned)a.copy_b),
+                   "l"(src), "r"(bytes), "r"(bar)
+                   : "memory");
   };
   const int h = lane / (S * S), ra = (lane / S) % S, cb = lane % S;
   int cur = -1;                  // current block
@@ -1157,11 +1284,11 @@ __global__ void __launch_bounds__(32 * kCtaWarps, 1) k_triple_cta(const __grid_c
   C* P = nullptr;                // the warp's partial slot (series + slot applied)
   LaneOps ops{};
   bool active = false, warp_active = false;
-  Acc<T> acc;
+  typename std::conditional<Q, AccQ, Acc<T>>::type acc;
   int lcm[4], loff[4];            // the lane's lines: last column, cell offset in the slot
   auto ld_block = [&](int b) {
     CtaBlock v;
-    const int4 r = __ldg(reinterpret_cast<const int4*>(a.blocks + b));
+    const int4 r = bl_s[b - b0];
     v.row0 = r.x;
     v.series = r.y;
     v.group = r.z;
@@ -1186,7 +1313,7 @@ __global__ void __launch_bounds__(32 * kCtaWarps, 1) k_triple_cta(const __grid_c
     c0 = t.col0 + cb;
     line0 = t.line0 + ra;
     nrows = t.nrows - ra;
-    const int base = (h & 1) ? a.copy_b / (int)sizeof(C) : 0;
+    const int base = (h & 1) ? a.copy_b / (int)sizeof(EL) : 0;
     ops.rows = base + (t.row_freq0 - a.f_lo) + ra;
     ops.cols = base + (t.col0 - a.f_lo) + cb;
     ops.g = base + (t.plane_freq + t.row_freq0 + t.col0 - a.f_lo) + ra + cb;
@@ -1214,8 +1341,10 @@ __global__ void __launch_bounds__(32 * kCtaWarps, 1) k_triple_cta(const __grid_c
 #pragma unroll
     for (int i = 0; i < 4; i++) {
       if (S * i >= nrows) continue;
-      const int cm = lcm[i];
-      C* dst = P + loff[i];
+      // fp32 (16 warps, 128 registers): the lines' ends are reloaded here
+      // rather than kept live through the compute loop
+      const int cm = Q ? __ldg(a.line_cmax + line0 + S * i) : lcm[i];
+      C* dst = P + (Q ? (int)(__ldg(a.line_start + line0 + S * i) - a.lo) : loff[i]);
 #pragma unroll
       for (int j = 0; j < 8; j++)
         if (c0 + S * j <= cm) dst[c0 + S * j] = acc.template cell<CONJ>(i, j);
@@ -1233,12 +1362,6 @@ __global__ void __launch_bounds__(32 * kCtaWarps, 1) k_triple_cta(const __grid_c
     cur = sg.block;
     enter(nb, 0);
   }
-  CtaStage pre[kCtaMaxDepth];
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int d2 = 1; d2 < kCtaMaxDepth; d2++)
-      if (d2 < depth && d2 < nst) pre[d2] = ld_stage(d2);
-  }
   asm volatile("griddepcontrol.wait;" ::: "memory");
   stamp_start(kStampTriple);  // E is written by the previous kernel
   asm volatile("griddepcontrol.launch_dependents;");
@@ -1246,14 +1369,14 @@ __global__ void __launch_bounds__(32 * kCtaWarps, 1) k_triple_cta(const __grid_c
   // would make the first stage wait for the whole burst), the rest of the
   // ring once it has landed
   if (threadIdx.x == 0 && nst > 0) issue(sg, 0);
+  int d = 0, par = 0, kb = 0;  // ring slot, its mbarrier phase, stage index within the block (mod phases)
   for (int k = 0; k < nst; k++) {
-    const int d = k % depth;
     const CtaStage sg_next = k + 1 < nst ? ld_stage(k + 1) : sg;
-    const CtaStage refill = k + depth < nst ? ld_stage(k + depth) : sg;
     if (sg.block != cur) {
       if (cur >= 0) finalize();
       cur = sg.block;
       enter(nb, k);
+      kb = 0;
     }
     if (sg_next.block != sg.block) nb = ld_block(sg_next.block);
     {
@@ -1261,7 +1384,6 @@ __global__ void __launch_bounds__(32 * kCtaWarps, 1) k_triple_cta(const __grid_c
       // highest warp slot first, so a spinning early warp would take issue
       // slots from the warps still computing on its SM sub-partition
       const unsigned bar = (unsigned)__cvta_generic_to_shared(&full[d]);
-      const unsigned par = (unsigned)(k / depth) & 1u;
       asm volatile(
           "{\n.reg .pred P1;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n@!P1 bra W_%=;\n}\n" ::"r"(
               bar),
@@ -1271,61 +1393,71 @@ __global__ void __launch_bounds__(32 * kCtaWarps, 1) k_triple_cta(const __grid_c
     if (tr && blockIdx.x == a.trace_cta && k < 64) {  // per-stage stamps of one CTA (diagnostics)
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      if (lane == 0) a.trace[4 * gridDim.x * kCtaWarps + 64 * warp + k] = t;
+      if (lane == 0) a.trace[4 * gridDim.x * NW + 64 * warp + k] = t;
     }
     if (k == 0) {
       stamp(1);
       if (threadIdx.x == 0) {
 #pragma unroll
         for (int d2 = 1; d2 < kCtaMaxDepth; d2++)
-          if (d2 < depth && d2 < nst) issue(pre[d2], d2);
+          if (d2 < depth && d2 < nst) issue(ld_stage(d2), d2);
       }
     }
-    const C* q = reinterpret_cast<const C*>(smraw + (size_t)d * a.slot_bytes);
+    const EL* q = reinterpret_cast<const EL*>(smraw + (size_t)d * a.slot_bytes);
     // phases > 1: the warp takes every phases-th STAGE of the block (whole
     // stages keep the 4-segment straight-line block; a warp running one
     // segment per stage measured ~40% of the FMA rate)
-    if (warp_active && (phases == 1 || (k - blk_k0) % phases == phase)) {
-      if (sg.nseg == 4) {
+    if (warp_active && kb == phase) {
+      if (Q) {  // one segment's code at a time: 4 unrolled segments spill at 128 registers
+        const EL* qt = q;
+#pragma unroll 1
+        for (int t = 0; t < sg.nseg; t++, qt += Lp) cta_cells<T, CONJ, ORDER4, S, Q>(qt, ops, acc);
+      } else if (sg.nseg == 4) {
 #pragma unroll
-        for (int t = 0; t < 4; t++) warp_cells<T, CONJ, ORDER4, S>(q + t * Lp, ops, acc);
+        for (int t = 0; t < 4; t++) cta_cells<T, CONJ, ORDER4, S, Q>(q + t * Lp, ops, acc);
       } else {
-        for (int t = 0; t < sg.nseg; t++) warp_cells<T, CONJ, ORDER4, S>(q + t * Lp, ops, acc);
+        for (int t = 0; t < sg.nseg; t++) cta_cells<T, CONJ, ORDER4, S, Q>(q + t * Lp, ops, acc);
       }
     }
     __syncwarp();
     if (tr && blockIdx.x == a.trace_cta && k < 64) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      if (lane == 0) a.trace[4 * gridDim.x * kCtaWarps + 512 + 64 * warp + k] = t;
+      if (lane == 0) a.trace[4 * gridDim.x * NW + 64 * NW + 64 * warp + k] = t;
     }
     if (lane == 0) {
-      __threadfence_block();
-      if (atomicAdd(&cnt[d], 1) == kCtaWarps - 1) {
+      // the warp's reads of slot d are complete (their values were consumed)
+      if (!Q) __threadfence_block();
+      if (atomicAdd(&cnt[d], 1) == NW - 1) {
         atomicExch(&cnt[d], 0);
-        if (k + depth < nst) issue(refill, d);
+        if (k + depth < nst) issue(ld_stage(k + depth), d);
       }
     }
     sg = sg_next;
+    if (++d == depth) {
+      d = 0;
+      par ^= 1;
+    }
+    if (++kb == phases) kb = 0;
   }
   if (cur >= 0) finalize();
   stamp(2);
 }
 
-template <typename T, int S>
+template <typename T, int S, bool Q>
 static cudaError_t configure_cta(size_t smem) {
   cudaError_t e;
-  if ((e = set_smem(k_triple_cta<T, true, false, S>, smem)) != cudaSuccess) return e;
-  if ((e = set_smem(k_triple_cta<T, false, false, S>, smem)) != cudaSuccess) return e;
-  if ((e = set_smem(k_triple_cta<T, true, true, S>, smem)) != cudaSuccess) return e;
-  return set_smem(k_triple_cta<T, false, true, S>, smem);
+  if ((e = set_smem(k_triple_cta<T, true, false, S, Q>, smem)) != cudaSuccess) return e;
+  if ((e = set_smem(k_triple_cta<T, false, false, S, Q>, smem)) != cudaSuccess) return e;
+  if ((e = set_smem(k_triple_cta<T, true, true, S, Q>, smem)) != cudaSuccess) return e;
+  return set_smem(k_triple_cta<T, false, true, S, Q>, smem);
 }
 
-template <typename T, bool CONJ, bool ORDER4, int S>
+template <typename T, bool CONJ, bool ORDER4, int S, bool Q>
 static cudaError_t launch_cta_pdl(const CtaTripleArgs& a, size_t smem, cudaStream_t st) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)a.nctas);
-  cfg.blockDim = dim3(32 * kCtaWarps);
+  cfg.blockDim = dim3(32 * (Q ? kCtaWarpsQ : kCtaWarps));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -1333,32 +1465,35 @@ static cudaError_t launch_cta_pdl(const CtaTripleArgs& a, size_t smem, cudaStrea
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_triple_cta<T, CONJ, ORDER4, S>, a);
+  return cudaLaunchKernelEx(&cfg, k_triple_cta<T, CONJ, ORDER4, S, Q>, a);
 }
 
-template <typename T, int S>
+template <typename T, int S, bool Q>
 static cudaError_t launch_cta_variant(const CtaTripleArgs& a, cudaStream_t st) {
-  const size_t smem = (size_t)a.depth * a.slot_bytes;
+  const size_t smem = (size_t)a.depth * a.slot_bytes + 16 * (size_t)(a.tab_stages + a.tab_blocks);
   static PerDevice configured;  // per instantiation and device: the largest ring enabled once
-  cudaError_t e = configured.once([] { return configure_cta<T, S>(kCtaMaxSmem); });
+  cudaError_t e = configured.once([] { return configure_cta<T, S, Q>(kCtaSmemLimit); });
   if (e != cudaSuccess) return e;
   const bool o4 = a.order == 4;
-  if (a.conj && !o4) return launch_cta_pdl<T, true, false, S>(a, smem, st);
-  if (!a.conj && !o4) return launch_cta_pdl<T, false, false, S>(a, smem, st);
-  if (a.conj) return launch_cta_pdl<T, true, true, S>(a, smem, st);
-  return launch_cta_pdl<T, false, true, S>(a, smem, st);
+  if (a.conj && !o4) return launch_cta_pdl<T, true, false, S, Q>(a, smem, st);
+  if (!a.conj && !o4) return launch_cta_pdl<T, false, false, S, Q>(a, smem, st);
+  if (a.conj) return launch_cta_pdl<T, true, true, S, Q>(a, smem, st);
+  return launch_cta_pdl<T, false, true, S, Q>(a, smem, st);
 }
 
 cudaError_t launch_triple_cta(const CtaTripleArgs& a, int precision, cudaStream_t st) {
   if (a.nctas <= 0) return cudaSuccess;
   if (a.tile_step != 2 && a.tile_step != 4) return cudaErrorInvalidValue;
-  if (a.depth < 1 || a.depth > kCtaMaxDepth || (size_t)a.depth * a.slot_bytes > kCtaMaxSmem)
+  if (a.depth < 1 || a.depth > kCtaMaxDepth || (size_t)a.depth * a.slot_bytes > kCtaMaxSmem ||
+      (size_t)a.depth * a.slot_bytes + 16 * (size_t)(a.tab_stages + a.tab_blocks) > kCtaSmemLimit)
     return cudaErrorInvalidValue;
   cudaError_t e;
-  if (precision == 32)
-    e = a.tile_step == 2 ? launch_cta_variant<float, 2>(a, st) : launch_cta_variant<float, 4>(a, st);
+  if (precision == 32 && a.quad)
+    e = a.tile_step == 2 ? launch_cta_variant<float, 2, true>(a, st) : launch_cta_variant<float, 4, true>(a, st);
+  else if (precision == 32)
+    e = a.tile_step == 2 ? launch_cta_variant<float, 2, false>(a, st) : launch_cta_variant<float, 4, false>(a, st);
   else
-    e = a.tile_step == 2 ? launch_cta_variant<double, 2>(a, st) : launch_cta_variant<double, 4>(a, st);
+    e = a.tile_step == 2 ? launch_cta_variant<double, 2, false>(a, st) : launch_cta_variant<double, 4, false>(a, st);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }

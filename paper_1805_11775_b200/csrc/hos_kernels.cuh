@@ -121,9 +121,12 @@ struct SlotInfo {
 // region's two tiles, and each warp takes every phases-th stage.  A BLOCK is one CTA's
 // segment range of one (series, group); its warps write partial slots
 // slot_base + phase.  A STAGE is up to 4 consecutive E rows of one block.
-constexpr int kCtaWarps = 8;
+constexpr int kCtaWarps = 8;    // float2 / double2 rows, ~252-register cells
+constexpr int kCtaWarpsQ = 16;  // fp32 quad rows (HOS_K2_QUAD=1), <= 128-register cells
+inline int cta_warps(int quad) { return quad ? kCtaWarpsQ : kCtaWarps; }
 constexpr int kCtaMaxDepth = 8;
-constexpr size_t kCtaMaxSmem = 220 * 1024;
+constexpr size_t kCtaMaxSmem = 220 * 1024;    // the staging ring
+constexpr size_t kCtaSmemLimit = 226 * 1024;  // ring + the CTA's stage / block tables (+ static smem <= 227 KB)
 struct CtaGroup {
   int32_t r0, n, phases;
   int32_t halves;     // 2: a region's two tiles go to different warps (n <= kCtaWarps / 2)
@@ -163,6 +166,9 @@ struct CtaTripleArgs {
   int order, conj;
   unsigned long long* trace;  // diagnostics (nullptr: off): per warp {start, first data, end, smid}
   int trace_cta;              // diagnostics: CTA whose per-stage times are traced
+  int quad;                   // fp32: E rows hold quads {re, im, im, im} (cells_q, 16 warps)
+  int tab_stages;             // stage-table entries reserved in shared memory (>= stages of any CTA)
+  int tab_blocks;             // block-table entries reserved in shared memory (>= blocks of any CTA)
   const int* ready;           // nullptr, or per E row: 1 once a concurrently running front end wrote it
   int* err;                   // streaming: set to 1 (host-mapped word) when a ready wait timed out
 };
@@ -187,13 +193,14 @@ constexpr int kFrontMaxM = 4096;
 // ready != nullptr: streaming launch (a PDL dependent of the consuming K2), publishing
 // ready[b*krows + s] = 1 with release semantics once E row s is written
 constexpr int kStreamFrontCtas = 20;  // SMs left to the streaming front end (K2 runs on the rest)
+// quad != 0 (fp32 only): E elements are quads {re, im, im, im} (16 bytes) for k_triple_cta
 cudaError_t launch_front(const void* x, int x_dtype, int64_t x_stride, int m, int nseg, int krows, int batch,
                          int taper, const double* taper_tab, const void* tw, int precision, int f_lo, int L, int Lp,
-                         void* E, cudaStream_t st, int* ready = nullptr);
+                         void* E, cudaStream_t st, int quad, int* ready = nullptr);
 cudaError_t launch_extend_half(const void* H, int m, int hstride, int rows, const void* /*unused*/,
-                               int f_lo, int L, int Lp, int precision, void* E, cudaStream_t st);
+                               int f_lo, int L, int Lp, int precision, void* E, cudaStream_t st, int quad);
 cudaError_t launch_extend_full(const void* S, int spec_dtype, int m, int rows, int f_lo, int L, int Lp,
-                               int precision, void* E, cudaStream_t st);
+                               int precision, void* E, cudaStream_t st, int quad);
 cudaError_t launch_expand_full(const void* H, int m, int hstride, int rows, int precision, void* out,
                                cudaStream_t st);
 cudaError_t launch_triple(const TripleArgs& a, int precision, cudaStream_t st);

@@ -18,8 +18,10 @@ lib = _native.lib()
 assert lib.hos_plan_k2_kind(plan.handle) == 1, "plan does not use k_triple_cta"
 x = torch.from_numpy(P.baseline_series(c)).cuda()
 out = plan.empty_out()
-nw = 148 * 8
-tr = torch.zeros(4 * nw + 2 * 64 * 8, dtype=torch.int64, device="cuda")
+W = 16  # warps per k_triple_cta CTA (fp32 quad kernel)
+nctas = lib.hos_plan_nctas(plan.handle)
+nw = 148 * W
+tr = torch.zeros(4 * nw + 2 * 64 * W, dtype=torch.int64, device="cuda")
 for _ in range(3):
     plan.estimate(x, out)
 lib.hos_plan_set_trace(plan.handle, ctypes.c_void_p(tr.data_ptr()))
@@ -29,11 +31,11 @@ torch.cuda.synchronize()
 lib.hos_plan_set_trace(plan.handle, None)
 tt = tr.cpu().numpy()
 t = tt[:4 * nw].reshape(nw, 4).astype(np.float64)
-st = tt[4 * nw:4 * nw + 512].reshape(8, 64).astype(np.float64)
-sd = tt[4 * nw + 512:].reshape(8, 64).astype(np.float64)
+st = tt[4 * nw:4 * nw + 64 * W].reshape(W, 64).astype(np.float64)
+sd = tt[4 * nw + 64 * W:].reshape(W, 64).astype(np.float64)
 t0 = t[:, 0].min()
 start, first, end = (t[:, 0] - t0) / 1e3, (t[:, 1] - t0) / 1e3, (t[:, 2] - t0) / 1e3
-cta = np.arange(nw) // 8
+cta = np.arange(nw) // W
 print(f"start {start.min():.2f}..{start.max():.2f} us; first data {np.median(first - start):.2f} us after start "
       f"(max {np.max(first - start):.2f}); end {end.min():.2f}..{end.max():.2f} (median {np.median(end):.2f})")
 ce = np.array([end[cta == i].max() for i in range(148)])
@@ -47,5 +49,7 @@ w0 = w0[w0 > 0]
 print("traced CTA, warp 0: stage-ready gaps (us):", np.diff(w0 / 1e3).round(2).tolist())
 base = st[st > 0].min()
 for k in range(0, 24, 1):
-    print(f"stage {k}: ready " + " ".join(f"{(st[w, k] - base) / 1e3:6.2f}" for w in range(8)) +
-          " | done " + " ".join(f"{(sd[w, k] - base) / 1e3:6.2f}" for w in range(8)))
+    if not st[:, k].any():
+        break
+    print(f"stage {k:2d}: ready " + " ".join(f"{(st[w, k] - base) / 1e3:5.1f}" for w in range(W)) +
+          " | done " + " ".join(f"{(sd[w, k] - base) / 1e3:5.1f}" for w in range(W)))
