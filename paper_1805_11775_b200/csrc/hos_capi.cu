@@ -55,6 +55,10 @@ struct hos_plan {
   int sms = 148;
   int max_line = 0;  // longest D_h line (cells)
   bool series_k4 = false;  // K4 as one CTA per series with the grid in shared memory
+  bool sep_k4 = false;     // ... as separable direct window sums (k_smooth_series_sep; else prefix sums)
+  int64_t sep_vitems = 0, sep_hitems = 0;  // k_smooth_series_sep work items
+  int32_t* d_series_slots = nullptr;    // per series: most partial slots of any region (main launch)
+  int32_t* d_s_series_slots = nullptr;  // ... of the streaming schedule
   int split_wa = 1, split_wb = 1;  // K2 WarpSplit weights for two-CTA-per-SM launches
   // K2 as k_triple_cta (CTA-staged full rows, host schedule) for the plan's main launch
   bool cta = false;
@@ -684,7 +688,11 @@ int run_box(hos_plan* p, void* out_dev, cudaStream_t st) {
 int run_smooth(hos_plan* p, void* out_dev, cudaStream_t st, int stage = -1, bool streaming = false) {
   const hos::SlotInfo si = main_slot_info(p, streaming);
   if (p->series_k4) {
-    if (stage != 5)
+    if (stage != 5 && p->sep_k4)
+      CUDA_TRY(hos::launch_smooth_series_sep(p->d_part, p->maxslots, p->geo.ncells, si, p->precision,
+                                             box_args(p, out_dev), p->geo.nlines, p->sep_vitems, p->sep_hitems,
+                                             streaming ? p->d_s_series_slots : p->d_series_slots, st));
+    else if (stage != 5)
       CUDA_TRY(hos::launch_smooth_series3(p->d_part, p->maxslots, p->geo.ncells, si, p->precision,
                                           box_args(p, out_dev), p->geo.nlines, st));
     return HOS_OK;
@@ -968,6 +976,12 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
     const char* env = std::getenv("HOS_K4_SERIES");  // "0": always line scans + box sums
     p->series_k4 = order == 3 && hos::smooth_series3_smem(g.ncells, g.nlines, g.rows, g.nregions, g.npoints) <= 200 * 1024 &&
                    !(env && env[0] == '0');
+    // separable direct window sums (default; HOS_K4_SEP=0: the prefix-sum kernel)
+    const char* sep = std::getenv("HOS_K4_SEP");
+    hos::smooth_series_sep_items(g.row_off.data(), g.rows, m3, &p->sep_vitems, &p->sep_hitems);
+    p->sep_k4 = p->series_k4 && !(sep && sep[0] == '0') && hos::smooth_series_sep_supports(m3) &&
+                hos::smooth_series_sep_smem(g.ncells, g.nlines, g.rows, g.nregions, g.npoints, m3, p->sep_vitems,
+                                            p->sep_hitems, precision) <= 200 * 1024;
   }
   // +4 elements: fp32 operands are staged from the 16-byte-aligned element at
   // or below their start, in whole 16-byte chunks (K2), so a copy may read up
@@ -1024,6 +1038,11 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
   if ((rc = upload(p, &p->d_line_tile0, g.line_tile0))) return bail(rc);
   if (p->stream_ok) {
     if ((rc = upload(p, &p->d_s_region_slots, ssched.region_slots))) return bail(rc);
+    {
+      int32_t mx = 1;
+      for (int32_t v : ssched.region_slots) mx = std::max(mx, v);
+      if ((rc = upload(p, &p->d_s_series_slots, std::vector<int32_t>(1, mx)))) return bail(rc);
+    }
     if ((rc = upload(p, &p->d_s_blocks, ssched.blocks))) return bail(rc);
     if ((rc = upload(p, &p->d_s_stages, ssched.stages))) return bail(rc);
     if ((rc = upload(p, &p->d_s_cta_stage0, ssched.cta_stage0))) return bail(rc);
@@ -1039,6 +1058,10 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
   }
   if (p->cta) {
     if ((rc = upload(p, &p->d_region_slots, sched.region_slots))) return bail(rc);
+    std::vector<int32_t> ss(batch, 1);
+    for (int b = 0; b < batch; b++)
+      for (int r = 0; r < g.nregions; r++) ss[b] = std::max(ss[b], sched.region_slots[(size_t)b * g.nregions + r]);
+    if ((rc = upload(p, &p->d_series_slots, ss))) return bail(rc);
     if ((rc = upload(p, &p->d_groups, sched.groups))) return bail(rc);
     if ((rc = upload(p, &p->d_blocks, sched.blocks))) return bail(rc);
     if ((rc = upload(p, &p->d_stages, sched.stages))) return bail(rc);
@@ -1048,6 +1071,9 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
     std::vector<int32_t> rs(g.nregions);
     for (size_t r = 0; r < rs.size(); r++) rs[r] = sp.region_slots((int)r, k);
     if ((rc = upload(p, &p->d_region_slots, rs))) return bail(rc);
+    int32_t mx = 1;
+    for (int32_t v : rs) mx = std::max(mx, v);
+    if ((rc = upload(p, &p->d_series_slots, std::vector<int32_t>(batch, mx)))) return bail(rc);
   }
   if ((rc = upload(p, &p->d_line_cmax, cmax))) return bail(rc);
   if ((rc = upload(p, &p->d_line_start, g.line_start))) return bail(rc);
@@ -1119,6 +1145,8 @@ void hos_plan_destroy(hos_plan* p) {
                   (void*)p->d_ready})
     if (b) cudaFree(b);
   if (p->h_err) cudaFreeHost(p->h_err);
+  for (void* b : {(void*)p->d_series_slots, (void*)p->d_s_series_slots})
+    if (b) cudaFree(b);
   for (void* b : {p->d_raw, p->d_send, p->d_mine, p->d_local, p->d_heads, p->d_vals, p->d_parts})
     if (b) cudaFree(b);
   void* bufs[] = {p->d_groups, p->d_blocks, p->d_stages, p->d_cta_stage0, p->d_tiles, p->d_line_tile0, p->d_region_slots, p->d_line_cmax, p->d_line_start, p->d_row_off, p->d_pair_k1, p->d_pair_k2,

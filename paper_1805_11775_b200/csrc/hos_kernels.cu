@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <cstdlib>
 #include <mutex>
+#include <algorithm>
 #include <string>
 #include <type_traits>
 #include <cstdint>
@@ -2039,6 +2040,212 @@ __global__ void __launch_bounds__(512, 2) k_smooth_series3(const P2* __restrict_
   }
   }
   }
+}
+
+// K4 for SMALL order-3 grids, SEPARABLE (default): each CTA smooths one
+// series at a time (persistent over series, ~4 CTAs per SM):
+//   V(k1, j)  = sum_{u < W} R(k1 + u, j)          (vertical window, direct sum)
+//   B(k1, k2) = sum_{v < W} V(k1, k2 + v) * scale (horizontal window, direct sum)
+// -- the reference's w x w box (tiled.py:36-47) as two 1-D windows.  Direct
+// sums of W terms in the compute precision (no long prefix chains), so fp32
+// mode stays ~1e-7 of max|B| (numpy emulation of cfg5: 1.1-1.6e-7) without
+// fp64 arithmetic.  The vertical pass reads the raw cells R straight from the
+// partial slots (coalesced along each line; slots summed in slot order for
+// the few series K2 cut between CTAs), each thread holding a strip of
+// kSepT + W - 1 cells of one column in registers and producing kSepT rows; V
+// lives in shared memory and the horizontal pass sums kSepT outputs per
+// thread from one strip of V.  Only V (not R) in shared memory keeps ~4 CTAs
+// per SM.  Measured on cfg5 (220 us for the prefix-sum kernel): 141 us.
+// Rejected (same box, cfg5): R staged by double-buffered bulk copies at one
+// CTA per SM (148-171 us), one warp per row block without CTA barriers
+// (237 us), register-only 2-D tiles (718 us, 166 registers).
+// Compile-time W (3/5/7/9, else the prefix-sum kernel), packed FADD2.
+constexpr int kSepT = 4;
+#ifndef HOS_SEP_THREADS
+#define HOS_SEP_THREADS 256
+#endif
+constexpr int kSepThreads = HOS_SEP_THREADS;
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  unsigned long long ra = *reinterpret_cast<unsigned long long*>(&a), rb = *reinterpret_cast<unsigned long long*>(&b), rd;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(rd) : "l"(ra), "l"(rb));
+  return *reinterpret_cast<float2*>(&rd);
+}
+__device__ __forceinline__ double2 add2(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+
+template <typename P2, int W>
+__global__ void __launch_bounds__(kSepThreads) k_smooth_series_sep(const P2* __restrict__ part, int64_t part_stride,
+                                                                  int64_t part_series_stride, SlotInfo si, BoxArgs a,
+                                                                  int nlines, int nvitems, int nhitems,
+                                                                  const int* __restrict__ series_slots) {
+  StampEnd stamp_end_(kStampSeries);
+  using T = decltype(P2{}.x);
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  const int ncells = (int)a.s_series_stride;
+  const int rows = a.rows;
+  const int nblk = (rows + kSepT - 1) / kSepT;
+  P2* V = reinterpret_cast<P2*>(sm_raw);                       // vertical sums, row-major (vo offsets)
+  int* ls = reinterpret_cast<int*>(V + (a.p_end - a.p_begin) + (int64_t)rows * (W - 1));  // nlines + 1
+  int* ro = ls + nlines + 1;                                   // rows + 1: output offset of each row
+  int* vo = ro + rows + 1;                                     // rows + 1: V offset of each row
+  int* vb = vo + rows + 1;                                     // nblk + 1: first vertical item of each block
+  int* hb = vb + nblk + 1;                                     // rows + 1: first horizontal item of each row
+  int* lt0 = hb + rows + 1;                                    // nlines: first tile of each line
+  int* rsl = lt0 + nlines;                                     // nregions: partial slots per region
+  unsigned short* vrow = reinterpret_cast<unsigned short*>(rsl + si.nregions);  // nvitems: block of each item
+  unsigned short* hrow = vrow + nvitems;                       // nhitems: row of each item
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  // static geometry, once per CTA (before the PDL wait: overlaps K2's tail)
+  for (int i = tid; i <= nlines; i += blockDim.x) ls[i] = (int)__ldg(a.line_start + i);
+  for (int i = tid; i <= rows; i += blockDim.x) ro[i] = (int)__ldg(a.row_off + i);
+  for (int i = tid; i < nlines; i += blockDim.x) lt0[i] = __ldg(si.line_tile0 + i);
+  __syncthreads();
+  if (tid == 0) {
+    int v = 0, h = 0;
+    for (int r = 0; r < rows; r++) {
+      vo[r] = v;
+      hb[r] = h;
+      const int len = ro[r + 1] - ro[r];
+      v += len + W - 1;
+      h += (len + kSepT - 1) / kSepT;
+    }
+    vo[rows] = v;
+    hb[rows] = h;
+    int it = 0;
+    for (int b = 0; b < nblk; b++) {
+      vb[b] = it;
+      int mx = 0;
+      for (int r = b * kSepT; r < min(rows, (b + 1) * kSepT); r++) mx = max(mx, ro[r + 1] - ro[r] + W - 1);
+      it += mx;
+    }
+    vb[nblk] = it;
+  }
+  __syncthreads();
+  for (int b = warp; b < nblk; b += nw)
+    for (int q = vb[b] + lane; q < vb[b + 1]; q += 32) vrow[q] = (unsigned short)b;
+  for (int r = warp; r < rows; r += nw)
+    for (int q = hb[r] + lane; q < hb[r + 1]; q += 32) hrow[q] = (unsigned short)r;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  stamp_start(kStampSeries);  // partial slots come from K2
+  const T sc = (T)a.scale;
+  const int vtot = vo[rows];
+  for (int series = blockIdx.x; series < a.batch; series += gridDim.x) {
+    const P2* src = part + series * part_series_stride;
+    const bool one = __ldg(series_slots + series) == 1;
+    __syncthreads();  // the previous series' reads of V (and rsl) are done
+    if (!one) {
+      for (int r = tid; r < si.nregions; r += blockDim.x) rsl[r] = __ldg(si.region_slots + series * si.rs_stride + r);
+      __syncthreads();
+    }
+    // vertical: item (row block b, column j) -> V(k1 + r, j) for the block's valid rows;
+    // loads past a short line read a neighbour's cells (clamped) and only feed rows that are not stored
+    for (int it = tid; it < nvitems; it += blockDim.x) {
+      const int b = vrow[it], j = it - vb[b], k1 = b * kSepT;
+      P2 x[kSepT + W - 1];
+      if (one) {
+#pragma unroll
+        for (int u = 0; u < kSepT + W - 1; u++) x[u] = __ldcs(src + min(ls[min(k1 + u, nlines - 1)] + j, ncells - 1));
+      } else {  // slots summed in slot order, fp64
+#pragma unroll
+        for (int u = 0; u < kSepT + W - 1; u++) {
+          const int l = min(k1 + u, nlines - 1);
+          const int c = min(ls[l] + j, ncells - 1);
+          const int lc = c < ls[l + 1] ? l : l + 1;  // the line the (clamped) cell belongs to
+          const int ns = rsl[(lt0[lc] + (c - ls[lc]) / si.tile_cols) / si.tiles_per_region];
+          double vr = 0.0, vi = 0.0;
+          for (int t = 0; t < ns; t++) {
+            const P2 q = __ldcs(src + (int64_t)t * part_stride + c);
+            vr += (double)q.x;
+            vi += (double)q.y;
+          }
+          x[u] = P2{(T)vr, (T)vi};
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < kSepT; r++) {
+        P2 acc = x[r];
+#pragma unroll
+        for (int u = 1; u < W; u++) acc = add2(acc, x[r + u]);
+        if (k1 + r < rows && j < ro[k1 + r + 1] - ro[k1 + r] + W - 1) V[vo[k1 + r] + j] = acc;
+      }
+    }
+    __syncthreads();
+    // horizontal: item (row k1, column block c) -> kSepT outputs B(k1, k2) = scale sum_{v < W} V(k1, k2 + v)
+    P2* out = (P2*)a.out + series * a.out_series_stride;
+    for (int it = tid; it < nhitems; it += blockDim.x) {
+      const int k1 = hrow[it], k2 = (it - hb[k1]) * kSepT;
+      const int len = ro[k1 + 1] - ro[k1];
+      const int v0 = vo[k1] + k2;
+      P2 y[kSepT + W - 1];
+#pragma unroll
+      for (int v = 0; v < kSepT + W - 1; v++) y[v] = V[min(v0 + v, vtot - 1)];
+      P2* o = out + ro[k1] + k2;
+#pragma unroll
+      for (int t = 0; t < kSepT; t++) {
+        P2 acc = y[t];
+#pragma unroll
+        for (int v = 1; v < W; v++) acc = add2(acc, y[t + v]);
+        if (k2 + t < len) __stcs(o + t, P2{acc.x * sc, acc.y * sc});
+      }
+    }
+  }
+}
+
+size_t smooth_series_sep_smem(int64_t ncells, int64_t nlines, int rows, int nregions, int64_t npoints, int w,
+                              int64_t nvitems, int64_t nhitems, int precision) {
+  if (nlines > 65535 || rows > 65535 || nvitems > 65535 || ncells > INT32_MAX / 2) return ~(size_t)0;
+  const size_t cs = precision == 32 ? 8 : 16;
+  const int nblk = (rows + kSepT - 1) / kSepT;
+  return (size_t)(npoints + (int64_t)rows * (w - 1)) * cs +
+         (size_t)(nlines + 1 + 3 * (rows + 1) + nblk + 1 + nlines + nregions) * sizeof(int) +
+         (size_t)(nvitems + nhitems) * sizeof(unsigned short) + 16;
+}
+
+// item counts of the separable smoother: vertical (row block, column) items
+// and horizontal (row, kSepT-column block) items
+void smooth_series_sep_items(const int64_t* row_off, int rows, int w, int64_t* nvitems, int64_t* nhitems) {
+  int64_t v = 0, h = 0;
+  for (int b = 0; b * kSepT < rows; b++) {
+    int64_t mx = 0;
+    for (int r = b * kSepT; r < std::min(rows, (b + 1) * kSepT); r++) mx = std::max(mx, row_off[r + 1] - row_off[r] + w - 1);
+    v += mx;
+  }
+  for (int r = 0; r < rows; r++) h += (row_off[r + 1] - row_off[r] + kSepT - 1) / kSepT;
+  *nvitems = v;
+  *nhitems = h;
+}
+
+bool smooth_series_sep_supports(int w) { return w == 3 || w == 5 || w == 7 || w == 9; }
+
+template <typename P2, int W>
+static cudaError_t sep_go(const P2* part, int64_t part_stride, int64_t pss, const SlotInfo& si, const BoxArgs& a,
+                          int64_t nlines, int64_t nvitems, int64_t nhitems, const int* series_slots, size_t sm,
+                          cudaStream_t st) {
+  auto kern = k_smooth_series_sep<P2, W>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSepThreads, sm);
+  const int grid = std::max(1, std::min(a.batch, device_sms() * std::max(1, per_sm)));
+  return launch_pdl_kernel(kern, dim3(grid), dim3(kSepThreads), sm, st, part, part_stride, pss, si, a, (int)nlines,
+                           (int)nvitems, (int)nhitems, series_slots);
+}
+
+cudaError_t launch_smooth_series_sep(const void* part, int nparts, int64_t part_stride, const SlotInfo& si,
+                                     int precision, const BoxArgs& a, int64_t nlines, int64_t nvitems,
+                                     int64_t nhitems, const int* series_slots, cudaStream_t st) {
+  if (!si.line_tile0 || !si.region_slots || !series_slots) return cudaErrorInvalidValue;
+  const size_t sm = smooth_series_sep_smem(a.s_series_stride, nlines, a.rows, si.nregions, a.p_end - a.p_begin, a.m3,
+                                           nvitems, nhitems, precision);
+  const int64_t pss = part_stride * nparts;
+#define HOS_SEP_CASE(P, WW)                                                                                  \
+  case WW:                                                                                                   \
+    return sep_go<P, WW>((const P*)part, part_stride, pss, si, a, nlines, nvitems, nhitems, series_slots, sm, st);
+  if (precision == 32) {
+    switch (a.m3) { HOS_SEP_CASE(float2, 3) HOS_SEP_CASE(float2, 5) HOS_SEP_CASE(float2, 7) HOS_SEP_CASE(float2, 9) }
+  } else {
+    switch (a.m3) { HOS_SEP_CASE(double2, 3) HOS_SEP_CASE(double2, 5) HOS_SEP_CASE(double2, 7) HOS_SEP_CASE(double2, 9) }
+  }
+#undef HOS_SEP_CASE
+  return cudaErrorInvalidValue;
 }
 
 size_t smooth_series3_smem(int64_t ncells, int64_t nlines, int rows, int nregions, int64_t npoints) {

@@ -14,6 +14,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <vector>
 
 #include "hos_geometry.h"
 
@@ -238,6 +239,15 @@ cudaError_t launch_box(const BoxArgs& a, cudaStream_t st);
 size_t smooth_series3_smem(int64_t ncells, int64_t nlines, int rows, int nregions, int64_t npoints);
 cudaError_t launch_smooth_series3(const void* part, int nparts, int64_t part_stride, const SlotInfo& si, int precision,
                                   const BoxArgs& a, int64_t nlines, cudaStream_t st);
+// separable variant (default for small order-3 grids, W in 3/5/7/9): vertical
+// then horizontal direct window sums in the compute precision
+size_t smooth_series_sep_smem(int64_t ncells, int64_t nlines, int rows, int nregions, int64_t npoints, int w,
+                              int64_t nvitems, int64_t nhitems, int precision);
+void smooth_series_sep_items(const int64_t* row_off, int rows, int w, int64_t* nvitems, int64_t* nhitems);
+bool smooth_series_sep_supports(int w);
+cudaError_t launch_smooth_series_sep(const void* part, int nparts, int64_t part_stride, const SlotInfo& si,
+                                     int precision, const BoxArgs& a, int64_t nlines, int64_t nvitems,
+                                     int64_t nhitems, const int* series_slots, cudaStream_t st);
 // raw[c] = sum_p part[p][c] (fp64 sum, stored in the compute precision)
 cudaError_t launch_reduce_parts(const void* part, int64_t part_stride, const SlotInfo& si, const int64_t* line_start,
                                 int64_t nlines, int lo, int precision, void* raw, cudaStream_t st);
