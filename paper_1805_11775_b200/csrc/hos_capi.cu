@@ -1085,8 +1085,11 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
     if ((rc = upload(p, &p->d_line_of_ab, g.line_of_ab))) return bail(rc);
   }
   {
-    std::vector<double> tab(m);
+    // m fp64 weights, then the same m weights rounded to fp32 (the fp32 front end)
+    std::vector<double> tab(m + (m + 1) / 2, 0.0);
     for (int u = 0; u < m; u++) tab[u] = 0.5 - 0.5 * std::cos(2.0 * M_PI * u / m);
+    float* t32 = reinterpret_cast<float*>(tab.data() + m);
+    for (int u = 0; u < m; u++) t32[u] = (float)tab[u];
     if ((rc = upload(p, &p->d_taper, tab))) return bail(rc);
   }
   {

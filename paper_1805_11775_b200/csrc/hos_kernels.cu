@@ -101,6 +101,11 @@ __device__ __forceinline__ double warp_sum(double v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
 
 }  // namespace
 
@@ -155,7 +160,8 @@ cudaError_t launch_prep(const void* x, int x_dtype, int64_t x_stride, int m, int
 
 // ===========================================================================
 // K0+1 (power-of-two m): fused segment + demean (+ taper) + FFT + extension.
-// One CTA per (segment pair, series): the fp64 means exactly as K0, the
+// One CTA per (segment pair, series): means and taper in the compute
+// precision (fp64 mode: exactly as K0; fp32 mode: fp32 sums, ~1e-7), the
 // demeaned (tapered) samples rounded to the compute precision as K0 stores
 // them, packed two segments per complex sequence (z = x_a + i x_b), a
 // radix-4 Stockham FFT in shared memory (natural-order output, twiddles
@@ -236,8 +242,14 @@ __global__ void __launch_bounds__(front_threads<LOG2M>() * front_pairs<LOG2M>(),
   CT* bufA = reinterpret_cast<CT*>(fsm) + grp * 3 * M;
   CT* bufB = bufA + M;
   CT* tws = bufB + M;  // twiddle table staged in shared memory
-  __shared__ double2 red_all[PPC][TH / 32];
-  double2* red = red_all[grp];
+  // demean / taper arithmetic: fp64 in fp64 mode, fp32 in fp32 mode (the
+  // demeaned samples are rounded to fp32 anyway; fp64 sums and F2F
+  // conversions were the front end's short-scoreboard stalls on cfg5)
+  using A = T;
+  using A2 = typename C2<A>::t;
+  __shared__ A2 red_all[PPC][TH / 32];
+  A2* red = red_all[grp];
+  const A* tabA = sizeof(T) == 4 ? reinterpret_cast<const A*>(tab + M) : reinterpret_cast<const A*>(tab);
   const int tid = threadIdx.x % TH;
   auto sync = [] {
     if constexpr (PPC > 1) __syncwarp();
@@ -275,33 +287,33 @@ __global__ void __launch_bounds__(front_threads<LOG2M>() * front_pairs<LOG2M>(),
   const int sa = 2 * pi;
   const bool has_b = sa + 1 < nseg;
   // samples and taper weights stay in registers between the means and the store
-  double wv[VPT];
-  double s_a = 0.0, s_b = 0.0;
+  A wv[VPT];
+  A s_a = A(0), s_b = A(0);
 #pragma unroll
   for (int i = 0; i < VPT; i++) {
     const int u = tid + i * TH;
     if (M % TH == 0 || u < M) {
-      wv[i] = taper ? tab[u] : 1.0;
-      s_a += (double)xa[i];
-      s_b += (double)xb[i];
+      wv[i] = taper ? tabA[u] : A(1);
+      s_a += (A)xa[i];
+      s_b += (A)xb[i];
     }
   }
   s_a = warp_sum(s_a);
   s_b = warp_sum(s_b);
-  if ((tid & 31) == 0) red[tid >> 5] = make_double2(s_a, s_b);
+  if ((tid & 31) == 0) red[tid >> 5] = A2{s_a, s_b};
   sync();
-  double ta = 0.0, tb = 0.0;
+  A ta = A(0), tb = A(0);
 #pragma unroll
   for (int w = 0; w < TH / 32; w++) {
     ta += red[w].x;
     tb += red[w].y;
   }
-  const double mean_a = ta / (double)M, mean_b = tb / (double)M;
+  const A mean_a = ta / (A)M, mean_b = tb / (A)M;
 #pragma unroll
   for (int i = 0; i < VPT; i++) {
     const int u = tid + i * TH;
     if (M % TH == 0 || u < M) {
-      double va = (double)xa[i] - mean_a, vb = (double)xb[i] - mean_b;
+      A va = (A)xa[i] - mean_a, vb = (A)xb[i] - mean_b;
       if (taper) {
         va *= wv[i];
         vb *= wv[i];
