@@ -120,6 +120,7 @@ struct hos_plan {
   void* d_heads = nullptr;      // nranks x halo (or nranks x block when the halo spans ranks)
   void* d_vals = nullptr;       // pmax: this rank's values
   void* d_parts = nullptr;      // nranks x pmax gathered values
+  int64_t* d_send_line = nullptr;  // per line: index of its first cell in the padded send buffer
   std::map<int, cufftHandle> ffts;  // rows -> plan
   // CUDA graphs of the whole stream-ordered pipeline, one per buffer binding
   struct GraphKey {
@@ -877,6 +878,10 @@ struct NcclApi {
   decltype(&ncclGetErrorString) error_string = nullptr;
   decltype(&ncclCommCount) comm_count = nullptr;
   decltype(&ncclCommUserRank) comm_rank = nullptr;
+  decltype(&ncclSend) send = nullptr;
+  decltype(&ncclRecv) recv = nullptr;
+  decltype(&ncclGroupStart) group_start = nullptr;
+  decltype(&ncclGroupEnd) group_end = nullptr;
 };
 const NcclApi* nccl_api(std::string* why) {
   static NcclApi api;
@@ -893,7 +898,12 @@ const NcclApi* nccl_api(std::string* why) {
       api.error_string = (decltype(api.error_string))dlsym(h, "ncclGetErrorString");
       api.comm_count = (decltype(api.comm_count))dlsym(h, "ncclCommCount");
       api.comm_rank = (decltype(api.comm_rank))dlsym(h, "ncclCommUserRank");
-      ok = api.reduce_scatter && api.all_gather && api.error_string && api.comm_count && api.comm_rank;
+      api.send = (decltype(api.send))dlsym(h, "ncclSend");
+      api.recv = (decltype(api.recv))dlsym(h, "ncclRecv");
+      api.group_start = (decltype(api.group_start))dlsym(h, "ncclGroupStart");
+      api.group_end = (decltype(api.group_end))dlsym(h, "ncclGroupEnd");
+      ok = api.reduce_scatter && api.all_gather && api.error_string && api.comm_count && api.comm_rank &&
+           api.send && api.recv && api.group_start && api.group_end;
     }
   }
   if (!ok && why) *why = "libnccl.so.2 (ncclReduceScatter, ncclAllGather) is not loadable";
@@ -1150,7 +1160,7 @@ void hos_plan_destroy(hos_plan* p) {
   if (p->h_err) cudaFreeHost(p->h_err);
   for (void* b : {(void*)p->d_series_slots, (void*)p->d_s_series_slots})
     if (b) cudaFree(b);
-  for (void* b : {p->d_raw, p->d_send, p->d_mine, p->d_local, p->d_heads, p->d_vals, p->d_parts})
+  for (void* b : {p->d_raw, p->d_send, p->d_mine, p->d_local, p->d_heads, p->d_vals, p->d_parts, (void*)p->d_send_line})
     if (b) cudaFree(b);
   void* bufs[] = {p->d_groups, p->d_blocks, p->d_stages, p->d_cta_stage0, p->d_tiles, p->d_line_tile0, p->d_region_slots, p->d_line_cmax, p->d_line_start, p->d_row_off, p->d_pair_k1, p->d_pair_k2,
                   p->d_pair_base, p->d_line_of_ab, p->d_taper, p->d_tw, p->d_seg, p->d_half, p->d_E, p->d_part,
@@ -1368,6 +1378,9 @@ int hos_estimate_host(hos_plan* p, const void* x_host, int x_dtype, int64_t x_st
   return HOS_OK;
 }
 
+int partial_raw_impl(hos_plan* p, const void* x_dev, int x_dtype, int seg_begin, int seg_end, void* raw_dev,
+                     cudaStream_t st, const int64_t* dst_line, size_t zero_bytes);
+
 int hos_partial_raw(hos_plan* p, const void* x_dev, int x_dtype, int seg_begin, int seg_end, void* raw_dev,
                     void* stream) {
   int rc = check_plan(p);
@@ -1379,10 +1392,19 @@ int hos_partial_raw(hos_plan* p, const void* x_dev, int x_dtype, int seg_begin, 
     return fail(HOS_EPARAM, "segment range [" + std::to_string(seg_begin) + ", " + std::to_string(seg_end) +
                                 ") outside [0, " + std::to_string(p->k) + ")");
   if (!raw_dev) return fail(HOS_EPARAM, "null buffer");
-  cudaStream_t st = (cudaStream_t)stream;
+  return partial_raw_impl(p, x_dev, x_dtype, seg_begin, seg_end, raw_dev, (cudaStream_t)stream, nullptr,
+                          p->geo.ncells * csize(p->precision));
+}
+
+// front end + K2 + slot reduction over segments [seg_begin, seg_end) of the
+// single series; cell c of line l lands at raw[dst_line[l] + c - line_start[l]]
+// (dst_line nullptr: raw[c]); an empty range zeroes zero_bytes of raw
+int partial_raw_impl(hos_plan* p, const void* x_dev, int x_dtype, int seg_begin, int seg_end, void* raw_dev,
+                     cudaStream_t st, const int64_t* dst_line, size_t zero_bytes) {
+  int rc = HOS_OK;
   const int nseg = seg_end - seg_begin;
   if (nseg == 0) {
-    CUDA_TRY(cudaMemsetAsync(raw_dev, 0, p->geo.ncells * csize(p->precision), st));
+    CUDA_TRY(cudaMemsetAsync(raw_dev, 0, zero_bytes, st));
     return HOS_OK;
   }
   // front end on the shard only, written at its own segment rows
@@ -1404,7 +1426,7 @@ int hos_partial_raw(hos_plan* p, const void* x_dev, int x_dtype, int seg_begin, 
   const hos::TripleArgs ta = triple_args(p, seg_begin, seg_end, n, 1);
   CUDA_TRY(hos::launch_triple(ta, p->precision, st));
   CUDA_TRY(hos::launch_reduce_parts(p->d_part, p->geo.ncells, slot_info(p, nseg, n), p->d_line_start, p->geo.nlines,
-                                    p->geo.win.lo, p->precision, raw_dev, st));
+                                    p->geo.win.lo, p->precision, raw_dev, st, dst_line));
   return HOS_OK;
 }
 
@@ -1805,6 +1827,7 @@ int hos_comm_attach(hos_plan* p, void* nccl_comm, int rank, int nranks) {
     const int64_t* R = L + kLayoutPerRank * r;
     pmax = std::max(pmax, R[13] - R[12]);
     local = std::max(local, std::max(R[11], R[9]) - R[8]);
+    local = std::max(local, block + halo);  // the reduce-scatter lands a whole padded block at its head
   }
   const size_t cs = csize(p->precision);
   const int64_t heads = in_next ? halo : block;
@@ -1813,6 +1836,17 @@ int hos_comm_attach(hos_plan* p, void* nccl_comm, int rank, int nranks) {
       (rc = alloc(p, &p->d_heads, (size_t)nranks * heads * cs)) || (rc = alloc(p, &p->d_vals, (size_t)pmax * cs)) ||
       (rc = alloc(p, &p->d_parts, (size_t)nranks * pmax * cs)))
     return rc;
+  {  // line -> padded send-buffer position: owner r's cells start at r * block
+    std::vector<int64_t> dl(p->geo.nlines);
+    int r = 0;
+    for (int64_t l = 0; l < p->geo.nlines; l++) {
+      while (r + 1 < nranks && l >= L[kLayoutPerRank * r + 5]) r++;  // own_l1 of rank r
+      dl[l] = (int64_t)r * block + (p->geo.line_start[l] - L[kLayoutPerRank * r + 8]);
+    }
+    if (p->d_send_line) cudaFree(p->d_send_line);
+    p->d_send_line = nullptr;
+    if ((rc = upload(p, &p->d_send_line, dl))) return rc;
+  }
   p->comm = nccl_comm;
   p->rank = rank;
   p->nranks = nranks;
@@ -1851,30 +1885,31 @@ int estimate_distributed_body(hos_plan* p, const void* x_dev, int x_dtype, void*
   const bool in_next = L[kLayoutPerRank * n + 2] != 0;
   const size_t cs = csize(p->precision);
   const ncclDataType_t dt = p->precision == 32 ? ncclFloat32 : ncclFloat64;  // complex as 2 reals
-  char* raw = (char*)p->d_raw;
-  // 1. partial raw sums of this rank's segments over all of D_h
-  if ((rc = hos_partial_raw(p, x_dev, x_dtype, (int)R[0], (int)R[1], raw, stream))) return rc;
-  // 2. reduce-scatter by owned line blocks (padded to a common block)
-  CUDA_TRY(cudaMemsetAsync(p->d_send, 0, (size_t)n * block * cs, st));
-  for (int r = 0; r < n; r++) {
-    const int64_t* Q = L + kLayoutPerRank * r;
-    if (Q[9] > Q[8])
-      CUDA_TRY(cudaMemcpyAsync((char*)p->d_send + (size_t)r * block * cs, raw + (size_t)Q[8] * cs,
-                               (size_t)(Q[9] - Q[8]) * cs, cudaMemcpyDeviceToDevice, st));
-  }
-  NCCL_TRY(api, api->reduce_scatter(p->d_send, p->d_mine, (size_t)block * 2, dt, ncclSum, comm, st));
-  // 3. local lines = own block + the halo past it (held by the following rank(s))
+  // 1. partial raw sums of this rank's segments over all of D_h, reduced from
+  // K2's slots straight into the padded reduce-scatter send buffer (rank r's
+  // owned cells at r * block; the padding is never written -- what NCCL sums
+  // into the padded tail of the received block is never read)
+  if ((rc = partial_raw_impl(p, x_dev, x_dtype, (int)R[0], (int)R[1], p->d_send, st, p->d_send_line,
+                             (size_t)n * block * cs)))
+    return rc;
+  // 2. reduce-scatter by owned line blocks, straight into the head of the
+  // local lines (own block, then the halo past it)
   const int64_t oc0 = R[8], oc1 = R[9], nc1 = R[11];
   char* local = (char*)p->d_local;
-  if (oc1 > oc0) CUDA_TRY(cudaMemcpyAsync(local, p->d_mine, (size_t)(oc1 - oc0) * cs, cudaMemcpyDeviceToDevice, st));
+  NCCL_TRY(api, api->reduce_scatter(p->d_send, local, (size_t)block * 2, dt, ncclSum, comm, st));
   const int64_t need = std::max<int64_t>(0, nc1 - oc1);
   if (in_next) {
-    NCCL_TRY(api, api->all_gather(p->d_mine, p->d_heads, (size_t)halo * 2, dt, comm, st));  // block heads
-    if (need)
-      CUDA_TRY(cudaMemcpyAsync(local + (size_t)(oc1 - oc0) * cs, (char*)p->d_heads + (size_t)(me + 1) * halo * cs,
-                               (size_t)need * cs, cudaMemcpyDeviceToDevice, st));
-  } else {
-    NCCL_TRY(api, api->all_gather(p->d_mine, p->d_heads, (size_t)block * 2, dt, comm, st));
+    // 3. halo: the w-1 lines past the own block are the head of rank me+1's
+    // block -- one send/recv pair per neighbour
+    const int64_t need_prev = me > 0 ? std::max<int64_t>(0, L[kLayoutPerRank * (me - 1) + 11] -
+                                                                L[kLayoutPerRank * (me - 1) + 9])
+                                     : 0;
+    NCCL_TRY(api, api->group_start());
+    if (need) NCCL_TRY(api, api->recv(local + (size_t)(oc1 - oc0) * cs, (size_t)need * 2, dt, me + 1, comm, st));
+    if (need_prev) NCCL_TRY(api, api->send(local, (size_t)need_prev * 2, dt, me - 1, comm, st));
+    NCCL_TRY(api, api->group_end());
+  } else {  // halo spans several ranks' blocks: gather every block
+    NCCL_TRY(api, api->all_gather(local, p->d_heads, (size_t)block * 2, dt, comm, st));
     for (int r = me + 1; r < n; r++) {
       const int64_t* Q = L + kLayoutPerRank * r;
       const int64_t lo = std::max(Q[8], oc1), hi = std::min(Q[9], nc1);

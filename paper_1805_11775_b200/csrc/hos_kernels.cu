@@ -2319,29 +2319,34 @@ cudaError_t launch_box(const BoxArgs& a, cudaStream_t st) {
 
 template <typename P2>
 __global__ void __launch_bounds__(256) k_reduce_parts(const P2* __restrict__ part, int64_t stride, SlotInfo si,
-                                                      const int64_t* __restrict__ line_start, P2* __restrict__ raw) {
+                                                      const int64_t* __restrict__ line_start, P2* __restrict__ raw,
+                                                      const int64_t* __restrict__ dst_line) {
   StampEnd stamp_end_(kStampReduce);
   stamp_start(kStampReduce);
   const int64_t l = blockIdx.x;
   const int64_t c0 = line_start[l], c1 = line_start[l + 1];
+  // dst_line: per line, where its first cell goes (the multi-GPU path writes
+  // the padded reduce-scatter send buffer directly); nullptr: cell order
+  P2* dst = raw + (dst_line ? dst_line[l] : c0) - c0;
   for (int64_t idx = c0 + threadIdx.x; idx < c1; idx += blockDim.x) {
     double sr = 0.0, si_ = 0.0;
     sum_slots(part, cell_slots(si, 1, l, idx - c0, 0), stride, idx, sr, si_);
-    raw[idx].x = sr;
-    raw[idx].y = si_;
+    dst[idx].x = sr;
+    dst[idx].y = si_;
   }
 }
 
 cudaError_t launch_reduce_parts(const void* part, int64_t part_stride, const SlotInfo& si, const int64_t* line_start,
-                                int64_t nlines, int lo, int precision, void* raw, cudaStream_t st) {
+                                int64_t nlines, int lo, int precision, void* raw, cudaStream_t st,
+                                const int64_t* dst_line) {
   (void)lo;
   if (nlines <= 0) return cudaSuccess;
   if (precision == 32)
     k_reduce_parts<float2><<<(unsigned)nlines, 256, 0, st>>>((const float2*)part, part_stride, si, line_start,
-                                                             (float2*)raw);
+                                                             (float2*)raw, dst_line);
   else
     k_reduce_parts<double2><<<(unsigned)nlines, 256, 0, st>>>((const double2*)part, part_stride, si, line_start,
-                                                              (double2*)raw);
+                                                              (double2*)raw, dst_line);
   return cudaGetLastError();
 }
 

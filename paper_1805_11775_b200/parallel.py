@@ -13,7 +13,7 @@ process per GPU, segments sharded across ranks, each rank computes partial
 raw sums over the whole dilated domain D_h (hos_partial_raw), the partials
 are reduce-scattered by contiguous line blocks (padded to a common count,
 as NCCL requires), each rank fetches the w-1 lines of halo it needs from the
-next rank (all_gather of block heads), smooths its own output rows
+next rank (one send/recv pair per neighbour), smooths its own output rows
 (hos_smooth_raw) and the lexicographic slices are all-gathered.  The
 collective plumbing is torch.distributed (NCCL on GPUs, gloo in the CPU
 tests); the compute hooks are injectable so the orchestration is tested on
@@ -288,13 +288,22 @@ def distributed_estimate(x, cfg: EstimationConfig, *, group=None, engine=None, g
     local[: oc1 - oc0] = mine[: oc1 - oc0]
     # halo: lines past the owned block, held by the following rank(s)
     if lay.halo_in_next:
-        head = engine.zeros(lay.halo, raw.dtype)
-        n_head = min(lay.halo, oc1 - oc0)
-        head[:n_head] = mine[:n_head]
-        heads = _all_gather(dist, engine, head, nranks, group)
+        # one send/recv pair per neighbour: rank r+1 sends the head of its
+        # block (the w-1 lines rank r's rows read past its own block)
         need = max(0, nc1 - oc1)
+        need_prev = max(0, lay.need_cells[rank - 1][1] - lay.own_cells[rank - 1][1]) if rank > 0 else 0
+        ops = []
+        recv_buf = engine.zeros(max(need, 1), raw.dtype)
         if need:
-            local[oc1 - oc0: oc1 - oc0 + need] = heads[rank + 1][:need]
+            ops.append(dist.P2POp(dist.irecv, engine.as_real(recv_buf), _global_rank(dist, group, rank + 1), group))
+        if need_prev:
+            ops.append(dist.P2POp(dist.isend, engine.as_real(mine[:need_prev].clone()),
+                                  _global_rank(dist, group, rank - 1), group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        if need:
+            local[oc1 - oc0: oc1 - oc0 + need] = recv_buf[:need]
     else:
         blocks = _all_gather(dist, engine, mine, nranks, group)
         for r in range(rank + 1, nranks):
@@ -361,6 +370,10 @@ def native_distributed_plan(cfg: EstimationConfig, group=None):
     plan.comm_attach(comm.value, rank, nranks)
     _NATIVE[key] = (plan, nccl, comm)
     return plan
+
+
+def _global_rank(dist, group, r):
+    return r if group is None else dist.get_global_rank(group, r)
 
 
 def _reduce_scatter(dist, engine, out, inp, group):
