@@ -292,18 +292,21 @@ def distributed_estimate(x, cfg: EstimationConfig, *, group=None, engine=None, g
         # block (the w-1 lines rank r's rows read past its own block)
         need = max(0, nc1 - oc1)
         need_prev = max(0, lay.need_cells[rank - 1][1] - lay.own_cells[rank - 1][1]) if rank > 0 else 0
+        # gloo moves point-to-point messages between host tensors only
+        host = dist.get_backend(group) == "gloo"
+        stage = (lambda t: t.cpu()) if host else (lambda t: t)
         ops = []
-        recv_buf = engine.zeros(max(need, 1), raw.dtype)
+        recv_buf = stage(engine.zeros(max(need, 1), raw.dtype))
         if need:
             ops.append(dist.P2POp(dist.irecv, engine.as_real(recv_buf), _global_rank(dist, group, rank + 1), group))
         if need_prev:
-            ops.append(dist.P2POp(dist.isend, engine.as_real(mine[:need_prev].clone()),
+            ops.append(dist.P2POp(dist.isend, engine.as_real(stage(mine[:need_prev]).clone()),
                                   _global_rank(dist, group, rank - 1), group))
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
         if need:
-            local[oc1 - oc0: oc1 - oc0 + need] = recv_buf[:need]
+            local[oc1 - oc0: oc1 - oc0 + need] = recv_buf[:need].to(local.device)
     else:
         blocks = _all_gather(dist, engine, mine, nranks, group)
         for r in range(rank + 1, nranks):
