@@ -121,6 +121,15 @@ struct hos_plan {
   void* d_vals = nullptr;       // pmax: this rank's values
   void* d_parts = nullptr;      // nranks x pmax gathered values
   int64_t* d_send_line = nullptr;  // per line: index of its first cell in the padded send buffer
+  // fused reduce-scatter over peer memory (HOS_DIST_P2P != 0): every rank's
+  // slot reduction stores its partial sums straight into the owner rank's
+  // landing buffer (nranks x block, one slot per source rank) through CUDA IPC
+  // mappings; the owner adds the slots in rank order after a barrier
+  bool p2p = false;
+  void* d_land = nullptr;
+  std::vector<void*> peer_land;               // per rank (this rank's own: d_land), IPC-opened
+  unsigned long long* d_p2p_line = nullptr;   // per line: address of its first cell in the owner's slot
+  void* d_bar = nullptr;                      // barrier all-gather scratch (nranks floats)
   std::map<int, cufftHandle> ffts;  // rows -> plan
   // CUDA graphs of the whole stream-ordered pipeline, one per buffer binding
   struct GraphKey {
@@ -917,6 +926,91 @@ const NcclApi* nccl_api(std::string* why) {
                                                        (api)->error_string(r_));                     \
   } while (0)
 
+namespace {
+
+void release_p2p(hos_plan* p) {
+  for (size_t r = 0; r < p->peer_land.size(); r++)
+    if (p->peer_land[r] && p->peer_land[r] != p->d_land) cudaIpcCloseMemHandle(p->peer_land[r]);
+  p->peer_land.clear();
+  for (void* b : {p->d_land, (void*)p->d_p2p_line, p->d_bar})
+    if (b) cudaFree(b);
+  p->d_land = nullptr;
+  p->d_p2p_line = nullptr;
+  p->d_bar = nullptr;
+  p->p2p = false;
+}
+
+// Landing buffers + IPC handle exchange over the communicator (one
+// all-gather of the 64-byte handles); any failure leaves the NCCL
+// reduce-scatter path in place (p->p2p false)
+int setup_p2p(hos_plan* p, const NcclApi* api, ncclComm_t comm, int me, int n) {
+  release_p2p(p);
+  // default: on with more than one rank (one rank has nothing to exchange and
+  // the plain send-layout reduction is faster: 13.7 vs 22 us on cfg2);
+  // HOS_DIST_P2P=1 forces it on (tests), =0 off
+  const char* env = std::getenv("HOS_DIST_P2P");
+  if (env ? env[0] == '0' : n == 1) return HOS_OK;
+  const int64_t* L = p->layout.data();
+  const int64_t block = L[kLayoutPerRank * n];
+  const size_t cs = csize(p->precision);
+  int rc = HOS_OK;
+  if ((rc = alloc(p, &p->d_land, (size_t)n * block * cs)) || (rc = alloc(p, &p->d_bar, (size_t)n * 8))) return rc;
+  p->peer_land.assign(n, nullptr);
+  p->peer_land[me] = p->d_land;
+  if (n > 1) {
+    cudaIpcMemHandle_t h;
+    if (cudaIpcGetMemHandle(&h, p->d_land) != cudaSuccess) {
+      cudaGetLastError();
+      release_p2p(p);
+      return HOS_OK;
+    }
+    void* dh = nullptr;
+    CUDA_TRY(cudaMalloc(&dh, (size_t)(n + 1) * sizeof(h)));
+    CUDA_TRY(cudaMemcpy((char*)dh + (size_t)n * sizeof(h), &h, sizeof(h), cudaMemcpyHostToDevice));
+    NCCL_TRY(api, api->all_gather((char*)dh + (size_t)n * sizeof(h), dh, sizeof(h), ncclInt8, comm, nullptr));
+    std::vector<cudaIpcMemHandle_t> all(n);
+    const cudaError_t e = cudaMemcpy(all.data(), dh, (size_t)n * sizeof(h), cudaMemcpyDeviceToHost);
+    cudaFree(dh);
+    CUDA_TRY(e);
+    for (int r = 0; r < n; r++) {
+      if (r == me) continue;
+      if (cudaIpcOpenMemHandle(&p->peer_land[r], all[r], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        p->peer_land[r] = nullptr;
+        release_p2p(p);  // every rank must agree: fall back only if all do (checked below)
+        break;
+      }
+    }
+    // agree: all ranks use p2p only if every rank opened every peer
+    float ok = p->peer_land.empty() ? 0.f : 1.f;
+    std::vector<float> oks(n, 0.f);
+    void* db = nullptr;
+    CUDA_TRY(cudaMalloc(&db, (size_t)(n + 1) * sizeof(float)));
+    CUDA_TRY(cudaMemcpy((float*)db + n, &ok, sizeof(float), cudaMemcpyHostToDevice));
+    NCCL_TRY(api, api->all_gather((float*)db + n, db, 1, ncclFloat32, comm, nullptr));
+    CUDA_TRY(cudaMemcpy(oks.data(), db, (size_t)n * sizeof(float), cudaMemcpyDeviceToHost));
+    cudaFree(db);
+    for (float v : oks)
+      if (v != 1.f) {
+        release_p2p(p);
+        return HOS_OK;
+      }
+  }
+  // per line: the address of its first cell in the owner's landing slot `me`
+  std::vector<unsigned long long> da(p->geo.nlines);
+  int r = 0;
+  for (int64_t l = 0; l < p->geo.nlines; l++) {
+    while (r + 1 < n && l >= L[kLayoutPerRank * r + 5]) r++;  // own_l1 of rank r
+    const int64_t off = (int64_t)me * block + (p->geo.line_start[l] - L[kLayoutPerRank * r + 8]);
+    da[l] = (unsigned long long)((char*)p->peer_land[r] + (size_t)off * cs);
+  }
+  if ((rc = upload(p, &p->d_p2p_line, da))) return rc;
+  p->p2p = true;
+  return HOS_OK;
+}
+
+}  // namespace
+
 extern "C" {
 
 const char* hos_version(void) { return "hos_b200 0.1.0 sm_100a"; }
@@ -1158,6 +1252,7 @@ void hos_plan_destroy(hos_plan* p) {
                   (void*)p->d_ready})
     if (b) cudaFree(b);
   if (p->h_err) cudaFreeHost(p->h_err);
+  release_p2p(p);
   for (void* b : {(void*)p->d_series_slots, (void*)p->d_s_series_slots})
     if (b) cudaFree(b);
   for (void* b : {p->d_raw, p->d_send, p->d_mine, p->d_local, p->d_heads, p->d_vals, p->d_parts, (void*)p->d_send_line})
@@ -1379,7 +1474,8 @@ int hos_estimate_host(hos_plan* p, const void* x_host, int x_dtype, int64_t x_st
 }
 
 int partial_raw_impl(hos_plan* p, const void* x_dev, int x_dtype, int seg_begin, int seg_end, void* raw_dev,
-                     cudaStream_t st, const int64_t* dst_line, size_t zero_bytes);
+                     cudaStream_t st, const int64_t* dst_line, size_t zero_bytes,
+                     const unsigned long long* dst_addr = nullptr);
 
 int hos_partial_raw(hos_plan* p, const void* x_dev, int x_dtype, int seg_begin, int seg_end, void* raw_dev,
                     void* stream) {
@@ -1400,10 +1496,20 @@ int hos_partial_raw(hos_plan* p, const void* x_dev, int x_dtype, int seg_begin, 
 // single series; cell c of line l lands at raw[dst_line[l] + c - line_start[l]]
 // (dst_line nullptr: raw[c]); an empty range zeroes zero_bytes of raw
 int partial_raw_impl(hos_plan* p, const void* x_dev, int x_dtype, int seg_begin, int seg_end, void* raw_dev,
-                     cudaStream_t st, const int64_t* dst_line, size_t zero_bytes) {
+                     cudaStream_t st, const int64_t* dst_line, size_t zero_bytes,
+                     const unsigned long long* dst_addr) {
   int rc = HOS_OK;
   const int nseg = seg_end - seg_begin;
   if (nseg == 0) {
+    if (dst_addr) {  // zero this rank's slot in every owner's landing buffer
+      const int64_t* L = p->layout.data();
+      const int n = p->nranks;
+      const int64_t block = L[kLayoutPerRank * n];
+      for (int r = 0; r < n; r++)
+        CUDA_TRY(cudaMemsetAsync((char*)p->peer_land[r] + (size_t)p->rank * block * csize(p->precision), 0,
+                                 (size_t)block * csize(p->precision), st));
+      return HOS_OK;
+    }
     CUDA_TRY(cudaMemsetAsync(raw_dev, 0, zero_bytes, st));
     return HOS_OK;
   }
@@ -1426,7 +1532,7 @@ int partial_raw_impl(hos_plan* p, const void* x_dev, int x_dtype, int seg_begin,
   const hos::TripleArgs ta = triple_args(p, seg_begin, seg_end, n, 1);
   CUDA_TRY(hos::launch_triple(ta, p->precision, st));
   CUDA_TRY(hos::launch_reduce_parts(p->d_part, p->geo.ncells, slot_info(p, nseg, n), p->d_line_start, p->geo.nlines,
-                                    p->geo.win.lo, p->precision, raw_dev, st, dst_line));
+                                    p->geo.win.lo, p->precision, raw_dev, st, dst_line, dst_addr));
   return HOS_OK;
 }
 
@@ -1847,6 +1953,7 @@ int hos_comm_attach(hos_plan* p, void* nccl_comm, int rank, int nranks) {
     p->d_send_line = nullptr;
     if ((rc = upload(p, &p->d_send_line, dl))) return rc;
   }
+  if ((rc = setup_p2p(p, api, (ncclComm_t)nccl_comm, rank, nranks))) return rc;
   p->comm = nccl_comm;
   p->rank = rank;
   p->nranks = nranks;
@@ -1889,14 +1996,25 @@ int estimate_distributed_body(hos_plan* p, const void* x_dev, int x_dtype, void*
   // K2's slots straight into the padded reduce-scatter send buffer (rank r's
   // owned cells at r * block; the padding is never written -- what NCCL sums
   // into the padded tail of the received block is never read)
-  if ((rc = partial_raw_impl(p, x_dev, x_dtype, (int)R[0], (int)R[1], p->d_send, st, p->d_send_line,
-                             (size_t)n * block * cs)))
-    return rc;
-  // 2. reduce-scatter by owned line blocks, straight into the head of the
-  // local lines (own block, then the halo past it)
   const int64_t oc0 = R[8], oc1 = R[9], nc1 = R[11];
   char* local = (char*)p->d_local;
-  NCCL_TRY(api, api->reduce_scatter(p->d_send, local, (size_t)block * 2, dt, ncclSum, comm, st));
+  if (p->p2p) {
+    // 1+2 fused: the slot reduction stores each owner's cells straight into
+    // its landing slot `me` over NVLink (peer stores from the epilogue
+    // kernel); a barrier (all-gather of one float per rank) orders them
+    // before every owner adds its nranks slots in rank order
+    if ((rc = partial_raw_impl(p, x_dev, x_dtype, (int)R[0], (int)R[1], nullptr, st, nullptr, 0, p->d_p2p_line)))
+      return rc;
+    NCCL_TRY(api, api->all_gather((char*)p->d_bar + (size_t)me * 4, p->d_bar, 1, ncclFloat32, comm, st));
+    CUDA_TRY(hos::launch_sum_land(p->d_land, n, block, oc1 - oc0, p->precision, local, st));
+  } else {
+    if ((rc = partial_raw_impl(p, x_dev, x_dtype, (int)R[0], (int)R[1], p->d_send, st, p->d_send_line,
+                               (size_t)n * block * cs)))
+      return rc;
+    // 2. reduce-scatter by owned line blocks, straight into the head of the
+    // local lines (own block, then the halo past it)
+    NCCL_TRY(api, api->reduce_scatter(p->d_send, local, (size_t)block * 2, dt, ncclSum, comm, st));
+  }
   const int64_t need = std::max<int64_t>(0, nc1 - oc1);
   if (in_next) {
     // 3. halo: the w-1 lines past the own block are the head of rank me+1's

@@ -2320,33 +2320,69 @@ cudaError_t launch_box(const BoxArgs& a, cudaStream_t st) {
 template <typename P2>
 __global__ void __launch_bounds__(256) k_reduce_parts(const P2* __restrict__ part, int64_t stride, SlotInfo si,
                                                       const int64_t* __restrict__ line_start, P2* __restrict__ raw,
-                                                      const int64_t* __restrict__ dst_line) {
+                                                      const int64_t* __restrict__ dst_line,
+                                                      const unsigned long long* __restrict__ dst_addr) {
   StampEnd stamp_end_(kStampReduce);
   stamp_start(kStampReduce);
   const int64_t l = blockIdx.x;
   const int64_t c0 = line_start[l], c1 = line_start[l + 1];
   // dst_line: per line, where its first cell goes (the multi-GPU path writes
-  // the padded reduce-scatter send buffer directly); nullptr: cell order
-  P2* dst = raw + (dst_line ? dst_line[l] : c0) - c0;
+  // the padded reduce-scatter send buffer directly); dst_addr: per line, the
+  // ADDRESS of its first cell's destination -- the owner rank's landing slot,
+  // a peer GPU's memory (the reduce-scatter fused into this epilogue as
+  // NVLink stores); neither: cell order
+  P2* dst = dst_addr ? reinterpret_cast<P2*>(dst_addr[l]) - c0 : raw + (dst_line ? dst_line[l] : c0) - c0;
   for (int64_t idx = c0 + threadIdx.x; idx < c1; idx += blockDim.x) {
     double sr = 0.0, si_ = 0.0;
     sum_slots(part, cell_slots(si, 1, l, idx - c0, 0), stride, idx, sr, si_);
     dst[idx].x = sr;
     dst[idx].y = si_;
   }
+  if (dst_addr) {  // peer stores visible before this rank reaches the barrier: the CTA
+    __syncthreads();  // barrier makes its threads' stores cumulative for one system-scope fence
+    if (threadIdx.x == 0) __threadfence_system();
+  }
+}
+
+// owner side of the fused reduce-scatter: out[i] = sum over source ranks r
+// (in rank order, fp64) of land[r * block + i] -- deterministic for a given
+// rank count, unlike a reduction whose order depends on arrival
+template <typename P2>
+__global__ void k_sum_land(const P2* __restrict__ land, int nranks, int64_t block, int64_t count, P2* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    double sr = 0.0, si = 0.0;
+    for (int r = 0; r < nranks; r++) {
+      const P2 v = land[(int64_t)r * block + i];
+      sr += (double)v.x;
+      si += (double)v.y;
+    }
+    out[i].x = sr;
+    out[i].y = si;
+  }
+}
+
+cudaError_t launch_sum_land(const void* land, int nranks, int64_t block, int64_t count, int precision, void* out,
+                            cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  if (precision == 32)
+    k_sum_land<float2><<<grid_for(count, 256), 256, 0, st>>>((const float2*)land, nranks, block, count, (float2*)out);
+  else
+    k_sum_land<double2><<<grid_for(count, 256), 256, 0, st>>>((const double2*)land, nranks, block, count,
+                                                              (double2*)out);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_reduce_parts(const void* part, int64_t part_stride, const SlotInfo& si, const int64_t* line_start,
                                 int64_t nlines, int lo, int precision, void* raw, cudaStream_t st,
-                                const int64_t* dst_line) {
+                                const int64_t* dst_line, const unsigned long long* dst_addr) {
   (void)lo;
   if (nlines <= 0) return cudaSuccess;
   if (precision == 32)
     k_reduce_parts<float2><<<(unsigned)nlines, 256, 0, st>>>((const float2*)part, part_stride, si, line_start,
-                                                             (float2*)raw, dst_line);
+                                                             (float2*)raw, dst_line, dst_addr);
   else
     k_reduce_parts<double2><<<(unsigned)nlines, 256, 0, st>>>((const double2*)part, part_stride, si, line_start,
-                                                              (double2*)raw, dst_line);
+                                                              (double2*)raw, dst_line, dst_addr);
   return cudaGetLastError();
 }
 

@@ -249,10 +249,14 @@ cudaError_t launch_smooth_series_sep(const void* part, int nparts, int64_t part_
                                      int precision, const BoxArgs& a, int64_t nlines, int64_t nvitems,
                                      int64_t nhitems, const int* series_slots, cudaStream_t st);
 // raw[c] = sum_p part[p][c] (fp64 sum, stored in the compute precision)
-// dst_line (optional): per line, the output index of its first cell (else raw[c])
+// dst_line (optional): per line, the output index of its first cell (else raw[c]);
+// dst_addr (optional, wins): per line, the address (possibly a peer GPU's) of its first cell
 cudaError_t launch_reduce_parts(const void* part, int64_t part_stride, const SlotInfo& si, const int64_t* line_start,
                                 int64_t nlines, int lo, int precision, void* raw, cudaStream_t st,
-                                const int64_t* dst_line = nullptr);
+                                const int64_t* dst_line = nullptr, const unsigned long long* dst_addr = nullptr);
+// out[i] = sum_{r < nranks} land[r * block + i], i < count (fp64, rank order)
+cudaError_t launch_sum_land(const void* land, int nranks, int64_t block, int64_t count, int precision, void* out,
+                            cudaStream_t st);
 cudaError_t launch_cast(const void* x, int x_dtype, int64_t n, int precision, void* out, cudaStream_t st);
 cudaError_t launch_peak_fp32(float2* buf, int blocks, int iters, cudaStream_t st);
 cudaError_t launch_peak_fp64(double* buf, int blocks, int iters, cudaStream_t st);

@@ -359,15 +359,19 @@ def _nccl_single_rank_comm():
 
 
 @pytest.mark.parametrize("order,m,k,w,prec", [(3, 256, 13, 9, "fp64"), (4, 64, 7, 5, "fp64"), (3, 1024, 64, 9, "fp32")])
-def test_capi_distributed_nccl_single_rank(cuda, order, m, k, w, prec):
-    """hos_comm_attach + hos_estimate_distributed (NCCL reduce-scatter / all-gather
-    inside the library) on a 1-rank communicator match the oracle and the
-    single-GPU path; the multi-rank layout is the one pinned against
+@pytest.mark.parametrize("p2p", ["1", "0"])
+def test_capi_distributed_nccl_single_rank(cuda, monkeypatch, order, m, k, w, prec, p2p):
+    """hos_comm_attach + hos_estimate_distributed on a 1-rank communicator
+    match the oracle and the single-GPU path, with the reduce-scatter fused
+    into the slot reduction as landing-slot stores (p2p=1: the rank's own
+    landing buffer stands in for the owner's) and with NCCL's reduce-scatter
+    (p2p=0); the multi-rank layout is the one pinned against
     parallel.shard_layout in test_api.py."""
     import torch
 
     from paper_1805_11775_b200 import _native
 
+    monkeypatch.setenv("HOS_DIST_P2P", p2p)
     nccl, comm = _nccl_single_rank_comm()
     try:
         x = np.random.default_rng(order * 1000 + m).standard_normal(m * k)
