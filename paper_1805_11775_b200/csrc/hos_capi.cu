@@ -405,6 +405,9 @@ hos::CtaTripleArgs cta_args(const hos_plan* p, bool streaming = false) {
   a.slot_bytes = p->cta_slot_bytes;
   a.copy_b = p->cta_copy_b;
   a.quad = p->quad ? 1 : 0;
+  a.refill_last = p->m >= 512 ? 1 : 0;  // long stages (cfg2); short ones (cfg4, cfg5) wait on empty[]
+  if (const char* env = std::getenv("HOS_K2_REFILL")) a.refill_last = env[0] == 'l';  // "last" | "empty"
+
   a.tab_stages = p->cta_tab_stages;
   a.tab_blocks = p->cta_tab_blocks;
   a.line_cmax = p->d_line_cmax;

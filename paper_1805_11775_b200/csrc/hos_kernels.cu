@@ -1198,7 +1198,9 @@ __global__ void __launch_bounds__(32 * (Q ? kCtaWarpsQ : kCtaWarps), 1)
   using L = K2Layout<T, S>;
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ __align__(8) unsigned long long full[kCtaMaxDepth];
-  __shared__ int cnt[kCtaMaxDepth];
+  __shared__ __align__(8) unsigned long long empty[kCtaMaxDepth];  // all NW warps done with a slot
+  __shared__ int cnt[kCtaMaxDepth];                                 // ... or counted (refill_last)
+  if (threadIdx.x < kCtaMaxDepth) cnt[threadIdx.x] = 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int k0 = __ldg(a.cta_stage0 + blockIdx.x), nst = __ldg(a.cta_stage0 + blockIdx.x + 1) - k0;
   const int depth = a.depth, Lp = a.Lp;
@@ -1238,7 +1240,8 @@ __global__ void __launch_bounds__(32 * (Q ? kCtaWarpsQ : kCtaWarps), 1)
   if (threadIdx.x == 0) {
     for (int d = 0; d < depth; d++) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&full[d])));
-      cnt[d] = 0;
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(&empty[d])),
+                   "r"(NW));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -1438,12 +1441,30 @@ __global__ void __launch_bounds__(32 * (Q ? kCtaWarpsQ : kCtaWarps), 1)
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
       if (lane == 0) a.trace[4 * gridDim.x * NW + 64 * NW + 64 * warp + k] = t;
     }
-    if (lane == 0) {
-      // the warp's reads of slot d are complete (their values were consumed)
-      if (!Q) __threadfence_block();
+    // slot d is free once all NW warps are done with it (their reads of the
+    // slot are complete: the values were consumed).  Two hand-offs, chosen by
+    // the host per plan (same-box A/B): refill_last -- the warp whose
+    // shared-memory count completes the stage issues the refill (cfg2: 34.0
+    // vs 34.7 us); else every warp arrives on empty[d] (non-blocking) and warp
+    // 0, which the arbiter favours least and so normally finishes a stage
+    // last, waits for the phase and issues it (cfg4 68.5 -> 67.1 us, cfg5
+    // 946 -> 929 us: short stages, where the counter round trip on every
+    // warp's path weighs more)
+    if (a.refill_last && lane == 0) {  // last-arriver refill: shared-memory counter
       if (atomicAdd(&cnt[d], 1) == NW - 1) {
         atomicExch(&cnt[d], 0);
         if (k + depth < nst) issue(ld_stage(k + depth), d);
+      }
+    } else if (lane == 0) {
+      const unsigned eb = (unsigned)__cvta_generic_to_shared(&empty[d]);
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(eb) : "memory");
+      if (warp == 0 && k + depth < nst) {
+        asm volatile(
+            "{\n.reg .pred P1;\nE_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n@!P1 bra E_%=;\n}\n" ::"r"(
+                eb),
+            "r"(par), "r"(1000000u)
+            : "memory");
+        issue(ld_stage(k + depth), d);
       }
     }
     sg = sg_next;

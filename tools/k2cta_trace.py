@@ -2,6 +2,7 @@
 per-CTA durations against their stage counts.  Exploration tool.
   python tools/k2cta_trace.py [cfg2]"""
 import ctypes
+import os
 import sys
 
 sys.path.insert(0, ".")
@@ -18,7 +19,7 @@ lib = _native.lib()
 assert lib.hos_plan_k2_kind(plan.handle) == 1, "plan does not use k_triple_cta"
 x = torch.from_numpy(P.baseline_series(c)).cuda()
 out = plan.empty_out()
-W = 16  # warps per k_triple_cta CTA (fp32 quad kernel)
+W = 16 if os.environ.get("HOS_K2_QUAD") == "1" else 8  # warps per k_triple_cta CTA
 nctas = lib.hos_plan_nctas(plan.handle)
 nw = 148 * W
 tr = torch.zeros(4 * nw + 2 * 64 * W, dtype=torch.int64, device="cuda")
