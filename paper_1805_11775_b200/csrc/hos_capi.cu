@@ -57,6 +57,10 @@ struct hos_plan {
   bool series_k4 = false;  // K4 as one CTA per series with the grid in shared memory
   bool sep_k4 = false;     // ... as separable direct window sums (k_smooth_series_sep; else prefix sums)
   int64_t sep_vitems = 0, sep_hitems = 0;  // k_smooth_series_sep work items
+  // separable K4 of order-3 grids (k_raw_cells + k_box_tiles) instead of line scans + prefix differences
+  bool tiles_k4 = false;
+  int box_ntiles = 0;
+  int32_t* d_box_tiles = nullptr;
   int32_t* d_series_slots = nullptr;    // per series: most partial slots of any region (main launch)
   int32_t* d_s_series_slots = nullptr;  // ... of the streaming schedule
   int split_wa = 1, split_wb = 1;  // K2 WarpSplit weights for two-CTA-per-SM launches
@@ -710,6 +714,16 @@ int run_smooth(hos_plan* p, void* out_dev, cudaStream_t st, int stage = -1, bool
                                           box_args(p, out_dev), p->geo.nlines, st));
     return HOS_OK;
   }
+  if (p->tiles_k4) {  // R (compute precision) in p->d_S, then the separable box tiles
+    if (stage != 5)
+      CUDA_TRY(hos::launch_raw_cells(p->d_part, p->maxslots, p->geo.ncells, si, p->precision, p->d_line_start,
+                                     p->geo.nlines, p->geo.ncells, p->batch, p->d_S, st));
+    if (p->timing && stage < 0) CUDA_TRY(cudaEventRecord(p->ev[5], st));
+    if (stage != 4)
+      CUDA_TRY(hos::launch_box_tiles(p->d_S, p->geo.ncells, p->precision, box_args(p, out_dev), p->d_box_tiles,
+                                     p->box_ntiles, st));
+    return HOS_OK;
+  }
   if (stage != 5)
     CUDA_TRY(hos::launch_line_scan(p->d_part, p->maxslots, p->geo.ncells, si, p->precision, p->d_line_start, 0,
                                    p->geo.nlines, p->geo.ncells, p->batch, p->d_S, st, p->max_line));
@@ -1086,6 +1100,11 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
     // separable direct window sums (default; HOS_K4_SEP=0: the prefix-sum kernel)
     const char* sep = std::getenv("HOS_K4_SEP");
     hos::smooth_series_sep_items(g.row_off.data(), g.rows, m3, &p->sep_vitems, &p->sep_hitems);
+    // opt-in (HOS_K4_TILES=1): separable tiles from materialised raw cells; measured
+    // slower than line scans + prefix differences (cfg2 box 14.1 vs 4.6 us: ~2K tile
+    // threads for 65K points leave the GPU latency-bound; cfg3 58 vs 52 us)
+    const char* tk = std::getenv("HOS_K4_TILES");
+    p->tiles_k4 = order == 3 && !p->series_k4 && hos::box_tiles_supports(m3) && tk && tk[0] == '1';
     p->sep_k4 = p->series_k4 && !(sep && sep[0] == '0') && hos::smooth_series_sep_supports(m3) &&
                 hos::smooth_series_sep_smem(g.ncells, g.nlines, g.rows, g.nregions, g.npoints, m3, p->sep_vitems,
                                             p->sep_hitems, precision) <= 200 * 1024;
@@ -1191,6 +1210,11 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
     if ((rc = upload(p, &p->d_pair_base, g.pair_base))) return bail(rc);
     if ((rc = upload(p, &p->d_line_of_ab, g.line_of_ab))) return bail(rc);
   }
+  if (p->tiles_k4) {
+    const std::vector<int32_t> bt = hos::box_tile_list(g.row_off.data(), g.rows);
+    p->box_ntiles = (int)bt.size();
+    if ((rc = upload(p, &p->d_box_tiles, bt))) return bail(rc);
+  }
   {
     // m fp64 weights, then the same m weights rounded to fp32 (the fp32 front end)
     std::vector<double> tab(m + (m + 1) / 2, 0.0);
@@ -1256,7 +1280,7 @@ void hos_plan_destroy(hos_plan* p) {
     if (b) cudaFree(b);
   if (p->h_err) cudaFreeHost(p->h_err);
   release_p2p(p);
-  for (void* b : {(void*)p->d_series_slots, (void*)p->d_s_series_slots})
+  for (void* b : {(void*)p->d_series_slots, (void*)p->d_s_series_slots, (void*)p->d_box_tiles})
     if (b) cudaFree(b);
   for (void* b : {p->d_raw, p->d_send, p->d_mine, p->d_local, p->d_heads, p->d_vals, p->d_parts, (void*)p->d_send_line})
     if (b) cudaFree(b);

@@ -2281,6 +2281,142 @@ cudaError_t launch_smooth_series_sep(const void* part, int nparts, int64_t part_
   return cudaErrorInvalidValue;
 }
 
+// ===========================================================================
+// K4 for order-3 grids that do not fit one CTA (cfg2, cfg3), SEPARABLE:
+//   K4a' k_raw_cells: R(c) = sum of the cell's partial slots (slot order, fp64),
+//        stored in the compute precision (no prefix scan);
+//   K4b' k_box_tiles: B(k1, k2) = scale sum_{v<W} sum_{u<W} R(k1 + u, k2 + v)
+//        -- the reference's w x w box (tiled.py:36-47) as two 1-D windows of
+//        direct sums in the compute precision (fp32 mode ~1e-7 of max|B|).
+// A K4b' thread owns an output tile of kBR rows x kBC columns: it walks the
+// tile's kBC + W - 1 columns, loads each column's strip of kBR + W - 1 cells
+// of R (L1/L2-resident), forms the kBR vertical sums and adds each into the
+// kBC horizontal accumulators it feeds: (kBR+W-1)(kBC+W-1)/(kBR kBC) = 6
+// loads of 8 bytes per output at W = 9, against 2W loads of 16-byte prefix
+// sums per output for the line-scan + prefix-difference pair.  Consecutive
+// threads take consecutive column blocks of a row block.
+constexpr int kBR = 4, kBC = 8;
+
+template <typename P2>
+__global__ void __launch_bounds__(256, 2) k_raw_cells(const P2* __restrict__ part, int nparts, int64_t part_stride,
+                                                   int64_t part_series_stride, SlotInfo si,
+                                                   const int64_t* __restrict__ line_start, int64_t ncells,
+                                                   P2* __restrict__ R) {
+  StampEnd stamp_end_(kStampScan);
+  asm volatile("griddepcontrol.launch_dependents;");  // K4b' may be scheduled as we retire
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  stamp_start(kStampScan);  // partial slots come from K2
+  const int64_t l = blockIdx.x;
+  const int series = blockIdx.y;
+  const int64_t c0 = line_start[l], c1 = line_start[l + 1];
+  const P2* src = part + series * part_series_stride;
+  P2* dst = R + series * ncells;
+  for (int64_t idx = c0 + threadIdx.x; idx < c1; idx += blockDim.x) {
+    double vr = 0.0, vi = 0.0;
+    sum_slots(src, cell_slots(si, nparts, l, idx - c0, series), part_stride, idx, vr, vi);
+    dst[idx] = P2{(decltype(P2{}.x))vr, (decltype(P2{}.x))vi};
+  }
+}
+
+// tiles: (row block << 16 | column block) codes of every kBR x kBC tile holding
+// at least one output point of rows [row_begin, row_end), ntiles entries
+template <typename P2, int W>
+__global__ void __launch_bounds__(128) k_box_tiles(const P2* __restrict__ R, int64_t ncells, BoxArgs a,
+                                                  const int* __restrict__ tiles, int ntiles) {
+  StampEnd stamp_end_(kStampBox);
+  using T = decltype(P2{}.x);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  stamp_start(kStampBox);  // R comes from K4a'
+  const int series = blockIdx.y;
+  const int tix = blockIdx.x * blockDim.x + threadIdx.x;
+  if (tix >= ntiles) return;
+  const int tcode = __ldg(tiles + tix);
+  const int k1 = (tcode >> 16) * kBR, c0 = (tcode & 0xffff) * kBC;
+  const P2* src = R + series * ncells;
+  int64_t lb[kBR + W - 1];  // line starts of the strip (clamped to the last line)
+#pragma unroll
+  for (int u = 0; u < kBR + W - 1; u++) lb[u] = __ldg(a.line_start + min(k1 + u, a.rows + W - 2));
+  P2 acc[kBR][kBC];
+#pragma unroll
+  for (int r = 0; r < kBR; r++)
+#pragma unroll
+    for (int t = 0; t < kBC; t++) acc[r][t] = P2{T(0), T(0)};
+#pragma unroll
+  for (int c = 0; c < kBC + W - 1; c++) {
+    P2 x[kBR + W - 1];
+#pragma unroll
+    for (int u = 0; u < kBR + W - 1; u++) x[u] = __ldg(src + min(lb[u] + c0 + c, ncells - 1));
+#pragma unroll
+    for (int r = 0; r < kBR; r++) {
+      P2 v = x[r];
+#pragma unroll
+      for (int u = 1; u < W; u++) v = add2(v, x[r + u]);
+#pragma unroll
+      for (int t = 0; t < kBC; t++)  // column c feeds outputs t with t <= c < t + W
+        if (c >= t && c < t + W) acc[r][t] = add2(acc[r][t], v);
+    }
+  }
+  const T sc = (T)a.scale;
+  P2* out = (P2*)a.out + series * a.out_series_stride;
+#pragma unroll
+  for (int r = 0; r < kBR; r++) {
+    const int row = k1 + r;
+    if (row >= a.rows) break;
+    const int64_t o0 = __ldg(a.row_off + row);
+    const int len = (int)(__ldg(a.row_off + row + 1) - o0);
+#pragma unroll
+    for (int t = 0; t < kBC; t++)
+      if (c0 + t < len) __stcs(out + (o0 - a.p_begin) + c0 + t, P2{acc[r][t].x * sc, acc[r][t].y * sc});
+  }
+}
+
+bool box_tiles_supports(int w) { return w == 3 || w == 5 || w == 7 || w == 9 || w == 11 || w == 17; }
+
+std::vector<int32_t> box_tile_list(const int64_t* row_off, int rows) {
+  std::vector<int32_t> t;
+  for (int b = 0; b * kBR < rows; b++) {
+    int64_t mx = 0;
+    for (int r = b * kBR; r < std::min(rows, (b + 1) * kBR); r++) mx = std::max(mx, row_off[r + 1] - row_off[r]);
+    for (int64_t c = 0; c * kBC < mx; c++) t.push_back((int32_t)((b << 16) | c));
+  }
+  return t;
+}
+
+cudaError_t launch_raw_cells(const void* part, int nparts, int64_t part_stride, const SlotInfo& si, int precision,
+                             const int64_t* line_start, int64_t nlines, int64_t ncells, int batch, void* R,
+                             cudaStream_t st) {
+  if (nlines <= 0 || batch <= 0) return cudaSuccess;
+  const int64_t pss = part_stride * nparts;
+  dim3 grid((unsigned)nlines, batch);
+  if (precision == 32)
+    return launch_pdl_kernel(k_raw_cells<float2>, grid, dim3(256), 0, st, (const float2*)part, nparts, part_stride,
+                             pss, si, line_start, ncells, (float2*)R);
+  return launch_pdl_kernel(k_raw_cells<double2>, grid, dim3(256), 0, st, (const double2*)part, nparts, part_stride,
+                           pss, si, line_start, ncells, (double2*)R);
+}
+
+cudaError_t launch_box_tiles(const void* R, int64_t ncells, int precision, const BoxArgs& a, const int* tiles,
+                             int ntiles, cudaStream_t st) {
+  if (ntiles <= 0 || a.batch <= 0) return cudaSuccess;
+  dim3 grid((unsigned)((ntiles + 127) / 128), a.batch);
+#define HOS_BT_CASE(P, WW)                                                                                   \
+  case WW:                                                                                                   \
+    return launch_pdl_kernel(k_box_tiles<P, WW>, grid, dim3(128), 0, st, (const P*)R, ncells, a, tiles, ntiles);
+  if (precision == 32) {
+    switch (a.m3) {
+      HOS_BT_CASE(float2, 3) HOS_BT_CASE(float2, 5) HOS_BT_CASE(float2, 7) HOS_BT_CASE(float2, 9)
+      HOS_BT_CASE(float2, 11) HOS_BT_CASE(float2, 17)
+    }
+  } else {
+    switch (a.m3) {
+      HOS_BT_CASE(double2, 3) HOS_BT_CASE(double2, 5) HOS_BT_CASE(double2, 7) HOS_BT_CASE(double2, 9)
+      HOS_BT_CASE(double2, 11) HOS_BT_CASE(double2, 17)
+    }
+  }
+#undef HOS_BT_CASE
+  return cudaErrorInvalidValue;
+}
+
 size_t smooth_series3_smem(int64_t ncells, int64_t nlines, int rows, int nregions, int64_t npoints) {
   if (nlines > 65535 || rows > 65535) return ~(size_t)0;  // 16-bit line / row tables
   return (size_t)ncells * sizeof(double2) + (size_t)(nlines + 1 + rows + 1 + nlines + nregions + rows + 1) * sizeof(int) +
