@@ -485,25 +485,32 @@ bool build_cta_schedule(const hos_plan* p, CtaSchedule& cs, int interleave_ctas 
   const int64_t row_bytes = (int64_t)p->Lp * (int64_t)e_bytes(p->precision);
   if (!cta_fits(g, p->precision)) return false;
   int segs = 0;
-  // stage shape: 4 segments staged twice (two bank offsets) by default;
-  // HOS_K2_SEGS / HOS_K2_COPIES (diagnostics) try 8-segment single-copy stages
-  int seg_try = 4, copies = 2;
-  if (const char* env = std::getenv("HOS_K2_SEGS")) seg_try = std::max(1, std::min(16, std::atoi(env)));
+  // Stage shape: the largest of 16 / 12 / 8 / 4 segments whose ring (staged
+  // twice, two bank offsets) still holds 3 slots -- every stage hand-off
+  // (mbarrier wait, refill bookkeeping) is paid once per stage, so longer
+  // stages amortise it (same-box A/B, K2 in-step: cfg2 4 -> 8 segments 35.6
+  // -> 32.5 us; cfg4 68.4 -> 63.3 -> 61.1 us at 8 / 16; cfg5 981 -> 888 ->
+  // 865 us).  M up to ~2048 fits 4-segment stages only (with 3 slots).
+  // HOS_K2_SEGS / HOS_K2_COPIES (diagnostics) force a stage size / one copy.
+  int copies = 2;
   if (const char* env = std::getenv("HOS_K2_COPIES")) copies = std::atoi(env) == 1 ? 1 : 2;
-  for (int s = seg_try; s >= seg_try && !segs; s--) {
+  std::vector<int> tries = {16, 12, 8, 4};
+  if (const char* env = std::getenv("HOS_K2_SEGS")) tries = {std::max(1, std::min(16, std::atoi(env)))};
+  for (size_t ti = 0; ti < tries.size() && !segs; ti++) {
+    const int s = tries[ti];
     const int64_t A = (s * row_bytes + 127) / 128 * 128;
     const int64_t slot = copies * A + 128;
     // 3 slots: a deeper ring lets the warp the scheduler favours run further
-    // ahead of its sub-partition partner, which then runs alone (cfg2 K2:
-    // depth 3 33.6 us, 4 33.8, 5 34.4, 6 35.3; 2 cannot hide the copies)
-    // order 4 (short rows, 8 x 16 tiles): 5 slots (cfg4 K2 3 / 4 / 5 / 6:
-    // 72.3 / 70.3 / 69.6 / 69.4 us; cfg5, order 3 at the same M, is flat)
+    // ahead of its sub-partition partner, which then runs alone (cfg2 K2 at
+    // 4-segment stages: depth 3 33.6 us, 4 33.8, 5 34.4, 6 35.3); order 4
+    // (short rows): 5 slots when they fit (at 16-segment stages 3 and 5 are even)
     int64_t depth = std::min<int64_t>({(int64_t)(p->order == 4 ? 5 : 3), (int64_t)hos::kCtaMaxDepth,
                                        (int64_t)hos::kCtaMaxSmem / slot});
     if (const char* env = std::getenv("HOS_CTA_DEPTH"))  // diagnostics
       depth = std::max<int64_t>(2, std::min<int64_t>({(int64_t)hos::kCtaMaxDepth, (int64_t)hos::kCtaMaxSmem / slot,
                                                        (int64_t)std::atoi(env)}));
-    if (depth >= 2) {
+    const bool last = ti + 1 == tries.size();
+    if (depth >= 3 || (last && depth >= 2)) {
       segs = s;
       cs.depth = (int)depth;
       cs.slot_bytes = (int)slot;

@@ -1428,11 +1428,14 @@ __global__ void __launch_bounds__(32 * (Q ? kCtaWarpsQ : kCtaWarps), 1)
         const EL* qt = q;
 #pragma unroll 1
         for (int t = 0; t < sg.nseg; t++, qt += Lp) cta_cells<T, CONJ, ORDER4, S, Q>(qt, ops, acc);
-      } else if (sg.nseg == 4) {
-#pragma unroll
-        for (int t = 0; t < 4; t++) cta_cells<T, CONJ, ORDER4, S, Q>(q + t * Lp, ops, acc);
       } else {
-        for (int t = 0; t < sg.nseg; t++) cta_cells<T, CONJ, ORDER4, S, Q>(q + t * Lp, ops, acc);
+        // straight-line blocks of 4 segments (stages of 4 or 8 segments), then the rest
+        int t = 0;
+        for (; t + 4 <= sg.nseg; t += 4) {
+#pragma unroll
+          for (int u = 0; u < 4; u++) cta_cells<T, CONJ, ORDER4, S, Q>(q + (t + u) * Lp, ops, acc);
+        }
+        for (; t < sg.nseg; t++) cta_cells<T, CONJ, ORDER4, S, Q>(q + t * Lp, ops, acc);
       }
     }
     __syncwarp();
