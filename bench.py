@@ -327,6 +327,14 @@ def kernel_spans(log):
         f = np.min(np.stack([np.pad(a, (0, len(log) - len(a)), constant_values=a.max()) for a in firsts]), axis=0)
         l_ = np.max(np.stack([np.pad(a, (0, len(log) - len(a))) for a in lasts]), axis=0)
         out["first_start_to_last_end"] = float(np.median((l_ - f) * 1e-6))
+    # hand-off gaps along the pipeline: next kernel's first start (after its PDL
+    # wait) minus the previous kernel's last end
+    order = [k for k in (0, 1, 2, 3, 4, 6, 5, 7) if log[:, 2 * k].any() and log[:, 2 * k + 1].any()]
+    for a_, b_ in zip(order, order[1:]):
+        ok = (log[:, 2 * a_ + 1] != 0) & (log[:, 2 * b_] != 0)
+        if ok.any():
+            gap = (~log[ok, 2 * b_]).astype(np.int64) - log[ok, 2 * a_ + 1].astype(np.int64)
+            out[f"gap_{STAMP_KINDS[a_]}_{STAMP_KINDS[b_]}"] = float(np.median(gap * 1e-6))
     return out
 
 
