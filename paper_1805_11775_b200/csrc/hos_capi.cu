@@ -74,6 +74,8 @@ struct hos_plan {
   hos::CtaBlock* d_blocks = nullptr;
   hos::CtaStage* d_stages = nullptr;
   int32_t* d_cta_stage0 = nullptr;
+  int4* d_cta_head = nullptr;    // per CTA {first stage, stages, first block, blocks}
+  int4* d_s_cta_head = nullptr;  // ... of the streaming schedule
   int64_t rs_stride = 0;  // d_region_slots entries per series
   // streaming host path (hos_estimate_host, zero-copy): the front end runs on
   // kStreamFrontCtas SMs reading the series over PCIe while k_triple_cta (an
@@ -403,6 +405,7 @@ hos::CtaTripleArgs cta_args(const hos_plan* p, bool streaming = false) {
   a.blocks = p->d_blocks;
   a.stages = p->d_stages;
   a.cta_stage0 = p->d_cta_stage0;
+  a.cta_head = p->d_cta_head;
   a.nctas = p->cta_nctas;
   a.depth = p->cta_depth;
   a.stage_segs = p->cta_stage_segs;
@@ -429,6 +432,7 @@ hos::CtaTripleArgs cta_args(const hos_plan* p, bool streaming = false) {
     a.blocks = p->d_s_blocks;
     a.stages = p->d_s_stages;
     a.cta_stage0 = p->d_s_cta_stage0;
+    a.cta_head = p->d_s_cta_head;
     a.nctas = p->s_nctas;
     a.tab_stages = p->s_tab_stages;
     a.tab_blocks = p->s_tab_blocks;
@@ -459,6 +463,15 @@ struct CtaSchedule {
   std::vector<int32_t> region_slots;  // batch x nregions
   int nctas = 0, depth = 0, stage_segs = 4, slot_bytes = 0, copy_b = 0, maxslots = 1;
   int tab_stages = 0, tab_blocks = 0;  // most stages / blocks of one CTA (shared-memory tables)
+  std::vector<int4> heads() const {     // per CTA {first stage, stages, first block, blocks}
+    std::vector<int4> h;
+    for (int c = 0; c + 1 < (int)cta_stage0.size(); c++) {
+      const int k0 = cta_stage0[c], n = cta_stage0[c + 1] - k0;
+      const int b0 = n > 0 ? stages[k0].block : 0;
+      h.push_back(make_int4(k0, n, b0, n > 0 ? stages[k0 + n - 1].block - b0 + 1 : 0));
+    }
+    return h;
+  }
   // fills tab_* (0: ring + tables exceed the CTA's shared memory, the kernel reads them from global)
   bool size_tables() {
     tab_stages = tab_blocks = 0;
@@ -1179,6 +1192,7 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
     if ((rc = upload(p, &p->d_s_blocks, ssched.blocks))) return bail(rc);
     if ((rc = upload(p, &p->d_s_stages, ssched.stages))) return bail(rc);
     if ((rc = upload(p, &p->d_s_cta_stage0, ssched.cta_stage0))) return bail(rc);
+    if ((rc = upload(p, &p->d_s_cta_head, ssched.heads()))) return bail(rc);
     if ((rc = alloc(p, (void**)&p->d_ready, (size_t)k * sizeof(int)))) return bail(rc);
     if (cudaHostAlloc((void**)&p->h_err, sizeof(int), cudaHostAllocMapped) != cudaSuccess ||
         cudaHostGetDevicePointer((void**)&p->d_err, p->h_err, 0) != cudaSuccess)
@@ -1199,6 +1213,8 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
     if ((rc = upload(p, &p->d_blocks, sched.blocks))) return bail(rc);
     if ((rc = upload(p, &p->d_stages, sched.stages))) return bail(rc);
     if ((rc = upload(p, &p->d_cta_stage0, sched.cta_stage0))) return bail(rc);
+    if ((rc = upload(p, &p->d_cta_head, sched.heads()))) return bail(rc);
+
   } else {
     const hos::WarpSplit sp = warp_split(p, k, p->nctas, batch);
     std::vector<int32_t> rs(g.nregions);
@@ -1291,7 +1307,7 @@ void hos_plan_destroy(hos_plan* p) {
     if (b) cudaFree(b);
   for (void* b : {p->d_raw, p->d_send, p->d_mine, p->d_local, p->d_heads, p->d_vals, p->d_parts, (void*)p->d_send_line})
     if (b) cudaFree(b);
-  void* bufs[] = {p->d_groups, p->d_blocks, p->d_stages, p->d_cta_stage0, p->d_tiles, p->d_line_tile0, p->d_region_slots, p->d_line_cmax, p->d_line_start, p->d_row_off, p->d_pair_k1, p->d_pair_k2,
+  void* bufs[] = {p->d_groups, p->d_blocks, p->d_stages, p->d_cta_stage0, p->d_cta_head, p->d_s_cta_head, p->d_tiles, p->d_line_tile0, p->d_region_slots, p->d_line_cmax, p->d_line_start, p->d_row_off, p->d_pair_k1, p->d_pair_k2,
                   p->d_pair_base, p->d_line_of_ab, p->d_taper, p->d_tw, p->d_seg, p->d_half, p->d_E, p->d_part,
                   p->d_S, p->d_xin, p->d_out};
   for (void* b : bufs)

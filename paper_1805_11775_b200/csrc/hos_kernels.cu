@@ -1202,7 +1202,8 @@ __global__ void __launch_bounds__(32 * (Q ? kCtaWarpsQ : kCtaWarps), 1)
   __shared__ int cnt[kCtaMaxDepth];                                 // ... or counted (refill_last)
   if (threadIdx.x < kCtaMaxDepth) cnt[threadIdx.x] = 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int k0 = __ldg(a.cta_stage0 + blockIdx.x), nst = __ldg(a.cta_stage0 + blockIdx.x + 1) - k0;
+  const int4 head = __ldg(a.cta_head + blockIdx.x);  // {first stage, stages, first block, blocks}
+  const int k0 = head.x, nst = head.y;
   const int depth = a.depth, Lp = a.Lp;
   unsigned long long* tr = a.trace ? a.trace + 4 * ((int64_t)blockIdx.x * NW + warp) : nullptr;
   auto stamp = [&](int i) {
@@ -1225,10 +1226,17 @@ __global__ void __launch_bounds__(32 * (Q ? kCtaWarpsQ : kCtaWarps), 1)
   // global loads on every warp's path
   // (tab_stages == 0: the tables did not fit next to the ring -- huge batches
   // on few SMs -- and are read from global memory)
-  const int b0 = nst > 0 ? __ldg(&a.stages[k0].block) : 0;
-  const int nb_cta = nst > 0 ? __ldg(&a.stages[k0 + nst - 1].block) - b0 + 1 : 0;
+  // The per-CTA head record (host-built) gives the stage and block ranges in
+  // one load.  (Copying the groups, tiles and line tables to shared memory as
+  // well measured no change of the front end -> K2 hand-off, 3.1-3.2 us on
+  // cfg2: K2's CTAs reach their SMs only as the front end's CTAs leave.)
+  const int b0 = head.z, nb_cta = head.w;
   const int4* st_s = reinterpret_cast<const int4*>(a.stages + k0);
   const int4* bl_s = reinterpret_cast<const int4*>(a.blocks + b0);
+  const CtaGroup* groups_s = a.groups;
+  const Tile* tiles_s = a.tiles;
+  const int32_t* lcmax_s = a.line_cmax;
+  const int64_t* lstart_s = a.line_start;
   if (a.tab_stages > 0) {
     int4* st_w = reinterpret_cast<int4*>(smraw + (size_t)depth * a.slot_bytes);
     int4* bl_w = st_w + a.tab_stages;
@@ -1313,7 +1321,7 @@ __global__ void __launch_bounds__(32 * (Q ? kCtaWarpsQ : kCtaWarps), 1)
   };
   auto enter = [&](const CtaBlock& blk, int k_first) {
     blk_k0 = k_first;  // the block's first stage (phases deal its stages round-robin)
-    const CtaGroup grp = a.groups[blk.group];
+    const CtaGroup grp = groups_s[blk.group];
     // warps per region: `halves` (2: each warp computes one tile of the
     // pair, the other half of its lanes idle) x `phases`
     phases = grp.phases;
@@ -1325,7 +1333,7 @@ __global__ void __launch_bounds__(32 * (Q ? kCtaWarpsQ : kCtaWarps), 1)
     const bool my_tile = grp.halves == 1 || (sub % grp.halves) == (h & 1);
     blk_row0 = blk.row0;
     P = (C*)a.part + ((int64_t)blk.series * a.maxslots + blk.slot_base + phase) * a.ncells;
-    const Tile t = a.tiles[(int64_t)region * L::NT + h];
+    const Tile t = tiles_s[(int64_t)region * L::NT + h];
     c0 = t.col0 + cb;
     line0 = t.line0 + ra;
     nrows = t.nrows - ra;
@@ -1340,8 +1348,8 @@ __global__ void __launch_bounds__(32 * (Q ? kCtaWarpsQ : kCtaWarps), 1)
       lcm[i] = -0x40000000;
       loff[i] = 0;
       if (S * i < nrows) {
-        lcm[i] = __ldg(a.line_cmax + line0 + S * i);
-        loff[i] = (int)(__ldg(a.line_start + line0 + S * i) - a.lo);
+        lcm[i] = lcmax_s[line0 + S * i];
+        loff[i] = (int)(lstart_s[line0 + S * i] - a.lo);
       }
     }
     if (role && my_tile) {
@@ -1359,8 +1367,8 @@ __global__ void __launch_bounds__(32 * (Q ? kCtaWarpsQ : kCtaWarps), 1)
       if (S * i >= nrows) continue;
       // fp32 (16 warps, 128 registers): the lines' ends are reloaded here
       // rather than kept live through the compute loop
-      const int cm = Q ? __ldg(a.line_cmax + line0 + S * i) : lcm[i];
-      C* dst = P + (Q ? (int)(__ldg(a.line_start + line0 + S * i) - a.lo) : loff[i]);
+      const int cm = Q ? lcmax_s[line0 + S * i] : lcm[i];
+      C* dst = P + (Q ? (int)(lstart_s[line0 + S * i] - a.lo) : loff[i]);
 #pragma unroll
       for (int j = 0; j < 8; j++)
         if (c0 + S * j <= cm) dst[c0 + S * j] = acc.template cell<CONJ>(i, j);
