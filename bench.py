@@ -353,7 +353,7 @@ def run_ours(args):
 
     import __graft_entry__
 
-    __graft_entry__.build()
+    __graft_entry__.ensure_built()
     import ctypes
 
     import paper_1805_11775_b200 as P

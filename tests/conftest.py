@@ -49,5 +49,5 @@ def cuda():
         pytest.skip("no CUDA device")
     import __graft_entry__
 
-    __graft_entry__.build()
+    __graft_entry__.ensure_built()
     return torch.device("cuda", 0)

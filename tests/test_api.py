@@ -214,7 +214,7 @@ def test_native_shard_layout_matches_python(m, w, k, n):
     """hos_shard_layout (the C-ABI multi-GPU path's layout) == parallel.shard_layout."""
     import __graft_entry__
 
-    __graft_entry__.build()
+    __graft_entry__.ensure_built()
     from paper_1805_11775_b200 import _native
 
     rows, lo, hi, cmax, line_start, row_off = _geom3(m, w)

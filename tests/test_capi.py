@@ -25,7 +25,7 @@ def declared_symbols():
 def lib():
     import __graft_entry__
 
-    __graft_entry__.build()
+    __graft_entry__.ensure_built()
     from paper_1805_11775_b200 import _native
 
     return _native.lib()

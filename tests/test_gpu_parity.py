@@ -295,7 +295,7 @@ def _gloo_gpu_worker(rank, world, port, cfgs, q):
     try:
         import __graft_entry__
 
-        __graft_entry__.build()
+        __graft_entry__.ensure_built()
         from paper_1805_11775_b200 import EstimationConfig, SegmentConfig, distributed_estimate
 
         res = []

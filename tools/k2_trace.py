@@ -9,7 +9,7 @@ import torch
 
 import __graft_entry__
 
-__graft_entry__.build()
+__graft_entry__.ensure_built()
 import paper_1805_11775_b200 as P
 from paper_1805_11775_b200 import _native
 
