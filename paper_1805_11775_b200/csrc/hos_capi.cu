@@ -61,6 +61,7 @@ struct hos_plan {
   bool tiles_k4 = false;
   int box_ntiles = 0;
   int32_t* d_box_tiles = nullptr;
+  uint16_t* d_cell_region = nullptr;  // region of every cell (k_raw_cells' slot counts)
   int32_t* d_series_slots = nullptr;    // per series: most partial slots of any region (main launch)
   int32_t* d_s_series_slots = nullptr;  // ... of the streaming schedule
   int split_wa = 1, split_wb = 1;  // K2 WarpSplit weights for two-CTA-per-SM launches
@@ -736,12 +737,12 @@ int run_smooth(hos_plan* p, void* out_dev, cudaStream_t st, int stage = -1, bool
   }
   if (p->tiles_k4) {  // R (compute precision) in p->d_S, then the separable box tiles
     if (stage != 5)
-      CUDA_TRY(hos::launch_raw_cells(p->d_part, p->maxslots, p->geo.ncells, si, p->precision, p->d_line_start,
-                                     p->geo.nlines, p->geo.ncells, p->batch, p->d_S, st));
+      CUDA_TRY(hos::launch_raw_cells(p->d_part, p->maxslots, p->geo.ncells, si.region_slots, si.rs_stride,
+                                     p->d_cell_region, p->geo.ncells, p->batch, p->precision, p->d_S, st));
     if (p->timing && stage < 0) CUDA_TRY(cudaEventRecord(p->ev[5], st));
     if (stage != 4)
-      CUDA_TRY(hos::launch_box_tiles(p->d_S, p->geo.ncells, p->precision, box_args(p, out_dev), p->d_box_tiles,
-                                     p->box_ntiles, st));
+      CUDA_TRY(hos::launch_box_tiles(p->d_S, p->geo.ncells, p->precision, box_args(p, out_dev),
+                                     (int)p->geo.nlines, p->d_box_tiles, p->box_ntiles, st));
     return HOS_OK;
   }
   if (stage != 5)
@@ -1120,11 +1121,12 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
     // separable direct window sums (default; HOS_K4_SEP=0: the prefix-sum kernel)
     const char* sep = std::getenv("HOS_K4_SEP");
     hos::smooth_series_sep_items(g.row_off.data(), g.rows, m3, &p->sep_vitems, &p->sep_hitems);
-    // opt-in (HOS_K4_TILES=1): separable tiles from materialised raw cells; measured
-    // slower than line scans + prefix differences (cfg2 box 14.1 vs 4.6 us: ~2K tile
-    // threads for 65K points leave the GPU latency-bound; cfg3 58 vs 52 us)
+    // separable K4 for line grids (default; HOS_K4_TILES=0: line scans + prefix
+    // differences): cfg2 scan + box 12.2 -> 7.3 us, step 60.3 -> 56.8 us;
+    // cfg3 79.4 -> 52.3 us (same box)
     const char* tk = std::getenv("HOS_K4_TILES");
-    p->tiles_k4 = order == 3 && !p->series_k4 && hos::box_tiles_supports(m3) && tk && tk[0] == '1';
+    p->tiles_k4 = order == 3 && !p->series_k4 && hos::box_tiles_supports(m3) && g.nregions < 65536 &&
+                  !(tk && tk[0] == '0');
     p->sep_k4 = p->series_k4 && !(sep && sep[0] == '0') && hos::smooth_series_sep_supports(m3) &&
                 hos::smooth_series_sep_smem(g.ncells, g.nlines, g.rows, g.nregions, g.npoints, m3, p->sep_vitems,
                                             p->sep_hitems, precision) <= 200 * 1024;
@@ -1237,6 +1239,9 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
     const std::vector<int32_t> bt = hos::box_tile_list(g.row_off.data(), g.rows);
     p->box_ntiles = (int)bt.size();
     if ((rc = upload(p, &p->d_box_tiles, bt))) return bail(rc);
+    const std::vector<uint16_t> cr = hos::cell_region_table(g.line_tile0.data(), g.line_start.data(), g.nlines,
+                                                            g.tile_cols, g.tiles_per_region);
+    if ((rc = upload(p, &p->d_cell_region, cr))) return bail(rc);
   }
   {
     // m fp64 weights, then the same m weights rounded to fp32 (the fp32 front end)
@@ -1303,7 +1308,8 @@ void hos_plan_destroy(hos_plan* p) {
     if (b) cudaFree(b);
   if (p->h_err) cudaFreeHost(p->h_err);
   release_p2p(p);
-  for (void* b : {(void*)p->d_series_slots, (void*)p->d_s_series_slots, (void*)p->d_box_tiles})
+  for (void* b : {(void*)p->d_series_slots, (void*)p->d_s_series_slots, (void*)p->d_box_tiles,
+                  (void*)p->d_cell_region})
     if (b) cudaFree(b);
   for (void* b : {p->d_raw, p->d_send, p->d_mine, p->d_local, p->d_heads, p->d_vals, p->d_parts, (void*)p->d_send_line})
     if (b) cudaFree(b);

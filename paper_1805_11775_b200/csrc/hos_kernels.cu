@@ -2295,89 +2295,141 @@ cudaError_t launch_smooth_series_sep(const void* part, int nparts, int64_t part_
 // ===========================================================================
 // K4 for order-3 grids that do not fit one CTA (cfg2, cfg3), SEPARABLE:
 //   K4a' k_raw_cells: R(c) = sum of the cell's partial slots (slot order, fp64),
-//        stored in the compute precision (no prefix scan);
-//   K4b' k_box_tiles: B(k1, k2) = scale sum_{v<W} sum_{u<W} R(k1 + u, k2 + v)
+//        stored in the compute precision (no prefix scan).  A thread owns two
+//        adjacent cells (fp32: one 16-byte load per slot) and issues every
+//        slot load before the adds: one dependent L2 round trip for the slots
+//        after the per-cell region -> slot-count lookups.
+//   K4b' k_box_tiles: B(k1, k2) = scale sum_{u<W} sum_{v<W} R(k1 + u, k2 + v)
 //        -- the reference's w x w box (tiled.py:36-47) as two 1-D windows of
 //        direct sums in the compute precision (fp32 mode ~1e-7 of max|B|).
-// A K4b' thread owns an output tile of kBR rows x kBC columns: it walks the
-// tile's kBC + W - 1 columns, loads each column's strip of kBR + W - 1 cells
-// of R (L1/L2-resident), forms the kBR vertical sums and adds each into the
-// kBC horizontal accumulators it feeds: (kBR+W-1)(kBC+W-1)/(kBR kBC) = 6
-// loads of 8 bytes per output at W = 9, against 2W loads of 16-byte prefix
-// sums per output for the line-scan + prefix-difference pair.  Consecutive
-// threads take consecutive column blocks of a row block.
-constexpr int kBR = 4, kBC = 8;
+//        A CTA owns a kTR x kTC output tile: it stages the (kTR+W-1) x
+//        (kTC+W-1) raw cells the tile reads into shared memory (one round
+//        trip: every thread's loads are issued together), forms the kTR rows
+//        of vertical sums V, then the outputs as horizontal sums of V.  The
+//        line / row tables are read before the PDL wait (static).
+// Order-3 line l is raw row k1 = l; output (k1, k2) reads line-local cells
+// k2 .. k2+W-1 of lines k1 .. k1+W-1 (box3_point's prefix differences).
+constexpr int kTR = 8, kTC = 32, kTileThreads = 128;
 
-template <typename P2>
-__global__ void __launch_bounds__(256, 2) k_raw_cells(const P2* __restrict__ part, int nparts, int64_t part_stride,
-                                                   int64_t part_series_stride, SlotInfo si,
-                                                   const int64_t* __restrict__ line_start, int64_t ncells,
-                                                   P2* __restrict__ R) {
+template <typename P2, int V>
+__global__ void __launch_bounds__(256) k_raw_cells(const P2* __restrict__ part, int64_t part_stride,
+                                                   int64_t part_series_stride,
+                                                   const unsigned short* __restrict__ cell_region,
+                                                   const int32_t* __restrict__ region_slots, int64_t rs_stride,
+                                                   int64_t ncells, P2* __restrict__ R) {
   StampEnd stamp_end_(kStampScan);
+  using T = decltype(P2{}.x);
+  const int series = blockIdx.y;
+  const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * V;
+  int ns[V];
+  if (c < ncells) {  // static tables: before the PDL wait
+#pragma unroll
+    for (int v = 0; v < V; v++)
+      ns[v] = c + v < ncells ? __ldg(region_slots + series * rs_stride + __ldg(cell_region + c + v)) : 0;
+  }
   asm volatile("griddepcontrol.launch_dependents;");  // K4b' may be scheduled as we retire
   asm volatile("griddepcontrol.wait;" ::: "memory");
   stamp_start(kStampScan);  // partial slots come from K2
-  const int64_t l = blockIdx.x;
-  const int series = blockIdx.y;
-  const int64_t c0 = line_start[l], c1 = line_start[l + 1];
-  const P2* src = part + series * part_series_stride;
-  P2* dst = R + series * ncells;
-  for (int64_t idx = c0 + threadIdx.x; idx < c1; idx += blockDim.x) {
-    double vr = 0.0, vi = 0.0;
-    sum_slots(src, cell_slots(si, nparts, l, idx - c0, series), part_stride, idx, vr, vi);
-    dst[idx] = P2{(decltype(P2{}.x))vr, (decltype(P2{}.x))vi};
+  if (c >= ncells) return;
+  const P2* src = part + series * part_series_stride + c;
+  int n = ns[0];
+#pragma unroll
+  for (int v = 1; v < V; v++) n = max(n, ns[v]);
+  double acc[2 * V];
+#pragma unroll
+  for (int i = 0; i < 2 * V; i++) acc[i] = 0.0;
+  constexpr int kChunk = 16;
+  using L = typename std::conditional<V == 2, float4, P2>::type;  // V == 2: fp32 cell pairs
+  for (int p0 = 0; p0 < n; p0 += kChunk) {
+    L x[kChunk];
+#pragma unroll
+    for (int t = 0; t < kChunk; t++)
+      if (p0 + t < n) x[t] = *reinterpret_cast<const L*>(src + (int64_t)(p0 + t) * part_stride);
+#pragma unroll
+    for (int t = 0; t < kChunk; t++) {
+      if (p0 + t < n) {
+        const T* e = reinterpret_cast<const T*>(&x[t]);
+#pragma unroll
+        for (int v = 0; v < V; v++)
+          if (p0 + t < ns[v]) {
+            acc[2 * v] += (double)e[2 * v];
+            acc[2 * v + 1] += (double)e[2 * v + 1];
+          }
+      }
+    }
+  }
+  P2* dst = R + series * ncells + c;
+  if constexpr (V == 2) {  // ncells even: the pair is whole
+    *reinterpret_cast<float4*>(dst) = make_float4((float)acc[0], (float)acc[1], (float)acc[2], (float)acc[3]);
+  } else {
+    dst[0] = P2{(T)acc[0], (T)acc[1]};
   }
 }
 
-// tiles: (row block << 16 | column block) codes of every kBR x kBC tile holding
-// at least one output point of rows [row_begin, row_end), ntiles entries
+// tiles: (row block << 16 | column block) codes of every kTR x kTC tile holding
+// at least one output point of rows [0, rows), ntiles entries
 template <typename P2, int W>
-__global__ void __launch_bounds__(128) k_box_tiles(const P2* __restrict__ R, int64_t ncells, BoxArgs a,
-                                                  const int* __restrict__ tiles, int ntiles) {
+__global__ void __launch_bounds__(kTileThreads) k_box_tiles(const P2* __restrict__ R, int64_t ncells, BoxArgs a,
+                                                           int nlines, const int* __restrict__ tiles) {
   StampEnd stamp_end_(kStampBox);
   using T = decltype(P2{}.x);
+  constexpr int NL = kTR + W - 1, NC = kTC + W - 1;
+  __shared__ P2 rs[NL][NC];
+  __shared__ P2 vs[kTR][NC + 1];
+  __shared__ int64_t lb[NL];
+  __shared__ int ll[NL];
+  __shared__ int64_t ro[kTR];
+  __shared__ int rl[kTR];
+  const int series = blockIdx.y;
+  const int tcode = __ldg(tiles + blockIdx.x);
+  const int k1 = (tcode >> 16) * kTR, c0 = (tcode & 0xffff) * kTC;
+  if (threadIdx.x < NL) {  // static line / row tables: before the PDL wait
+    const int l = k1 + threadIdx.x;
+    const int64_t s0 = l < nlines ? __ldg(a.line_start + l) : 0;
+    lb[threadIdx.x] = s0;
+    ll[threadIdx.x] = l < nlines ? (int)(__ldg(a.line_start + l + 1) - s0) : 0;
+  } else if (threadIdx.x >= 32 && threadIdx.x < 32 + kTR) {
+    const int r = k1 + threadIdx.x - 32;
+    const int64_t o0 = r < a.rows ? __ldg(a.row_off + r) : 0;
+    ro[threadIdx.x - 32] = o0;
+    rl[threadIdx.x - 32] = r < a.rows ? (int)(__ldg(a.row_off + r + 1) - o0) : 0;
+  }
+  __syncthreads();
   asm volatile("griddepcontrol.wait;" ::: "memory");
   stamp_start(kStampBox);  // R comes from K4a'
-  const int series = blockIdx.y;
-  const int tix = blockIdx.x * blockDim.x + threadIdx.x;
-  if (tix >= ntiles) return;
-  const int tcode = __ldg(tiles + tix);
-  const int k1 = (tcode >> 16) * kBR, c0 = (tcode & 0xffff) * kBC;
   const P2* src = R + series * ncells;
-  int64_t lb[kBR + W - 1];  // line starts of the strip (clamped to the last line)
+  constexpr int kLoads = (NL * NC + kTileThreads - 1) / kTileThreads;
+  P2 x[kLoads];
 #pragma unroll
-  for (int u = 0; u < kBR + W - 1; u++) lb[u] = __ldg(a.line_start + min(k1 + u, a.rows + W - 2));
-  P2 acc[kBR][kBC];
-#pragma unroll
-  for (int r = 0; r < kBR; r++)
-#pragma unroll
-    for (int t = 0; t < kBC; t++) acc[r][t] = P2{T(0), T(0)};
-#pragma unroll
-  for (int c = 0; c < kBC + W - 1; c++) {
-    P2 x[kBR + W - 1];
-#pragma unroll
-    for (int u = 0; u < kBR + W - 1; u++) x[u] = __ldg(src + min(lb[u] + c0 + c, ncells - 1));
-#pragma unroll
-    for (int r = 0; r < kBR; r++) {
-      P2 v = x[r];
-#pragma unroll
-      for (int u = 1; u < W; u++) v = add2(v, x[r + u]);
-#pragma unroll
-      for (int t = 0; t < kBC; t++)  // column c feeds outputs t with t <= c < t + W
-        if (c >= t && c < t + W) acc[r][t] = add2(acc[r][t], v);
-    }
+  for (int t = 0; t < kLoads; t++) {
+    const int i = threadIdx.x + t * kTileThreads;
+    const int u = i / NC, c = i - u * NC;
+    x[t] = P2{T(0), T(0)};
+    if (i < NL * NC && c0 + c < ll[u]) x[t] = src[lb[u] + c0 + c];
   }
+#pragma unroll
+  for (int t = 0; t < kLoads; t++) {
+    const int i = threadIdx.x + t * kTileThreads;
+    if (i < NL * NC) rs[i / NC][i % NC] = x[t];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kTR * NC; i += kTileThreads) {
+    const int r = i / NC, c = i - r * NC;
+    P2 v = rs[r][c];
+#pragma unroll
+    for (int u = 1; u < W; u++) v = add2(v, rs[r + u][c]);
+    vs[r][c] = v;
+  }
+  __syncthreads();
   const T sc = (T)a.scale;
   P2* out = (P2*)a.out + series * a.out_series_stride;
+  for (int i = threadIdx.x; i < kTR * kTC; i += kTileThreads) {
+    const int r = i / kTC, c = i - r * kTC;
+    if (c0 + c >= rl[r]) continue;
+    P2 v = vs[r][c];
 #pragma unroll
-  for (int r = 0; r < kBR; r++) {
-    const int row = k1 + r;
-    if (row >= a.rows) break;
-    const int64_t o0 = __ldg(a.row_off + row);
-    const int len = (int)(__ldg(a.row_off + row + 1) - o0);
-#pragma unroll
-    for (int t = 0; t < kBC; t++)
-      if (c0 + t < len) __stcs(out + (o0 - a.p_begin) + c0 + t, P2{acc[r][t].x * sc, acc[r][t].y * sc});
+    for (int u = 1; u < W; u++) v = add2(v, vs[r][c + u]);
+    __stcs(out + ro[r] + c0 + c, P2{v.x * sc, v.y * sc});
   }
 }
 
@@ -2385,34 +2437,49 @@ bool box_tiles_supports(int w) { return w == 3 || w == 5 || w == 7 || w == 9 || 
 
 std::vector<int32_t> box_tile_list(const int64_t* row_off, int rows) {
   std::vector<int32_t> t;
-  for (int b = 0; b * kBR < rows; b++) {
+  for (int b = 0; b * kTR < rows; b++) {
     int64_t mx = 0;
-    for (int r = b * kBR; r < std::min(rows, (b + 1) * kBR); r++) mx = std::max(mx, row_off[r + 1] - row_off[r]);
-    for (int64_t c = 0; c * kBC < mx; c++) t.push_back((int32_t)((b << 16) | c));
+    for (int r = b * kTR; r < std::min(rows, (b + 1) * kTR); r++) mx = std::max(mx, row_off[r + 1] - row_off[r]);
+    for (int64_t c = 0; c * kTC < mx; c++) t.push_back((int32_t)((b << 16) | c));
   }
   return t;
 }
 
-cudaError_t launch_raw_cells(const void* part, int nparts, int64_t part_stride, const SlotInfo& si, int precision,
-                             const int64_t* line_start, int64_t nlines, int64_t ncells, int batch, void* R,
-                             cudaStream_t st) {
-  if (nlines <= 0 || batch <= 0) return cudaSuccess;
-  const int64_t pss = part_stride * nparts;
-  dim3 grid((unsigned)nlines, batch);
-  if (precision == 32)
-    return launch_pdl_kernel(k_raw_cells<float2>, grid, dim3(256), 0, st, (const float2*)part, nparts, part_stride,
-                             pss, si, line_start, ncells, (float2*)R);
-  return launch_pdl_kernel(k_raw_cells<double2>, grid, dim3(256), 0, st, (const double2*)part, nparts, part_stride,
-                           pss, si, line_start, ncells, (double2*)R);
+std::vector<uint16_t> cell_region_table(const int32_t* line_tile0, const int64_t* line_start, int64_t nlines,
+                                        int tile_cols, int tiles_per_region) {
+  std::vector<uint16_t> t((size_t)line_start[nlines]);
+  for (int64_t l = 0; l < nlines; l++)
+    for (int64_t c = line_start[l]; c < line_start[l + 1]; c++)
+      t[(size_t)c] = (uint16_t)((line_tile0[l] + (c - line_start[l]) / tile_cols) / tiles_per_region);
+  return t;
 }
 
-cudaError_t launch_box_tiles(const void* R, int64_t ncells, int precision, const BoxArgs& a, const int* tiles,
-                             int ntiles, cudaStream_t st) {
+cudaError_t launch_raw_cells(const void* part, int nparts, int64_t part_stride, const int32_t* region_slots,
+                             int64_t rs_stride, const unsigned short* cell_region, int64_t ncells, int batch,
+                             int precision, void* R, cudaStream_t st) {
+  if (ncells <= 0 || batch <= 0) return cudaSuccess;
+  const int64_t pss = part_stride * nparts;
+  if (precision == 32 && part_stride % 2 == 0 && ncells % 2 == 0) {
+    dim3 grid((unsigned)((ncells / 2 + 255) / 256), batch);
+    return launch_pdl_kernel(k_raw_cells<float2, 2>, grid, dim3(256), 0, st, (const float2*)part, part_stride, pss,
+                             cell_region, region_slots, rs_stride, ncells, (float2*)R);
+  }
+  dim3 grid((unsigned)((ncells + 255) / 256), batch);
+  if (precision == 32)
+    return launch_pdl_kernel(k_raw_cells<float2, 1>, grid, dim3(256), 0, st, (const float2*)part, part_stride, pss,
+                             cell_region, region_slots, rs_stride, ncells, (float2*)R);
+  return launch_pdl_kernel(k_raw_cells<double2, 1>, grid, dim3(256), 0, st, (const double2*)part, part_stride, pss,
+                           cell_region, region_slots, rs_stride, ncells, (double2*)R);
+}
+
+cudaError_t launch_box_tiles(const void* R, int64_t ncells, int precision, const BoxArgs& a, int nlines,
+                             const int* tiles, int ntiles, cudaStream_t st) {
   if (ntiles <= 0 || a.batch <= 0) return cudaSuccess;
-  dim3 grid((unsigned)((ntiles + 127) / 128), a.batch);
-#define HOS_BT_CASE(P, WW)                                                                                   \
-  case WW:                                                                                                   \
-    return launch_pdl_kernel(k_box_tiles<P, WW>, grid, dim3(128), 0, st, (const P*)R, ncells, a, tiles, ntiles);
+  dim3 grid((unsigned)ntiles, a.batch);
+#define HOS_BT_CASE(P, WW)                                                                             \
+  case WW:                                                                                             \
+    return launch_pdl_kernel(k_box_tiles<P, WW>, grid, dim3(kTileThreads), 0, st, (const P*)R, ncells, a, \
+                             nlines, tiles);
   if (precision == 32) {
     switch (a.m3) {
       HOS_BT_CASE(float2, 3) HOS_BT_CASE(float2, 5) HOS_BT_CASE(float2, 7) HOS_BT_CASE(float2, 9)

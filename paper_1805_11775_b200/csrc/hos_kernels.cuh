@@ -251,14 +251,17 @@ cudaError_t launch_smooth_series_sep(const void* part, int nparts, int64_t part_
                                      int precision, const BoxArgs& a, int64_t nlines, int64_t nvitems,
                                      int64_t nhitems, const int* series_slots, cudaStream_t st);
 // separable K4 for order-3 grids that do not fit one CTA (cfg2, cfg3): slot sums
-// into R (compute precision), then kBR x kBC output tiles of direct window sums
+// into R (compute precision), then kTR x kTC output tiles of direct window sums
 bool box_tiles_supports(int w);
 std::vector<int32_t> box_tile_list(const int64_t* row_off, int rows);
-cudaError_t launch_raw_cells(const void* part, int nparts, int64_t part_stride, const SlotInfo& si, int precision,
-                             const int64_t* line_start, int64_t nlines, int64_t ncells, int batch, void* R,
-                             cudaStream_t st);
-cudaError_t launch_box_tiles(const void* R, int64_t ncells, int precision, const BoxArgs& a, const int* tiles,
-                             int ntiles, cudaStream_t st);
+// region of every cell (the K2 region whose slots hold it), for k_raw_cells
+std::vector<uint16_t> cell_region_table(const int32_t* line_tile0, const int64_t* line_start, int64_t nlines,
+                                        int tile_cols, int tiles_per_region);
+cudaError_t launch_raw_cells(const void* part, int nparts, int64_t part_stride, const int32_t* region_slots,
+                             int64_t rs_stride, const unsigned short* cell_region, int64_t ncells, int batch,
+                             int precision, void* R, cudaStream_t st);
+cudaError_t launch_box_tiles(const void* R, int64_t ncells, int precision, const BoxArgs& a, int nlines,
+                             const int* tiles, int ntiles, cudaStream_t st);
 // raw[c] = sum_p part[p][c] (fp64 sum, stored in the compute precision)
 // dst_line (optional): per line, the output index of its first cell (else raw[c]);
 // dst_addr (optional, wins): per line, the address (possibly a peer GPU's) of its first cell
