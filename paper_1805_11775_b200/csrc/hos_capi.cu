@@ -90,6 +90,20 @@ struct hos_plan {
   int* d_ready = nullptr;
   cudaStream_t side = nullptr;
   cudaEvent_t e_fork = nullptr, e_join = nullptr;
+  // chunked host path (hos_estimate_host, page-locked buffers): the series
+  // crosses PCIe in `chunks` copy-engine transfers of chunk_k segments on
+  // c_copy while the front end and a k_triple_cta launch per chunk (one
+  // schedule of chunk_k segments, its E rows shifted per chunk) add each
+  // chunk's products into the same partial slots
+  int chunks = 0, chunk_k = 0;
+  int c_nctas = 0, c_tab_stages = 0, c_tab_blocks = 0;
+  hos::CtaBlock* d_c_blocks = nullptr;
+  hos::CtaStage* d_c_stages = nullptr;
+  int32_t* d_c_cta_stage0 = nullptr;
+  int4* d_c_cta_head = nullptr;
+  int32_t* d_c_region_slots = nullptr;
+  cudaStream_t c_copy = nullptr;
+  std::vector<cudaEvent_t> c_ev;  // chunk i landed (c_ev[chunks]: fork)
   int hstride = 0;   // complex elements per half-spectrum row
   int L = 0, Lp = 0; // extended-spectrum length / pitch (complex elements)
   // device tables
@@ -388,14 +402,34 @@ hos::TripleArgs triple_args(const hos_plan* p, int seg_begin, int seg_end, int n
 }
 
 // partial slots of the plan's main K2 launch (k_triple_cta or k_triple_w)
-hos::SlotInfo main_slot_info(const hos_plan* p, bool streaming = false) {
+enum Sched { kMainSched = 0, kStreamSched = 1, kChunkSched = 2 };
+hos::SlotInfo main_slot_info(const hos_plan* p, int sched = kMainSched) {
   hos::SlotInfo si = slot_info(p, p->k, p->nctas);
-  si.region_slots = streaming ? p->d_s_region_slots : p->d_region_slots;
-  si.rs_stride = streaming ? 0 : p->rs_stride;
+  si.region_slots = sched == kStreamSched ? p->d_s_region_slots
+                    : sched == kChunkSched ? p->d_c_region_slots
+                                           : p->d_region_slots;
+  si.rs_stride = sched == kMainSched ? p->rs_stride : 0;
   return si;
 }
 
-hos::CtaTripleArgs cta_args(const hos_plan* p, bool streaming = false) {
+hos::CtaTripleArgs cta_args(const hos_plan* p, bool streaming = false);
+// K2 over chunk `c` of the chunked host path (rows shifted, slots accumulated after chunk 0)
+hos::CtaTripleArgs chunk_args(const hos_plan* p, int c) {
+  hos::CtaTripleArgs a = cta_args(p);
+  a.blocks = p->d_c_blocks;
+  a.stages = p->d_c_stages;
+  a.cta_stage0 = p->d_c_cta_stage0;
+  a.cta_head = p->d_c_cta_head;
+  a.nctas = p->c_nctas;
+  a.tab_stages = p->c_tab_stages;
+  a.tab_blocks = p->c_tab_blocks;
+  a.trace = nullptr;
+  a.row_shift = c * p->chunk_k;
+  a.accumulate = c > 0 ? 1 : 0;
+  return a;
+}
+
+hos::CtaTripleArgs cta_args(const hos_plan* p, bool streaming) {
   hos::CtaTripleArgs a{};
   a.E = p->d_E;
   a.Lp = p->Lp;
@@ -492,9 +526,9 @@ int stream_front_ctas() {
   return hos::kStreamFrontCtas;
 }
 
-bool build_cta_schedule(const hos_plan* p, CtaSchedule& cs, int interleave_ctas = 0) {
+bool build_cta_schedule(const hos_plan* p, CtaSchedule& cs, int interleave_ctas = 0, int k_override = 0) {
   const hos::Geometry& g = p->geo;
-  const int R = g.nregions, K = p->k, B = p->batch;
+  const int R = g.nregions, K = k_override > 0 ? k_override : p->k, B = p->batch;
   if (R <= 0 || K <= 0) return false;
   const int64_t row_bytes = (int64_t)p->Lp * (int64_t)e_bytes(p->precision);
   if (!cta_fits(g, p->precision)) return false;
@@ -723,8 +757,9 @@ int run_box(hos_plan* p, void* out_dev, cudaStream_t st) {
 
 // K4 of the whole grid: one CTA per series in shared memory when the grid is
 // small (order 3), else line scans + box sums
-int run_smooth(hos_plan* p, void* out_dev, cudaStream_t st, int stage = -1, bool streaming = false) {
-  const hos::SlotInfo si = main_slot_info(p, streaming);
+int run_smooth(hos_plan* p, void* out_dev, cudaStream_t st, int stage = -1, int sched = kMainSched) {
+  const hos::SlotInfo si = main_slot_info(p, sched);
+  const bool streaming = sched == kStreamSched;
   if (p->series_k4) {
     if (stage != 5 && p->sep_k4)
       CUDA_TRY(hos::launch_smooth_series_sep(p->d_part, p->maxslots, p->geo.ncells, si, p->precision,
@@ -1273,6 +1308,37 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
       }
     }
   }
+  {
+    // chunked host path: equal chunks of >= 32 segments (HOS_CHUNKS=n, 0/1: off).
+    // Two chunks (cfg2 e2e 153.5 -> 148.7 us, same box): every chunk adds a
+    // front-end and a K2 launch (~8 us of fixed cost each: 4 chunks 164 us,
+    // 8 chunks 205 us), and a copy running under the kernels slows both
+    // (tools/dma_interference.py), so finer chunks lose
+    const char* env = std::getenv("HOS_CHUNKS");
+    const int want = env ? std::atoi(env) : 2;
+    CtaSchedule cs;
+    if (p->cta && p->fused && batch == 1 && want > 1 && k % want == 0 && k / want >= 32 &&
+        build_cta_schedule(p, cs, 0, k / want) && cs.groups.size() == sched.groups.size() &&
+        cs.depth == p->cta_depth && cs.slot_bytes == p->cta_slot_bytes && cs.copy_b == p->cta_copy_b) {
+      p->chunks = want;
+      p->chunk_k = k / want;
+      p->c_nctas = cs.nctas;
+      p->c_tab_stages = cs.tab_stages;
+      p->c_tab_blocks = cs.tab_blocks;
+      p->maxslots = std::max(p->maxslots, cs.maxslots);
+      if ((rc = upload(p, &p->d_c_blocks, cs.blocks))) return bail(rc);
+      if ((rc = upload(p, &p->d_c_stages, cs.stages))) return bail(rc);
+      if ((rc = upload(p, &p->d_c_cta_stage0, cs.cta_stage0))) return bail(rc);
+      if ((rc = upload(p, &p->d_c_cta_head, cs.heads()))) return bail(rc);
+      if ((rc = upload(p, &p->d_c_region_slots, cs.region_slots))) return bail(rc);
+      p->c_ev.assign(want + 1, nullptr);
+      for (auto& e : p->c_ev)
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+          return bail(fail(HOS_ECUDA, "cannot create the chunked host path's events"));
+      if (cudaStreamCreateWithFlags(&p->c_copy, cudaStreamNonBlocking) != cudaSuccess)
+        return bail(fail(HOS_ECUDA, "cannot create the chunked host path's copy stream"));
+    }
+  }
   const size_t rows = (size_t)batch * k;
   if ((rc = alloc(p, &p->d_seg, rows * m * rsize(precision)))) return bail(rc);
   if ((rc = alloc(p, &p->d_half, rows * p->hstride * csize(precision)))) return bail(rc);
@@ -1307,6 +1373,12 @@ void hos_plan_destroy(hos_plan* p) {
                   (void*)p->d_ready})
     if (b) cudaFree(b);
   if (p->h_err) cudaFreeHost(p->h_err);
+  for (void* b : {(void*)p->d_c_blocks, (void*)p->d_c_stages, (void*)p->d_c_cta_stage0, (void*)p->d_c_cta_head,
+                  (void*)p->d_c_region_slots})
+    if (b) cudaFree(b);
+  for (cudaEvent_t e : p->c_ev)
+    if (e) cudaEventDestroy(e);
+  if (p->c_copy) cudaStreamDestroy(p->c_copy);
   release_p2p(p);
   for (void* b : {(void*)p->d_series_slots, (void*)p->d_s_series_slots, (void*)p->d_box_tiles,
                   (void*)p->d_cell_region})
@@ -1479,6 +1551,32 @@ int hos_estimate_host(hos_plan* p, const void* x_host, int x_dtype, int64_t x_st
   cudaGetLastError();
   const char* zc_env = std::getenv("HOS_ZEROCOPY");
   const bool zero_copy = pinned && p->fused && ai.devicePointer && ao.devicePointer && !(zc_env && zc_env[0] == '0');
+  // chunked: copy-engine transfers of the series in chunks on c_copy; per
+  // chunk the front end (device-resident samples) and K2 (accumulating into
+  // the partial slots) run while the next chunk crosses PCIe; the smoothing
+  // writes the values straight into host memory
+  const char* ch_env = std::getenv("HOS_CHUNKED");
+  const bool chunked = zero_copy && p->chunks > 1 && !p->stream_ok && !p->timing && !p->trace &&
+                       !(ch_env && ch_env[0] == '0');
+  auto ch_body = [&](cudaStream_t s) -> int {
+    const size_t cb = (size_t)p->chunk_k * p->m * es;
+    CUDA_TRY(cudaEventRecord(p->c_ev[p->chunks], s));  // fork: the copies follow the caller's prior work
+    CUDA_TRY(cudaStreamWaitEvent(p->c_copy, p->c_ev[p->chunks], 0));
+    const bool nocopy = std::getenv("HOS_CHUNK_NOCOPY") != nullptr;  // diagnostics: compute chain alone
+    for (int c = 0; c < p->chunks; c++) {
+      if (!nocopy)
+        CUDA_TRY(cudaMemcpyAsync((char*)p->d_xin + c * cb, (const char*)x_host + c * cb, cb,
+                                 cudaMemcpyHostToDevice, p->c_copy));
+      CUDA_TRY(cudaEventRecord(p->c_ev[c], p->c_copy));
+    }
+    for (int c = 0; c < p->chunks; c++) {
+      CUDA_TRY(cudaStreamWaitEvent(s, p->c_ev[c], 0));
+      int r = fused_front(p, p->d_xin, x_dtype, (int64_t)km, c * p->chunk_k, p->chunk_k, 1, s, p->quad);
+      if (r) return r;
+      CUDA_TRY(hos::launch_triple_cta(chunk_args(p, c), p->precision, s));
+    }
+    return run_smooth(p, ao.devicePointer, s, -1, kChunkSched);
+  };
   auto zc_body = [&](cudaStream_t s) -> int {
     if (p->timing) CUDA_TRY(cudaEventRecord(p->ev[0], s));
     if (p->stream_ok && !p->timing) {
@@ -1494,7 +1592,7 @@ int hos_estimate_host(hos_plan* p, const void* x_host, int x_dtype, int64_t x_st
                                  p->d_tw, p->precision, p->geo.f_lo, p->L, p->Lp, p->d_E, s, p->quad ? 1 : 0,
                                  p->d_ready));
       CUDA_TRY(cudaMemsetAsync(p->d_ready, 0, sizeof(int), s));
-      return run_smooth(p, ao.devicePointer, s, -1, true);
+      return run_smooth(p, ao.devicePointer, s, -1, kStreamSched);
     }
     int r = fused_front(p, ai.devicePointer, x_dtype, x_stride, 0, p->k, p->batch, s, p->quad);
     if (r) return r;
@@ -1502,7 +1600,10 @@ int hos_estimate_host(hos_plan* p, const void* x_host, int x_dtype, int64_t x_st
       for (int i = 1; i <= 3; i++) CUDA_TRY(cudaEventRecord(p->ev[i], s));
     return run_back(p, ao.devicePointer, s);
   };
-  if (pinned && p->use_graphs && !p->timing && !p->trace) {
+  if (chunked) {
+    const hos_plan::GraphKey key{4, x_host, x_dtype, x_stride, out_host};
+    if ((rc = p->use_graphs ? run_graph(p, key, st, ch_body) : ch_body(st))) return rc;
+  } else if (pinned && p->use_graphs && !p->timing && !p->trace) {
     const hos_plan::GraphKey key{zero_copy ? 3 : 2, x_host, x_dtype, x_stride, out_host};
     if ((rc = zero_copy ? run_graph(p, key, st, zc_body) : run_graph(p, key, st, body))) return rc;
   } else if (zero_copy) {

@@ -1258,7 +1258,7 @@ __global__ void __launch_bounds__(32 * (Q ? kCtaWarpsQ : kCtaWarps), 1)
   auto ld_stage = [&](int k) {
     CtaStage v;
     const int4 r = st_s[k];
-    v.row = r.x;
+    v.row = r.x + a.row_shift;
     v.nseg = r.y;
     v.block = r.z;
     v.pad = r.w;
@@ -1370,8 +1370,18 @@ __global__ void __launch_bounds__(32 * (Q ? kCtaWarpsQ : kCtaWarps), 1)
       const int cm = Q ? lcmax_s[line0 + S * i] : lcm[i];
       C* dst = P + (Q ? (int)(lstart_s[line0 + S * i] - a.lo) : loff[i]);
 #pragma unroll
-      for (int j = 0; j < 8; j++)
-        if (c0 + S * j <= cm) dst[c0 + S * j] = acc.template cell<CONJ>(i, j);
+      if (a.accumulate) {  // chunked host path: the slots hold the earlier chunks' sums
+#pragma unroll
+        for (int j = 0; j < 8; j++)
+          if (c0 + S * j <= cm) {
+            const C v = acc.template cell<CONJ>(i, j), o = dst[c0 + S * j];
+            dst[c0 + S * j] = C{o.x + v.x, o.y + v.y};
+          }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; j++)
+          if (c0 + S * j <= cm) dst[c0 + S * j] = acc.template cell<CONJ>(i, j);
+      }
     }
   };
   // the stage table is read one stage ahead (and the possible refill's

@@ -174,6 +174,8 @@ struct CtaTripleArgs {
   int tab_blocks;             // block-table entries reserved in shared memory (>= blocks of any CTA)
   const int* ready;           // nullptr, or per E row: 1 once a concurrently running front end wrote it
   int* err;                   // streaming: set to 1 (host-mapped word) when a ready wait timed out
+  int row_shift;              // added to every stage's E row (chunked host path: the chunk's first segment)
+  int accumulate;             // 1: add the block sums into the partial slots (later chunks), 0: store them
 };
 // in-step kernel timing slots (hos_plan_set_stamps): [kind][~first start | last end][SM]
 enum StampKind { kStampFront = 0, kStampPrep, kStampExtend, kStampTriple, kStampScan, kStampBox, kStampSeries,
