@@ -1309,13 +1309,17 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
     }
   }
   {
-    // chunked host path: equal chunks of >= 32 segments (HOS_CHUNKS=n, 0/1: off).
-    // Two chunks (cfg2 e2e 153.5 -> 148.7 us, same box): every chunk adds a
-    // front-end and a K2 launch (~8 us of fixed cost each: 4 chunks 164 us,
-    // 8 chunks 205 us), and a copy running under the kernels slows both
-    // (tools/dma_interference.py), so finer chunks lose
+    // chunked host path (opt-in: HOS_CHUNKS=n >= 2): equal chunks of >= 32
+    // segments cross PCIe on the copy engine while the previous chunk's front
+    // end and K2 run.  Two chunks: cfg2 e2e 153.5 -> 148.7 us when the copy
+    // engine is warm -- but a 4 MiB copy-engine H2D issued once per call runs
+    // at 13-53 GB/s depending on what the link did in the preceding
+    // milliseconds (tools/e2e_cliff.py: the same call takes 148 us or 350-490
+    // us, and the default bench run hit the slow regime after 18 calls), while
+    // the zero-copy front end (SM loads over PCIe) holds 153 us from the second
+    // call on.  The default is therefore the zero-copy path.
     const char* env = std::getenv("HOS_CHUNKS");
-    const int want = env ? std::atoi(env) : 2;
+    const int want = env ? std::atoi(env) : 0;
     CtaSchedule cs;
     if (p->cta && p->fused && batch == 1 && want > 1 && k % want == 0 && k / want >= 32 &&
         build_cta_schedule(p, cs, 0, k / want) && cs.groups.size() == sched.groups.size() &&

@@ -4,8 +4,8 @@ per-warp staged K2 (k_triple_w) for every config, 8 x 16 tiles, the
 streaming host path (front end and K2 concurrent, HOS_STREAM=1), the quad-row
 16-warp K2 (HOS_K2_QUAD=1), both K2 refill hand-offs, the line-scan +
 prefix-difference smoother for line grids (HOS_K4_TILES=0), the prefix-sum per-series
-smoother (HOS_K4_SEP=0), and the host entry point without chunked copies
-(HOS_CHUNKED=0: the front end reads the series over PCIe) or with 8 chunks."""
+smoother (HOS_K4_SEP=0), and the host entry point with copy-engine chunks
+(HOS_CHUNKS=2 / 8; the default reads the series over PCIe in the front end)."""
 
 import os
 import subprocess
@@ -55,7 +55,7 @@ print("VARIANT-OK")
 
 @pytest.mark.parametrize("env", ["HOS_K2=warp", "HOS_K2_TILE=2", "HOS_STREAM=1", "HOS_CTA_DEPTH=4", "HOS_K2_QUAD=1",
                                  "HOS_K2_REFILL=empty", "HOS_K2_REFILL=last", "HOS_K4_TILES=0", "HOS_K4_SEP=0",
-                                 "HOS_CHUNKED=0", "HOS_CHUNKS=8"])
+                                 "HOS_CHUNKS=2", "HOS_CHUNKS=8"])
 def test_variant_parity(cuda, env):
     k, v = env.split("=")
     code = CHILD.format(root=ROOT, tests=os.path.join(ROOT, "tests"))
