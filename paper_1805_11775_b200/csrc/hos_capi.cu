@@ -57,6 +57,8 @@ struct hos_plan {
   bool series_k4 = false;  // K4 as one CTA per series with the grid in shared memory
   bool sep_k4 = false;     // ... as separable direct window sums (k_smooth_series_sep; else prefix sums)
   int64_t sep_vitems = 0, sep_hitems = 0;  // k_smooth_series_sep work items
+  bool pipe_k4 = false;    // ... pipelined (k_smooth_series_pipe: bulk-copied raw cells, conflict-free passes)
+  hos::PipeDims pipe_dims;
   // separable K4 of order-3 grids (k_raw_cells + k_box_tiles) instead of line scans + prefix differences
   bool tiles_k4 = false;
   int box_ntiles = 0;
@@ -761,7 +763,11 @@ int run_smooth(hos_plan* p, void* out_dev, cudaStream_t st, int stage = -1, int 
   const hos::SlotInfo si = main_slot_info(p, sched);
   const bool streaming = sched == kStreamSched;
   if (p->series_k4) {
-    if (stage != 5 && p->sep_k4)
+    if (stage != 5 && p->pipe_k4)
+      CUDA_TRY(hos::launch_smooth_series_pipe(p->d_part, p->maxslots, p->geo.ncells, si, p->precision,
+                                              box_args(p, out_dev), p->geo.nlines, p->pipe_dims,
+                                              streaming ? p->d_s_series_slots : p->d_series_slots, st));
+    else if (stage != 5 && p->sep_k4)
       CUDA_TRY(hos::launch_smooth_series_sep(p->d_part, p->maxslots, p->geo.ncells, si, p->precision,
                                              box_args(p, out_dev), p->geo.nlines, p->sep_vitems, p->sep_hitems,
                                              streaming ? p->d_s_series_slots : p->d_series_slots, st));
@@ -1165,6 +1171,12 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
     p->sep_k4 = p->series_k4 && !(sep && sep[0] == '0') && hos::smooth_series_sep_supports(m3) &&
                 hos::smooth_series_sep_smem(g.ncells, g.nlines, g.rows, g.nregions, g.npoints, m3, p->sep_vitems,
                                             p->sep_hitems, precision) <= 200 * 1024;
+    // pipelined variant (default; HOS_K4_PIPE=0: k_smooth_series_sep)
+    const char* pk = std::getenv("HOS_K4_PIPE");
+    p->pipe_dims = hos::smooth_series_pipe_dims(g.row_off.data(), g.rows, m3);
+    p->pipe_k4 = p->sep_k4 && !(pk && pk[0] == '0') &&
+                 hos::smooth_series_pipe_smem(g.ncells, g.nlines, g.rows, g.nregions, m3, p->pipe_dims, precision) <=
+                     220 * 1024;
   }
   // +4 elements: fp32 operands are staged from the 16-byte-aligned element at
   // or below their start, in whole 16-byte chunks (K2), so a copy may read up
@@ -1350,7 +1362,8 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
   if ((rc = alloc(p, &p->d_E, e_bytes))) return bail(rc);
   if (cudaMemset(p->d_E, 0, e_bytes) != cudaSuccess)  // pad elements stay defined
     return bail(fail(HOS_ECUDA, "cudaMemset failed"));
-  if ((rc = alloc(p, &p->d_part, (size_t)batch * p->maxslots * g.ncells * csize(precision)))) return bail(rc);
+  // +64: k_smooth_series_pipe's bulk copy of a series rounds its size up to 16 bytes
+  if ((rc = alloc(p, &p->d_part, (size_t)batch * p->maxslots * g.ncells * csize(precision) + 64))) return bail(rc);
   if ((rc = alloc(p, (void**)&p->d_S, (size_t)batch * g.ncells * 16))) return bail(rc);
   if ((rc = alloc(p, &p->d_xin, rows * m * 8))) return bail(rc);
   if ((rc = alloc(p, &p->d_out, (size_t)batch * g.npoints * csize(precision)))) return bail(rc);

@@ -2303,6 +2303,297 @@ cudaError_t launch_smooth_series_sep(const void* part, int nparts, int64_t part_
 }
 
 // ===========================================================================
+// K4 for SMALL order-3 grids, SEPARABLE and PIPELINED (default when it fits):
+// the same two 1-D direct window sums as k_smooth_series_sep, restructured so
+// the kernel is bound by HBM rather than by load latency and index arithmetic.
+//   * a series' raw cells R are contiguous in its partial slot: one elected
+//     thread lands them in shared memory with ONE cp.async.bulk (mbarrier
+//     transaction count), issued as soon as the previous series' vertical
+//     pass has consumed the buffer -- the copy of series s+1 runs under the
+//     horizontal pass and the output stores of series s; two 512-thread CTAs
+//     per SM keep ~2 x 42 KB of reads in flight per SM (cfg5);
+//   * vertical pass: item (block of kPipeT rows, column j) reads a strip of
+//     kPipeT+W-1 cells of one column from shared memory (lanes along j:
+//     conflict-free) through a per-block int4 table of line starts, writes V;
+//   * horizontal pass: item (row, pair of outputs) reads W+1 consecutive V
+//     cells as 16-byte loads (lanes 16 bytes apart: conflict-free; the strip
+//     form of k_smooth_series_sep had 6.6 M bank conflicts per launch) and
+//     forms two outputs from a shared inner sum.
+// Series K2 cut between CTAs (several partial slots) are filled by all
+// threads, slots summed in slot order in fp64, as in k_smooth_series_sep.
+constexpr int kPipeT = 4;
+#ifndef HOS_PIPE_THREADS
+#define HOS_PIPE_THREADS 512
+#endif
+constexpr int kPipeThreads = HOS_PIPE_THREADS;
+
+struct PipeLayout {  // shared-memory layout (bytes from the 128-byte aligned base)
+  size_t R, V, tabs, vrow, hrow, bar, total;
+  int ltab;     // ints per vertical block record (line starts then {V offset, width} per row)
+  int vtot;     // V cells (rows padded to even)
+};
+
+__host__ __device__ inline PipeLayout pipe_layout(int64_t ncells, int nlines, int rows, int nregions, int w,
+                                                  int nvitems, int nhitems, int maxw, const int64_t vtot, size_t cs) {
+  PipeLayout L{};
+  const int nblk = (rows + kPipeT - 1) / kPipeT;
+  auto up = [](size_t x, size_t a) { return (x + a - 1) / a * a; };
+  L.ltab = (int)up((size_t)(kPipeT + w - 1) + 2 * kPipeT, 4);
+  L.vtot = (int)vtot;
+  size_t o = 0;
+  L.R = o;
+  o = up(o + (size_t)(ncells + maxw + 4) * cs, 128);  // +maxw: strips past the last line read in-buffer garbage
+  L.V = o;
+  o = up(o + (size_t)(vtot + 16) * cs, 16);
+  L.tabs = o;  // ints: blk records | row records (int4 {vo, ro, len, hb}) | lines (ls, lt0) | rsl | vb
+  o = up(o + ((size_t)nblk * L.ltab + 4 * (size_t)(rows + 1) + 2 * (size_t)(nlines + 1) + nregions + nblk + 1) * 4, 16);
+  L.vrow = o;
+  o = up(o + (size_t)nvitems * 2, 16);
+  L.hrow = o;
+  o = up(o + (size_t)nhitems * 2, 16);
+  L.bar = o;
+  L.total = o + 16;
+  return L;
+}
+
+template <typename P2>
+__device__ __forceinline__ void lds_pair(const P2* p, P2& a, P2& b);
+template <>
+__device__ __forceinline__ void lds_pair<float2>(const float2* p, float2& a, float2& b) {
+  const float4 v = *reinterpret_cast<const float4*>(p);
+  a = make_float2(v.x, v.y);
+  b = make_float2(v.z, v.w);
+}
+template <>
+__device__ __forceinline__ void lds_pair<double2>(const double2* p, double2& a, double2& b) {
+  a = p[0];
+  b = p[1];
+}
+
+template <typename P2, int W>
+__global__ void __launch_bounds__(kPipeThreads) k_smooth_series_pipe(const P2* __restrict__ part, int64_t part_stride,
+                                                                    int64_t part_series_stride, SlotInfo si, BoxArgs a,
+                                                                    int nlines, int nvitems, int nhitems, int maxw,
+                                                                    int vtot,
+                                                                    const int* __restrict__ series_slots) {
+  StampEnd stamp_end_(kStampSeries);
+  using T = decltype(P2{}.x);
+  constexpr int NX = kPipeT + W - 1;  // strip length
+  extern __shared__ __align__(128) unsigned char sm_raw[];
+  const int ncells = (int)a.s_series_stride;
+  const int rows = a.rows;
+  const int nblk = (rows + kPipeT - 1) / kPipeT;
+  const PipeLayout L = pipe_layout(ncells, nlines, rows, si.nregions, W, nvitems, nhitems, maxw, vtot, sizeof(P2));
+  P2* Rb = reinterpret_cast<P2*>(sm_raw + L.R);  // the landed cells start at Rb + shift (0 or 1)
+  P2* V = reinterpret_cast<P2*>(sm_raw + L.V);
+  int* blk = reinterpret_cast<int*>(sm_raw + L.tabs);        // nblk x ltab
+  int4* rowrec = reinterpret_cast<int4*>(blk + (size_t)nblk * L.ltab);  // rows + 1: {vo, ro, len, hb}
+  int* ls = reinterpret_cast<int*>(rowrec + rows + 1);       // nlines + 1
+  int* lt0 = ls + nlines + 1;                                // nlines + 1
+  int* rsl = lt0 + nlines + 1;                               // nregions
+  int* vb = rsl + si.nregions;                               // nblk + 1
+  unsigned short* vrow = reinterpret_cast<unsigned short*>(sm_raw + L.vrow);
+  unsigned short* hrow = reinterpret_cast<unsigned short*>(sm_raw + L.hrow);
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(sm_raw + L.bar);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  // ---- static geometry, once per CTA (before the PDL wait: overlaps K2's tail)
+  for (int i = tid; i <= nlines; i += blockDim.x) ls[i] = (int)__ldg(a.line_start + i);
+  for (int i = tid; i < nlines; i += blockDim.x) lt0[i] = __ldg(si.line_tile0 + i);
+  for (int i = tid; i <= rows; i += blockDim.x) rowrec[i].y = (int)__ldg(a.row_off + i);
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int v = 0, h = 0;
+    for (int r = 0; r < rows; r++) {
+      const int len = rowrec[r + 1].y - rowrec[r].y;
+      rowrec[r].x = v;
+      rowrec[r].z = len;
+      rowrec[r].w = h;
+      v += (len + W - 1 + 1) & ~1;  // rows of V start on 16-byte boundaries (fp32)
+      h += (len + 1) / 2;
+    }
+    rowrec[rows].x = v;
+    rowrec[rows].z = 0;
+    rowrec[rows].w = h;
+    int it = 0;
+    for (int b = 0; b < nblk; b++) {
+      vb[b] = it;
+      int mx = 0;
+      for (int r = b * kPipeT; r < min(rows, (b + 1) * kPipeT); r++) mx = max(mx, rowrec[r].z + W - 1);
+      it += mx;
+    }
+    vb[nblk] = it;
+  }
+  __syncthreads();
+  for (int i = tid; i < nblk * L.ltab; i += blockDim.x) {
+    const int b = i / L.ltab, e = i - b * L.ltab, k1 = b * kPipeT;
+    int v = 0;
+    if (e < NX) v = ls[min(k1 + e, nlines - 1)];
+    else if (e < NX + kPipeT) v = k1 + (e - NX) < rows ? rowrec[k1 + (e - NX)].x : 0;                 // V offset of the row
+    else if (e < NX + 2 * kPipeT) v = k1 + (e - NX - kPipeT) < rows ? rowrec[k1 + (e - NX - kPipeT)].z + W - 1 : 0;  // width
+    blk[i] = v;
+  }
+  for (int b = warp; b < nblk; b += nw)
+    for (int q = vb[b] + lane; q < vb[b + 1]; q += 32) vrow[q] = (unsigned short)b;
+  for (int r = warp; r < rows; r += nw)
+    for (int q = rowrec[r].w + lane; q < rowrec[r + 1].w; q += 32) hrow[q] = (unsigned short)r;
+  __syncthreads();
+  const unsigned bar_s = (unsigned)__cvta_generic_to_shared(bar);
+  const unsigned rb_s = (unsigned)__cvta_generic_to_shared(Rb);
+  // fill of one series into the R buffer: bulk copy (one slot) or slot sums by
+  // all threads; returns the cell shift of the landed data (bulk: the copy
+  // starts at the 16-byte aligned cell at or below the series' first)
+  auto fill = [&](int series, bool one) -> int {
+    const P2* src = part + series * part_series_stride;
+    if (one) {
+      const int shift = sizeof(P2) == 8 ? (int)((reinterpret_cast<unsigned long long>(src) >> 3) & 1) : 0;
+      if (tid == 0) {
+        const unsigned bytes = (unsigned)((((size_t)(ncells + shift) * sizeof(P2)) + 15) & ~(size_t)15);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_s), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(rb_s),
+                     "l"(src - shift), "r"(bytes), "r"(bar_s)
+                     : "memory");
+      }
+      return shift;
+    }
+    for (int r = tid; r < si.nregions; r += blockDim.x) rsl[r] = __ldg(si.region_slots + series * si.rs_stride + r);
+    __syncthreads();
+    for (int l = warp; l < nlines; l += nw) {
+      const int l0 = ls[l], len = ls[l + 1] - l0, t0 = lt0[l];
+      for (int c = lane; c < len; c += 32) {
+        const int ns = rsl[(t0 + c / si.tile_cols) / si.tiles_per_region];
+        double vr = 0.0, vi = 0.0;
+        for (int t = 0; t < ns; t++) {
+          const P2 q = __ldcs(src + (int64_t)t * part_stride + l0 + c);
+          vr += (double)q.x;
+          vi += (double)q.y;
+        }
+        Rb[l0 + c] = P2{(T)vr, (T)vi};
+      }
+    }
+    return 0;
+  };
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  stamp_start(kStampSeries);  // partial slots come from K2
+  const T sc = (T)a.scale;
+  int series = blockIdx.x;
+  bool one = series < a.batch && __ldg(series_slots + series) == 1;
+  int shift = series < a.batch ? fill(series, one) : 0;
+  unsigned par = 0;
+  for (; series < a.batch; series += gridDim.x) {
+    if (one) {  // the bulk copy of this series has landed
+      asm volatile(
+          "{\n.reg .pred P1;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n@!P1 bra W_%=;\n}\n" ::"r"(
+              bar_s),
+          "r"(par), "r"(1000000u)
+          : "memory");
+      par ^= 1;
+    }
+    __syncthreads();  // slot-sum fills are visible; the previous series' reads of V are done
+    const P2* R = Rb + shift;
+    // ---- vertical: item (row block b, column j) -> V(k1 + r, j), r < kPipeT
+    for (int it = tid; it < nvitems; it += blockDim.x) {
+      const int b = vrow[it], j = it - vb[b];
+      const int* rec = blk + b * L.ltab;
+      P2 x[NX];
+#pragma unroll
+      for (int u = 0; u < NX; u++) x[u] = R[rec[u] + j];
+#pragma unroll
+      for (int r = 0; r < kPipeT; r++) {
+        P2 acc = x[r];
+#pragma unroll
+        for (int u = 1; u < W; u++) acc = add2(acc, x[r + u]);
+        if (j < rec[NX + kPipeT + r]) V[rec[NX + r] + j] = acc;
+      }
+    }
+    __syncthreads();  // V complete; R consumed
+    const int next = series + gridDim.x;
+    const int cur_series = series;
+    if (next < a.batch) {
+      one = __ldg(series_slots + next) == 1;
+      shift = fill(next, one);
+    }
+    // ---- horizontal: item (row k1, output pair) -> B(k1, k2), B(k1, k2 + 1)
+    P2* out = (P2*)a.out + cur_series * a.out_series_stride;
+    for (int it = tid; it < nhitems; it += blockDim.x) {
+      const int k1 = hrow[it];
+      const int4 rr = rowrec[k1];  // {vo, ro, len, hb}
+      const int k2 = 2 * (it - rr.w);
+      const P2* vp = V + rr.x + k2;
+      P2 y[W + 1];
+#pragma unroll
+      for (int v = 0; v < W + 1; v += 2) lds_pair(vp + v, y[v], y[v + 1]);
+      P2 inner = y[1];
+#pragma unroll
+      for (int v = 2; v < W; v++) inner = add2(inner, y[v]);
+      const P2 b0 = add2(inner, y[0]), b1 = add2(inner, y[W]);
+      P2* o = out + rr.y + k2;
+      __stcs(o, P2{b0.x * sc, b0.y * sc});
+      if (k2 + 1 < rr.z) __stcs(o + 1, P2{b1.x * sc, b1.y * sc});
+    }
+  }
+}
+
+// V cells (rows padded to even), widest V row and the item counts
+PipeDims smooth_series_pipe_dims(const int64_t* row_off, int rows, int w) {
+  PipeDims d{};
+  for (int b = 0; b * kPipeT < rows; b++) {
+    int64_t mx = 0;
+    for (int r = b * kPipeT; r < std::min(rows, (b + 1) * kPipeT); r++) mx = std::max(mx, row_off[r + 1] - row_off[r] + w - 1);
+    d.nvitems += mx;
+    d.maxw = std::max(d.maxw, (int)mx);
+  }
+  for (int r = 0; r < rows; r++) {
+    const int64_t len = row_off[r + 1] - row_off[r];
+    d.nhitems += (len + 1) / 2;
+    d.vtot += (len + w - 1 + 1) & ~(int64_t)1;
+  }
+  return d;
+}
+
+size_t smooth_series_pipe_smem(int64_t ncells, int64_t nlines, int rows, int nregions, int w, const PipeDims& d,
+                               int precision) {
+  if (nlines > 65535 || rows > 65535 || ncells > INT32_MAX / 4 || d.nvitems > INT32_MAX / 4) return ~(size_t)0;
+  return pipe_layout(ncells, (int)nlines, rows, nregions, w, (int)d.nvitems, (int)d.nhitems, d.maxw, d.vtot,
+                     precision == 32 ? 8 : 16)
+      .total;
+}
+
+template <typename P2, int W>
+static cudaError_t pipe_go(const P2* part, int64_t part_stride, int64_t pss, const SlotInfo& si, const BoxArgs& a,
+                           int64_t nlines, const PipeDims& d, const int* series_slots, size_t sm, cudaStream_t st) {
+  auto kern = k_smooth_series_pipe<P2, W>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPipeThreads, sm);
+  const int grid = std::max(1, std::min(a.batch, device_sms() * std::max(1, per_sm)));
+  return launch_pdl_kernel(kern, dim3(grid), dim3(kPipeThreads), sm, st, part, part_stride, pss, si, a, (int)nlines,
+                           (int)d.nvitems, (int)d.nhitems, d.maxw, (int)d.vtot, series_slots);
+}
+
+cudaError_t launch_smooth_series_pipe(const void* part, int nparts, int64_t part_stride, const SlotInfo& si,
+                                      int precision, const BoxArgs& a, int64_t nlines, const PipeDims& d,
+                                      const int* series_slots, cudaStream_t st) {
+  if (!si.line_tile0 || !si.region_slots || !series_slots) return cudaErrorInvalidValue;
+  const size_t sm = smooth_series_pipe_smem(a.s_series_stride, nlines, a.rows, si.nregions, a.m3, d, precision);
+  const int64_t pss = part_stride * nparts;
+#define HOS_PIPE_CASE(P, WW)                                                                       \
+  case WW:                                                                                         \
+    return pipe_go<P, WW>((const P*)part, part_stride, pss, si, a, nlines, d, series_slots, sm, st);
+  if (precision == 32) {
+    switch (a.m3) { HOS_PIPE_CASE(float2, 3) HOS_PIPE_CASE(float2, 5) HOS_PIPE_CASE(float2, 7) HOS_PIPE_CASE(float2, 9) }
+  } else {
+    switch (a.m3) { HOS_PIPE_CASE(double2, 3) HOS_PIPE_CASE(double2, 5) HOS_PIPE_CASE(double2, 7) HOS_PIPE_CASE(double2, 9) }
+  }
+#undef HOS_PIPE_CASE
+  return cudaErrorInvalidValue;
+}
+
+// ===========================================================================
 // K4 for order-3 grids that do not fit one CTA (cfg2, cfg3), SEPARABLE:
 //   K4a' k_raw_cells: R(c) = sum of the cell's partial slots (slot order, fp64),
 //        stored in the compute precision (no prefix scan).  A thread owns two

@@ -252,6 +252,19 @@ bool smooth_series_sep_supports(int w);
 cudaError_t launch_smooth_series_sep(const void* part, int nparts, int64_t part_stride, const SlotInfo& si,
                                      int precision, const BoxArgs& a, int64_t nlines, int64_t nvitems,
                                      int64_t nhitems, const int* series_slots, cudaStream_t st);
+// pipelined separable variant (default when its shared memory fits): the
+// series' raw cells land by one bulk copy while the previous series' outputs
+// are formed
+struct PipeDims {
+  int64_t nvitems = 0, nhitems = 0, vtot = 0;
+  int maxw = 0;
+};
+PipeDims smooth_series_pipe_dims(const int64_t* row_off, int rows, int w);
+size_t smooth_series_pipe_smem(int64_t ncells, int64_t nlines, int rows, int nregions, int w, const PipeDims& d,
+                               int precision);
+cudaError_t launch_smooth_series_pipe(const void* part, int nparts, int64_t part_stride, const SlotInfo& si,
+                                      int precision, const BoxArgs& a, int64_t nlines, const PipeDims& d,
+                                      const int* series_slots, cudaStream_t st);
 // separable K4 for order-3 grids that do not fit one CTA (cfg2, cfg3): slot sums
 // into R (compute precision), then kTR x kTC output tiles of direct window sums
 bool box_tiles_supports(int w);
