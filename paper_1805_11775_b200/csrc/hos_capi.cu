@@ -58,7 +58,8 @@ struct hos_plan {
   bool sep_k4 = false;     // ... as separable direct window sums (k_smooth_series_sep; else prefix sums)
   int64_t sep_vitems = 0, sep_hitems = 0;  // k_smooth_series_sep work items
   bool pipe_k4 = false;    // ... pipelined (k_smooth_series_pipe: bulk-copied raw cells, conflict-free passes)
-  hos::PipeDims pipe_dims;
+  hos::PipeLayout pipe_layout{};
+  unsigned char* d_pipe_tables = nullptr;
   // separable K4 of order-3 grids (k_raw_cells + k_box_tiles) instead of line scans + prefix differences
   bool tiles_k4 = false;
   int box_ntiles = 0;
@@ -765,7 +766,8 @@ int run_smooth(hos_plan* p, void* out_dev, cudaStream_t st, int stage = -1, int 
   if (p->series_k4) {
     if (stage != 5 && p->pipe_k4)
       CUDA_TRY(hos::launch_smooth_series_pipe(p->d_part, p->maxslots, p->geo.ncells, si, p->precision,
-                                              box_args(p, out_dev), p->geo.nlines, p->pipe_dims,
+                                              box_args(p, out_dev), p->pipe_layout, p->d_pipe_tables,
+                                              p->d_cell_region,
                                               streaming ? p->d_s_series_slots : p->d_series_slots, st));
     else if (stage != 5 && p->sep_k4)
       CUDA_TRY(hos::launch_smooth_series_sep(p->d_part, p->maxslots, p->geo.ncells, si, p->precision,
@@ -1173,10 +1175,7 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
                                             p->sep_hitems, precision) <= 200 * 1024;
     // pipelined variant (default; HOS_K4_PIPE=0: k_smooth_series_sep)
     const char* pk = std::getenv("HOS_K4_PIPE");
-    p->pipe_dims = hos::smooth_series_pipe_dims(g.row_off.data(), g.rows, m3);
-    p->pipe_k4 = p->sep_k4 && !(pk && pk[0] == '0') &&
-                 hos::smooth_series_pipe_smem(g.ncells, g.nlines, g.rows, g.nregions, m3, p->pipe_dims, precision) <=
-                     220 * 1024;
+    p->pipe_k4 = p->sep_k4 && !(pk && pk[0] == '0') && g.nregions < 65536;
   }
   // +4 elements: fp32 operands are staged from the 16-byte-aligned element at
   // or below their start, in whole 16-byte chunks (K2), so a copy may read up
@@ -1281,6 +1280,19 @@ int hos_plan_create(hos_plan** out, int order, int m, int k, int m3, int conjuga
     if ((rc = upload(p, &p->d_pair_k2, g.pair_k2))) return bail(rc);
     if ((rc = upload(p, &p->d_pair_base, g.pair_base))) return bail(rc);
     if ((rc = upload(p, &p->d_line_of_ab, g.line_of_ab))) return bail(rc);
+  }
+  if (p->pipe_k4) {
+    hos::PipePlan pp = hos::smooth_series_pipe_plan(g.row_off.data(), g.rows, g.line_start.data(), g.nlines, g.ncells,
+                                                    g.nregions, m3, precision);
+    if (pp.L.total <= 220 * 1024) {
+      p->pipe_layout = pp.L;
+      if ((rc = upload(p, &p->d_pipe_tables, pp.tables))) return bail(rc);
+      const std::vector<uint16_t> cr = hos::cell_region_table(g.line_tile0.data(), g.line_start.data(), g.nlines,
+                                                              g.tile_cols, g.tiles_per_region);
+      if ((rc = upload(p, &p->d_cell_region, cr))) return bail(rc);
+    } else {
+      p->pipe_k4 = false;
+    }
   }
   if (p->tiles_k4) {
     const std::vector<int32_t> bt = hos::box_tile_list(g.row_off.data(), g.rows);
@@ -1398,7 +1410,7 @@ void hos_plan_destroy(hos_plan* p) {
   if (p->c_copy) cudaStreamDestroy(p->c_copy);
   release_p2p(p);
   for (void* b : {(void*)p->d_series_slots, (void*)p->d_s_series_slots, (void*)p->d_box_tiles,
-                  (void*)p->d_cell_region})
+                  (void*)p->d_cell_region, (void*)p->d_pipe_tables})
     if (b) cudaFree(b);
   for (void* b : {p->d_raw, p->d_send, p->d_mine, p->d_local, p->d_heads, p->d_vals, p->d_parts, (void*)p->d_send_line})
     if (b) cudaFree(b);

@@ -1,5 +1,6 @@
 // sm_100a kernels of the HOS hot path; see hos_kernels.cuh for the map.
 #include "hos_kernels.cuh"
+#include <cstring>
 
 #include <cuda_runtime.h>
 #include <cstdlib>
@@ -2312,49 +2313,34 @@ cudaError_t launch_smooth_series_sep(const void* part, int nparts, int64_t part_
 //     pass has consumed the buffer -- the copy of series s+1 runs under the
 //     horizontal pass and the output stores of series s; two 512-thread CTAs
 //     per SM keep ~2 x 42 KB of reads in flight per SM (cfg5);
-//   * vertical pass: item (block of kPipeT rows, column j) reads a strip of
-//     kPipeT+W-1 cells of one column from shared memory (lanes along j:
-//     conflict-free) through a per-block int4 table of line starts, writes V;
-//   * horizontal pass: item (row, pair of outputs) reads W+1 consecutive V
-//     cells as 16-byte loads (lanes 16 bytes apart: conflict-free; the strip
-//     form of k_smooth_series_sep had 6.6 M bank conflicts per launch) and
-//     forms two outputs from a shared inner sum.
-// Series K2 cut between CTAs (several partial slots) are filled by all
-// threads, slots summed in slot order in fp64, as in k_smooth_series_sep.
-constexpr int kPipeT = 4;
+//   * every static table (per-block line starts, row records, item -> block /
+//     row maps) is built once per plan on the host and copied to shared
+//     memory as one image (16-byte loads) before the PDL wait;
+//   * vertical pass: item (block of kPipeTV rows, column j) reads
+//     kPipeTV+W-1 cells of one column from shared memory (lanes along j:
+//     conflict-free), writes kPipeTV cells of V (swizzled, see vswz_unit);
+//   * horizontal pass: item (row, kPipeT consecutive outputs) reads its strip
+//     of V as 16-byte loads and streams the outputs to HBM;
+//   * both passes form the kPipeT window sums of a strip from a shared core:
+//     W + 3 kPipeT - 6 packed adds instead of kPipeT (W - 1) (13 vs 24, W = 7).
+// Series K2 cut between CTAs (several partial slots): all threads sum the
+// slots in slot order in fp64, four cells per thread with every load of a
+// round in flight together.
+constexpr int kPipeT = 4;   // window sums formed together from one strip (horizontal item: kPipeT outputs)
+constexpr int kPipeTV = 4;  // rows per vertical block (kPipeTV / kPipeT overlapping strips per column)
 #ifndef HOS_PIPE_THREADS
 #define HOS_PIPE_THREADS 512
 #endif
 constexpr int kPipeThreads = HOS_PIPE_THREADS;
 
-struct PipeLayout {  // shared-memory layout (bytes from the 128-byte aligned base)
-  size_t R, V, tabs, vrow, hrow, bar, total;
-  int ltab;     // ints per vertical block record (line starts then {V offset, width} per row)
-  int vtot;     // V cells (rows padded to even)
-};
-
-__host__ __device__ inline PipeLayout pipe_layout(int64_t ncells, int nlines, int rows, int nregions, int w,
-                                                  int nvitems, int nhitems, int maxw, const int64_t vtot, size_t cs) {
-  PipeLayout L{};
-  const int nblk = (rows + kPipeT - 1) / kPipeT;
-  auto up = [](size_t x, size_t a) { return (x + a - 1) / a * a; };
-  L.ltab = (int)up((size_t)(kPipeT + w - 1) + 2 * kPipeT, 4);
-  L.vtot = (int)vtot;
-  size_t o = 0;
-  L.R = o;
-  o = up(o + (size_t)(ncells + maxw + 4) * cs, 128);  // +maxw: strips past the last line read in-buffer garbage
-  L.V = o;
-  o = up(o + (size_t)(vtot + 16) * cs, 16);
-  L.tabs = o;  // ints: blk records | row records (int4 {vo, ro, len, hb}) | lines (ls, lt0) | rsl | vb
-  o = up(o + ((size_t)nblk * L.ltab + 4 * (size_t)(rows + 1) + 2 * (size_t)(nlines + 1) + nregions + nblk + 1) * 4, 16);
-  L.vrow = o;
-  o = up(o + (size_t)nvitems * 2, 16);
-  L.hrow = o;
-  o = up(o + (size_t)nhitems * 2, 16);
-  L.bar = o;
-  L.total = o + 16;
-  return L;
-}
+// V is stored swizzled: a horizontal item reads 16-byte units u, u+1, ... and
+// consecutive lanes start kPipeT/2 = 2 units apart, so 8 lanes of a 16-byte
+// load would hit only 4 of the 8 bank groups; flipping bit 0 of the unit index
+// in every other group of 8 units makes them distinct (fp32; fp64 cells are
+// one unit each and the map is the identity there by the same formula on
+// cell pairs -- harmless).
+__device__ __forceinline__ int vswz_unit(int u) { return u ^ ((u >> 3) & 1); }
+__device__ __forceinline__ int vswz_cell(int c) { return (vswz_unit(c >> 1) << 1) | (c & 1); }
 
 template <typename P2>
 __device__ __forceinline__ void lds_pair(const P2* p, P2& a, P2& b);
@@ -2370,76 +2356,71 @@ __device__ __forceinline__ void lds_pair<double2>(const double2* p, double2& a, 
   b = p[1];
 }
 
+// o[r] = x[r] + ... + x[r + W - 1], r < kPipeT, from a strip of kPipeT + W - 1
+// values.  W >= kPipeT: the terms x[kPipeT-1 .. W-1] every window shares are
+// summed once; the windows add suffix sums of the strip's head and prefix
+// sums of its tail.  (Fixed association: deterministic.)
 template <typename P2, int W>
-__global__ void __launch_bounds__(kPipeThreads) k_smooth_series_pipe(const P2* __restrict__ part, int64_t part_stride,
+__device__ __forceinline__ void strip_sums(const P2* x, P2* o) {
+  constexpr int T = kPipeT;
+  if constexpr (W >= T) {
+    P2 core = x[T - 1];
+#pragma unroll
+    for (int u = T; u < W; u++) core = add2(core, x[u]);
+    P2 suf[T], pre[T];
+    suf[T - 2] = x[T - 2];
+#pragma unroll
+    for (int r = T - 3; r >= 0; r--) suf[r] = add2(x[r], suf[r + 1]);
+    pre[1] = x[W];
+#pragma unroll
+    for (int r = 2; r < T; r++) pre[r] = add2(pre[r - 1], x[W + r - 1]);
+    o[0] = add2(suf[0], core);
+#pragma unroll
+    for (int r = 1; r < T - 1; r++) o[r] = add2(add2(suf[r], core), pre[r]);
+    o[T - 1] = add2(core, pre[T - 1]);
+  } else {
+#pragma unroll
+    for (int r = 0; r < T; r++) {
+      P2 acc = x[r];
+#pragma unroll
+      for (int u = 1; u < W; u++) acc = add2(acc, x[r + u]);
+      o[r] = acc;
+    }
+  }
+}
+
+template <typename P2, int W>
+__global__ void __launch_bounds__(kPipeThreads, sizeof(P2) == 8 ? 2 : 1) k_smooth_series_pipe(const P2* __restrict__ part, int64_t part_stride,
                                                                     int64_t part_series_stride, SlotInfo si, BoxArgs a,
-                                                                    int nlines, int nvitems, int nhitems, int maxw,
-                                                                    int vtot,
+                                                                    const __grid_constant__ PipeLayout L,
+                                                                    const int4* __restrict__ tables,
+                                                                    const unsigned short* __restrict__ cell_region,
                                                                     const int* __restrict__ series_slots) {
   StampEnd stamp_end_(kStampSeries);
   using T = decltype(P2{}.x);
-  constexpr int NX = kPipeT + W - 1;  // strip length
+  constexpr int NX = kPipeT + W - 1;     // strip length
+  constexpr int NXV = kPipeTV + W - 1;   // cells of one column a vertical item reads
+  constexpr int kRecInts = (NXV + 2 * kPipeTV + 1 + 3) / 4 * 4;  // block record: line starts, V offsets, widths, max width
   extern __shared__ __align__(128) unsigned char sm_raw[];
   const int ncells = (int)a.s_series_stride;
-  const int rows = a.rows;
-  const int nblk = (rows + kPipeT - 1) / kPipeT;
-  const PipeLayout L = pipe_layout(ncells, nlines, rows, si.nregions, W, nvitems, nhitems, maxw, vtot, sizeof(P2));
   P2* Rb = reinterpret_cast<P2*>(sm_raw + L.R);  // the landed cells start at Rb + shift (0 or 1)
   P2* V = reinterpret_cast<P2*>(sm_raw + L.V);
-  int* blk = reinterpret_cast<int*>(sm_raw + L.tabs);        // nblk x ltab
-  int4* rowrec = reinterpret_cast<int4*>(blk + (size_t)nblk * L.ltab);  // rows + 1: {vo, ro, len, hb}
-  int* ls = reinterpret_cast<int*>(rowrec + rows + 1);       // nlines + 1
-  int* lt0 = ls + nlines + 1;                                // nlines + 1
-  int* rsl = lt0 + nlines + 1;                               // nregions
-  int* vb = rsl + si.nregions;                               // nblk + 1
-  unsigned short* vrow = reinterpret_cast<unsigned short*>(sm_raw + L.vrow);
-  unsigned short* hrow = reinterpret_cast<unsigned short*>(sm_raw + L.hrow);
+  const int* blk = reinterpret_cast<const int*>(sm_raw + L.tabs);              // nblk x ltab
+  const int* wbo = reinterpret_cast<const int*>(sm_raw + L.vb);                // warps + 1: the warp's range in wbl
+  const unsigned short* wbl = reinterpret_cast<const unsigned short*>(sm_raw + L.vrow);  // row blocks, warp by warp
+  const int2* hdesc = reinterpret_cast<const int2*>(sm_raw + L.hrow);            // per horizontal item
+  int* rsl = reinterpret_cast<int*>(sm_raw + L.rsl);                           // nregions: slots per region
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(sm_raw + L.bar);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  // ---- static geometry, once per CTA (before the PDL wait: overlaps K2's tail)
-  for (int i = tid; i <= nlines; i += blockDim.x) ls[i] = (int)__ldg(a.line_start + i);
-  for (int i = tid; i < nlines; i += blockDim.x) lt0[i] = __ldg(si.line_tile0 + i);
-  for (int i = tid; i <= rows; i += blockDim.x) rowrec[i].y = (int)__ldg(a.row_off + i);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // ---- static tables: one host-built image (before the PDL wait: overlaps K2's tail)
+  {
+    int4* dst = reinterpret_cast<int4*>(sm_raw + L.tabs);
+    for (int i = tid; i < L.table_bytes / 16; i += blockDim.x) dst[i] = __ldg(tables + i);
+  }
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncthreads();
-  if (tid == 0) {
-    int v = 0, h = 0;
-    for (int r = 0; r < rows; r++) {
-      const int len = rowrec[r + 1].y - rowrec[r].y;
-      rowrec[r].x = v;
-      rowrec[r].z = len;
-      rowrec[r].w = h;
-      v += (len + W - 1 + 1) & ~1;  // rows of V start on 16-byte boundaries (fp32)
-      h += (len + 1) / 2;
-    }
-    rowrec[rows].x = v;
-    rowrec[rows].z = 0;
-    rowrec[rows].w = h;
-    int it = 0;
-    for (int b = 0; b < nblk; b++) {
-      vb[b] = it;
-      int mx = 0;
-      for (int r = b * kPipeT; r < min(rows, (b + 1) * kPipeT); r++) mx = max(mx, rowrec[r].z + W - 1);
-      it += mx;
-    }
-    vb[nblk] = it;
-  }
-  __syncthreads();
-  for (int i = tid; i < nblk * L.ltab; i += blockDim.x) {
-    const int b = i / L.ltab, e = i - b * L.ltab, k1 = b * kPipeT;
-    int v = 0;
-    if (e < NX) v = ls[min(k1 + e, nlines - 1)];
-    else if (e < NX + kPipeT) v = k1 + (e - NX) < rows ? rowrec[k1 + (e - NX)].x : 0;                 // V offset of the row
-    else if (e < NX + 2 * kPipeT) v = k1 + (e - NX - kPipeT) < rows ? rowrec[k1 + (e - NX - kPipeT)].z + W - 1 : 0;  // width
-    blk[i] = v;
-  }
-  for (int b = warp; b < nblk; b += nw)
-    for (int q = vb[b] + lane; q < vb[b + 1]; q += 32) vrow[q] = (unsigned short)b;
-  for (int r = warp; r < rows; r += nw)
-    for (int q = rowrec[r].w + lane; q < rowrec[r + 1].w; q += 32) hrow[q] = (unsigned short)r;
   __syncthreads();
   const unsigned bar_s = (unsigned)__cvta_generic_to_shared(bar);
   const unsigned rb_s = (unsigned)__cvta_generic_to_shared(Rb);
@@ -2462,17 +2443,44 @@ __global__ void __launch_bounds__(kPipeThreads) k_smooth_series_pipe(const P2* _
     }
     for (int r = tid; r < si.nregions; r += blockDim.x) rsl[r] = __ldg(si.region_slots + series * si.rs_stride + r);
     __syncthreads();
-    for (int l = warp; l < nlines; l += nw) {
-      const int l0 = ls[l], len = ls[l + 1] - l0, t0 = lt0[l];
-      for (int c = lane; c < len; c += 32) {
-        const int ns = rsl[(t0 + c / si.tile_cols) / si.tiles_per_region];
-        double vr = 0.0, vi = 0.0;
-        for (int t = 0; t < ns; t++) {
-          const P2 q = __ldcs(src + (int64_t)t * part_stride + l0 + c);
-          vr += (double)q.x;
-          vi += (double)q.y;
+    for (int base = 0; base < ncells; base += 4 * blockDim.x) {
+      double vr[4], vi[4];
+      int ns[4], mx = 1;
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const int c = base + tid + k * blockDim.x;
+        ns[k] = 0;
+        vr[k] = vi[k] = 0.0;
+        if (c < ncells) {
+          const P2 q = __ldcs(src + c);
+          ns[k] = __ldg(cell_region + c);  // region for now
+          vr[k] = (double)q.x;
+          vi[k] = (double)q.y;
         }
-        Rb[l0 + c] = P2{(T)vr, (T)vi};
+      }
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const int c = base + tid + k * blockDim.x;
+        ns[k] = c < ncells ? rsl[ns[k]] : 0;
+        mx = max(mx, ns[k]);
+      }
+      for (int t = 1; t < mx; t++) {
+        P2 q[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+          q[k] = P2{};
+          if (t < ns[k]) q[k] = __ldcs(src + (int64_t)t * part_stride + base + tid + k * blockDim.x);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+          vr[k] += (double)q[k].x;
+          vi[k] += (double)q[k].y;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const int c = base + tid + k * blockDim.x;
+        if (c < ncells) Rb[c] = P2{(T)vr[k], (T)vi[k]};
       }
     }
     return 0;
@@ -2493,97 +2501,187 @@ __global__ void __launch_bounds__(kPipeThreads) k_smooth_series_pipe(const P2* _
           : "memory");
       par ^= 1;
     }
+    const int next = series + gridDim.x;
+    // the next series' slot count is needed right after the vertical pass: load it now
+    const int next_slots = next < a.batch ? __ldg(series_slots + next) : 1;
     __syncthreads();  // slot-sum fills are visible; the previous series' reads of V are done
     const P2* R = Rb + shift;
-    // ---- vertical: item (row block b, column j) -> V(k1 + r, j), r < kPipeT
-    for (int it = tid; it < nvitems; it += blockDim.x) {
-      const int b = vrow[it], j = it - vb[b];
-      const int* rec = blk + b * L.ltab;
-      P2 x[NX];
+    // ---- vertical: each warp owns a host-balanced list of row blocks; per block the
+    // record (line starts, V offsets, widths) is loaded once, lanes run over the columns
+    for (int q = wbo[warp]; q < wbo[warp + 1]; q++) {
+      const int4* rec4 = reinterpret_cast<const int4*>(blk + (int)wbl[q] * L.ltab);
+      int rec[kRecInts];
 #pragma unroll
-      for (int u = 0; u < NX; u++) x[u] = R[rec[u] + j];
+      for (int e = 0; e < kRecInts; e += 4) {
+        const int4 t = rec4[e >> 2];
+        rec[e] = t.x;
+        rec[e + 1] = t.y;
+        rec[e + 2] = t.z;
+        rec[e + 3] = t.w;
+      }
+      const int width = rec[NXV + 2 * kPipeTV];
+      for (int j = lane; j < width; j += 32) {
+        P2 x[NXV], o[kPipeTV];
 #pragma unroll
-      for (int r = 0; r < kPipeT; r++) {
-        P2 acc = x[r];
+        for (int u = 0; u < NXV; u++) x[u] = R[rec[u] + j];
 #pragma unroll
-        for (int u = 1; u < W; u++) acc = add2(acc, x[r + u]);
-        if (j < rec[NX + kPipeT + r]) V[rec[NX + r] + j] = acc;
+        for (int g = 0; g < kPipeTV; g += kPipeT) strip_sums<P2, W>(x + g, o + g);
+#pragma unroll
+        for (int r = 0; r < kPipeTV; r++)
+          if (j < rec[NXV + kPipeTV + r]) V[vswz_cell(rec[NXV + r] + j)] = o[r];
       }
     }
     __syncthreads();  // V complete; R consumed
-    const int next = series + gridDim.x;
     const int cur_series = series;
     if (next < a.batch) {
-      one = __ldg(series_slots + next) == 1;
+      one = next_slots == 1;
       shift = fill(next, one);
     }
-    // ---- horizontal: item (row k1, output pair) -> B(k1, k2), B(k1, k2 + 1)
+    // ---- horizontal: item (row k1, kPipeT outputs from k2) -> B(k1, k2 + t)
     P2* out = (P2*)a.out + cur_series * a.out_series_stride;
-    for (int it = tid; it < nhitems; it += blockDim.x) {
-      const int k1 = hrow[it];
-      const int4 rr = rowrec[k1];  // {vo, ro, len, hb}
-      const int k2 = 2 * (it - rr.w);
-      const P2* vp = V + rr.x + k2;
-      P2 y[W + 1];
+    for (int it = tid; it < L.nhitems; it += blockDim.x) {
+      const int2 hd = hdesc[it];  // {first V cell (even), output offset | (valid outputs - 1) << 28}
+      const int u0 = hd.x >> 1;
+      const int nout = (hd.y >> 28) & 3;
+      P2 y[NX + 1], o[kPipeT];  // NX + 1: W odd -> whole 16-byte pairs
 #pragma unroll
-      for (int v = 0; v < W + 1; v += 2) lds_pair(vp + v, y[v], y[v + 1]);
-      P2 inner = y[1];
+      for (int v = 0; v < NX + 1; v += 2) lds_pair(V + 2 * vswz_unit(u0 + (v >> 1)), y[v], y[v + 1]);
+      strip_sums<P2, W>(y, o);
+      P2* op = out + (hd.y & 0x0fffffff);
 #pragma unroll
-      for (int v = 2; v < W; v++) inner = add2(inner, y[v]);
-      const P2 b0 = add2(inner, y[0]), b1 = add2(inner, y[W]);
-      P2* o = out + rr.y + k2;
-      __stcs(o, P2{b0.x * sc, b0.y * sc});
-      if (k2 + 1 < rr.z) __stcs(o + 1, P2{b1.x * sc, b1.y * sc});
+      for (int t = 0; t < kPipeT; t++)
+        if (t <= nout) __stcs(op + t, P2{o[t].x * sc, o[t].y * sc});
     }
   }
 }
 
-// V cells (rows padded to even), widest V row and the item counts
-PipeDims smooth_series_pipe_dims(const int64_t* row_off, int rows, int w) {
-  PipeDims d{};
-  for (int b = 0; b * kPipeT < rows; b++) {
-    int64_t mx = 0;
-    for (int r = b * kPipeT; r < std::min(rows, (b + 1) * kPipeT); r++) mx = std::max(mx, row_off[r + 1] - row_off[r] + w - 1);
-    d.nvitems += mx;
-    d.maxw = std::max(d.maxw, (int)mx);
+// Host side: the shared-memory layout and the image of the static tables.
+PipePlan smooth_series_pipe_plan(const int64_t* row_off, int rows, const int64_t* line_start, int64_t nlines,
+                                 int64_t ncells, int nregions, int w, int precision) {
+  PipePlan pp{};
+  PipeLayout& L = pp.L;
+  const size_t cs = precision == 32 ? 8 : 16;
+  const int T = kPipeT, TV = kPipeTV, NXV = TV + w - 1;
+  const int nblk = (rows + TV - 1) / TV;
+  if (nlines > 65535 || rows > 65535 || nblk > 65535 || ncells > INT32_MAX / 4 || (w & 1) == 0 ||
+      row_off[rows] >= (1 << 28)) {
+    L.total = ~(size_t)0;
+    return pp;
   }
+  auto up = [](size_t x, size_t a) { return (x + a - 1) / a * a; };
+  L.ltab = (int)up((size_t)NXV + 2 * TV + 1, 4);
+  // row records and item counts
+  std::vector<int32_t> rowrec(4 * (size_t)rows), blk((size_t)nblk * L.ltab, 0), bw(nblk);
+  int64_t v = 0, h = 0;
+  int maxw = 0;
   for (int r = 0; r < rows; r++) {
     const int64_t len = row_off[r + 1] - row_off[r];
-    d.nhitems += (len + 1) / 2;
-    d.vtot += (len + w - 1 + 1) & ~(int64_t)1;
+    rowrec[4 * r + 0] = (int32_t)v;
+    rowrec[4 * r + 1] = (int32_t)row_off[r];
+    rowrec[4 * r + 2] = (int32_t)len;
+    rowrec[4 * r + 3] = (int32_t)h;
+    v += (len + T - 1) / T * T + w - 1;  // a strip of the row's last item stays inside the row (even: W odd)
+    h += (len + T - 1) / T;
   }
-  return d;
-}
-
-size_t smooth_series_pipe_smem(int64_t ncells, int64_t nlines, int rows, int nregions, int w, const PipeDims& d,
-                               int precision) {
-  if (nlines > 65535 || rows > 65535 || ncells > INT32_MAX / 4 || d.nvitems > INT32_MAX / 4) return ~(size_t)0;
-  return pipe_layout(ncells, (int)nlines, rows, nregions, w, (int)d.nvitems, (int)d.nhitems, d.maxw, d.vtot,
-                     precision == 32 ? 8 : 16)
-      .total;
+  L.vtot = (int)v;
+  L.nhitems = (int)h;
+  int64_t it = 0;
+  for (int b = 0; b < nblk; b++) {
+    int mx = 0;
+    for (int r = b * TV; r < std::min(rows, (b + 1) * TV); r++) mx = std::max<int>(mx, rowrec[4 * r + 2] + w - 1);
+    it += mx;
+    bw[b] = mx;
+    maxw = std::max(maxw, mx);
+    int32_t* rec = blk.data() + (size_t)b * L.ltab;
+    for (int u = 0; u < NXV; u++) rec[u] = (int32_t)line_start[std::min<int64_t>(b * TV + u, nlines - 1)];
+    for (int r = 0; r < TV; r++) {
+      const int k1 = b * TV + r;
+      rec[NXV + r] = k1 < rows ? rowrec[4 * k1] : 0;
+      rec[NXV + TV + r] = k1 < rows ? rowrec[4 * k1 + 2] + w - 1 : 0;
+    }
+    rec[NXV + 2 * TV] = mx;
+  }
+  L.nvitems = (int)it;
+  // row blocks dealt to the CTA's warps, longest first to the least loaded warp
+  // (a block costs ceil(width / 32) column passes)
+  const int nwarps = kPipeThreads / 32;
+  std::vector<int> order(nblk), load(nwarps, 0);
+  for (int b = 0; b < nblk; b++) order[b] = b;
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return bw[x] > bw[y]; });
+  std::vector<std::vector<uint16_t>> lists(nwarps);
+  for (int b : order) {
+    int best = 0;
+    for (int q = 1; q < nwarps; q++)
+      if (load[q] < load[best]) best = q;
+    lists[best].push_back((uint16_t)b);
+    load[best] += (bw[b] + 31) / 32;
+  }
+  std::vector<int32_t> vb(nwarps + 1, 0);
+  std::vector<uint16_t> vrow;
+  for (int q = 0; q < nwarps; q++) {
+    vb[q] = (int32_t)vrow.size();
+    vrow.insert(vrow.end(), lists[q].begin(), lists[q].end());
+  }
+  vb[nwarps] = (int32_t)vrow.size();
+  // horizontal items: {first V cell, output offset | (valid outputs - 1) << 28}
+  std::vector<int32_t> hrow(2 * (size_t)h);
+  for (int r = 0; r < rows; r++) {
+    const int len = rowrec[4 * r + 2];
+    for (int k2 = 0, q = rowrec[4 * r + 3]; k2 < len; k2 += T, q++) {
+      hrow[2 * q] = rowrec[4 * r] + k2;
+      hrow[2 * q + 1] = (rowrec[4 * r + 1] + k2) | ((std::min(T, len - k2) - 1) << 28);
+    }
+  }
+  // layout
+  size_t o = 0;
+  L.R = o;
+  o = up(o + (size_t)(ncells + maxw + 4) * cs, 128);  // +maxw: strips past the last line read in-buffer garbage
+  L.V = o;
+  o = up(o + (size_t)(up(L.vtot, 32) + 32) * cs, 16);  // the swizzle permutes cells within aligned groups of 32
+  L.tabs = o;
+  o = up(o + blk.size() * 4, 16);
+  L.rowrec = o;  // (row records are folded into the horizontal descriptors)
+  L.vb = o;
+  o = up(o + vb.size() * 4, 16);
+  L.vrow = o;
+  o = up(o + vrow.size() * 2, 16);
+  L.hrow = o;
+  o = up(o + hrow.size() * 4, 16);
+  L.table_bytes = (int)(o - L.tabs);
+  L.rsl = o;
+  o = up(o + (size_t)nregions * 4, 16);
+  L.bar = o;
+  L.total = o + 16;
+  pp.tables.assign(L.table_bytes, 0);
+  auto put = [&](size_t off, const void* src, size_t n) { std::memcpy(pp.tables.data() + (off - L.tabs), src, n); };
+  put(L.tabs, blk.data(), blk.size() * 4);
+  put(L.vb, vb.data(), vb.size() * 4);
+  put(L.vrow, vrow.data(), vrow.size() * 2);
+  put(L.hrow, hrow.data(), hrow.size() * 4);
+  return pp;
 }
 
 template <typename P2, int W>
 static cudaError_t pipe_go(const P2* part, int64_t part_stride, int64_t pss, const SlotInfo& si, const BoxArgs& a,
-                           int64_t nlines, const PipeDims& d, const int* series_slots, size_t sm, cudaStream_t st) {
+                           const PipeLayout& L, const void* tables, const unsigned short* cell_region,
+                           const int* series_slots, cudaStream_t st) {
   auto kern = k_smooth_series_pipe<P2, W>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPipeThreads, sm);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPipeThreads, L.total);
   const int grid = std::max(1, std::min(a.batch, device_sms() * std::max(1, per_sm)));
-  return launch_pdl_kernel(kern, dim3(grid), dim3(kPipeThreads), sm, st, part, part_stride, pss, si, a, (int)nlines,
-                           (int)d.nvitems, (int)d.nhitems, d.maxw, (int)d.vtot, series_slots);
+  return launch_pdl_kernel(kern, dim3(grid), dim3(kPipeThreads), L.total, st, part, part_stride, pss, si, a, L,
+                           (const int4*)tables, cell_region, series_slots);
 }
 
 cudaError_t launch_smooth_series_pipe(const void* part, int nparts, int64_t part_stride, const SlotInfo& si,
-                                      int precision, const BoxArgs& a, int64_t nlines, const PipeDims& d,
-                                      const int* series_slots, cudaStream_t st) {
-  if (!si.line_tile0 || !si.region_slots || !series_slots) return cudaErrorInvalidValue;
-  const size_t sm = smooth_series_pipe_smem(a.s_series_stride, nlines, a.rows, si.nregions, a.m3, d, precision);
+                                      int precision, const BoxArgs& a, const PipeLayout& L, const void* tables,
+                                      const unsigned short* cell_region, const int* series_slots, cudaStream_t st) {
+  if (!si.region_slots || !series_slots || !tables || !cell_region) return cudaErrorInvalidValue;
   const int64_t pss = part_stride * nparts;
-#define HOS_PIPE_CASE(P, WW)                                                                       \
-  case WW:                                                                                         \
-    return pipe_go<P, WW>((const P*)part, part_stride, pss, si, a, nlines, d, series_slots, sm, st);
+#define HOS_PIPE_CASE(P, WW)                                                                                   \
+  case WW:                                                                                                     \
+    return pipe_go<P, WW>((const P*)part, part_stride, pss, si, a, L, tables, cell_region, series_slots, st);
   if (precision == 32) {
     switch (a.m3) { HOS_PIPE_CASE(float2, 3) HOS_PIPE_CASE(float2, 5) HOS_PIPE_CASE(float2, 7) HOS_PIPE_CASE(float2, 9) }
   } else {

@@ -255,16 +255,22 @@ cudaError_t launch_smooth_series_sep(const void* part, int nparts, int64_t part_
 // pipelined separable variant (default when its shared memory fits): the
 // series' raw cells land by one bulk copy while the previous series' outputs
 // are formed
-struct PipeDims {
-  int64_t nvitems = 0, nhitems = 0, vtot = 0;
-  int maxw = 0;
+struct PipeLayout {  // shared-memory layout (byte offsets) and item counts
+  size_t R, V, tabs, rowrec, vb, vrow, hrow, rsl, bar, total;
+  int table_bytes;  // [tabs, tabs + table_bytes): the host-built table image
+  int ltab;         // ints per vertical block record
+  int vtot, nvitems, nhitems;
 };
-PipeDims smooth_series_pipe_dims(const int64_t* row_off, int rows, int w);
-size_t smooth_series_pipe_smem(int64_t ncells, int64_t nlines, int rows, int nregions, int w, const PipeDims& d,
-                               int precision);
+struct PipePlan {
+  PipeLayout L;
+  std::vector<unsigned char> tables;
+};
+// L.total == ~0: the grid does not qualify
+PipePlan smooth_series_pipe_plan(const int64_t* row_off, int rows, const int64_t* line_start, int64_t nlines,
+                                 int64_t ncells, int nregions, int w, int precision);
 cudaError_t launch_smooth_series_pipe(const void* part, int nparts, int64_t part_stride, const SlotInfo& si,
-                                      int precision, const BoxArgs& a, int64_t nlines, const PipeDims& d,
-                                      const int* series_slots, cudaStream_t st);
+                                      int precision, const BoxArgs& a, const PipeLayout& L, const void* tables,
+                                      const unsigned short* cell_region, const int* series_slots, cudaStream_t st);
 // separable K4 for order-3 grids that do not fit one CTA (cfg2, cfg3): slot sums
 // into R (compute precision), then kTR x kTC output tiles of direct window sums
 bool box_tiles_supports(int w);
