@@ -435,11 +435,199 @@ static void front_go(const Tin* x, int64_t x_stride, int nseg, int krows, int ba
                                                                       L, Lp, E, ready);
 }
 
+// ---------------------------------------------------------------------------
+// K0+1 for m = 256, fp32 compute: REGISTER FFT.  The radix-4 Stockham kernel
+// above makes four shared-memory round trips per transform and is bound by
+// shared-memory bandwidth on cfg5 (160 K transforms: ~3600 8-byte accesses
+// each).  Here 256 = 16 x 16: with n = 16 n1 + n2 and k = k1 + 16 k2,
+//   Z[k1 + 16 k2] = sum_n2 W16^(n2 k2) [ W256^(n2 k1) sum_n1 z[16 n1 + n2] W16^(n1 k1) ]
+// so a thread (n2 = its lane in a 16-lane group) transforms its 16 strided
+// samples in registers (two radix-4 passes, constant twiddles), multiplies by
+// W256^(n2 k1) from a [k1][n2] table, the group transposes through a padded
+// 16 x 17 shared tile (ONE conflict-free round trip), and thread k1 transforms
+// the 16 values of its row: it then holds Z[k1 + 16 k2].  The partner bins
+// Z[256 - f] of the two-real-segment separation live in thread 16 - k1 at
+// register 15 - k2: 32 warp shuffles, no second exchange.  A warp runs two
+// transforms (four segments) at a time, samples of the next pair in flight.
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) { return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
+
+// forward 16-point DFT in registers, natural order in and out
+__device__ __forceinline__ void fft16(float2 (&a)[16]) {
+  constexpr float C1 = 0.92387953251128674f, S1 = 0.38268343236508977f, H = 0.70710678118654752f;
+  // W16^m = (cos(pi m / 8), -sin(pi m / 8)) for m = n0 k1
+  const float2 w16[10] = {{1.f, 0.f}, {C1, -S1}, {H, -H}, {S1, -C1}, {0.f, -1.f}, {-S1, -C1}, {-H, -H}, {-C1, -S1},
+                          {-1.f, 0.f}, {-C1, S1}};
+  float2 c[4][4];
+#pragma unroll
+  for (int n0 = 0; n0 < 4; n0++) {
+    const float2 a0 = a[n0], a1 = a[n0 + 4], a2 = a[n0 + 8], a3 = a[n0 + 12];
+    const float2 s02 = make_float2(a0.x + a2.x, a0.y + a2.y), d02 = make_float2(a0.x - a2.x, a0.y - a2.y);
+    const float2 s13 = make_float2(a1.x + a3.x, a1.y + a3.y);
+    const float2 m13 = make_float2(a1.y - a3.y, a3.x - a1.x);  // -i (a1 - a3)
+    c[n0][0] = make_float2(s02.x + s13.x, s02.y + s13.y);
+    c[n0][1] = make_float2(d02.x + m13.x, d02.y + m13.y);
+    c[n0][2] = make_float2(s02.x - s13.x, s02.y - s13.y);
+    c[n0][3] = make_float2(d02.x - m13.x, d02.y - m13.y);
+  }
+#pragma unroll
+  for (int n0 = 1; n0 < 4; n0++)
+#pragma unroll
+    for (int k1 = 1; k1 < 4; k1++) c[n0][k1] = cmul(c[n0][k1], w16[n0 * k1]);
+#pragma unroll
+  for (int k1 = 0; k1 < 4; k1++) {
+    const float2 a0 = c[0][k1], a1 = c[1][k1], a2 = c[2][k1], a3 = c[3][k1];
+    const float2 s02 = make_float2(a0.x + a2.x, a0.y + a2.y), d02 = make_float2(a0.x - a2.x, a0.y - a2.y);
+    const float2 s13 = make_float2(a1.x + a3.x, a1.y + a3.y);
+    const float2 m13 = make_float2(a1.y - a3.y, a3.x - a1.x);
+    a[k1] = make_float2(s02.x + s13.x, s02.y + s13.y);
+    a[k1 + 4] = make_float2(d02.x + m13.x, d02.y + m13.y);
+    a[k1 + 8] = make_float2(s02.x - s13.x, s02.y - s13.y);
+    a[k1 + 12] = make_float2(d02.x - m13.x, d02.y - m13.y);
+  }
+}
+
+constexpr int kR16Warps = 4;
+#ifndef HOS_R16_MINB
+#define HOS_R16_MINB 4
+#endif
+template <typename Tin, bool Q>
+__global__ void __launch_bounds__(32 * kR16Warps, HOS_R16_MINB)
+    k_front_r16(const Tin* __restrict__ x, int64_t x_stride, int nseg, int krows, int taper,
+                const double* __restrict__ tab, const float2* __restrict__ tw, int f_lo, int L, int Lp,
+                typename EElem<float, Q>::t* __restrict__ E, int* __restrict__ ready) {
+  StampEnd stamp_end_(kStampFront);
+  stamp_start(kStampFront);
+  constexpr int M = 256, R = 16;
+  __shared__ float2 S[kR16Warps][2][R][R + 1];  // the transpose tiles (row pitch 17: conflict-free both ways)
+  __shared__ float2 twt[R][R];                  // twt[k1][n2] = W256^(n2 k1)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, half = lane >> 4, t = lane & 15;
+  for (int i = threadIdx.x; i < R * R; i += blockDim.x) twt[i >> 4][i & 15] = tw[((i >> 4) * (i & 15)) & (M - 1)];
+  const float* tabf = reinterpret_cast<const float*>(tab + M);  // fp32 taper weights
+  float wv[R];
+#pragma unroll
+  for (int n1 = 0; n1 < R; n1++) wv[n1] = taper ? tabf[R * n1 + t] : 1.f;
+  __syncthreads();
+  const int b = blockIdx.y;
+  constexpr int PPC = 2 * kR16Warps;  // pairs per CTA pass
+  const int pstride = gridDim.x * PPC;
+  int pi = blockIdx.x * PPC + 2 * warp + half;  // this 16-lane group's pair
+  if (2 * (pi - half) >= nseg) return;          // whole warp
+  Tin xa[R], xb[R];
+  auto load = [&](int pair) {
+    const int s0 = 2 * pair;
+    if (s0 >= nseg) {
+#pragma unroll
+      for (int n1 = 0; n1 < R; n1++) xa[n1] = xb[n1] = Tin(0);
+      return;
+    }
+    const bool hb = s0 + 1 < nseg;
+    const Tin* src = x + (int64_t)b * x_stride + (int64_t)s0 * M + t;
+#pragma unroll
+    for (int n1 = 0; n1 < R; n1++) {
+      xa[n1] = src[R * n1];
+      xb[n1] = hb ? src[M + R * n1] : Tin(0);
+    }
+  };
+  load(pi);
+  float2(*tile)[R + 1] = S[warp][half];
+  using EL = EElem<float, Q>;
+  for (;;) {
+    const int sa = 2 * pi;
+    const bool valid = sa < nseg, has_b = sa + 1 < nseg;
+    float s_a = 0.f, s_b = 0.f;
+#pragma unroll
+    for (int n1 = 0; n1 < R; n1++) {
+      s_a += (float)xa[n1];
+      s_b += (float)xb[n1];
+    }
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {
+      s_a += __shfl_xor_sync(0xffffffffu, s_a, o);
+      s_b += __shfl_xor_sync(0xffffffffu, s_b, o);
+    }
+    const float mean_a = s_a / (float)M, mean_b = s_b / (float)M;
+    float2 z[R];
+#pragma unroll
+    for (int n1 = 0; n1 < R; n1++) z[n1] = make_float2(((float)xa[n1] - mean_a) * wv[n1], ((float)xb[n1] - mean_b) * wv[n1]);
+    const int pn = pi + pstride;
+    const bool more = 2 * (pn - half) < nseg;  // warp-uniform
+    if (more) load(pn);                        // in flight during the transform
+    fft16(z);                                  // over n1: z[k1]
+#pragma unroll
+    for (int k1 = 1; k1 < R; k1++) z[k1] = cmul(z[k1], twt[k1][t]);
+#pragma unroll
+    for (int k1 = 0; k1 < R; k1++) tile[k1][t] = z[k1];
+    __syncwarp();
+#pragma unroll
+    for (int n2 = 0; n2 < R; n2++) z[n2] = tile[t][n2];
+    __syncwarp();  // the tile is free for the next pair
+    fft16(z);      // over n2: z[k2] = Z[t + 16 k2]
+    if (threadIdx.x == 0 && !more) asm volatile("griddepcontrol.launch_dependents;");
+    // X_a(f) = (Z(f) + conj Z(-f)) / 2,  X_b(f) = (Z(f) - conj Z(-f)) / 2i;  Z(256 - f) for f = t + 16 k2 is
+    // register 15 - k2 of lane 16 - t (lane 0: its own register (16 - k2) mod 16)
+    typename EL::t* row = E + ((int64_t)b * krows + sa) * Lp;
+    const int src_lane = (half << 4) | ((R - t) & 15);
+#pragma unroll
+    for (int k2 = 0; k2 < R; k2++) {
+      float2 zn;
+      zn.x = __shfl_sync(0xffffffffu, z[R - 1 - k2].x, src_lane);
+      zn.y = __shfl_sync(0xffffffffu, z[R - 1 - k2].y, src_lane);
+      if (t == 0) zn = z[(R - k2) & 15];
+      const float2 zz = z[k2];
+      const int j = (t + R * k2 - f_lo) & (M - 1);
+      if (valid && j < L) {
+        row[j] = EL::make(make_float2(0.5f * (zz.x + zn.x), 0.5f * (zz.y - zn.y)));
+        if (has_b) row[Lp + j] = EL::make(make_float2(0.5f * (zz.y + zn.y), 0.5f * (zn.x - zz.x)));
+      }
+    }
+    if (ready) {  // publish the pair's rows to a concurrently running K2
+      __syncwarp();
+      if (t == 0 && valid) {
+        __threadfence();
+        int* f = ready + (int64_t)b * krows + sa;
+        asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(f), "r"(1) : "memory");
+        if (has_b) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(f + 1), "r"(1) : "memory");
+      }
+    }
+    if (!more) break;
+    pi = pn;
+  }
+}
+
+template <typename Tin, bool Q>
+static void front_r16_go(const Tin* x, int64_t x_stride, int nseg, int krows, int batch, int taper, const double* tab,
+                         const float2* tw, int f_lo, int L, int Lp, typename EElem<float, Q>::t* E, int* ready,
+                         cudaStream_t st) {
+  auto kern = k_front_r16<Tin, Q>;
+  constexpr int PPC = 2 * kR16Warps;
+  const int pairs = (nseg + 1) / 2;
+  int grid = (pairs + PPC - 1) / PPC;
+  grid = std::min(grid, std::max(1, device_sms() * 2 * HOS_R16_MINB / std::max(1, batch)));
+  if (ready) {
+    launch_pdl_kernel(kern, dim3(grid, batch), dim3(32 * kR16Warps), 0, st, x, x_stride, nseg, krows, taper, tab, tw,
+                      f_lo, L, Lp, E, ready);
+    return;
+  }
+  kern<<<dim3(grid, batch), 32 * kR16Warps, 0, st>>>(x, x_stride, nseg, krows, taper, tab, tw, f_lo, L, Lp, E, ready);
+}
+
 template <typename Tin, typename T, bool Q>
 static cudaError_t front_dispatch(int log2m, const Tin* x, int64_t x_stride, int nseg, int krows, int batch,
                                   int taper, const double* tab, const typename C2<T>::t* tw, int f_lo, int L, int Lp,
                                   void* E, int* ready, cudaStream_t st) {
   using ET = typename EElem<T, Q>::t;
+  if constexpr (sizeof(T) == 4) {
+    static const bool r16 = [] {
+      const char* e = std::getenv("HOS_FRONT_R16");  // "0": the shared-memory Stockham kernel for m = 256 too
+      return !(e && e[0] == '0');
+    }();
+    // many transforms only: a warp runs two pairs at a time, so a small grid (cfg4: 512 pairs -> 64 CTAs)
+    // leaves SMs idle (cfg4 front 2.6 us with the Stockham kernel, 3.8 us here)
+    if (log2m == 8 && L <= 256 && r16 && (int64_t)((nseg + 1) / 2) * batch >= 16 * device_sms()) {
+      front_r16_go<Tin, Q>(x, x_stride, nseg, krows, batch, taper, tab, tw, f_lo, L, Lp, (ET*)E, ready, st);
+      return cudaGetLastError();
+    }
+  }
 #define HOS_FRONT_CASE(LG) \
   case LG:                                                                                                   \
     front_go<LG, Tin, T, Q>(x, x_stride, nseg, krows, batch, taper, tab, tw, f_lo, L, Lp, (ET*)E, ready, st); \
