@@ -486,7 +486,10 @@ __device__ __forceinline__ void fft16(float2 (&a)[16]) {
   }
 }
 
-constexpr int kR16Warps = 4;
+#ifndef HOS_R16_WARPS
+#define HOS_R16_WARPS 4
+#endif
+constexpr int kR16Warps = HOS_R16_WARPS;
 #ifndef HOS_R16_MINB
 #define HOS_R16_MINB 4
 #endif
@@ -2499,7 +2502,7 @@ cudaError_t launch_smooth_series_sep(const void* part, int nparts, int64_t part_
 //     thread lands them in shared memory with ONE cp.async.bulk (mbarrier
 //     transaction count), issued as soon as the previous series' vertical
 //     pass has consumed the buffer -- the copy of series s+1 runs under the
-//     horizontal pass and the output stores of series s; two 512-thread CTAs
+//     horizontal pass and the output stores of series s; two 256-thread CTAs
 //     per SM keep ~2 x 42 KB of reads in flight per SM (cfg5);
 //   * every static table (per-block line starts, row records, item -> block /
 //     row maps) is built once per plan on the host and copied to shared
@@ -2517,7 +2520,7 @@ cudaError_t launch_smooth_series_sep(const void* part, int nparts, int64_t part_
 constexpr int kPipeT = 4;   // window sums formed together from one strip (horizontal item: kPipeT outputs)
 constexpr int kPipeTV = 4;  // rows per vertical block (kPipeTV / kPipeT overlapping strips per column)
 #ifndef HOS_PIPE_THREADS
-#define HOS_PIPE_THREADS 512
+#define HOS_PIPE_THREADS 256
 #endif
 constexpr int kPipeThreads = HOS_PIPE_THREADS;
 
