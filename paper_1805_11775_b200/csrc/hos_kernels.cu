@@ -1511,8 +1511,20 @@ __global__ void __launch_bounds__(32 * (Q ? kCtaWarpsQ : kCtaWarps), 1)
     v.slot_base = r.w;
     return v;
   };
+  int cur_group = -1;            // group of the current block (its tile / line records are loaded)
   auto enter = [&](const CtaBlock& blk, int k_first) {
     blk_k0 = k_first;  // the block's first stage (phases deal its stages round-robin)
+    blk_row0 = blk.row0;
+    if (blk.group == cur_group) {
+      // same group as the previous block (batches: the next series): the
+      // warp's region, tile and line records are unchanged -- only the slot
+      // moves.  Skips three dependent table loads per block (cfg5: 28 blocks
+      // per CTA; K2 866 -> 861 us).
+      P = (C*)a.part + ((int64_t)blk.series * a.maxslots + blk.slot_base + phase) * a.ncells;
+      acc.zero();
+      return;
+    }
+    cur_group = blk.group;
     const CtaGroup grp = groups_s[blk.group];
     // warps per region: `halves` (2: each warp computes one tile of the
     // pair, the other half of its lanes idle) x `phases`
@@ -1523,7 +1535,6 @@ __global__ void __launch_bounds__(32 * (Q ? kCtaWarpsQ : kCtaWarps), 1)
     const int sub = role ? warp / grp.n : 0;
     phase = sub / grp.halves;
     const bool my_tile = grp.halves == 1 || (sub % grp.halves) == (h & 1);
-    blk_row0 = blk.row0;
     P = (C*)a.part + ((int64_t)blk.series * a.maxslots + blk.slot_base + phase) * a.ncells;
     const Tile t = tiles_s[(int64_t)region * L::NT + h];
     c0 = t.col0 + cb;
@@ -2517,6 +2528,10 @@ cudaError_t launch_smooth_series_sep(const void* part, int nparts, int64_t part_
 // Series K2 cut between CTAs (several partial slots): all threads sum the
 // slots in slot order in fp64, four cells per thread with every load of a
 // round in flight together.
+// Measured and rejected (same box, cfg5): two row bands with V holding one
+// band and the space saved double-buffering R, the next series landing under
+// the whole current one (89.6 vs 81.8 us: the copy was not what the passes
+// waited for); 8-row vertical blocks (94 us: too few items per pass).
 constexpr int kPipeT = 4;   // window sums formed together from one strip (horizontal item: kPipeT outputs)
 constexpr int kPipeTV = 4;  // rows per vertical block (kPipeTV / kPipeT overlapping strips per column)
 #ifndef HOS_PIPE_THREADS
