@@ -548,7 +548,8 @@ def run_ours(args):
             roof_s = {"bound": "hbm", "achieved": round(nbytes / (smooth_ms * 1e-3) / 1e9, 1), "peak": hbm[0],
                       "unit": "GB/s", "frac": round(nbytes / (smooth_ms * 1e-3) / 1e9 / hbm[0], 4),
                       "algorithmic_bytes": nbytes, "kernel_ms": round(smooth_ms, 5),
-                      "kernels": "k_smooth_series3" if in_step.get("series_smooth") else "k_line_scan + k_box",
+                      "kernels": ("k_smooth_series_pipe" if in_step.get("series_smooth") else
+                                  "k_raw_cells + k_box_tiles" if c.order == 3 else "k_line_scan + k_box4"),
                       "peak_source": hbm[1],
                       "note": "(|D_h| + |P|) x complex bytes x series / in-step smoothing span; the grid of a "
                               "single cfg2-4 series is L2-resident, so the HBM gate is cfg5"}
@@ -575,10 +576,10 @@ def run_ours(args):
             "roofline_smoothing": roof_s,
             "clocks": clocks,
             "gpu_launches": lib.hos_plan_launches(plan.handle) * args.steps if (world == 1 or by_series) else None,
-            "gpu_launches_note": "per step: front end (k_front: fused demean+Hann+FFT+extension; or k_prep + "
+            "gpu_launches_note": "per step: front end (k_front / k_front_r16: fused demean+Hann+FFT+extension; or k_prep + "
                                  "cuFFT + k_extend_half for non-power-of-two M, cuFFT not counted), k_triple_cta (k_triple_w for large M), "
-                                 "smoothing (k_line_scan + k_box3/k_box4, or k_smooth_series3 for grids that fit in "
-                                 "shared memory)",
+                                 "smoothing (order 3: k_raw_cells + k_box_tiles, or k_smooth_series_pipe for batched "
+                                 "grids that fit in shared memory; order 4: k_line_scan + k_box4)",
         }
         if not args.no_cpu_baseline and world == 1:
             cb = cpu_reference(args.config, steps=1, warmup=1, budget_s=60.0)
