@@ -132,10 +132,11 @@ int hos_dft_rows(const void* x_dev, int x_dtype, int rows, int m, int precision,
 
 /* End to end with HOST buffers, synchronous.  Page-locked buffers: the
  * values are written in place over PCIe by the smoothing kernel, and the
- * series is read in place by the front end (zero-copy) or, for single-series
- * plans whose k splits into 2 chunks (HOS_CHUNKS), copied chunk by chunk by
- * the copy engine while the previous chunk's front end and triple product
- * run; replayed as one CUDA graph per buffer binding -- the buffers must stay
+ * series is read in place by the front end (zero-copy; the default) or, with
+ * HOS_CHUNKS=n set at plan creation (single-series plans whose k splits into
+ * n chunks), copied chunk by chunk by the copy engine while the previous
+ * chunk's front end and triple product run; replayed as one CUDA graph per
+ * buffer binding -- the buffers must stay
  * allocated and page-locked while the plan may reuse the binding.  Pageable
  * buffers are staged with copies.  stream NULL = the plan's private stream. */
 int hos_estimate_host(hos_plan* plan, const void* x_host, int x_dtype, int64_t x_stride,
