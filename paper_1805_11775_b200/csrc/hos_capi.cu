@@ -452,6 +452,11 @@ hos::CtaTripleArgs cta_args(const hos_plan* p, bool streaming) {
   a.quad = p->quad ? 1 : 0;
   a.refill_last = p->m >= 512 ? 1 : 0;  // long stages (cfg2); short ones (cfg4, cfg5) wait on empty[]
   if (const char* env = std::getenv("HOS_K2_REFILL")) a.refill_last = env[0] == 'l';  // "last" | "empty"
+  // warp-pair skew (see k_triple_cta): same-box A/B, K2 in-step -- cfg2 32.6 -> 31.7 us at 3000 cycles
+  // (1000: 32.8, 5000: 32.9), cfg5 865 -> 846 us (1000-5000 alike); order 4 (cfg4) loses 3 %, so off there.
+  // The gain is small because a warp alone on its sub-partition only reaches ~47 % of the pipe.
+  a.skew_cycles = p->order == 3 && !p->quad ? 3000 : 0;
+  if (const char* env = std::getenv("HOS_K2_SKEW")) a.skew_cycles = std::max(0, std::atoi(env));
 
   a.tab_stages = p->cta_tab_stages;
   a.tab_blocks = p->cta_tab_blocks;

@@ -1634,6 +1634,16 @@ __global__ void __launch_bounds__(32 * (Q ? kCtaWarpsQ : kCtaWarps), 1)
     }
     if (k == 0) {
       stamp(1);
+      // Skew: warps w and w + 4 share an SM sub-partition and would walk the
+      // stages in lockstep, so both sit in the stage hand-off (release,
+      // refill bookkeeping, next wait: ~0.3-0.4 us of a ~3 us stage on cfg2)
+      // at the same time and the FMA pipe idles.  Starting the second warp of
+      // each pair about half a stage later keeps one of them computing while
+      // the other hands off; nothing re-synchronises them afterwards.
+      if (a.skew_cycles > 0 && (warp & 4)) {
+        const long long t0 = clock64();
+        while (clock64() - t0 < a.skew_cycles) __nanosleep(100);
+      }
       if (threadIdx.x == 0) {
 #pragma unroll
         for (int d2 = 1; d2 < kCtaMaxDepth; d2++)
@@ -1682,7 +1692,7 @@ __global__ void __launch_bounds__(32 * (Q ? kCtaWarpsQ : kCtaWarps), 1)
     } else if (lane == 0) {
       const unsigned eb = (unsigned)__cvta_generic_to_shared(&empty[d]);
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(eb) : "memory");
-      if (warp == 0 && k + depth < nst) {
+      if (warp == (a.skew_cycles > 0 ? 4 : 0) && k + depth < nst) {  // skewed: warps 4.. finish a stage last
         asm volatile(
             "{\n.reg .pred P1;\nE_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n@!P1 bra E_%=;\n}\n" ::"r"(
                 eb),

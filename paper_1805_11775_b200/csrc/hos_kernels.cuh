@@ -169,6 +169,7 @@ struct CtaTripleArgs {
   int trace_cta;              // diagnostics: CTA whose per-stage times are traced
   int quad;                   // fp32: E rows hold quads {re, im, im, im} (cells_q, 16 warps)
   int refill_last;            // 1: the warp completing a stage's count refills it; 0: warp 0 waits on empty[]
+  int skew_cycles;            // > 0: the second warp of every SM sub-partition starts its first stage this much later
   const int4* cta_head;       // per CTA {first stage, stages, first block, blocks} (one load)
   int tab_stages;             // stage-table entries reserved in shared memory (>= stages of any CTA)
   int tab_blocks;             // block-table entries reserved in shared memory (>= blocks of any CTA)

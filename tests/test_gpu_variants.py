@@ -54,7 +54,7 @@ print("VARIANT-OK")
 
 
 @pytest.mark.parametrize("env", ["HOS_K2=warp", "HOS_K2_TILE=2", "HOS_STREAM=1", "HOS_CTA_DEPTH=4", "HOS_K2_QUAD=1",
-                                 "HOS_K2_REFILL=empty", "HOS_K2_REFILL=last", "HOS_K4_TILES=0", "HOS_K4_SEP=0", "HOS_K4_PIPE=0", "HOS_FRONT_R16=0",
+                                 "HOS_K2_REFILL=empty", "HOS_K2_REFILL=last", "HOS_K2_SKEW=0", "HOS_K4_TILES=0", "HOS_K4_SEP=0", "HOS_K4_PIPE=0", "HOS_FRONT_R16=0",
                                  "HOS_CHUNKS=2", "HOS_CHUNKS=8"])
 def test_variant_parity(cuda, env):
     k, v = env.split("=")
