@@ -494,6 +494,26 @@ def test_small_batches_vs_oracle(cuda, prec, batch, m, k, w):
         assert O.north_star_error(np.asarray(vals[s]), ref) <= TOL[prec], s
 
 
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("k,w,taper", [(5, 5, "hann"), (4, 9, None)])
+def test_register_fft_front_end_vs_oracle(cuda, dtype, k, w, taper):
+    """Large batches of m = 256 series in fp32 mode take the register-FFT front
+    end (k_front_r16: >= 16 segment pairs per SM) and the pipelined smoother;
+    odd k leaves the last pair with one segment; both input dtypes."""
+    import torch
+
+    P = api()
+    batch, m = 1300, 256
+    rng = np.random.default_rng(k * 100 + w)
+    x = rng.standard_normal((batch, m * k)).astype(dtype)
+    cfg = P.EstimationConfig(3, P.SegmentConfig(m=m, k=k), w, precision="fp32", taper=taper)
+    vals = P.estimate_batch(torch.from_numpy(x).to(cuda), cfg)
+    assert vals.shape == (batch, P.principal_domain(3, m).shape[0])
+    for s in (0, 1, 147, 148, batch // 2, batch - 1):
+        dom, ref = O.estimate(x[s].astype(np.float64), 3, m, k, w, True, taper)
+        assert O.north_star_error(np.asarray(vals[s]), ref) <= TOL["fp32"], s
+
+
 def test_acceptance_criterion1_compare_grids(cuda):
     """The reference's acceptance criterion 1 (tests/test_acceptance.py:76-103)
     on the GPU path: for QPC series, every plan's fp64 grid is within

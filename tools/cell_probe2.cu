@@ -140,5 +140,8 @@ int main() {
   run<1, 16, 1, 4>("B one acc, 16 warps, unroll 4", E, out, Lp, peak);
   run<1, 12, 1, 2>("B one acc, 12 warps, unroll 2", E, out, Lp, peak);
   run<1, 8, 2, 2>("B one acc, 8 warps x 2 CTAs, unroll 2", E, out, Lp, peak);
+  run<0, 12, 1, 1>("A two acc, 12 warps (168 regs), unroll 1", E, out, Lp, peak);
+  run<0, 12, 1, 2>("A two acc, 12 warps (168 regs), unroll 2", E, out, Lp, peak);
+  run<0, 4, 1, 4>("A two acc, 4 warps (one per sub-partition)", E, out, Lp, peak);
   return 0;
 }
