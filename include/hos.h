@@ -98,6 +98,10 @@ int64_t hos_plan_units(const hos_plan* plan);
 /* Triple-product work per series actually issued by the kernel (cells incl.
  * tile padding) times K; units/issued is the tiling efficiency. */
 int64_t hos_plan_issued(const hos_plan* plan);
+/* Elements per row of the staged segment spectra E (the frequency window
+ * [f_lo, f_hi] the triple product reads): the front end writes K rows of
+ * this many complex values per series. */
+int64_t hos_plan_row_len(const hos_plan* plan);
 /* Device bytes the plan holds. */
 size_t hos_plan_device_bytes(const hos_plan* plan);
 /* Number of this library's kernels one hos_estimate launches: 4 with the fused

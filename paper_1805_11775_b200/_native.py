@@ -41,6 +41,7 @@ EXPORTED_SYMBOLS = {
     "hos_plan_cells": (_i64, [_p]),
     "hos_plan_units": (_i64, [_p]),
     "hos_plan_issued": (_i64, [_p]),
+    "hos_plan_row_len": (_i64, [_p]),
     "hos_plan_device_bytes": (ctypes.c_size_t, [_p]),
     "hos_plan_launches": (_i, [_p]),
     "hos_estimate": (_i, [_p, _p, _i, _i64, _p, _p]),
@@ -154,6 +155,7 @@ class Plan:
         self.cells = int(L.hos_plan_cells(handle))
         self.units = int(L.hos_plan_units(handle))
         self.issued = int(L.hos_plan_issued(handle))
+        self.row_len = int(L.hos_plan_row_len(handle))
         self.lines = int(L.hos_plan_lines(handle))
         self.complex_dtype = torch.complex64 if self.precision == 32 else torch.complex128
 

@@ -1433,6 +1433,7 @@ int64_t hos_plan_npoints(const hos_plan* p) { return p ? p->geo.npoints : -1; }
 int64_t hos_plan_cells(const hos_plan* p) { return p ? p->geo.ncells : -1; }
 int64_t hos_plan_units(const hos_plan* p) { return p ? p->geo.ncells * (int64_t)p->k : -1; }
 int64_t hos_plan_issued(const hos_plan* p) { return p ? p->geo.issued_cells * (int64_t)p->k : -1; }
+int64_t hos_plan_row_len(const hos_plan* p) { return p ? p->L : -1; }
 size_t hos_plan_device_bytes(const hos_plan* p) { return p ? p->bytes : 0; }
 int hos_plan_launches(const hos_plan* p) {
   // kernels of this library per hos_estimate: [fused front | K0, K1 around

@@ -2,7 +2,7 @@
 CFGS=$1; shift
 for c in $CFGS; do
   for e in "$@"; do
-    env $e timeout 300 python bench.py --config $c --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/abe.log 2>&1
+    env $e timeout 300 python bench.py --config $c --steps 20 --warmup 3 --no-cpu-baseline --no-secondary > gpurun_out/abe.log 2>&1
     tail -1 gpurun_out/abe.log | python -c "
 import json,sys
 try:

@@ -1,4 +1,4 @@
-B="python bench.py --config cfg2 --steps 3 --warmup 3 --no-cpu-baseline"
+B="python bench.py --config cfg2 --steps 3 --warmup 3 --no-cpu-baseline --no-secondary"
 $B > gpurun_out/k4n_plain.log 2>&1 || exit 1
 for k in k_raw_cells k_box_tiles; do
 ncu --set full --clock-control none --cache-control none --import-source on -k regex:$k -s 3 -c 1 -o gpurun_out/k4n_$k $B > gpurun_out/k4n_ncu_$k.log 2>&1
