@@ -2543,6 +2543,10 @@ cudaError_t launch_smooth_series_sep(const void* part, int nparts, int64_t part_
 // the whole current one (89.6 vs 81.8 us: the copy was not what the passes
 // waited for); 8-row vertical blocks (94 us: too few items per pass).
 constexpr int kPipeT = 4;   // window sums formed together from one strip (horizontal item: kPipeT outputs)
+#ifndef HOS_PIPE_HALIGN
+#define HOS_PIPE_HALIGN 1  // 4 and 8 (row-aligned 16-byte load phases) measured even: fewer conflicts, more idle lanes
+#endif
+constexpr int kPipeHAlign = HOS_PIPE_HALIGN;  // horizontal items of a row start on this many items
 constexpr int kPipeTV = 4;  // rows per vertical block (kPipeTV / kPipeT overlapping strips per column)
 #ifndef HOS_PIPE_THREADS
 #define HOS_PIPE_THREADS 256
@@ -2756,7 +2760,8 @@ __global__ void __launch_bounds__(kPipeThreads, sizeof(P2) == 8 ? 2 : 1) k_smoot
     // ---- horizontal: item (row k1, kPipeT outputs from k2) -> B(k1, k2 + t)
     P2* out = (P2*)a.out + cur_series * a.out_series_stride;
     for (int it = tid; it < L.nhitems; it += blockDim.x) {
-      const int2 hd = hdesc[it];  // {first V cell (even), output offset | (valid outputs - 1) << 28}
+      const int2 hd = hdesc[it];  // {first V cell (even), output offset | (valid outputs - 1) << 28}; x < 0: padding
+      if (hd.x < 0) continue;
       const int u0 = hd.x >> 1;
       const int nout = (hd.y >> 28) & 3;
       P2 y[NX + 1], o[kPipeT];  // NX + 1: W odd -> whole 16-byte pairs
@@ -2790,6 +2795,9 @@ PipePlan smooth_series_pipe_plan(const int64_t* row_off, int rows, const int64_t
   std::vector<int32_t> rowrec(4 * (size_t)rows), blk((size_t)nblk * L.ltab, 0), bw(nblk);
   int64_t v = 0, h = 0;
   int maxw = 0;
+  // a row's horizontal items start on a multiple of kPipeHAlign items: the 8
+  // lanes of a 16-byte shared load phase then read one row, where the V
+  // swizzle makes them conflict-free (padding items are skipped)
   for (int r = 0; r < rows; r++) {
     const int64_t len = row_off[r + 1] - row_off[r];
     rowrec[4 * r + 0] = (int32_t)v;
@@ -2797,7 +2805,7 @@ PipePlan smooth_series_pipe_plan(const int64_t* row_off, int rows, const int64_t
     rowrec[4 * r + 2] = (int32_t)len;
     rowrec[4 * r + 3] = (int32_t)h;
     v += (len + T - 1) / T * T + w - 1;  // a strip of the row's last item stays inside the row (even: W odd)
-    h += (len + T - 1) / T;
+    h += ((len + T - 1) / T + kPipeHAlign - 1) / kPipeHAlign * kPipeHAlign;
   }
   L.vtot = (int)v;
   L.nhitems = (int)h;
@@ -2840,7 +2848,7 @@ PipePlan smooth_series_pipe_plan(const int64_t* row_off, int rows, const int64_t
   }
   vb[nwarps] = (int32_t)vrow.size();
   // horizontal items: {first V cell, output offset | (valid outputs - 1) << 28}
-  std::vector<int32_t> hrow(2 * (size_t)h);
+  std::vector<int32_t> hrow(2 * (size_t)h, -1);
   for (int r = 0; r < rows; r++) {
     const int len = rowrec[4 * r + 2];
     for (int k2 = 0, q = rowrec[4 * r + 3]; k2 < len; k2 += T, q++) {
