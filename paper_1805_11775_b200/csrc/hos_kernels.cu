@@ -2538,10 +2538,18 @@ cudaError_t launch_smooth_series_sep(const void* part, int nparts, int64_t part_
 // Series K2 cut between CTAs (several partial slots): all threads sum the
 // slots in slot order in fp64, four cells per thread with every load of a
 // round in flight together.
-// Measured and rejected (same box, cfg5): two row bands with V holding one
-// band and the space saved double-buffering R, the next series landing under
-// the whole current one (89.6 vs 81.8 us: the copy was not what the passes
-// waited for); 8-row vertical blocks (94 us: too few items per pass).
+// Anatomy on cfg5 (82 us; diagnostic builds, same box): fills and barriers
+// alone 41 us (one 42 KB copy in flight per CTA = 4.3 TB/s of reads; chunked
+// copies of 4 / 16 KB change nothing), + both passes without the output
+// stores 68 us.  Measured and rejected: two row bands with V holding one band,
+// the space saved double-buffering R so the next series lands under the
+// whole current one, descriptors read through L1 (108 us; the same code with
+// one band and one buffer 92 us); 8-row vertical blocks (94 us: too few items
+// per pass); row-aligned horizontal items (even).  In the step the kernel
+// also competes with the write-back of K2's partial slots still dirty in L2
+// (175 MB written just before it, 126 MB of L2), so the DRAM side sees more
+// than the algorithmic bytes; not writing the slots at all (smoothing inside
+// K2 for series one CTA block covers) is the remaining lever.
 constexpr int kPipeT = 4;   // window sums formed together from one strip (horizontal item: kPipeT outputs)
 #ifndef HOS_PIPE_HALIGN
 #define HOS_PIPE_HALIGN 1  // 4 and 8 (row-aligned 16-byte load phases) measured even: fewer conflicts, more idle lanes
