@@ -583,15 +583,6 @@ __global__ void __launch_bounds__(32 * kR16Warps, HOS_R16_MINB)
         if (has_b) row[Lp + j] = EL::make(make_float2(0.5f * (zz.y + zn.y), 0.5f * (zn.x - zz.x)));
       }
     }
-    if (ready) {  // publish the pair's rows to a concurrently running K2
-      __syncwarp();
-      if (t == 0 && valid) {
-        __threadfence();
-        int* f = ready + (int64_t)b * krows + sa;
-        asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(f), "r"(1) : "memory");
-        if (has_b) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(f + 1), "r"(1) : "memory");
-      }
-    }
     if (!more) break;
     pi = pn;
   }
@@ -626,7 +617,8 @@ static cudaError_t front_dispatch(int log2m, const Tin* x, int64_t x_stride, int
     }();
     // many transforms only: a warp runs two pairs at a time, so a small grid (cfg4: 512 pairs -> 64 CTAs)
     // leaves SMs idle (cfg4 front 2.6 us with the Stockham kernel, 3.8 us here)
-    if (log2m == 8 && L <= 256 && r16 && (int64_t)((nseg + 1) / 2) * batch >= 16 * device_sms()) {
+    // (not for the streaming host path: its ready-flag publication is only exercised with k_front)
+    if (log2m == 8 && L <= 256 && r16 && !ready && (int64_t)((nseg + 1) / 2) * batch >= 16 * device_sms()) {
       front_r16_go<Tin, Q>(x, x_stride, nseg, krows, batch, taper, tab, tw, f_lo, L, Lp, (ET*)E, ready, st);
       return cudaGetLastError();
     }
