@@ -20,6 +20,7 @@ Fixtures:
                     output rows (k1) through the reference's own
                     _compute_values (hospectra/spectra.py:391) on the tapered
                     spectra; cfg5: full grids of selected series
+  cfg2_full.npz     BASELINE cfg2: the WHOLE grid (65,792 points) from the same seam
   qpc1024.npz       the acceptance QPC case (generate_qpc(.1,.15,1024,0,seed 7),
                     m3=5): peak bin and values of selected rows
 """
@@ -140,6 +141,21 @@ def make_rows(name):
     print(name, "rows", len(pos), f"{time.time() - t0:.1f}s")
 
 
+def make_full(name="cfg2"):
+    """The WHOLE principal-domain grid of a BASELINE config from the reference's
+    operator seam (single process, a few seconds for cfg2): cfg2_full.npz."""
+    c = signals.baseline_config(name)
+    t0 = time.time()
+    x = signals.baseline_series(c).astype(np.float64)
+    xs = sha(signals.baseline_series(c))
+    spec = tapered_spectra(x, c.m, c.k)
+    cfg = H.EstimationConfig(c.order, H.SegmentConfig(m=c.m, k=c.k), c.m3)
+    dom = H.principal_domain(c.order, c.m)
+    vals = _compute_values(H.SegmentSpectrumSet(spectra=spec), cfg, dom)
+    np.savez_compressed(os.path.join(HERE, f"{name}_full.npz"), x_sha=xs, npoints=np.array(len(dom)), val=vals)
+    print(name, "full grid", len(dom), f"{time.time() - t0:.1f}s")
+
+
 def make_cfg5(series=(0, 1, 4095)):
     c = signals.baseline_config("cfg5")
     t0 = time.time()
@@ -167,12 +183,14 @@ def make_qpc():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["small", "cfg1", "qpc", "cfg2", "cfg4", "cfg5", "cfg3"]
+    which = sys.argv[1:] or ["small", "cfg1", "qpc", "cfg2", "cfg2full", "cfg4", "cfg5", "cfg3"]
     for w in which:
         if w == "small":
             make_small()
         elif w == "cfg1":
             make_cfg1()
+        elif w == "cfg2full":
+            make_full("cfg2")
         elif w == "qpc":
             make_qpc()
         elif w == "cfg5":

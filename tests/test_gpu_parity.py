@@ -83,6 +83,14 @@ def test_cfg2_full_grid_vs_oracle(cuda, prec):
     ref = O.parallel_efficient(spec, 3, c.m3, True, workers=8)
     err = north_star(g.values, ref)
     assert err <= TOL[prec], f"cfg2 {prec}: {err:.3e}"
+    # ... and the reference's own whole grid (hospectra._compute_values on all 65,792 points)
+    full = golden("cfg2_full.npz")
+    assert len(g.values) == int(full["npoints"])
+    err = north_star(g.values, full["val"])
+    assert err <= TOL[prec], f"cfg2 {prec} vs reference full grid: {err:.3e}"
+    if prec == "fp64":  # the reference's per-point bar (1e-9 relative, 1e-12 x max floor)
+        d = np.abs(g.values - full["val"])
+        assert np.all(d <= 1e-9 * np.abs(full["val"]) + 1e-12 * np.abs(full["val"]).max())
 
 
 @pytest.mark.parametrize("name,prec", [("cfg3", "fp32"), ("cfg3", "fp64"), ("cfg4", "fp32"), ("cfg4", "fp64")])
