@@ -20,7 +20,8 @@ Fixtures:
                     output rows (k1) through the reference's own
                     _compute_values (hospectra/spectra.py:391) on the tapered
                     spectra; cfg5: full grids of selected series
-  cfg2_full.npz     BASELINE cfg2: the WHOLE grid (65,792 points) from the same seam
+  cfg2_full.npz,    BASELINE cfg2 / cfg4: the WHOLE grid (65,792 / 61,721 points) from the same seam
+  cfg4_full.npz
   qpc1024.npz       the acceptance QPC case (generate_qpc(.1,.15,1024,0,seed 7),
                     m3=5): peak bin and values of selected rows
 """
@@ -183,7 +184,7 @@ def make_qpc():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["small", "cfg1", "qpc", "cfg2", "cfg2full", "cfg4", "cfg5", "cfg3"]
+    which = sys.argv[1:] or ["small", "cfg1", "qpc", "cfg2", "cfg2full", "cfg4", "cfg4full", "cfg5", "cfg3"]
     for w in which:
         if w == "small":
             make_small()
@@ -191,6 +192,8 @@ if __name__ == "__main__":
             make_cfg1()
         elif w == "cfg2full":
             make_full("cfg2")
+        elif w == "cfg4full":
+            make_full("cfg4")
         elif w == "qpc":
             make_qpc()
         elif w == "cfg5":

@@ -93,6 +93,27 @@ def test_cfg2_full_grid_vs_oracle(cuda, prec):
         assert np.all(d <= 1e-9 * np.abs(full["val"]) + 1e-12 * np.abs(full["val"]).max())
 
 
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+def test_cfg4_full_grid_vs_reference(cuda, prec):
+    """Trispectrum config, every point of the grid against the reference's own
+    values (cfg4_full.npz from hospectra._compute_values)."""
+    import torch
+
+    P = api()
+    c = P.baseline_config("cfg4")
+    x = P.baseline_series(c)
+    full = golden("cfg4_full.npz")
+    assert hashlib.sha256(x.tobytes()).hexdigest() == str(full["x_sha"])
+    cfg = P.EstimationConfig(4, P.SegmentConfig(m=c.m, k=c.k), c.m3, precision=prec, taper="hann")
+    g = P.estimate_spectrum(torch.from_numpy(x).to(cuda), cfg)
+    assert len(g.values) == int(full["npoints"])
+    err = north_star(g.values, full["val"])
+    assert err <= TOL[prec], f"cfg4 {prec} vs reference full grid: {err:.3e}"
+    if prec == "fp64":
+        d = np.abs(g.values - full["val"])
+        assert np.all(d <= 1e-9 * np.abs(full["val"]) + 1e-12 * np.abs(full["val"]).max())
+
+
 @pytest.mark.parametrize("name,prec", [("cfg3", "fp32"), ("cfg3", "fp64"), ("cfg4", "fp32"), ("cfg4", "fp64")])
 def test_baseline_rows_vs_reference(cuda, name, prec):
     import torch
