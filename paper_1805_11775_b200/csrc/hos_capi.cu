@@ -596,7 +596,8 @@ bool build_cta_schedule(const hos_plan* p, CtaSchedule& cs, int interleave_ctas 
   const int ng = (int)cs.groups.size();
   auto weight = [&](int gi) -> int64_t {
     const hos::CtaGroup& gr = cs.groups[gi];
-    return gr.n == W ? W : std::max<int64_t>(W / gr.phases, 4);
+    static const int64_t floor_w = [] { const char* e = std::getenv("HOS_K2_REMW"); return e ? (int64_t)std::atoi(e) : (int64_t)3; }();  // cfg2: 4 left the remainder group's CTAs idle from 23 of 33 us; 3: K2 31.9 -> 31.6 us; 2: 37.9
+    return gr.n == W ? W : std::max<int64_t>(W / gr.phases, floor_w);
   };
   if (interleave_ctas > 0) {
     // Streaming schedule (host path, series arriving over PCIe while K2
