@@ -1585,8 +1585,16 @@ int hos_estimate_host(hos_plan* p, const void* x_host, int x_dtype, int64_t x_st
   const bool pinned = cudaPointerGetAttributes(&ai, x_host) == cudaSuccess && ai.type == cudaMemoryTypeHost &&
                       cudaPointerGetAttributes(&ao, out_host) == cudaSuccess && ao.type == cudaMemoryTypeHost;
   cudaGetLastError();
-  const char* zc_env = std::getenv("HOS_ZEROCOPY");
-  const bool zero_copy = pinned && p->fused && ai.devicePointer && ao.devicePointer && !(zc_env && zc_env[0] == '0');
+  const char* zc_env = std::getenv("HOS_ZEROCOPY");  // "0": never, "1": always (with page-locked buffers)
+  // Large batches go through the copy engines instead: the per-series
+  // smoother writes its outputs as 8-byte pieces 32 bytes apart, which cross
+  // PCIe as small writes (cfg5, 327 MB in + 136 MB out: 22.9 ms zero-copy,
+  // 9.4 ms with one H2D and one D2H copy), and copies this long run at the
+  // link rate (the cold-link behaviour of small copies does not matter).
+  const size_t host_bytes = (size_t)p->batch * (km * es + (size_t)p->geo.npoints * csize(p->precision));
+  const bool zc_size = p->batch == 1 || host_bytes <= ((size_t)16 << 20);
+  const bool zero_copy = pinned && p->fused && ai.devicePointer && ao.devicePointer &&
+                         (zc_env ? zc_env[0] != '0' : zc_size);
   // chunked: copy-engine transfers of the series in chunks on c_copy; per
   // chunk the front end (device-resident samples) and K2 (accumulating into
   // the partial slots) run while the next chunk crosses PCIe; the smoothing
